@@ -1,0 +1,80 @@
+// Local block GEMM interface used by the SUMMA schedules and the layers.
+//
+// Replaces the reference's CPU kernels matmul / matmul_nt / matmul_tn
+// (reference proj/src/matrix.cpp:142-216) and the `add` that accumulates
+// SUMMA steps (proj/src/algorithms.cpp:42). One call computes
+//
+//     C[b] (op)= alpha * sum_seg  opA(A_seg[b]) * opB(B_seg[b])
+//
+// for a (possibly two-level batched) set of row-major views, where
+// opA(A) = A ([M,K]) or A^T (A stored [K,M]), opB(B) = B ([K,N]) or B^T
+// (B stored [N,K]). The K dimension may be split over up to kMaxSegments
+// separately-stored panels: this is how the q SUMMA steps of one
+// Tesseract product accumulate in a single tensor-memory accumulator
+// instead of q launches plus q-1 HBM round trips of C.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tess {
+
+enum class DType : int { F32 = 0, BF16 = 1, F64 = 2 };
+
+inline int dtype_size(DType t) {
+  return t == DType::F32 ? 4 : t == DType::BF16 ? 2 : 8;
+}
+
+// Epilogue applied to v = alpha * acc (fp32) for every output element.
+enum class Epi : int {
+  Store = 0,   // C = v
+  Accum = 1,   // C += v            (C fp32; weight-gradient accumulation)
+  Resid = 2,   // C = v + R         (residual add fused into the producer)
+  Gelu = 3,    // Z = v; C = gelu(v) with the exact erf GeLU
+};
+
+constexpr int kMaxSegments = 4;
+
+struct GemmSeg {
+  const void* a = nullptr;  // A panel for this K range
+  const void* b = nullptr;  // B panel for this K range
+  int64_t k = 0;            // K extent of the panel
+};
+
+struct GemmDesc {
+  int64_t M = 0, N = 0;
+  int64_t nb0 = 1, nb1 = 1;  // batch extents (attention: heads, samples)
+  int nseg = 1;
+  GemmSeg seg[kMaxSegments];
+  bool trans_a = false;  // A stored [K, M] (TN products)
+  bool trans_b = false;  // B stored [N, K] (NT products)
+  int64_t lda = 0, as0 = 0, as1 = 0;  // element strides: row, batch0, batch1
+  int64_t ldb = 0, bs0 = 0, bs1 = 0;
+  DType in = DType::BF16;             // A and B element type
+  void* c = nullptr;
+  DType c_type = DType::F32;
+  int64_t ldc = 0, cs0 = 0, cs1 = 0;
+  const void* r = nullptr;            // residual, same type/strides as C
+  int64_t ldr = 0, rs0 = 0, rs1 = 0;
+  void* z = nullptr;                  // Gelu pre-activation output (bf16 or C type)
+  int64_t ldz = 0, zs0 = 0, zs1 = 0;
+  float alpha = 1.0f;
+  Epi epi = Epi::Store;
+};
+
+// bf16 inputs on 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream);
+
+// fp32 inputs, fp32 FMA on CUDA cores: the fp32 parity path (config 1 of
+// BASELINE.json: fp32 within 1e-5 of the fp64 reference).
+cudaError_t gemm_f32_simt(const GemmDesc& d, cudaStream_t stream);
+
+// Dispatch on d.in. Returns cudaErrorInvalidValue on unsupported layouts
+// (e.g. bf16 rows that are not 16-byte aligned, which TMA cannot address).
+cudaError_t gemm(const GemmDesc& d, cudaStream_t stream);
+
+// Last dispatch-level error text (thread local), for the C-ABI's
+// tess_last_error.
+const char* gemm_last_error();
+
+}  // namespace tess

@@ -1,0 +1,674 @@
+// Persistent, warp-specialised bf16 GEMM for sm_100a (tcgen05 + TMEM + TMA).
+//
+// This is the B200 replacement for the reference's local block products
+// matmul / matmul_nt / matmul_tn (proj/src/matrix.cpp:142-216) as called by
+// nn_product_rank / nt_product_rank / tn_product_rank
+// (proj/src/algorithms.cpp:34-76) and by the per-head attention loops
+// (proj/src/layers.cpp:392-405, 430-448).
+//
+// CTA layout (192 threads, one CTA per SM, grid = min(tiles, #SMs)):
+//   warp 0      TMA producer: one elected lane streams A/B k-blocks into a
+//               STAGES-deep shared-memory ring (128B-swizzled boxes).
+//   warp 1      MMA issuer + TMEM owner: one lane issues
+//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) into a
+//               double-buffered fp32 accumulator in tensor memory and
+//               commits each stage back to the producer.
+//   warps 2..5  epilogue: tcgen05.ld the accumulator (warp w reads TMEM lanes
+//               32*(w%4)..+31), apply alpha / bias-free epilogue (store,
+//               accumulate, residual add, exact-erf GeLU) and write C.
+// The accumulator is double buffered (2*BN TMEM columns), so the epilogue of
+// tile i overlaps the MMAs of tile i+1.
+//
+// Operand majorness is a template parameter, so the three Tesseract
+// variants need no transposes in HBM:
+//   NN  A K-major (row-major [M,K]),  B MN-major (row-major [K,N])
+//   NT  A K-major,                    B K-major  (row-major [N,K])
+//   TN  A MN-major (row-major [K,M]), B MN-major
+#include "gemm.h"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+namespace tess {
+namespace sm100 {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int kThreads = 192;
+
+struct Params {
+  CUtensorMap tma_a[kMaxSegments];
+  CUtensorMap tma_b[kMaxSegments];
+  int seg_kb[kMaxSegments];
+  int nseg;
+  int total_kb;
+  int M, N;
+  int nb0;
+  int tiles_m, tiles_n, tiles_per_batch, num_tiles;
+  int group_m;
+  void* c;
+  int c_bf16;
+  long long ldc, cs0, cs1;
+  const void* r;
+  long long ldr, rs0, rs1;
+  void* z;
+  long long ldz, zs0, zs1;
+  float alpha;
+  int epi;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map,
+                                            uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::"
+      "bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0),
+      "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor for a 128B-swizzled canonical layout.
+//   K-major : rows of 128 B (64 bf16 of K), 8-row atoms SBO=1024 B apart.
+//   MN-major: rows of 128 B (64 bf16 of M/N) per K index, 8-K-row atoms
+//             SBO=1024 B apart, 64-wide M/N chunks LBO bytes apart.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo,
+                                               uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc,
+                                         uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 "
+      "[%0];" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+        "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]),
+        "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float gelu_erf(float v) {
+  return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+}
+
+// Tile index -> (batch0, batch1, m0, n0). Within a batch, tiles are grouped
+// group_m tiles tall so that one wave of CTAs shares A and B panels in L2.
+__device__ __forceinline__ void decode_tile(const Params& p, int tile, int& b0,
+                                            int& b1, int& m0, int& n0) {
+  const int b = tile / p.tiles_per_batch;
+  const int r = tile - b * p.tiles_per_batch;
+  b0 = b % p.nb0;
+  b1 = b / p.nb0;
+  const int width = p.group_m * p.tiles_n;
+  const int g = r / width;
+  const int first_m = g * p.group_m;
+  const int gm = min(p.tiles_m - first_m, p.group_m);
+  const int in = r - g * width;
+  const int tm = first_m + in % gm;
+  const int tn = in / gm;
+  m0 = tm * BM;
+  n0 = tn;  // scaled by BN by the caller
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <typename T>
+__device__ __forceinline__ T* batch_ptr(void* base, long long s0, long long s1,
+                                        int b0, int b1) {
+  return reinterpret_cast<T*>(base) + s0 * b0 + s1 * b1;
+}
+
+// Writes 32 consecutive columns [n, n+32) of one output row.
+__device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0,
+                                                   int b1, int m, int n,
+                                                   const uint32_t (&acc)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * p.alpha;
+  const int epi = p.epi;
+  const bool full = (n + 32 <= p.N);
+  const int nvalid = full ? 32 : max(0, p.N - n);
+
+  if (p.c_bf16) {
+    __nv_bfloat16* crow =
+        batch_ptr<__nv_bfloat16>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n;
+    if (epi == (int)Epi::Resid) {
+      const __nv_bfloat16* rrow =
+          batch_ptr<__nv_bfloat16>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
+          (long long)m * p.ldr + n;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 rv = *reinterpret_cast<const uint4*>(rrow + q * 8);
+          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[q * 8 + e] += __bfloat162float(rb[e]);
+        }
+      } else {
+        for (int j = 0; j < nvalid; ++j) v[j] += __bfloat162float(rrow[j]);
+      }
+    } else if (epi == (int)Epi::Gelu) {
+      __nv_bfloat16* zrow = batch_ptr<__nv_bfloat16>(p.z, p.zs0, p.zs1, b0, b1) +
+                            (long long)m * p.ldz + n;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 out;
+          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            o2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+          *reinterpret_cast<uint4*>(zrow + q * 8) = out;
+        }
+      } else {
+        for (int j = 0; j < nvalid; ++j) zrow[j] = __float2bfloat16_rn(v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    }
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 out;
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          o2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+        *reinterpret_cast<uint4*>(crow + q * 8) = out;
+      }
+    } else {
+      for (int j = 0; j < nvalid; ++j) crow[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* crow = batch_ptr<float>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n;
+    if (epi == (int)Epi::Accum) {
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = *reinterpret_cast<const float4*>(crow + q * 4);
+          v[q * 4 + 0] += o.x;
+          v[q * 4 + 1] += o.y;
+          v[q * 4 + 2] += o.z;
+          v[q * 4 + 3] += o.w;
+        }
+      } else {
+        for (int j = 0; j < nvalid; ++j) v[j] += crow[j];
+      }
+    } else if (epi == (int)Epi::Resid) {
+      const float* rrow = batch_ptr<float>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
+                          (long long)m * p.ldr + n;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = *reinterpret_cast<const float4*>(rrow + q * 4);
+          v[q * 4 + 0] += o.x;
+          v[q * 4 + 1] += o.y;
+          v[q * 4 + 2] += o.z;
+          v[q * 4 + 3] += o.w;
+        }
+      } else {
+        for (int j = 0; j < nvalid; ++j) v[j] += rrow[j];
+      }
+    } else if (epi == (int)Epi::Gelu) {
+      float* zrow = batch_ptr<float>(p.z, p.zs0, p.zs1, b0, b1) + (long long)m * p.ldz + n;
+      for (int j = 0; j < nvalid; ++j) zrow[j] = v[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    }
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(crow + q * 4) =
+            make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+    } else {
+      for (int j = 0; j < nvalid; ++j) crow[j] = v[j];
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < p.nseg; ++s) {
+      prefetch_tmap(&p.tma_a[s]);
+      prefetch_tmap(&p.tma_b[s]);
+    }
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(tmem_slot)),
+        "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        int b0, b1, m0, tn;
+        decode_tile(p, tile, b0, b1, m0, tn);
+        const int n0 = tn * BN;
+        for (int s = 0; s < p.nseg; ++s) {
+          const CUtensorMap* ma = &p.tma_a[s];
+          const CUtensorMap* mb = &p.tma_b[s];
+          for (int kb = 0; kb < p.seg_kb[s]; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * C::STAGE_BYTES;
+            uint8_t* sb = sa + C::A_BYTES;
+            mbar_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+            const int k = kb * BK;
+            if (!A_MN) {
+              tma_load_4d(sa, ma, &full_bar[stage], k, m0, b0, b1);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BM / 64; ++c)
+                tma_load_4d(sa + c * 8192, ma, &full_bar[stage], m0 + c * 64, k, b0, b1);
+            }
+            if (!B_MN) {
+              tma_load_4d(sb, mb, &full_bar[stage], k, n0, b0, b1);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BN / 64; ++c)
+                tma_load_4d(sb + c * 8192, mb, &full_bar[stage], n0 + c * 64, k, b0, b1);
+            }
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      const uint32_t idesc = (1u << 4)     // D = f32
+                             | (1u << 7)   // A = bf16
+                             | (1u << 10)  // B = bf16
+                             | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.total_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc(sa + k * 2048, 8192, 1024)
+                                     : make_sdesc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc(sb + k * 2048, 8192, 1024)
+                                     : make_sdesc(sb + k * 32, 16, 1024);
+            mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // -------------------------------------------------- epilogue warps
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int b0, b1, m0, tn;
+      decode_tile(p, tile, b0, b1, m0, tn);
+      const int n0 = tn * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int m = m0 + quad * 32 + lane;
+      const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(trow + c * 32, r);
+        const int n = n0 + c * 32;
+        if (m < p.M && n < p.N) epilogue_row_chunk(p, b0, b1, m, n, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+                     tmem_base),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+  });
+  return fn;
+}
+
+// Encodes a 4-D bf16 view [inner, outer, nb0, nb1] with a {64, box_outer}
+// box and 128B swizzle. Strides are in elements.
+bool encode_view(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer,
+                 int64_t ld, int64_t nb0, int64_t s0, int64_t nb1, int64_t s1,
+                 int box_outer, std::string* err) {
+  auto fn = encode_fn();
+  if (!fn) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  const int64_t dense = ld * outer;
+  if (nb0 <= 1) s0 = dense;
+  if (nb1 <= 1) s1 = s0 * (nb0 > 1 ? nb0 : 1);
+  cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)nb0,
+                        (cuuint64_t)nb1};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)s0 * 2,
+                           (cuuint64_t)s1 * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_outer, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  for (int i = 0; i < 3; ++i) {
+    if (strides[i] % 16 != 0) {
+      *err = "bf16 GEMM operand stride not 16-byte aligned (TMA)";
+      return false;
+    }
+  }
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) {
+    *err = "bf16 GEMM operand base not 16-byte aligned (TMA)";
+    return false;
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr),
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch(const Params& p, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;  // per instantiation; benign race
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = std::min(p.num_tiles, num_sms());
+  kern<<<grid, kThreads, C::SMEM_BYTES, stream>>>(p);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_bn(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
+  if (!a_mn && b_mn) return launch<BN, false, true>(p, s);
+  if (!a_mn && !b_mn) return launch<BN, false, false>(p, s);
+  if (a_mn && b_mn) return launch<BN, true, true>(p, s);
+  return launch<BN, true, false>(p, s);
+}
+
+}  // namespace sm100
+
+namespace {
+thread_local std::string g_gemm_err;
+}
+
+const char* gemm_last_error() { return g_gemm_err.c_str(); }
+
+cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
+  using namespace sm100;
+  if (d.in != DType::BF16) {
+    g_gemm_err = "gemm_bf16_sm100: inputs must be bf16";
+    return cudaErrorInvalidValue;
+  }
+  if (d.nseg < 1 || d.nseg > kMaxSegments || d.M <= 0 || d.N <= 0) {
+    g_gemm_err = "gemm_bf16_sm100: bad shape/segments";
+    return cudaErrorInvalidValue;
+  }
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  const int BN = d.N > 128 ? 256 : 128;
+  const bool a_mn = d.trans_a;   // A stored [K, M]: M contiguous
+  const bool b_mn = !d.trans_b;  // B stored [K, N]: N contiguous
+  int total_kb = 0;
+  for (int s = 0; s < d.nseg; ++s) {
+    const int64_t K = d.seg[s].k;
+    if (K <= 0 || K % 8 != 0) {
+      g_gemm_err = "gemm_bf16_sm100: K must be a positive multiple of 8";
+      return cudaErrorInvalidValue;
+    }
+    std::string err;
+    bool ok;
+    if (!a_mn)
+      ok = encode_view(&p.tma_a[s], d.seg[s].a, K, d.M, d.lda, d.nb0, d.as0, d.nb1,
+                       d.as1, BM, &err);
+    else
+      ok = encode_view(&p.tma_a[s], d.seg[s].a, d.M, K, d.lda, d.nb0, d.as0, d.nb1,
+                       d.as1, 64, &err);
+    if (ok) {
+      if (!b_mn)
+        ok = encode_view(&p.tma_b[s], d.seg[s].b, K, d.N, d.ldb, d.nb0, d.bs0, d.nb1,
+                         d.bs1, BN, &err);
+      else
+        ok = encode_view(&p.tma_b[s], d.seg[s].b, d.N, K, d.ldb, d.nb0, d.bs0, d.nb1,
+                         d.bs1, 64, &err);
+    }
+    if (!ok) {
+      g_gemm_err = "gemm_bf16_sm100: " + err;
+      return cudaErrorInvalidValue;
+    }
+    p.seg_kb[s] = static_cast<int>((K + BK - 1) / BK);
+    total_kb += p.seg_kb[s];
+  }
+  const int cvec = d.c_type == DType::BF16 ? 8 : 4;
+  if (d.ldc % cvec != 0 || reinterpret_cast<uintptr_t>(d.c) % 16 != 0 ||
+      (d.r && (d.ldr % cvec != 0 || reinterpret_cast<uintptr_t>(d.r) % 16 != 0)) ||
+      (d.z && (d.ldz % cvec != 0 || reinterpret_cast<uintptr_t>(d.z) % 16 != 0))) {
+    g_gemm_err = "gemm_bf16_sm100: output rows must be 16-byte aligned";
+    return cudaErrorInvalidValue;
+  }
+  if ((d.epi == Epi::Resid && !d.r) || (d.epi == Epi::Gelu && !d.z) ||
+      (d.epi == Epi::Accum && d.c_type != DType::F32)) {
+    g_gemm_err = "gemm_bf16_sm100: epilogue operands missing or wrong type";
+    return cudaErrorInvalidValue;
+  }
+  p.nseg = d.nseg;
+  p.total_kb = total_kb;
+  p.M = static_cast<int>(d.M);
+  p.N = static_cast<int>(d.N);
+  p.nb0 = static_cast<int>(d.nb0);
+  p.tiles_m = static_cast<int>((d.M + BM - 1) / BM);
+  p.tiles_n = static_cast<int>((d.N + BN - 1) / BN);
+  p.tiles_per_batch = p.tiles_m * p.tiles_n;
+  const long long nt = (long long)p.tiles_per_batch * d.nb0 * d.nb1;
+  if (nt > (1ll << 31) - 1) {
+    g_gemm_err = "gemm_bf16_sm100: too many tiles";
+    return cudaErrorInvalidValue;
+  }
+  p.num_tiles = static_cast<int>(nt);
+  p.group_m = 16;
+  p.c = d.c;
+  p.c_bf16 = d.c_type == DType::BF16;
+  p.ldc = d.ldc;
+  p.cs0 = d.cs0;
+  p.cs1 = d.cs1;
+  p.r = d.r;
+  p.ldr = d.ldr;
+  p.rs0 = d.rs0;
+  p.rs1 = d.rs1;
+  p.z = d.z;
+  p.ldz = d.ldz;
+  p.zs0 = d.zs0;
+  p.zs1 = d.zs1;
+  p.alpha = d.alpha;
+  p.epi = static_cast<int>(d.epi);
+  cudaError_t e = BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
+                            : launch_bn<128>(p, a_mn, b_mn, stream);
+  if (e != cudaSuccess) g_gemm_err = std::string("gemm_bf16_sm100 launch: ") +
+                                     cudaGetErrorString(e);
+  return e;
+}
+
+}  // namespace tess
