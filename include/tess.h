@@ -1,0 +1,263 @@
+/*
+ * tess.h -- C-ABI of the B200-native Tesseract (2.5-D tensor parallel) path.
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (tesseract-sim, /root/reference/proj/include/tsim). Each entry point names
+ * the reference interface it replaces as `ref: file:line`. All functions are
+ * extern "C", exception-free and return a tess_status mirroring the
+ * reference's exception taxonomy (error.hpp:11-48); the message of the last
+ * failure on the calling thread is available from tess_last_error().
+ *
+ * Ownership: callers own every buffer they pass. A tess_ctx owns its
+ * communicators, events and device workspace (SUMMA panels, partial sums,
+ * layer caches). One tess_ctx per rank; a ctx is used by one host thread at
+ * a time (ref: runtime.hpp:91-94, RankCtx is per-thread). Per-rank calls are
+ * asynchronous on the given CUDA stream (cudaStream_t passed as void*; NULL
+ * means the legacy default stream).
+ *
+ * Dtypes: TESS_F32 computes in fp32 on CUDA cores (the fp32 parity mode,
+ * rel. error <= 1e-5 vs the fp64 reference); TESS_BF16 stores activations and
+ * weights in bf16 and runs every contraction on tcgen05 tensor cores with fp32
+ * accumulation (weight gradients, LayerNorm statistics, softmax and all
+ * reductions are fp32).
+ */
+#ifndef TESS_H_
+#define TESS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TESS_OK = 0,
+  TESS_ERR_SHAPE = 1,          /* ref: error.hpp:16 ShapeError */
+  TESS_ERR_DIVISIBILITY = 2,   /* ref: error.hpp:22 DivisibilityError */
+  TESS_ERR_GRID = 3,           /* ref: error.hpp:28 GridError */
+  TESS_ERR_SPMD = 4,           /* ref: error.hpp:34 SpmdError (rank failure, mismatched
+                                  collective, deadlock, NCCL error) */
+  TESS_ERR_IO = 5,             /* ref: error.hpp:39 IoError */
+  TESS_ERR_CONFIG = 6,         /* ref: error.hpp:44 ConfigError */
+  TESS_ERR_CUDA = 7,           /* CUDA runtime / launch failure */
+  TESS_ERR_UNSUPPORTED = 8,    /* layout the sm_100a kernels cannot address */
+  TESS_ERR_INVALID = 9         /* null handle / bad enum */
+} tess_status;
+
+typedef enum { TESS_F32 = 0, TESS_BF16 = 1, TESS_F64 = 2 } tess_dtype;
+
+/* ref: grid.hpp:30 GroupKind {Row, Column, Depth} */
+typedef enum { TESS_ROW = 0, TESS_COL = 1, TESS_DEPTH = 2 } tess_group;
+
+/* ref: algorithms.hpp:15 MatmulVariant {NN, NT, TN} */
+typedef enum { TESS_NN = 0, TESS_NT = 1, TESS_TN = 2 } tess_variant;
+
+/* ref: shard.hpp:27 Scheme (the two Tesseract layouts) */
+typedef enum { TESS_SCHEME_A = 0, TESS_SCHEME_B = 1 } tess_scheme;
+
+/* ref: layers.hpp:187 LayerOp */
+typedef enum {
+  TESS_OP_FEEDFORWARD = 0,
+  TESS_OP_ATTENTION = 1,
+  TESS_OP_LAYERNORM = 2,
+  TESS_OP_BIAS_ADD = 3,
+  TESS_OP_BLOCK = 4
+} tess_layer_op;
+
+/* ref: runtime.hpp:20 CollectiveKind (meter index) */
+typedef enum {
+  TESS_KIND_BROADCAST = 0,
+  TESS_KIND_REDUCE = 1,
+  TESS_KIND_ALL_REDUCE = 2,
+  TESS_KIND_SHIFT = 3,
+  TESS_KIND_P2P = 4
+} tess_kind;
+
+/* tess_matmul flags */
+#define TESS_ACCUMULATE 0x1u      /* C += result (fp32 C) instead of C = result */
+#define TESS_SUM_OVER_DEPTH 0x2u  /* TN: all-reduce the layer partial over depth
+                                     (ref: algorithms.cpp:72-74) */
+
+typedef struct tess_ctx tess_ctx;
+
+/* Transformer geometry, ref: layers.hpp:22-27 LayerDims */
+typedef struct {
+  int batch, seq, hidden, heads;
+} tess_layer_dims;
+
+/* Per-rank parameter shard, ref: layers.hpp:70-75 BlockShard. Device
+ * pointers. Weights are TesseractB blocks in the compute dtype:
+ * w_qkv [h/q, 3h/q] (per-head interleaved Q|K|V columns, layers.hpp:38-41),
+ * w_proj [h/q, h/q], w_ff1 [h/q, 4h/q], w_ff2 [4h/q, h/q]. LayerNorm
+ * vectors are the j-slice [h/q] in fp32. */
+typedef struct {
+  const void* w_qkv;
+  const void* w_proj;
+  const void* w_ff1;
+  const void* w_ff2;
+  const float* ln1_gain;
+  const float* ln1_bias;
+  const float* ln2_gain;
+  const float* ln2_bias;
+  double eps;
+} tess_block_shard;
+
+/* Per-rank gradient shard (fp32 device buffers, same shapes as the shard),
+ * ref: layers.hpp:79-82 BlockShardGrads. Any pointer may be NULL. */
+typedef struct {
+  float* w_qkv;
+  float* w_proj;
+  float* w_ff1;
+  float* w_ff2;
+  float* ln1_gain;
+  float* ln1_bias;
+  float* ln2_gain;
+  float* ln2_bias;
+} tess_block_grads;
+
+/* Flat communication meter, ref: runtime.hpp:24-69 CommStats (counted in
+ * matrix elements, flat per-message counting) for ONE rank. by_kind holds
+ * [messages, elements] charged on this rank's send side per tess_kind. */
+typedef struct {
+  uint64_t sent_messages, sent_elements, received_messages, received_elements;
+  uint64_t by_kind[5][2];
+} tess_comm_stats;
+
+/* ------------------------------------------------------------------ grid
+ * ref: grid.hpp:47-85 GridSpec; pure host functions. */
+const char* tess_last_error(void);
+const char* tess_version(void);
+tess_status tess_grid_check(int q, int d, int allow_d_gt_q);           /* ref: grid.cpp:26-37 */
+tess_status tess_grid_parse(const char* text, int allow_d_gt_q, int* q,
+                            int* d);                                   /* ref: grid.cpp:133-169 */
+tess_status tess_grid_rank_of(int q, int d, int i, int j, int k, int* rank); /* ref: grid.cpp:43-49 */
+tess_status tess_grid_coord_of(int q, int d, int rank, int* i, int* j,
+                               int* k);                                /* ref: grid.cpp:51-61 */
+tess_status tess_grid_block_row(int q, int d, int i, int j, int k, int* h); /* ref: grid.cpp:63-69 */
+tess_status tess_grid_group(int q, int d, int i, int j, int k, tess_group g,
+                            int* group_index, int* slot, int* group_size); /* ref: grid.cpp:71-104 */
+tess_status tess_grid_member_at(int q, int d, tess_group g, int group_index,
+                                int slot, int* i, int* j, int* k);     /* ref: grid.cpp:106-131 */
+
+/* ------------------------------------------------------- contexts / comms
+ * ref: runtime.hpp:95-136 RankCtx, runtime.hpp:179-191 run_spmd. */
+
+/* NCCL backend, one process per GPU: world communicator from a shared
+ * ncclUniqueId (128 bytes, made by rank 0 with tess_nccl_unique_id and
+ * distributed by the launcher), then ncclCommSplit into the row
+ * (color k*q+i, key j), column (color k*q+j, key i) and depth
+ * (color i*q+j, key k) communicators (ref: grid.cpp:79-95). */
+tess_status tess_nccl_unique_id(void* out128);
+tess_status tess_init_nccl(int q, int d, int allow_d_gt_q, int rank, int device,
+                           const void* unique_id128, tess_ctx** out);
+
+/* In-process backend: creates p = d*q*q contexts (one per rank, rank r on
+ * devices[r], or all on the current device when devices is NULL). Each
+ * context must be driven by its own host thread (as the reference's
+ * SpmdRunner does); collectives rendezvous on the host and move data with
+ * stream-ordered device copies / peer reads, summing in slot-ascending order
+ * like the reference engine (ref: runtime.cpp:221-372). */
+tess_status tess_init_local(int q, int d, int allow_d_gt_q, const int* devices,
+                            tess_ctx** out_per_rank);
+tess_status tess_destroy(tess_ctx* ctx);
+tess_status tess_coord(const tess_ctx* ctx, int* rank, int* i, int* j, int* k);
+tess_status tess_group_comm(tess_ctx* ctx, tess_group g, void** nccl_comm);
+tess_status tess_get_comm_stats(const tess_ctx* ctx, tess_comm_stats* out);
+tess_status tess_reset_comm_stats(tess_ctx* ctx);
+/* Enables the reference trace format "<rank>:<step> <kind> <group> <root>
+ * <bytes>" (ref: runtime.hpp:71-85, runtime.cpp:90-96); bytes are counted
+ * as elements * 8 like the reference. */
+tess_status tess_set_trace(tess_ctx* ctx, int enable);
+tess_status tess_trace_text(const tess_ctx* ctx, char* buf, size_t cap, size_t* needed);
+
+/* ------------------------------------------------------------ collectives
+ * ref: runtime.hpp:105-121. Device buffers; fp32 sums. */
+tess_status tess_broadcast(tess_ctx* ctx, tess_group g, int root_slot, void* buf,
+                           size_t bytes, size_t elements, void* stream);
+tess_status tess_reduce(tess_ctx* ctx, tess_group g, int root_slot, const float* send,
+                        float* recv, size_t n, void* stream);
+tess_status tess_all_reduce(tess_ctx* ctx, tess_group g, float* buf, size_t n, void* stream);
+tess_status tess_barrier(tess_ctx* ctx);
+
+/* ------------------------------------------------------------- partition
+ * ref: shard.cpp:68-98 (partition) and 139-183 (combine). `global` is a
+ * device (or host) row-major [rows, cols] matrix of dtype; `local` the
+ * rank's device block. Bit-exact copies. */
+tess_status tess_partition(tess_ctx* ctx, tess_scheme scheme, tess_dtype dtype,
+                           const void* global, int64_t rows, int64_t cols, void* local,
+                           void* stream);
+tess_status tess_unpartition(tess_ctx* ctx, tess_scheme scheme, tess_dtype dtype,
+                             const void* local, int64_t rows, int64_t cols, void* global,
+                             void* stream);
+
+/* --------------------------------------------------------------- products
+ * ref: algorithms.hpp:91-96 nn/nt/tn_product_rank. Local block shapes:
+ *   NN: a [ar, ak] (TesseractA), b [ak, bn] (TesseractB) -> c [ar, bn]
+ *   NT: a [ar, an] (TesseractA), b [br, an] (TesseractB) -> c [ar, br]
+ *   TN: a [ar, an] (TesseractA), b [ar, bn] (TesseractA) -> c [an, bn]
+ *       (+ depth all-reduce with TESS_SUM_OVER_DEPTH)
+ * `in` is the dtype of a and b; c_type F32 or the input dtype. */
+tess_status tess_matmul(tess_ctx* ctx, tess_variant v, tess_dtype in, const void* a,
+                        int64_t a_rows, int64_t a_cols, const void* b, int64_t b_rows,
+                        int64_t b_cols, void* c, tess_dtype c_type, uint32_t flags,
+                        void* stream);
+
+/* ----------------------------------------------------------------- layers
+ * ref: layers.hpp:123-161 (rank-level fwd/bwd) and layers.cpp:604-692
+ * (layer_run). x, dy, y, dx are the rank's TesseractA activation blocks
+ * [batch*seq/(d*q), hidden/q] in the compute dtype (device or pinned/pageable
+ * host memory; host buffers are staged through the context). The forward
+ * cache lives in the context until the matching backward (one outstanding
+ * forward per op per context). `x` must stay valid until the backward.
+ * grads may be NULL (the collective sequence is unchanged, ref:
+ * layers.cpp:372-377); with accumulate=0 gradients are overwritten, else
+ * added (ref: layers.cpp:368-371 add()). dbias (BiasAdd) is fp32 [hidden/q],
+ * valid on i == 0 ranks (ref: layers.cpp:507-517). */
+tess_status tess_layer_forward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
+                               const tess_layer_dims* dims, const tess_block_shard* shard,
+                               const void* bias_row0, const void* x, void* y, void* stream);
+tess_status tess_layer_backward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
+                                const tess_layer_dims* dims, const tess_block_shard* shard,
+                                const void* dy, void* dx, tess_block_grads* grads,
+                                int accumulate, float* dbias, void* stream);
+
+/* ---------------------------------------------------------- global level
+ * Whole-matrix operators with host fp64 buffers, mirroring the reference's
+ * value-semantics API: partition -> per-rank SPMD (one host thread per rank,
+ * in-process backend) -> combine. `compute` selects TESS_F32 or TESS_BF16
+ * (inputs are rounded once to it). devices: p device ordinals or NULL (all
+ * ranks on the current device). stats_rank: p x 4 counters [sent msgs,
+ * sent elems, recv msgs, recv elems] and stats_kind: 5 x 2, both optional,
+ * with the reference's CommStats semantics. */
+tess_status tess_tesseract_matmul(int q, int d, int allow_d_gt_q, tess_variant v,
+                                  tess_dtype compute, const double* a, int64_t a_rows,
+                                  int64_t a_cols, const double* b, int64_t b_rows,
+                                  int64_t b_cols, double* c, const int* devices,
+                                  uint64_t* stats_rank, uint64_t* stats_kind);
+/* ref: algorithms.hpp:54-57 */
+tess_status tess_tesseract_backward(int q, int d, int allow_d_gt_q, tess_dtype compute,
+                                    const double* dc, const double* a, const double* b,
+                                    int64_t m, int64_t k, int64_t n, double* da,
+                                    double* db, const int* devices, uint64_t* stats_rank,
+                                    uint64_t* stats_kind);
+/* ref: algorithms.hpp:78-80 tesseract_backward_dense */
+tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q, int d,
+                           int allow_d_gt_q, tess_dtype compute, const double* x,
+                           const double* dy, const double* const* params, double eps,
+                           double* y, double* dx, double* const* grads, double* dbias,
+                           const int* devices, uint64_t* stats_rank,
+                           uint64_t* stats_kind);
+/* ref: layers.hpp:195-197 layer_run; params/grads: 8 host fp64 arrays in
+ * BlockParams order (w_qkv, w_proj, w_ff1, w_ff2, ln1_gain, ln1_bias,
+ * ln2_gain, ln2_bias); grads may be NULL; dbias [hidden] for BiasAdd. */
+
+/* Number of kernels launched by this library on the calling process since
+ * load (for the bench's gpu_launches claim). */
+uint64_t tess_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TESS_H_ */

@@ -1,0 +1,550 @@
+"""B200-native Tesseract (2.5-D tensor parallelism, arXiv 2105.14500).
+
+Python host mirror of the reference's C++ operator API (tesseract-sim,
+proj/include/tsim/*.hpp) over the C-ABI library ``libtess.so``
+(include/tess.h). Names, argument meaning and error behaviour follow the
+reference:
+
+    GridSpec(q, d, allow_d_gt_q)           grid.hpp:47-85
+    tesseract_matmul(a, b, grid, variant)  algorithms.hpp:54-57
+    tesseract_backward_dense(dc, a, b, g)  algorithms.hpp:78-80
+    layer_run(op, x, dy, params, dims, g)  layers.hpp:195-197
+    ShapeError / DivisibilityError / GridError / SpmdError / ConfigError
+                                           error.hpp:11-48
+
+Every compute call runs the CUDA path (sm_100a tcgen05 GEMMs and the
+memory-bound kernels of libtess.so). There is no CPU fallback: importing this
+package without the built library raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtess.so")
+
+__all__ = [
+    "GridSpec", "RankCoord", "CommStats", "AlgoResult", "LayerDims", "LayerRunResult",
+    "tesseract_matmul", "tesseract_backward_dense", "layer_run", "TessError", "ShapeError",
+    "DivisibilityError", "GridError", "SpmdError", "ConfigError", "IoError", "CudaError",
+    "UnsupportedError", "lib", "RankContext", "init_local", "init_nccl", "nccl_unique_id",
+    "PARAM_NAMES", "LAYER_OPS",
+]
+
+
+# ----------------------------------------------------------------- errors
+class TessError(RuntimeError):
+    """Base of the reference's exception taxonomy (error.hpp:11)."""
+
+
+class ShapeError(TessError):
+    pass
+
+
+class DivisibilityError(TessError):
+    pass
+
+
+class GridError(TessError):
+    pass
+
+
+class SpmdError(TessError):
+    pass
+
+
+class IoError(TessError):
+    pass
+
+
+class ConfigError(TessError):
+    pass
+
+
+class CudaError(TessError):
+    pass
+
+
+class UnsupportedError(TessError):
+    pass
+
+
+_STATUS = {1: ShapeError, 2: DivisibilityError, 3: GridError, 4: SpmdError, 5: IoError,
+           6: ConfigError, 7: CudaError, 8: UnsupportedError, 9: TessError}
+
+F32, BF16, F64 = 0, 1, 2
+_DTYPES = {"f32": F32, "fp32": F32, "float32": F32, "bf16": BF16, "bfloat16": BF16}
+ROW, COL, DEPTH = 0, 1, 2
+_VARIANTS = {"nn": 0, "nt": 1, "tn": 2}
+LAYER_OPS = {"feedforward": 0, "attention": 1, "layernorm": 2, "bias_add": 3, "block": 4}
+PARAM_NAMES = ("w_qkv", "w_proj", "w_ff1", "w_ff2", "ln1_gain", "ln1_bias", "ln2_gain",
+               "ln2_bias")
+KIND_NAMES = ("broadcast", "reduce", "all_reduce", "shift", "p2p")
+
+
+# ---------------------------------------------------------------- library
+class _LayerDimsC(C.Structure):
+    _fields_ = [("batch", C.c_int), ("seq", C.c_int), ("hidden", C.c_int), ("heads", C.c_int)]
+
+
+class BlockShardC(C.Structure):
+    _fields_ = [("w_qkv", C.c_void_p), ("w_proj", C.c_void_p), ("w_ff1", C.c_void_p),
+                ("w_ff2", C.c_void_p), ("ln1_gain", C.c_void_p), ("ln1_bias", C.c_void_p),
+                ("ln2_gain", C.c_void_p), ("ln2_bias", C.c_void_p), ("eps", C.c_double)]
+
+
+class BlockGradsC(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in PARAM_NAMES]
+
+
+class CommStatsC(C.Structure):
+    _fields_ = [("sent_messages", C.c_uint64), ("sent_elements", C.c_uint64),
+                ("received_messages", C.c_uint64), ("received_elements", C.c_uint64),
+                ("by_kind", (C.c_uint64 * 2) * 5)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i, i64, u32, dp = C.c_void_p, C.c_int, C.c_int64, C.c_uint32, C.POINTER(C.c_double)
+    ip, u64p = C.POINTER(C.c_int), C.POINTER(C.c_uint64)
+    sig = {
+        "tess_last_error": ([], C.c_char_p),
+        "tess_version": ([], C.c_char_p),
+        "tess_kernel_launches": ([], C.c_uint64),
+        "tess_grid_check": ([i, i, i], i),
+        "tess_grid_parse": ([C.c_char_p, i, ip, ip], i),
+        "tess_grid_rank_of": ([i, i, i, i, i, ip], i),
+        "tess_grid_coord_of": ([i, i, i, ip, ip, ip], i),
+        "tess_grid_block_row": ([i, i, i, i, i, ip], i),
+        "tess_grid_group": ([i, i, i, i, i, i, ip, ip, ip], i),
+        "tess_grid_member_at": ([i, i, i, i, i, ip, ip, ip], i),
+        "tess_nccl_unique_id": ([vp], i),
+        "tess_init_nccl": ([i, i, i, i, i, vp, C.POINTER(vp)], i),
+        "tess_init_local": ([i, i, i, ip, C.POINTER(vp)], i),
+        "tess_destroy": ([vp], i),
+        "tess_coord": ([vp, ip, ip, ip, ip], i),
+        "tess_group_comm": ([vp, i, C.POINTER(vp)], i),
+        "tess_get_comm_stats": ([vp, C.POINTER(CommStatsC)], i),
+        "tess_reset_comm_stats": ([vp], i),
+        "tess_set_trace": ([vp, i], i),
+        "tess_trace_text": ([vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], i),
+        "tess_broadcast": ([vp, i, i, vp, C.c_size_t, C.c_size_t, vp], i),
+        "tess_reduce": ([vp, i, i, vp, vp, C.c_size_t, vp], i),
+        "tess_all_reduce": ([vp, i, vp, C.c_size_t, vp], i),
+        "tess_barrier": ([vp], i),
+        "tess_partition": ([vp, i, i, vp, i64, i64, vp, vp], i),
+        "tess_unpartition": ([vp, i, i, vp, i64, i64, vp, vp], i),
+        "tess_matmul": ([vp, i, i, vp, i64, i64, vp, i64, i64, vp, i, u32, vp], i),
+        "tess_layer_forward": ([vp, i, i, C.POINTER(_LayerDimsC), C.POINTER(BlockShardC), vp,
+                                vp, vp, vp], i),
+        "tess_layer_backward": ([vp, i, i, C.POINTER(_LayerDimsC), C.POINTER(BlockShardC), vp,
+                                 vp, C.POINTER(BlockGradsC), i, vp, vp], i),
+        "tess_tesseract_matmul": ([i, i, i, i, i, dp, i64, i64, dp, i64, i64, dp, ip, u64p,
+                                   u64p], i),
+        "tess_tesseract_backward": ([i, i, i, i, dp, dp, dp, i64, i64, i64, dp, dp, ip, u64p,
+                                     u64p], i),
+        "tess_layer_run": ([i, C.POINTER(_LayerDimsC), i, i, i, i, dp, dp, C.POINTER(dp),
+                            C.c_double, dp, dp, C.POINTER(dp), dp, ip, u64p, u64p], i),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib.tess_last_error().decode(errors="replace")
+        raise _STATUS.get(status, TessError)(msg)
+
+
+def _dtype(dtype) -> int:
+    if isinstance(dtype, int):
+        return dtype
+    try:
+        return _DTYPES[str(dtype).lower()]
+    except KeyError:
+        raise ValueError(f"dtype must be one of {sorted(_DTYPES)}") from None
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _devices(devices, p):
+    if devices is None:
+        return None
+    arr = (C.c_int * p)(*devices)
+    if len(devices) != p:
+        raise ValueError("devices must list one ordinal per rank")
+    return arr
+
+
+# ------------------------------------------------------------------ grid
+@dataclasses.dataclass(frozen=True, order=True)
+class RankCoord:
+    i: int = 0
+    j: int = 0
+    k: int = 0
+
+
+class GridSpec:
+    """[q, q, d] grid, rank = k*q*q + i*q + j (grid.hpp:47-85)."""
+
+    _FAMILIES = {"row": ROW, "column": COL, "col": COL, "depth": DEPTH, ROW: ROW, COL: COL,
+                 DEPTH: DEPTH}
+
+    def __init__(self, q: int, d: int, allow_d_gt_q: bool = False):
+        _check(lib.tess_grid_check(q, d, int(allow_d_gt_q)))
+        self._q, self._d, self.allow_d_gt_q = q, d, bool(allow_d_gt_q)
+
+    @staticmethod
+    def parse(text: str, allow_d_gt_q: bool = False) -> "GridSpec":
+        q, d = C.c_int(), C.c_int()
+        _check(lib.tess_grid_parse(text.encode(), int(allow_d_gt_q), C.byref(q), C.byref(d)))
+        return GridSpec(q.value, d.value, allow_d_gt_q)
+
+    def q(self) -> int:
+        return self._q
+
+    def d(self) -> int:
+        return self._d
+
+    def size(self) -> int:
+        return self._d * self._q * self._q
+
+    def valid(self, c: RankCoord) -> bool:
+        return 0 <= c.i < self._q and 0 <= c.j < self._q and 0 <= c.k < self._d
+
+    def rank_of(self, c: RankCoord) -> int:
+        r = C.c_int()
+        if not self.valid(c):
+            raise GridError(f"coordinate ({c.i},{c.j},{c.k}) out of range for grid {self}")
+        _check(lib.tess_grid_rank_of(self._q, self._d, c.i, c.j, c.k, C.byref(r)))
+        return r.value
+
+    def coord_of(self, rank: int) -> RankCoord:
+        i, j, k = C.c_int(), C.c_int(), C.c_int()
+        if not 0 <= rank < self.size():
+            raise GridError(f"rank {rank} out of range for grid {self}")
+        _check(lib.tess_grid_coord_of(self._q, self._d, rank, C.byref(i), C.byref(j), C.byref(k)))
+        return RankCoord(i.value, j.value, k.value)
+
+    def block_row(self, c: RankCoord) -> int:
+        h = C.c_int()
+        _check(lib.tess_grid_block_row(self._q, self._d, c.i, c.j, c.k, C.byref(h)))
+        return h.value
+
+    def _group(self, c: RankCoord, kind):
+        gi, sl, gs = C.c_int(), C.c_int(), C.c_int()
+        _check(lib.tess_grid_group(self._q, self._d, c.i, c.j, c.k, self._FAMILIES[kind],
+                                   C.byref(gi), C.byref(sl), C.byref(gs)))
+        return gi.value, sl.value, gs.value
+
+    def group_size(self, kind) -> int:
+        return self._d if self._FAMILIES[kind] == DEPTH else self._q
+
+    def group_count(self, kind) -> int:
+        return self._q * self._q if self._FAMILIES[kind] == DEPTH else self._q * self._d
+
+    def group_index(self, c: RankCoord, kind) -> int:
+        return self._group(c, kind)[0]
+
+    def slot_in_group(self, c: RankCoord, kind) -> int:
+        return self._group(c, kind)[1]
+
+    def member_at(self, kind, group_index: int, slot: int) -> RankCoord:
+        i, j, k = C.c_int(), C.c_int(), C.c_int()
+        _check(lib.tess_grid_member_at(self._q, self._d, self._FAMILIES[kind], group_index, slot,
+                                       C.byref(i), C.byref(j), C.byref(k)))
+        return RankCoord(i.value, j.value, k.value)
+
+    def group_of(self, c: RankCoord, kind) -> List[RankCoord]:
+        gi = self.group_index(c, kind)
+        return [self.member_at(kind, gi, s) for s in range(self.group_size(kind))]
+
+    def __eq__(self, other):
+        return isinstance(other, GridSpec) and (self._q, self._d) == (other._q, other._d)
+
+    def __repr__(self):
+        return f"[{self._q},{self._q},{self._d}]"
+
+    to_string = __repr__
+
+
+# ----------------------------------------------------------------- stats
+class CommStats:
+    """Flat meter (runtime.hpp:24-69): per-rank [sent msgs, sent elems, recv
+    msgs, recv elems] and per-kind [messages, elements]."""
+
+    def __init__(self, per_rank: np.ndarray, per_kind: np.ndarray):
+        self.per_rank = np.asarray(per_rank, dtype=np.uint64).reshape(-1, 4)
+        self.per_kind = np.asarray(per_kind, dtype=np.uint64).reshape(5, 2)
+
+    def rank_count(self):
+        return self.per_rank.shape[0]
+
+    def sent_messages(self, r):
+        return int(self.per_rank[r, 0])
+
+    def sent_elements(self, r):
+        return int(self.per_rank[r, 1])
+
+    def received_messages(self, r):
+        return int(self.per_rank[r, 2])
+
+    def received_elements(self, r):
+        return int(self.per_rank[r, 3])
+
+    def total_sent_messages(self):
+        return int(self.per_rank[:, 0].sum())
+
+    def total_sent_elements(self):
+        return int(self.per_rank[:, 1].sum())
+
+    def total_received_messages(self):
+        return int(self.per_rank[:, 2].sum())
+
+    def total_received_elements(self):
+        return int(self.per_rank[:, 3].sum())
+
+    def by_kind(self, kind: str):
+        k = KIND_NAMES.index(kind)
+        return int(self.per_kind[k, 0]), int(self.per_kind[k, 1])
+
+    def __eq__(self, other):
+        return (isinstance(other, CommStats) and (self.per_rank == other.per_rank).all()
+                and (self.per_kind == other.per_kind).all())
+
+
+@dataclasses.dataclass
+class AlgoResult:
+    value: np.ndarray
+    stats: CommStats
+
+
+def _stats_bufs(p):
+    return np.zeros((p, 4), dtype=np.uint64), np.zeros((5, 2), dtype=np.uint64)
+
+
+def _u64(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+# ------------------------------------------------------ global operators
+def tesseract_matmul(a, b, grid: GridSpec, variant: str = "nn", dtype="f32",
+                     devices: Optional[Sequence[int]] = None) -> AlgoResult:
+    """[q,q,d] product (algorithms.cpp:131-186) on the GPU.
+
+    variant nn: C = A B; nt: C = A B^T; tn: C = A^T B (+ depth all-reduce).
+    dtype 'f32' (CUDA-core fp32) or 'bf16' (tcgen05, fp32 accumulate; the
+    returned value is the fp32 result before any cast)."""
+    a, b = _f64(a), _f64(b)
+    v = _VARIANTS[variant]
+    shape = {0: (a.shape[0], b.shape[1]), 1: (a.shape[0], b.shape[0]),
+             2: (a.shape[1], b.shape[1])}[v]
+    c = np.zeros(shape)
+    sr, sk = _stats_bufs(grid.size())
+    _check(lib.tess_tesseract_matmul(grid.q(), grid.d(), int(grid.allow_d_gt_q), v, _dtype(dtype),
+                                     _dptr(a), a.shape[0], a.shape[1], _dptr(b), b.shape[0],
+                                     b.shape[1], _dptr(c), _devices(devices, grid.size()),
+                                     _u64(sr), _u64(sk)))
+    return AlgoResult(c, CommStats(sr, sk))
+
+
+@dataclasses.dataclass
+class DenseBackwardResult:
+    a_grad: np.ndarray
+    b_grad: np.ndarray
+    stats: CommStats
+
+
+def tesseract_backward_dense(c_grad, a, b, grid: GridSpec, dtype="f32",
+                             devices: Optional[Sequence[int]] = None) -> DenseBackwardResult:
+    """dA = dC B^T (NT), dB = A^T dC (TN + depth all-reduce), algorithms.cpp:188-242."""
+    dc, a, b = _f64(c_grad), _f64(a), _f64(b)
+    m, k = a.shape
+    n = b.shape[1]
+    if dc.shape != (m, n) or b.shape[0] != k:
+        raise ShapeError("tesseract_backward: shapes inconsistent with C = A*B")
+    da, db = np.zeros((m, k)), np.zeros((k, n))
+    sr, sk = _stats_bufs(grid.size())
+    _check(lib.tess_tesseract_backward(grid.q(), grid.d(), int(grid.allow_d_gt_q), _dtype(dtype),
+                                       _dptr(dc), _dptr(a), _dptr(b), m, k, n, _dptr(da),
+                                       _dptr(db), _devices(devices, grid.size()), _u64(sr),
+                                       _u64(sk)))
+    return DenseBackwardResult(da, db, CommStats(sr, sk))
+
+
+@dataclasses.dataclass
+class LayerDims:
+    batch: int
+    seq: int
+    hidden: int
+    heads: int
+
+    def c(self):
+        return _LayerDimsC(self.batch, self.seq, self.hidden, self.heads)
+
+
+@dataclasses.dataclass
+class LayerRunResult:
+    y: np.ndarray
+    dx: np.ndarray
+    grads: Dict[str, np.ndarray]
+    dbias: np.ndarray
+    stats: CommStats
+
+
+def _param_shapes(h):
+    return [(h, 3 * h), (h, h), (h, 4 * h), (4 * h, h), (1, h), (1, h), (1, h), (1, h)]
+
+
+def layer_run(op: str, x, dy, params: Dict[str, np.ndarray], dims: LayerDims, grid: GridSpec,
+              dtype="f32", eps: float = 1e-5,
+              devices: Optional[Sequence[int]] = None) -> LayerRunResult:
+    """Forward + backward of one layer op in one SPMD run (layers.cpp:604-692)."""
+    x, dy = _f64(x), _f64(dy)
+    h = dims.hidden
+    if x.shape != (dims.batch * dims.seq, h) or dy.shape != x.shape:
+        raise ShapeError("shard_activation: activation must be [batch*seq, hidden]")
+    prm = [_f64(params[n]) for n in PARAM_NAMES]
+    for p_, s_ in zip(prm, _param_shapes(h)):
+        if p_.size != s_[0] * s_[1]:
+            raise ShapeError("layer_run: parameter shape mismatch")
+    grads = [np.zeros(s) for s in _param_shapes(h)]
+    y, dx, dbias = np.zeros_like(x), np.zeros_like(x), np.zeros(h)
+    P = (C.POINTER(C.c_double) * 8)(*[_dptr(t) for t in prm])
+    G = (C.POINTER(C.c_double) * 8)(*[_dptr(t) for t in grads])
+    sr, sk = _stats_bufs(grid.size())
+    dc = dims.c()
+    _check(lib.tess_layer_run(LAYER_OPS[op], C.byref(dc), grid.q(), grid.d(),
+                              int(grid.allow_d_gt_q), _dtype(dtype), _dptr(x), _dptr(dy), P, eps,
+                              _dptr(y), _dptr(dx), G, _dptr(dbias),
+                              _devices(devices, grid.size()), _u64(sr), _u64(sk)))
+    return LayerRunResult(y, dx, dict(zip(PARAM_NAMES, grads)), dbias, CommStats(sr, sk))
+
+
+# ------------------------------------------------------- per-rank contexts
+class RankContext:
+    """One rank's tess_ctx (the RankCtx of runtime.hpp:95-136). Device
+    buffers are passed as integer pointers (e.g. torch.Tensor.data_ptr())."""
+
+    def __init__(self, handle: int):
+        self.h = C.c_void_p(handle)
+        r, i, j, k = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib.tess_coord(self.h, C.byref(r), C.byref(i), C.byref(j), C.byref(k)))
+        self.rank = r.value
+        self.coord = RankCoord(i.value, j.value, k.value)
+
+    def close(self):
+        if self.h:
+            _check(lib.tess_destroy(self.h))
+            self.h = None
+
+    def stats(self) -> dict:
+        s = CommStatsC()
+        _check(lib.tess_get_comm_stats(self.h, C.byref(s)))
+        return {"sent_messages": s.sent_messages, "sent_elements": s.sent_elements,
+                "received_messages": s.received_messages,
+                "received_elements": s.received_elements,
+                "by_kind": [[s.by_kind[k][0], s.by_kind[k][1]] for k in range(5)]}
+
+    def reset_stats(self):
+        _check(lib.tess_reset_comm_stats(self.h))
+
+    def set_trace(self, on=True):
+        _check(lib.tess_set_trace(self.h, int(on)))
+
+    def trace(self) -> str:
+        need = C.c_size_t()
+        _check(lib.tess_trace_text(self.h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(lib.tess_trace_text(self.h, buf, need.value, None))
+        return buf.value.decode()
+
+    def barrier(self):
+        _check(lib.tess_barrier(self.h))
+
+    def broadcast(self, group, root, ptr, nbytes, elements, stream=0):
+        _check(lib.tess_broadcast(self.h, group, root, ptr, nbytes, elements, stream))
+
+    def reduce(self, group, root, send, recv, n, stream=0):
+        _check(lib.tess_reduce(self.h, group, root, send, recv, n, stream))
+
+    def all_reduce(self, group, buf, n, stream=0):
+        _check(lib.tess_all_reduce(self.h, group, buf, n, stream))
+
+    def partition(self, scheme: int, dtype, global_ptr, rows, cols, local_ptr, stream=0):
+        _check(lib.tess_partition(self.h, scheme, _dtype(dtype), global_ptr, rows, cols,
+                                  local_ptr, stream))
+
+    def unpartition(self, scheme: int, dtype, local_ptr, rows, cols, global_ptr, stream=0):
+        _check(lib.tess_unpartition(self.h, scheme, _dtype(dtype), local_ptr, rows, cols,
+                                    global_ptr, stream))
+
+    def matmul(self, variant: str, dtype, a, a_rows, a_cols, b, b_rows, b_cols, c, c_dtype="f32",
+               accumulate=False, sum_over_depth=False, stream=0):
+        flags = (1 if accumulate else 0) | (2 if sum_over_depth else 0)
+        _check(lib.tess_matmul(self.h, _VARIANTS[variant], _dtype(dtype), a, a_rows, a_cols, b,
+                               b_rows, b_cols, c, _dtype(c_dtype), flags, stream))
+
+    def layer_forward(self, op, dtype, dims: LayerDims, shard: BlockShardC, x, y,
+                      bias_row0=None, stream=0):
+        dc = dims.c()
+        _check(lib.tess_layer_forward(self.h, LAYER_OPS[op], _dtype(dtype), C.byref(dc),
+                                      C.byref(shard), bias_row0, x, y, stream))
+
+    def layer_backward(self, op, dtype, dims: LayerDims, shard: BlockShardC, dy, dx,
+                       grads: Optional[BlockGradsC] = None, accumulate=False, dbias=None,
+                       stream=0):
+        dc = dims.c()
+        _check(lib.tess_layer_backward(self.h, LAYER_OPS[op], _dtype(dtype), C.byref(dc),
+                                       C.byref(shard), dy, dx,
+                                       C.byref(grads) if grads is not None else None,
+                                       int(accumulate), dbias, stream))
+
+
+def init_local(grid: GridSpec, devices: Optional[Sequence[int]] = None) -> List[RankContext]:
+    """In-process contexts for every rank (drive each from its own thread)."""
+    p = grid.size()
+    out = (C.c_void_p * p)()
+    _check(lib.tess_init_local(grid.q(), grid.d(), int(grid.allow_d_gt_q),
+                               _devices(devices, p), out))
+    return [RankContext(out[r]) for r in range(p)]
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.tess_nccl_unique_id(buf))
+    return buf.raw
+
+
+def init_nccl(grid: GridSpec, rank: int, device: int, unique_id: bytes) -> RankContext:
+    """One process per GPU: NCCL world + row/column/depth ncclCommSplit."""
+    out = C.c_void_p()
+    uid = C.create_string_buffer(bytes(unique_id), 128)
+    _check(lib.tess_init_nccl(grid.q(), grid.d(), int(grid.allow_d_gt_q), rank, device, uid,
+                              C.byref(out)))
+    return RankContext(out.value)
+
+
+def kernel_launches() -> int:
+    return int(lib.tess_kernel_launches())

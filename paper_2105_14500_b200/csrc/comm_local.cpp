@@ -1,0 +1,263 @@
+// In-process, thread-per-rank communicator (see comm.h).
+//
+// Protocol per collective on a group of g ranks (all members call it in the
+// same program order, as the reference requires, runtime.hpp:91-94):
+//   phase A: every member records a "ready" event on its stream after the
+//            data it contributes (or the buffer it will overwrite) is ready,
+//            posts {pointer, event, signature} and meets the others at a host
+//            barrier; signatures must agree (runtime.cpp:236-248).
+//   move   : receivers / reducers make their stream wait on the peers'
+//            ready events and move data with device copies or a slot-
+//            ascending sum kernel that reads the peers' buffers directly.
+//   phase B: members post "done" events and meet again; anyone whose buffer
+//            is read by others waits on those events before reusing it.
+// Posts are double buffered by call parity, so two barriers per call are
+// enough. A failing rank marks the world failed and every waiter aborts
+// with TESS_ERR_SPMD instead of deadlocking (runtime.cpp:422-471).
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+
+#include "comm.h"
+
+namespace tess {
+
+namespace {
+
+struct Post {
+  const void* ptr = nullptr;
+  cudaEvent_t ev = nullptr;
+  int kind = -1;
+  int root = -1;
+  size_t bytes = 0;
+};
+
+struct Rendezvous {
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<Post> a[2], b[2];
+};
+
+}  // namespace
+
+struct LocalWorld {
+  Grid grid;
+  std::vector<int> devices;
+  std::vector<std::unique_ptr<Rendezvous>> rv[3];
+  Rendezvous world;
+  std::atomic<bool> failed{false};
+  std::mutex fail_mu;
+  std::string failure;
+
+  void mark_failed(const std::string& why) {
+    std::lock_guard<std::mutex> lk(fail_mu);
+    if (!failed.exchange(true)) failure = why;
+  }
+
+  void wait(Rendezvous& r, int gsize) {
+    std::unique_lock<std::mutex> lk(r.mu);
+    const uint64_t g = r.gen;
+    if (++r.arrived == gsize) {
+      r.arrived = 0;
+      ++r.gen;
+      r.cv.notify_all();
+      return;
+    }
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(600);
+    while (r.gen == g) {
+      r.cv.wait_for(lk, std::chrono::milliseconds(20));
+      if (r.gen != g) break;
+      if (failed.load()) fail(TESS_ERR_SPMD, "aborted: another rank failed (" + failure + ")");
+      if (std::chrono::steady_clock::now() > deadline) {
+        mark_failed("collective rendezvous timed out (deadlock?)");
+        fail(TESS_ERR_SPMD, "collective rendezvous timed out (deadlock?)");
+      }
+    }
+  }
+};
+
+std::shared_ptr<LocalWorld> make_local_world(const Grid& g, const std::vector<int>& devices) {
+  auto w = std::make_shared<LocalWorld>();
+  w->grid = g;
+  w->devices = devices;
+  for (int f = 0; f < 3; ++f) {
+    const int n = g.group_count(Family(f));
+    const int gs = g.group_size(Family(f));
+    for (int i = 0; i < n; ++i) {
+      auto r = std::make_unique<Rendezvous>();
+      for (int p = 0; p < 2; ++p) {
+        r->a[p].resize(gs);
+        r->b[p].resize(gs);
+      }
+      w->rv[f].push_back(std::move(r));
+    }
+  }
+  // Peer access between distinct devices so sum kernels can read peers.
+  std::vector<int> uniq;
+  for (int dv : devices)
+    if (std::find(uniq.begin(), uniq.end(), dv) == uniq.end()) uniq.push_back(dv);
+  for (int a : uniq)
+    for (int b : uniq) {
+      if (a == b) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a, b);
+      if (can) {
+        cudaSetDevice(a);
+        cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          fail(TESS_ERR_CUDA, "cudaDeviceEnablePeerAccess failed");
+        cudaGetLastError();
+      }
+    }
+  if (!devices.empty()) cudaSetDevice(devices[0]);
+  return w;
+}
+
+namespace {
+
+class LocalComm : public Comm {
+ public:
+  LocalComm(std::shared_ptr<LocalWorld> w, int rank) : w_(std::move(w)), rank_(rank) {
+    c_ = w_->grid.coord_of(rank);
+    device_ = w_->devices[rank];
+    TESS_CUDA(cudaSetDevice(device_));
+    for (int f = 0; f < 3; ++f)
+      for (int p = 0; p < 2; ++p) {
+        TESS_CUDA(cudaEventCreateWithFlags(&ev_a_[f][p], cudaEventDisableTiming));
+        TESS_CUDA(cudaEventCreateWithFlags(&ev_b_[f][p], cudaEventDisableTiming));
+      }
+  }
+
+  ~LocalComm() override {
+    cudaSetDevice(device_);
+    for (int f = 0; f < 3; ++f)
+      for (int p = 0; p < 2; ++p) {
+        cudaEventDestroy(ev_a_[f][p]);
+        cudaEventDestroy(ev_b_[f][p]);
+      }
+    if (scratch_) cudaFree(scratch_);
+  }
+
+  void bcast(Family f, int root, void* buf, size_t bytes, cudaStream_t s) override {
+    Ctx x = enter(f, 0, root, bytes, buf, s);
+    if (!x.rv) return;
+    if (x.slot != root && bytes) {
+      TESS_CUDA(cudaStreamWaitEvent(s, x.rv->a[x.par][root].ev, 0));
+      TESS_CUDA(cudaMemcpyAsync(buf, x.rv->a[x.par][root].ptr, bytes, cudaMemcpyDefault, s));
+    }
+    TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
+    x.rv->b[x.par][x.slot] = {buf, ev_b_[f][x.par], 0, root, bytes};
+    w_->wait(*x.rv, x.gsize);
+    if (x.slot == root)
+      for (int o = 0; o < x.gsize; ++o)
+        if (o != root) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][o].ev, 0));
+  }
+
+  void reduce(Family f, int root, const float* send, float* recv, size_t n,
+              cudaStream_t s) override {
+    Ctx x = enter(f, 1, root, n * 4, send, s);
+    if (!x.rv) {
+      if (recv != send && n) TESS_CUDA(cudaMemcpyAsync(recv, send, n * 4, cudaMemcpyDefault, s));
+      return;
+    }
+    if (x.slot == root && n) {
+      const float* ptrs[8];
+      for (int o = 0; o < x.gsize; ++o) {
+        if (o != x.slot) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->a[x.par][o].ev, 0));
+        ptrs[o] = static_cast<const float*>(x.rv->a[x.par][o].ptr);
+      }
+      launch_sum_f32(ptrs, x.gsize, recv, n, s);
+    }
+    TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
+    x.rv->b[x.par][x.slot] = {recv, ev_b_[f][x.par], 1, root, n * 4};
+    w_->wait(*x.rv, x.gsize);
+    if (x.slot != root) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][root].ev, 0));
+  }
+
+  void allreduce(Family f, float* buf, size_t n, cudaStream_t s) override {
+    Ctx x = enter(f, 2, 0, n * 4, buf, s);
+    if (!x.rv) return;
+    if (n) {
+      ensure_scratch(n);
+      const float* ptrs[8];
+      for (int o = 0; o < x.gsize; ++o) {
+        if (o != x.slot) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->a[x.par][o].ev, 0));
+        ptrs[o] = static_cast<const float*>(x.rv->a[x.par][o].ptr);
+      }
+      launch_sum_f32(ptrs, x.gsize, scratch_, n, s);
+    }
+    TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
+    x.rv->b[x.par][x.slot] = {buf, ev_b_[f][x.par], 2, 0, n * 4};
+    w_->wait(*x.rv, x.gsize);
+    if (n) {
+      for (int o = 0; o < x.gsize; ++o)
+        if (o != x.slot) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][o].ev, 0));
+      TESS_CUDA(cudaMemcpyAsync(buf, scratch_, n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+
+  void barrier() override { w_->wait(w_->world, w_->grid.size()); }
+
+ private:
+  struct Ctx {
+    Rendezvous* rv = nullptr;
+    int slot = 0, gsize = 1, par = 0;
+  };
+
+  Ctx enter(Family f, int kind, int root, size_t bytes, const void* ptr, cudaStream_t s) {
+    Ctx x;
+    const Grid& g = w_->grid;
+    x.gsize = g.group_size(f);
+    x.slot = g.slot_in_group(c_, f);
+    if (root < 0 || root >= x.gsize)
+      fail(TESS_ERR_SPMD, "collective root slot " + std::to_string(root) + " out of range");
+    if (x.gsize == 1) return x;
+    if (x.gsize > 8) fail(TESS_ERR_UNSUPPORTED, "local backend supports groups of <= 8");
+    TESS_CUDA(cudaSetDevice(device_));
+    x.rv = w_->rv[f][g.group_index(c_, f)].get();
+    x.par = static_cast<int>(calls_[f]++ & 1);
+    TESS_CUDA(cudaEventRecord(ev_a_[f][x.par], s));
+    x.rv->a[x.par][x.slot] = {ptr, ev_a_[f][x.par], kind, root, bytes};
+    w_->wait(*x.rv, x.gsize);
+    const Post& p0 = x.rv->a[x.par][0];
+    const Post& me = x.rv->a[x.par][x.slot];
+    if (p0.kind != me.kind || p0.root != me.root || p0.bytes != me.bytes) {
+      const std::string msg = "mismatched collective in " +
+                              std::string(f == ROW ? "row" : f == COL ? "col" : "depth") +
+                              " group " + std::to_string(g.group_index(c_, f)) + " at rank " +
+                              std::to_string(rank_);
+      w_->mark_failed(msg);
+      fail(TESS_ERR_SPMD, msg);
+    }
+    return x;
+  }
+
+  void ensure_scratch(size_t n) {
+    if (n <= scratch_n_) return;
+    if (scratch_) TESS_CUDA(cudaFree(scratch_));
+    TESS_CUDA(cudaMalloc(&scratch_, n * 4));
+    scratch_n_ = n;
+  }
+
+  std::shared_ptr<LocalWorld> w_;
+  int rank_;
+  Coord c_;
+  int device_;
+  cudaEvent_t ev_a_[3][2], ev_b_[3][2];
+  uint64_t calls_[3] = {0, 0, 0};
+  float* scratch_ = nullptr;
+  size_t scratch_n_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_local_comm(std::shared_ptr<LocalWorld> w, int rank) {
+  return std::make_unique<LocalComm>(std::move(w), rank);
+}
+
+void local_world_fail(LocalWorld* w, const std::string& why) { w->mark_failed(why); }
+
+}  // namespace tess

@@ -1,0 +1,184 @@
+// NCCL backend: one process per GPU over NVLink 5 / NVSwitch.
+//
+// World communicator from a shared ncclUniqueId, then three ncclCommSplits
+// whose (color, key) follow the reference's group geometry
+// (proj/src/grid.cpp:79-95):
+//   row    color = k*q + i, key = j   (slot in row group)
+//   column color = k*q + j, key = i
+//   depth  color = i*q + j, key = k
+// so NCCL rank == reference slot in every group and root slots map 1:1.
+// Collective mapping (reference runtime.hpp:105-121):
+//   broadcast -> ncclBroadcast(root = slot)
+//   reduce    -> ncclReduce(sum, root = slot)
+//   all_reduce-> ncclAllReduce(sum)
+// For the q = 2, d <= 2 target grids every group is a 2-party exchange, so
+// the sums are a single commutative fp32 add and are identical on both ranks.
+//
+// NCCL is resolved at run time (dlopen) instead of being a link-time
+// dependency: the process may already hold a different libnccl.so.2 (e.g. the
+// one bundled with PyTorch), and two NCCL builds cannot share one process.
+// Order: an already-loaded libnccl.so.2, $TESS_NCCL_LIBRARY, the system one.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "comm.h"
+
+namespace tess {
+
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
+  ncclResult_t (*CommCount)(const ncclComm_t, int*);
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) {
+      const char* env = std::getenv("TESS_NCCL_LIBRARY");
+      if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* n) {
+      void* p = dlsym(h, n);
+      if (!p && err.empty()) err = std::string("libnccl.so.2 lacks ") + n;
+      return p;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommSplit = reinterpret_cast<decltype(api.CommSplit)>(sym("ncclCommSplit"));
+    api.CommCount = reinterpret_cast<decltype(api.CommCount)>(sym("ncclCommCount"));
+    api.CommUserRank = reinterpret_cast<decltype(api.CommUserRank)>(sym("ncclCommUserRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.Reduce = reinterpret_cast<decltype(api.Reduce)>(sym("ncclReduce"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  });
+  if (!err.empty()) fail(TESS_ERR_SPMD, err);
+  return api;
+}
+
+}  // namespace
+
+#define TESS_NCCL(expr)                                                              \
+  do {                                                                               \
+    ncclResult_t r_ = (expr);                                                        \
+    if (r_ != ncclSuccess)                                                           \
+      ::tess::fail(TESS_ERR_SPMD, std::string(#expr) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+void nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  TESS_NCCL(nccl().GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+}
+
+namespace {
+
+class NcclComm : public Comm {
+ public:
+  NcclComm(const Grid& g, int rank, const void* uid128) : g_(g), rank_(rank) {
+    c_ = g.coord_of(rank);
+    ncclUniqueId id;
+    std::memcpy(&id, uid128, sizeof(id));
+    TESS_NCCL(nccl().CommInitRank(&world_, g.size(), id, rank));
+    for (int f = 0; f < 3; ++f) {
+      const Family fam = Family(f);
+      if (g.group_size(fam) == 1) {
+        comm_[f] = nullptr;
+        // Every rank must still take part in the split (collective call).
+        TESS_NCCL(nccl().CommSplit(world_, NCCL_SPLIT_NOCOLOR, 0, &comm_[f], nullptr));
+        comm_[f] = nullptr;
+        continue;
+      }
+      TESS_NCCL(nccl().CommSplit(world_, g.group_index(c_, fam), g.slot_in_group(c_, fam),
+                              &comm_[f], nullptr));
+      int nr = 0, me = 0;
+      TESS_NCCL(nccl().CommCount(comm_[f], &nr));
+      TESS_NCCL(nccl().CommUserRank(comm_[f], &me));
+      if (nr != g.group_size(fam) || me != g.slot_in_group(c_, fam))
+        fail(TESS_ERR_SPMD, "ncclCommSplit produced an unexpected group layout");
+    }
+  }
+
+  ~NcclComm() override {
+    for (int f = 0; f < 3; ++f)
+      if (comm_[f]) nccl().CommDestroy(comm_[f]);
+    if (world_) nccl().CommDestroy(world_);
+  }
+
+  void bcast(Family f, int root, void* buf, size_t bytes, cudaStream_t s) override {
+    if (!comm_[f] || !bytes) return;
+    TESS_NCCL(nccl().Broadcast(buf, buf, bytes, ncclUint8, root, comm_[f], s));
+  }
+
+  void reduce(Family f, int root, const float* send, float* recv, size_t n,
+              cudaStream_t s) override {
+    if (!comm_[f]) {
+      if (recv != send && n) TESS_CUDA(cudaMemcpyAsync(recv, send, n * 4, cudaMemcpyDeviceToDevice, s));
+      return;
+    }
+    if (!n) return;
+    // Non-root recv buffers are ignored by NCCL; pass send to keep it valid.
+    const bool is_root = g_.slot_in_group(c_, f) == root;
+    TESS_NCCL(nccl().Reduce(send, is_root ? recv : const_cast<float*>(send), n, ncclFloat32,
+                         ncclSum, root, comm_[f], s));
+  }
+
+  void allreduce(Family f, float* buf, size_t n, cudaStream_t s) override {
+    if (!comm_[f] || !n) return;
+    TESS_NCCL(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, comm_[f], s));
+  }
+
+  void barrier() override {
+    // A tiny all-reduce on the world communicator, then wait for it.
+    float* tmp = nullptr;
+    TESS_CUDA(cudaMalloc(&tmp, 4));
+    TESS_CUDA(cudaMemset(tmp, 0, 4));
+    TESS_NCCL(nccl().AllReduce(tmp, tmp, 1, ncclFloat32, ncclSum, world_, 0));
+    TESS_CUDA(cudaStreamSynchronize(0));
+    TESS_CUDA(cudaFree(tmp));
+  }
+
+  void* nccl_comm(Family f) override { return comm_[f]; }
+
+ private:
+  Grid g_;
+  int rank_;
+  Coord c_;
+  ncclComm_t world_ = nullptr;
+  ncclComm_t comm_[3] = {nullptr, nullptr, nullptr};
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_nccl_comm(const Grid& g, int rank, const void* uid128) {
+  return std::make_unique<NcclComm>(g, rank, uid128);
+}
+
+}  // namespace tess

@@ -1,0 +1,138 @@
+// Grid geometry (reference proj/src/grid.cpp), workspace, metered collectives.
+#include <charconv>
+
+#include "ctx.h"
+
+namespace tess {
+
+Grid::Grid(int q_, int d_, bool allow) : q(q_), d(d_) {
+  // ref: grid.cpp:26-37
+  if (q < 1 || d < 1)
+    fail(TESS_ERR_GRID, "grid " + str() + ": q and d must be >= 1");
+  if (d > q && !allow)
+    fail(TESS_ERR_GRID, "grid " + str() +
+                            ": depth d exceeds dimension q (pass allow_d_gt_q to permit)");
+}
+
+int Grid::rank_of(const Coord& c) const {
+  if (!valid(c)) fail(TESS_ERR_GRID, "coordinate out of range for grid " + str());
+  return c.k * q * q + c.i * q + c.j;  // ref: grid.cpp:43-49
+}
+
+Coord Grid::coord_of(int rank) const {
+  if (rank < 0 || rank >= size())
+    fail(TESS_ERR_GRID, "rank " + std::to_string(rank) + " out of range for grid " + str());
+  Coord c;  // ref: grid.cpp:51-61
+  c.k = rank / (q * q);
+  c.i = (rank / q) % q;
+  c.j = rank % q;
+  return c;
+}
+
+Coord Grid::member_at(Family f, int gi, int slot) const {
+  Coord c;  // ref: grid.cpp:106-131
+  if (f == ROW) c = {gi % q, slot, gi / q};
+  else if (f == COL) c = {slot, gi % q, gi / q};
+  else c = {gi / q, gi % q, slot};
+  if (!valid(c)) fail(TESS_ERR_GRID, "group member out of range for grid " + str());
+  return c;
+}
+
+// ref: grid.cpp:133-169 ("[q,q,d]" with positioned errors)
+Grid parse_grid(const std::string& text, bool allow) {
+  size_t pos = 0;
+  auto bad = [&](size_t at, const std::string& what) {
+    fail(TESS_ERR_CONFIG, "grid '" + text + "': " + what + " at position " + std::to_string(at));
+  };
+  auto expect = [&](char ch) {
+    if (pos >= text.size() || text[pos] != ch) bad(pos, std::string("expected '") + ch + "'");
+    ++pos;
+  };
+  auto number = [&]() {
+    int v = 0;
+    auto res = std::from_chars(text.data() + pos, text.data() + text.size(), v);
+    if (res.ec != std::errc() || res.ptr == text.data() + pos) bad(pos, "expected an integer");
+    pos = static_cast<size_t>(res.ptr - text.data());
+    return v;
+  };
+  expect('[');
+  const int q1 = number();
+  expect(',');
+  const size_t q2_pos = pos;
+  const int q2 = number();
+  expect(',');
+  const int d = number();
+  expect(']');
+  if (pos != text.size()) bad(pos, "trailing characters");
+  if (q1 != q2)
+    bad(q2_pos, "the first two extents must match (got " + std::to_string(q1) + " and " +
+                    std::to_string(q2) + ")");
+  return Grid(q1, d, allow);
+}
+
+// ------------------------------------------------------------ workspace
+Workspace::~Workspace() { release_all(); }
+
+void* Workspace::get(const std::string& name, size_t bytes) {
+  Buf& b = bufs_[name];
+  if (bytes == 0) bytes = 16;
+  if (b.bytes < bytes) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    if (b.ptr) TESS_CUDA(cudaFree(b.ptr));
+    b.ptr = nullptr;
+    b.bytes = 0;
+    // round up to 2 MiB to limit regrowth churn
+    const size_t rounded = (bytes + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+    TESS_CUDA(cudaMalloc(&b.ptr, rounded));
+    b.bytes = rounded;
+    cudaSetDevice(prev);
+  }
+  return b.ptr;
+}
+
+void Workspace::release_all() {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device_);
+  for (auto& kv : bufs_)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  bufs_.clear();
+  cudaSetDevice(prev);
+}
+
+size_t Workspace::bytes_held() const {
+  size_t t = 0;
+  for (auto& kv : bufs_) t += kv.second.bytes;
+  return t;
+}
+
+// ------------------------------------------------------- collectives
+static void trace_event(Ctx& c, int kind, Family f, int root, uint64_t elements) {
+  const uint64_t step = c.step++;
+  if (c.trace_on)
+    c.trace.push_back({c.rank, step, kind, static_cast<int>(f), root, elements * 8});
+}
+
+void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t elements,
+                cudaStream_t s) {
+  c.meter.bcast(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, elements);
+  trace_event(c, 0, f, root, elements);
+  c.comm->bcast(f, root, buf, bytes, s);
+}
+
+void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, size_t n,
+                 cudaStream_t s) {
+  c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, n, false);
+  trace_event(c, 1, f, root, n);
+  c.comm->reduce(f, root, send, recv, n, s);
+}
+
+void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s) {
+  c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), 0, n, true);
+  trace_event(c, 2, f, 0, n);
+  c.comm->allreduce(f, buf, n, s);
+}
+
+}  // namespace tess

@@ -1,0 +1,431 @@
+// Whole-matrix operators over host fp64 buffers (reference value-semantics
+// API): tesseract_matmul (algorithms.cpp:131-186), tesseract_backward_dense
+// (algorithms.cpp:188-242) and layer_run (layers.cpp:604-692).
+//
+// partition -> one host thread per rank driving its own tess_ctx over the
+// in-process backend (the SpmdRunner of runtime.cpp:534-554) -> combine with
+// the reference's replica checks (shard.cpp:139-183, layers.cpp:184-228).
+// Inputs are rounded once to the compute dtype on the device.
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+
+#include "kernels/kernels.h"
+#include "ops.h"
+
+using namespace tess;
+
+namespace tess {
+extern thread_local std::string g_last_error;
+}
+
+namespace {
+
+struct Runner {
+  Grid g;
+  std::vector<int> devs;
+  std::vector<tess_ctx*> ctx;
+
+  Runner(int q, int d, bool allow, const int* devices) : g(q, d, allow) {
+    int cur = 0;
+    TESS_CUDA(cudaGetDevice(&cur));
+    devs.resize(g.size());
+    for (int r = 0; r < g.size(); ++r) devs[r] = devices ? devices[r] : cur;
+    ctx.resize(g.size(), nullptr);
+    if (tess_init_local(q, d, allow, devs.data(), ctx.data()) != TESS_OK)
+      fail(TESS_ERR_CUDA, std::string("init_local: ") + g_last_error);
+  }
+  ~Runner() {
+    for (auto* c : ctx)
+      if (c) tess_destroy(c);
+  }
+
+  std::vector<int> unique_devices() const {
+    std::vector<int> u;
+    for (int dv : devs)
+      if (std::find(u.begin(), u.end(), dv) == u.end()) u.push_back(dv);
+    return u;
+  }
+
+  // Runs fn on every rank in its own thread; the first root-cause failure
+  // is rethrown (rank failures become SpmdError with the coordinate, like
+  // runtime.cpp:540-553; CUDA / unsupported-layout errors keep their status).
+  void run(const std::function<void(Ctx&, cudaStream_t)>& fn) {
+    std::mutex mu;
+    bool have = false;
+    tess_status st = TESS_OK;
+    std::string msg;
+    int first_rank = -1;
+    std::vector<std::thread> th;
+    for (int r = 0; r < g.size(); ++r) {
+      th.emplace_back([&, r] {
+        Ctx& c = *ctx[r];
+        cudaStream_t s = nullptr;
+        try {
+          TESS_CUDA(cudaSetDevice(c.device));
+          TESS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+          fn(c, s);
+          TESS_CUDA(cudaStreamSynchronize(s));
+        } catch (const tess::Error& e) {
+          local_world_fail(c.world.get(), e.what());
+          std::lock_guard<std::mutex> lk(mu);
+          const bool aborted = std::string(e.what()).rfind("aborted:", 0) == 0;
+          if (!have || (!aborted && msg.rfind("aborted:", 0) == 0)) {
+            have = true;
+            st = e.status;
+            msg = e.what();
+            first_rank = r;
+          }
+        }
+        if (s) {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    if (have) {
+      const Coord c = g.coord_of(first_rank);
+      const std::string where = "rank (" + std::to_string(c.i) + "," + std::to_string(c.j) +
+                                "," + std::to_string(c.k) + ") failed: ";
+      if (st == TESS_ERR_CUDA || st == TESS_ERR_UNSUPPORTED) fail(st, where + msg);
+      fail(TESS_ERR_SPMD, where + msg);
+    }
+  }
+
+  void stats(uint64_t* sr, uint64_t* sk) const {
+    if (sr)
+      for (int r = 0; r < g.size(); ++r) {
+        const Meter& m = ctx[r]->meter;
+        sr[4 * r + 0] = m.sent_msgs;
+        sr[4 * r + 1] = m.sent_elems;
+        sr[4 * r + 2] = m.recv_msgs;
+        sr[4 * r + 3] = m.recv_elems;
+      }
+    if (sk) {
+      std::memset(sk, 0, sizeof(uint64_t) * 10);
+      for (int r = 0; r < g.size(); ++r)
+        for (int k = 0; k < 5; ++k) {
+          sk[2 * k] += ctx[r]->meter.kind[k][0];
+          sk[2 * k + 1] += ctx[r]->meter.kind[k][1];
+        }
+    }
+  }
+};
+
+// Device copy of a host fp64 matrix rounded to `t`, one per device.
+struct DevMat {
+  std::vector<std::pair<int, void*>> per_dev;
+  ~DevMat() {
+    for (auto& pd : per_dev) {
+      cudaSetDevice(pd.first);
+      cudaFree(pd.second);
+    }
+  }
+  void* on(int dev) const {
+    for (auto& pd : per_dev)
+      if (pd.first == dev) return pd.second;
+    fail(TESS_ERR_INVALID, "matrix not resident on device");
+  }
+};
+
+void upload(DevMat& m, const std::vector<int>& devs, const double* host, size_t n, DType t) {
+  for (int dv : devs) {
+    TESS_CUDA(cudaSetDevice(dv));
+    void* d64 = nullptr;
+    void* dt = nullptr;
+    TESS_CUDA(cudaMalloc(&d64, std::max<size_t>(n, 1) * 8));
+    TESS_CUDA(cudaMalloc(&dt, std::max<size_t>(n, 1) * dtype_size(t)));
+    if (n) {
+      TESS_CUDA(cudaMemcpy(d64, host, n * 8, cudaMemcpyHostToDevice));
+      k_convert(d64, DType::F64, dt, t, n, nullptr);
+    }
+    TESS_CUDA(cudaDeviceSynchronize());
+    TESS_CUDA(cudaFree(d64));
+    m.per_dev.push_back({dv, dt});
+  }
+}
+
+void call(tess_status s) {
+  if (s != TESS_OK) fail(s, g_last_error);
+}
+
+// Local block of a global device matrix, in workspace `name`.
+void* take_block(Ctx& c, tess_scheme sch, DType t, const void* global, int64_t rows,
+                 int64_t cols, const std::string& name, cudaStream_t s) {
+  const int64_t rb = sch == TESS_SCHEME_A ? rows / (c.grid.q * c.grid.d) : rows / c.grid.q;
+  const int64_t cb = cols / c.grid.q;
+  void* local = c.ws->get(name, (size_t)rb * cb * dtype_size(t));
+  call(tess_partition(&c, sch, t == DType::F32 ? TESS_F32 : TESS_BF16, global, rows, cols, local, s));
+  return local;
+}
+
+float h2f(uint16_t h) {
+  uint32_t u = (uint32_t)h << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// Copies a rank's device block (dtype t) to a host float vector.
+std::vector<float> fetch(const void* dev, size_t n, DType t, cudaStream_t s) {
+  std::vector<float> out(n);
+  if (!n) return out;
+  if (t == DType::F32) {
+    TESS_CUDA(cudaMemcpyAsync(out.data(), dev, n * 4, cudaMemcpyDeviceToHost, s));
+    TESS_CUDA(cudaStreamSynchronize(s));
+  } else {
+    std::vector<uint16_t> tmp(n);
+    TESS_CUDA(cudaMemcpyAsync(tmp.data(), dev, n * 2, cudaMemcpyDeviceToHost, s));
+    TESS_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < n; ++i) out[i] = h2f(tmp[i]);
+  }
+  return out;
+}
+
+// Host combine of per-rank blocks (ref shard.cpp:139-183): TesseractA blocks
+// placed at (h, j); TesseractB blocks at (i, j) with k > 0 replicas required
+// to be bit-identical to k == 0.
+void combine(const Grid& g, tess_scheme sch, const std::vector<std::vector<float>>& blocks,
+             int64_t rows, int64_t cols, double* out) {
+  const int q = g.q, d = g.d;
+  const int64_t rb = sch == TESS_SCHEME_A ? rows / ((int64_t)q * d) : rows / q;
+  const int64_t cb = cols / q;
+  for (int r = 0; r < g.size(); ++r) {
+    const Coord c = g.coord_of(r);
+    if (sch == TESS_SCHEME_B && c.k > 0) {
+      const auto& ref = blocks[g.rank_of({c.i, c.j, 0})];
+      if (std::memcmp(ref.data(), blocks[r].data(), ref.size() * 4) != 0)
+        fail(TESS_ERR_SHAPE, "combine: replica divergence at rank (" + std::to_string(c.i) + "," +
+                                 std::to_string(c.j) + "," + std::to_string(c.k) + ")");
+      continue;
+    }
+    const int64_t r0 = (sch == TESS_SCHEME_A ? g.block_row(c) : c.i) * rb;
+    const int64_t c0 = (int64_t)c.j * cb;
+    for (int64_t i = 0; i < rb; ++i)
+      for (int64_t j = 0; j < cb; ++j) out[(r0 + i) * cols + c0 + j] = blocks[r][i * cb + j];
+  }
+}
+
+void require_div(int64_t v, int64_t by, const char* scheme, const char* dim) {
+  if (by == 0 || v % by != 0)
+    fail(TESS_ERR_DIVISIBILITY, std::string(scheme) + ": " + dim + " (" + std::to_string(v) +
+                                    ") not divisible by " + std::to_string(by));
+}
+
+DType compute_type(tess_dtype t) {
+  if (t == TESS_F32) return DType::F32;
+  if (t == TESS_BF16) return DType::BF16;
+  fail(TESS_ERR_UNSUPPORTED, "compute dtype must be TESS_F32 or TESS_BF16");
+}
+
+template <typename F>
+tess_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return TESS_OK;
+  } catch (const tess::Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TESS_ERR_INVALID;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+tess_status tess_tesseract_matmul(int q, int d, int allow, tess_variant v, tess_dtype compute,
+                                  const double* a, int64_t ar, int64_t ac, const double* b,
+                                  int64_t br, int64_t bc, double* c, const int* devices,
+                                  uint64_t* sr, uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    Grid g(q, d, allow != 0);
+    // shape checks (ref algorithms.cpp:23-31, 153-158, 170-174)
+    int64_t cr = 0, cc = 0;
+    tess_scheme bsch = TESS_SCHEME_B, csch = TESS_SCHEME_A;
+    if (v == TESS_NN) {
+      if (ac != br) fail(TESS_ERR_SHAPE, "tesseract_matmul(nn): A.cols (" + std::to_string(ac) +
+                                             ") != B.rows (" + std::to_string(br) + ")");
+      cr = ar, cc = bc;
+    } else if (v == TESS_NT) {
+      if (ac != bc) fail(TESS_ERR_SHAPE, "tesseract_matmul(nt): A.cols (" + std::to_string(ac) +
+                                             ") != B.cols (" + std::to_string(bc) + ")");
+      cr = ar, cc = br;
+    } else if (v == TESS_TN) {
+      if (ar != br) fail(TESS_ERR_SHAPE, "tesseract_matmul(tn): A.rows (" + std::to_string(ar) +
+                                             ") != B.rows (" + std::to_string(br) + ")");
+      cr = ac, cc = bc;
+      bsch = TESS_SCHEME_A;
+      csch = TESS_SCHEME_B;
+    } else {
+      fail(TESS_ERR_INVALID, "bad variant");
+    }
+    // partition divisibility (ref shard.cpp:74-98)
+    require_div(ar, (int64_t)q * d, "tesseract-a", "rows");
+    require_div(ac, q, "tesseract-a", "cols");
+    require_div(br, bsch == TESS_SCHEME_A ? (int64_t)q * d : q,
+                bsch == TESS_SCHEME_A ? "tesseract-a" : "tesseract-b", "rows");
+    require_div(bc, q, bsch == TESS_SCHEME_A ? "tesseract-a" : "tesseract-b", "cols");
+    Runner R(q, d, allow != 0, devices);
+    DevMat dA, dB;
+    upload(dA, R.unique_devices(), a, (size_t)ar * ac, t);
+    upload(dB, R.unique_devices(), b, (size_t)br * bc, t);
+    const int p = g.size();
+    std::vector<std::vector<float>> blocks(p);
+    R.run([&](Ctx& x, cudaStream_t s) {
+      void* la = take_block(x, TESS_SCHEME_A, t, dA.on(x.device), ar, ac, "g.a", s);
+      void* lb = take_block(x, bsch, t, dB.on(x.device), br, bc, "g.b", s);
+      const int64_t lar = ar / ((int64_t)q * d), lac = ac / q;
+      const int64_t lbr = bsch == TESS_SCHEME_A ? br / ((int64_t)q * d) : br / q, lbc = bc / q;
+      const int64_t lcr = csch == TESS_SCHEME_A ? cr / ((int64_t)q * d) : cr / q, lcc = cc / q;
+      float* lc = static_cast<float*>(x.ws->get("g.c", (size_t)lcr * lcc * 4));
+      const tess_dtype td = t == DType::F32 ? TESS_F32 : TESS_BF16;
+      call(tess_matmul(&x, v, td, la, lar, lac, lb, lbr, lbc, lc, TESS_F32,
+                       v == TESS_TN ? TESS_SUM_OVER_DEPTH : 0u, s));
+      blocks[x.rank] = fetch(lc, (size_t)lcr * lcc, DType::F32, s);
+    });
+    combine(g, csch, blocks, cr, cc, c);
+    R.stats(sr, sk);
+  });
+}
+
+tess_status tess_tesseract_backward(int q, int d, int allow, tess_dtype compute, const double* dc,
+                                    const double* a, const double* b, int64_t m, int64_t k,
+                                    int64_t n, double* da, double* db, const int* devices,
+                                    uint64_t* sr, uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    Grid g(q, d, allow != 0);
+    require_div(m, (int64_t)q * d, "tesseract-a", "rows");
+    require_div(k, q, "tesseract-a", "cols");
+    require_div(n, q, "tesseract-a", "cols");
+    Runner R(q, d, allow != 0, devices);
+    DevMat dDC, dA, dB;
+    upload(dDC, R.unique_devices(), dc, (size_t)m * n, t);
+    upload(dA, R.unique_devices(), a, (size_t)m * k, t);
+    upload(dB, R.unique_devices(), b, (size_t)k * n, t);
+    const int p = g.size();
+    std::vector<std::vector<float>> ga(p), gb(p);
+    const int64_t mr = m / ((int64_t)q * d), kc = k / q, nc = n / q;
+    R.run([&](Ctx& x, cudaStream_t s) {
+      void* ldc = take_block(x, TESS_SCHEME_A, t, dDC.on(x.device), m, n, "g.dc", s);
+      void* la = take_block(x, TESS_SCHEME_A, t, dA.on(x.device), m, k, "g.a", s);
+      void* lb = take_block(x, TESS_SCHEME_B, t, dB.on(x.device), k, n, "g.b", s);
+      float* lda = static_cast<float*>(x.ws->get("g.da", (size_t)mr * kc * 4));
+      float* ldb = static_cast<float*>(x.ws->get("g.db", (size_t)kc * nc * 4));
+      const tess_dtype td = t == DType::F32 ? TESS_F32 : TESS_BF16;
+      // ref algorithms.cpp:209-216: dA via NT, dB via TN + depth all-reduce
+      call(tess_matmul(&x, TESS_NT, td, ldc, mr, nc, lb, kc, nc, lda, TESS_F32, 0u, s));
+      call(tess_matmul(&x, TESS_TN, td, la, mr, kc, ldc, mr, nc, ldb, TESS_F32,
+                       TESS_SUM_OVER_DEPTH, s));
+      ga[x.rank] = fetch(lda, (size_t)mr * kc, DType::F32, s);
+      gb[x.rank] = fetch(ldb, (size_t)kc * nc, DType::F32, s);
+    });
+    combine(g, TESS_SCHEME_A, ga, m, k, da);
+    combine(g, TESS_SCHEME_B, gb, k, n, db);
+    R.stats(sr, sk);
+  });
+}
+
+tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q, int d, int allow,
+                           tess_dtype compute, const double* x, const double* dy,
+                           const double* const* params, double eps, double* y, double* dx,
+                           double* const* grads, double* dbias, const int* devices,
+                           uint64_t* sr, uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    if (!dims || !x || !dy || !params || !y || !dx) fail(TESS_ERR_INVALID, "null argument");
+    Grid g(q, d, allow != 0);
+    const tess_layer_dims D = *dims;
+    // divisibility as shard_activation (ref layers.cpp:115-136)
+    Runner R(q, d, allow != 0, devices);
+    tess::RankDims rd0 = rank_dims(*R.ctx[0], D);
+    const int64_t h = D.hidden, T = (int64_t)D.batch * D.seq;
+    const int64_t wshape[4][2] = {{h, 3 * h}, {h, h}, {h, 4 * h}, {4 * h, h}};
+    DevMat dx_, ddy;
+    upload(dx_, R.unique_devices(), x, (size_t)T * h, t);
+    upload(ddy, R.unique_devices(), dy, (size_t)T * h, t);
+    DevMat W[4], LN[4];
+    for (int i = 0; i < 4; ++i)
+      upload(W[i], R.unique_devices(), params[i], (size_t)(wshape[i][0] * wshape[i][1]), t);
+    for (int i = 0; i < 4; ++i) upload(LN[i], R.unique_devices(), params[4 + i], (size_t)h, DType::F32);
+    const int p = g.size();
+    const int64_t hq = rd0.hq, rows = rd0.rows;
+    std::vector<std::vector<float>> ys(p), dxs(p), dbs(p);
+    std::vector<std::vector<float>> gw[8];
+    for (auto& v : gw) v.resize(p);
+    R.run([&](Ctx& c, cudaStream_t s) {
+      tess::RankDims rd = rank_dims(c, D);
+      void* lx = take_block(c, TESS_SCHEME_A, t, dx_.on(c.device), T, h, "g.x", s);
+      void* ldy = take_block(c, TESS_SCHEME_A, t, ddy.on(c.device), T, h, "g.dy", s);
+      tess_block_shard sh;
+      const void* wl[4];
+      for (int i = 0; i < 4; ++i)
+        wl[i] = take_block(c, TESS_SCHEME_B, t, W[i].on(c.device), wshape[i][0], wshape[i][1],
+                           "g.w" + std::to_string(i), s);
+      sh.w_qkv = wl[0];
+      sh.w_proj = wl[1];
+      sh.w_ff1 = wl[2];
+      sh.w_ff2 = wl[3];
+      const float* lnv[4];
+      for (int i = 0; i < 4; ++i)
+        lnv[i] = static_cast<const float*>(LN[i].on(c.device)) + (int64_t)c.coord.j * hq;
+      sh.ln1_gain = lnv[0];
+      sh.ln1_bias = lnv[1];
+      sh.ln2_gain = lnv[2];
+      sh.ln2_bias = lnv[3];
+      sh.eps = eps;
+      const int64_t gsz[8] = {hq * 3 * hq, hq * hq, hq * 4 * hq, 4 * hq * hq, hq, hq, hq, hq};
+      float* gp[8];
+      for (int i = 0; i < 8; ++i) {
+        gp[i] = static_cast<float*>(c.ws->get("g.grad" + std::to_string(i), (size_t)gsz[i] * 4));
+        TESS_CUDA(cudaMemsetAsync(gp[i], 0, (size_t)gsz[i] * 4, s));
+      }
+      tess_block_grads gr{gp[0], gp[1], gp[2], gp[3], gp[4], gp[5], gp[6], gp[7]};
+      void* ly = c.ws->get("g.y", (size_t)rows * hq * dtype_size(t));
+      void* ldx = c.ws->get("g.dxo", (size_t)rows * hq * dtype_size(t));
+      float* ldb = static_cast<float*>(c.ws->get("g.dbias", (size_t)hq * 4));
+      TESS_CUDA(cudaMemsetAsync(ldb, 0, hq * 4, s));
+      const tess_dtype td = t == DType::F32 ? TESS_F32 : TESS_BF16;
+      // ref layers.cpp:631-683; BiasAdd uses ln1_bias owned by the i == 0 row
+      const void* brow = c.coord.i == 0 ? lnv[1] : nullptr;
+      call(tess_layer_forward(&c, op, td, &D, &sh, brow, lx, ly, s));
+      call(tess_layer_backward(&c, op, td, &D, &sh, ldy, ldx, &gr, 1, ldb, s));
+      ys[c.rank] = fetch(ly, (size_t)rows * hq, t, s);
+      dxs[c.rank] = fetch(ldx, (size_t)rows * hq, t, s);
+      dbs[c.rank] = fetch(ldb, (size_t)hq, DType::F32, s);
+      for (int i = 0; i < 8; ++i) gw[i][c.rank] = fetch(gp[i], (size_t)gsz[i], DType::F32, s);
+    });
+    combine(g, TESS_SCHEME_A, ys, T, h, y);
+    combine(g, TESS_SCHEME_A, dxs, T, h, dx);
+    if (grads) {
+      for (int i = 0; i < 4; ++i)
+        if (grads[i]) combine(g, TESS_SCHEME_B, gw[i], wshape[i][0], wshape[i][1], grads[i]);
+      // LayerNorm vectors: j-slices, replicas over (i, k) must agree
+      // (ref layers.cpp:197-213).
+      for (int i = 4; i < 8; ++i) {
+        if (!grads[i]) continue;
+        for (int j = 0; j < q; ++j) {
+          const auto& ref = gw[i][g.rank_of({0, j, 0})];
+          for (int ii = 0; ii < q; ++ii)
+            for (int k = 0; k < d; ++k)
+              if (std::memcmp(ref.data(), gw[i][g.rank_of({ii, j, k})].data(), hq * 4) != 0)
+                fail(TESS_ERR_SHAPE, "combine_block_grads: layernorm replica divergence");
+          for (int64_t cc = 0; cc < hq; ++cc) grads[i][j * hq + cc] = ref[cc];
+        }
+      }
+    }
+    if (dbias && op == TESS_OP_BIAS_ADD)
+      for (int j = 0; j < q; ++j)
+        for (int64_t cc = 0; cc < hq; ++cc) dbias[j * hq + cc] = dbs[g.rank_of({0, j, 0})][cc];
+    R.stats(sr, sk);
+  });
+}
+
+}  // extern "C"

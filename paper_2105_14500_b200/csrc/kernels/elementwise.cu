@@ -1,0 +1,548 @@
+// Memory-bound kernels: conversions, residual/bias adds, GeLU backward,
+// LayerNorm (row-distributed statistics), softmax and its backward,
+// deterministic column sums, and the slot-ordered sum used by the in-process
+// communicator. Each replaces a CPU loop of the reference (file:line at the
+// declaration in kernels.h).
+#include <cuda_bf16.h>
+
+#include "../core.h"
+#include "kernels.h"
+
+namespace tess {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+int grid_for(size_t n, int per_thread = 1) {
+  size_t blocks = (n + (size_t)kBlock * per_thread - 1) / ((size_t)kBlock * per_thread);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p, size_t i);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p, size_t i) {
+  return p[i];
+}
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p, size_t i) {
+  return __bfloat162float(p[i]);
+}
+template <>
+__device__ __forceinline__ float ldf<double>(const double* p, size_t i) {
+  return static_cast<float>(p[i]);
+}
+
+template <typename T>
+__device__ __forceinline__ void stf(T* p, size_t i, float v);
+template <>
+__device__ __forceinline__ void stf<float>(float* p, size_t i, float v) {
+  p[i] = v;
+}
+template <>
+__device__ __forceinline__ void stf<__nv_bfloat16>(__nv_bfloat16* p, size_t i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
+template <>
+__device__ __forceinline__ void stf<double>(double* p, size_t i, float v) {
+  p[i] = v;
+}
+
+// Dispatch a functor templated on element type.
+#define TESS_DISPATCH(dt, T, ...)                     \
+  switch (dt) {                                       \
+    case DType::F32: {                                \
+      using T = float;                                \
+      __VA_ARGS__;                                    \
+      break;                                          \
+    }                                                 \
+    case DType::BF16: {                               \
+      using T = __nv_bfloat16;                        \
+      __VA_ARGS__;                                    \
+      break;                                          \
+    }                                                 \
+    default:                                          \
+      fail(TESS_ERR_INVALID, "unsupported dtype");    \
+  }
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) t += red[w];  // fixed order: deterministic
+  return t;
+}
+
+// ------------------------------------------------------------- convert
+template <typename S, typename D>
+__device__ __forceinline__ D cvt(S v);
+template <> __device__ __forceinline__ float cvt<double, float>(double v) { return (float)v; }
+template <> __device__ __forceinline__ __nv_bfloat16 cvt<double, __nv_bfloat16>(double v) {
+  return __double2bfloat16(v);
+}
+template <> __device__ __forceinline__ double cvt<float, double>(float v) { return v; }
+template <> __device__ __forceinline__ double cvt<__nv_bfloat16, double>(__nv_bfloat16 v) {
+  return (double)__bfloat162float(v);
+}
+template <> __device__ __forceinline__ __nv_bfloat16 cvt<float, __nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <> __device__ __forceinline__ float cvt<__nv_bfloat16, float>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <> __device__ __forceinline__ float cvt<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ double cvt<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16, __nv_bfloat16>(__nv_bfloat16 v) {
+  return v;
+}
+
+template <typename S, typename D>
+__global__ void convert_kernel(const S* __restrict__ src, D* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = cvt<S, D>(src[i]);
+}
+
+template <typename S>
+void convert_from(const S* src, void* dst, DType dt, size_t n, cudaStream_t s) {
+  const int g = grid_for(n);
+  switch (dt) {
+    case DType::F32:
+      convert_kernel<S, float><<<g, kBlock, 0, s>>>(src, (float*)dst, n);
+      break;
+    case DType::BF16:
+      convert_kernel<S, __nv_bfloat16><<<g, kBlock, 0, s>>>(src, (__nv_bfloat16*)dst, n);
+      break;
+    case DType::F64:
+      convert_kernel<S, double><<<g, kBlock, 0, s>>>(src, (double*)dst, n);
+      break;
+  }
+}
+
+// ----------------------------------------------------------------- add
+template <typename TA, typename TB, typename TO>
+__global__ void add_kernel(const TA* a, const TB* b, TO* out, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    stf<TO>(out, i, ldf<TA>(a, i) + ldf<TB>(b, i));
+}
+
+template <typename T>
+__global__ void bias_add_kernel(const T* x, const float* bias, T* out, int64_t rows,
+                                int64_t cols) {
+  const size_t n = (size_t)rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    stf<T>(out, i, ldf<T>(x, i) + bias[i % cols]);
+}
+
+template <typename T>
+__global__ void gelu_bwd_kernel(const float* __restrict__ dh, const T* __restrict__ z,
+                                T* __restrict__ dz, size_t n) {
+  const float kInvSqrt2 = 0.70710678118654752f, kInvSqrt2Pi = 0.39894228040143268f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float v = ldf<T>(z, i);
+    const float g = 0.5f * (1.0f + erff(v * kInvSqrt2)) + v * kInvSqrt2Pi * __expf(-0.5f * v * v);
+    stf<T>(dz, i, dh[i] * g);
+  }
+}
+
+// Column partial sums over row chunks: scratch[chunk][c] (+ optional second
+// quantity for LayerNorm parameter gradients).
+constexpr int kRowChunk = 64;
+
+template <typename T>
+__global__ void colsum_partial_kernel(const T* x, int64_t rows, int64_t cols, float* part) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * kRowChunk;
+  if (c >= cols) return;
+  float acc = 0.f;
+  const int64_t r1 = min(rows, r0 + kRowChunk);
+  for (int64_t r = r0; r < r1; ++r) acc += ldf<T>(x, r * cols + c);
+  part[(int64_t)blockIdx.y * cols + c] = acc;
+}
+
+__global__ void colsum_finalize_kernel(const float* part, int64_t nchunk, int64_t cols,
+                                       int64_t nq, float* out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= cols * nq) return;
+  const int64_t qi = c / cols, cc = c % cols;
+  float acc = 0.f;
+  for (int64_t k = 0; k < nchunk; ++k) acc += part[(k * nq + qi) * cols + cc];
+  out[c] = acc;
+}
+
+// ------------------------------------------------------------ LayerNorm
+template <typename T>
+__global__ void ln_stats_kernel(const T* __restrict__ x, int64_t w, float* __restrict__ stats) {
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const T* row = x + r * w;
+  float s = 0.f;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) s += ldf<T>(row, c);
+  s = block_sum(s, red);
+  const float mu = s / (float)w;
+  float m2 = 0.f;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    const float dv = ldf<T>(row, c) - mu;
+    m2 += dv * dv;
+  }
+  m2 = block_sum(m2, red);
+  if (threadIdx.x == 0) {
+    stats[3 * r + 0] = s;
+    stats[3 * r + 1] = m2;
+    stats[3 * r + 2] = (float)w * mu * mu;
+  }
+}
+
+template <typename T>
+__global__ void ln_apply_kernel(const T* __restrict__ x, const float* __restrict__ stats,
+                                int64_t w, float n, const float* __restrict__ gain,
+                                const float* __restrict__ bias, float eps, T* __restrict__ y,
+                                float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  const int64_t r = blockIdx.x;
+  const float s0 = stats[3 * r], s1 = stats[3 * r + 1], s2 = stats[3 * r + 2];
+  const float mean = s0 / n;
+  float var = (s1 + (s2 - n * mean * mean)) / n;
+  if (var < 0.f) var = 0.f;
+  const float rstd = 1.0f / sqrtf(var + eps);
+  const T* row = x + r * w;
+  T* yrow = y + r * w;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x)
+    stf<T>(yrow, c, gain[c] * ((ldf<T>(row, c) - mean) * rstd) + bias[c]);
+  if (threadIdx.x == 0) {
+    mean_out[r] = mean;
+    rstd_out[r] = rstd;
+  }
+}
+
+template <typename TD, typename TX>
+__global__ void ln_bwd_stats_kernel(const TD* __restrict__ dy, const TX* __restrict__ x,
+                                    const float* __restrict__ mean, const float* __restrict__ rstd,
+                                    const float* __restrict__ gain, int64_t w,
+                                    float* __restrict__ stats) {
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  const float mu = mean[r], rs = rstd[r];
+  float a = 0.f, b = 0.f;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    const float dxh = ldf<TD>(dy, r * w + c) * gain[c];
+    const float xh = (ldf<TX>(x, r * w + c) - mu) * rs;
+    a += dxh;
+    b += xh * dxh;
+  }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    stats[2 * r] = a;
+    stats[2 * r + 1] = b;
+  }
+}
+
+template <typename TD, typename TX, typename TR, typename TO>
+__global__ void ln_bwd_apply_kernel(const TD* __restrict__ dy, const TX* __restrict__ x,
+                                    const float* __restrict__ mean, const float* __restrict__ rstd,
+                                    const float* __restrict__ gain, const float* __restrict__ stats,
+                                    int64_t w, float n, const TR* __restrict__ resid,
+                                    TO* __restrict__ dx) {
+  const int64_t r = blockIdx.x;
+  const float mu = mean[r], rs = rstd[r];
+  const float md = stats[2 * r] / n, mxd = stats[2 * r + 1] / n;
+  for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+    const size_t i = r * w + c;
+    const float dxh = ldf<TD>(dy, i) * gain[c];
+    const float xh = (ldf<TX>(x, i) - mu) * rs;
+    float v = rs * (dxh - md - xh * mxd);
+    if (resid) v += ldf<TR>(resid, i);
+    stf<TO>(dx, i, v);
+  }
+}
+
+template <typename TD, typename TX>
+__global__ void ln_params_partial_kernel(const TD* dy, const TX* x, const float* mean,
+                                         const float* rstd, int64_t rows, int64_t w,
+                                         float* part) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * kRowChunk;
+  if (c >= w) return;
+  float dg = 0.f, db = 0.f;
+  const int64_t r1 = min(rows, r0 + kRowChunk);
+  for (int64_t r = r0; r < r1; ++r) {
+    const float d = ldf<TD>(dy, r * w + c);
+    dg += d * (ldf<TX>(x, r * w + c) - mean[r]) * rstd[r];
+    db += d;
+  }
+  part[((int64_t)blockIdx.y * 2 + 0) * w + c] = dg;
+  part[((int64_t)blockIdx.y * 2 + 1) * w + c] = db;
+}
+
+// ------------------------------------------------------------- softmax
+// One warp per row; rows cached in registers when L % 4 == 0 and L <= 128*NV.
+template <typename T, int NV>
+__global__ void softmax_fwd_reg_kernel(const float* __restrict__ S, T* __restrict__ P,
+                                       int64_t rows, int64_t L) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float4* srow = reinterpret_cast<const float4*>(S + r * L);
+  const int nv = static_cast<int>(L / 4);
+  float4 v[NV];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int idx = lane + k * 32;
+    if (idx < nv) {
+      v[k] = srow[idx];
+      mx = fmaxf(mx, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int idx = lane + k * 32;
+    if (idx < nv) {
+      v[k].x = __expf(v[k].x - mx);
+      v[k].y = __expf(v[k].y - mx);
+      v[k].z = __expf(v[k].z - mx);
+      v[k].w = __expf(v[k].w - mx);
+      sum += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = 1.0f / sum;
+  T* prow = P + r * L;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int idx = lane + k * 32;
+    if (idx < nv) {
+      stf<T>(prow, 4 * idx + 0, v[k].x * inv);
+      stf<T>(prow, 4 * idx + 1, v[k].y * inv);
+      stf<T>(prow, 4 * idx + 2, v[k].z * inv);
+      stf<T>(prow, 4 * idx + 3, v[k].w * inv);
+    }
+  }
+}
+
+template <typename T>
+__global__ void softmax_fwd_generic_kernel(const float* __restrict__ S, T* __restrict__ P,
+                                           int64_t rows, int64_t L) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* srow = S + r * L;
+  float mx = -INFINITY;
+  for (int64_t c = lane; c < L; c += 32) mx = fmaxf(mx, srow[c]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+  for (int64_t c = lane; c < L; c += 32) sum += __expf(srow[c] - mx);
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float inv = 1.0f / sum;
+  for (int64_t c = lane; c < L; c += 32) stf<T>(P + r * L, c, __expf(srow[c] - mx) * inv);
+}
+
+template <typename T>
+__global__ void softmax_bwd_kernel(const T* __restrict__ P, const float* __restrict__ dP,
+                                   T* __restrict__ dS, int64_t rows, int64_t L, float scale) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const T* prow = P + r * L;
+  const float* drow = dP + r * L;
+  float dot = 0.f;
+  for (int64_t c = lane; c < L; c += 32) dot += ldf<T>(prow, c) * drow[c];
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  for (int64_t c = lane; c < L; c += 32) {
+    const float p = ldf<T>(prow, c);
+    stf<T>(dS + r * L, c, scale * p * (drow[c] - dot));
+  }
+}
+
+// ------------------------------------------------------- comm helper
+struct SumArgs {
+  const float* in[8];
+};
+
+__global__ void sum_kernel(SumArgs a, int n_in, float* out, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float acc = a.in[0][i];
+    for (int k = 1; k < n_in; ++k) acc += a.in[k][i];  // slot-ascending
+    out[i] = acc;
+  }
+}
+
+}  // namespace
+
+std::atomic<uint64_t> g_launches{0};
+
+void launch_sum_f32(const float* const* in, int n_in, float* out, size_t n, cudaStream_t s) {
+  SumArgs a;
+  for (int k = 0; k < n_in && k < 8; ++k) a.in[k] = in[k];
+  sum_kernel<<<grid_for(n), kBlock, 0, s>>>(a, n_in, out, n);
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_convert(const void* src, DType st, void* dst, DType dt, size_t n, cudaStream_t s) {
+  if (!n) return;
+  switch (st) {
+    case DType::F32: convert_from((const float*)src, dst, dt, n, s); break;
+    case DType::BF16: convert_from((const __nv_bfloat16*)src, dst, dt, n, s); break;
+    case DType::F64: convert_from((const double*)src, dst, dt, n, s); break;
+  }
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_add(const void* a, DType ta, const void* b, DType tb, void* out, DType to, size_t n,
+           cudaStream_t s) {
+  if (!n) return;
+  const int g = grid_for(n);
+  TESS_DISPATCH(ta, TA, TESS_DISPATCH(tb, TB, TESS_DISPATCH(to, TO,
+      add_kernel<TA, TB, TO><<<g, kBlock, 0, s>>>((const TA*)a, (const TB*)b, (TO*)out, n))));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_bias_add(const void* x, const float* bias, void* out, DType t, int64_t rows,
+                int64_t cols, cudaStream_t s) {
+  const size_t n = (size_t)rows * cols;
+  if (!n) return;
+  TESS_DISPATCH(t, T, bias_add_kernel<T><<<grid_for(n), kBlock, 0, s>>>((const T*)x, bias,
+                                                                          (T*)out, rows, cols));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_gelu_bwd(const float* dh, const void* z, void* dz, DType t, size_t n, cudaStream_t s) {
+  if (!n) return;
+  TESS_DISPATCH(t, T, gelu_bwd_kernel<T><<<grid_for(n), kBlock, 0, s>>>(dh, (const T*)z,
+                                                                          (T*)dz, n));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+size_t k_colsum_scratch_floats(int64_t rows, int64_t cols) {
+  return (size_t)((rows + kRowChunk - 1) / kRowChunk) * cols;
+}
+
+void k_colsum(const void* x, DType t, int64_t rows, int64_t cols, float* out, float* scratch,
+              cudaStream_t s) {
+  if (cols <= 0) return;
+  const int64_t nchunk = (rows + kRowChunk - 1) / kRowChunk;
+  if (nchunk == 0) {
+    TESS_CUDA(cudaMemsetAsync(out, 0, cols * 4, s));
+    return;
+  }
+  dim3 g((unsigned)((cols + kBlock - 1) / kBlock), (unsigned)nchunk);
+  TESS_DISPATCH(t, T, colsum_partial_kernel<T><<<g, kBlock, 0, s>>>((const T*)x, rows, cols,
+                                                                      scratch));
+  colsum_finalize_kernel<<<(unsigned)((cols + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      scratch, nchunk, cols, 1, out);
+  count_launch(2);
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_ln_stats(const void* x, DType t, int64_t rows, int64_t w, float* stats, cudaStream_t s) {
+  if (!rows) return;
+  TESS_DISPATCH(t, T, ln_stats_kernel<T><<<(unsigned)rows, kBlock, 0, s>>>((const T*)x, w, stats));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_ln_apply(const void* x, DType t, const float* stats, int64_t rows, int64_t w,
+                double hidden_total, const float* gain, const float* bias, double eps, void* y,
+                float* mean, float* rstd, cudaStream_t s) {
+  if (!rows) return;
+  TESS_DISPATCH(t, T, ln_apply_kernel<T><<<(unsigned)rows, kBlock, 0, s>>>(
+                          (const T*)x, stats, w, (float)hidden_total, gain, bias, (float)eps,
+                          (T*)y, mean, rstd));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_ln_bwd_stats(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                    const float* rstd, const float* gain, int64_t rows, int64_t w, float* stats,
+                    cudaStream_t s) {
+  if (!rows) return;
+  TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX,
+      ln_bwd_stats_kernel<TD, TX><<<(unsigned)rows, kBlock, 0, s>>>(
+          (const TD*)dy, (const TX*)x, mean, rstd, gain, w, stats)));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_ln_bwd_apply(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                    const float* rstd, const float* gain, const float* stats, int64_t rows,
+                    int64_t w, double hidden_total, const void* resid, DType tr, void* dx,
+                    DType to, cudaStream_t s) {
+  if (!rows) return;
+  TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR, TESS_DISPATCH(to, TO,
+      ln_bwd_apply_kernel<TD, TX, TR, TO><<<(unsigned)rows, kBlock, 0, s>>>(
+          (const TD*)dy, (const TX*)x, mean, rstd, gain, stats, w, (float)hidden_total,
+          (const TR*)resid, (TO*)dx)))));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+size_t k_ln_params_scratch_floats(int64_t rows, int64_t w) {
+  return (size_t)((rows + kRowChunk - 1) / kRowChunk) * 2 * w;
+}
+
+void k_ln_bwd_params(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                     const float* rstd, int64_t rows, int64_t w, float* out2w, float* scratch,
+                     cudaStream_t s) {
+  const int64_t nchunk = (rows + kRowChunk - 1) / kRowChunk;
+  if (nchunk == 0) {
+    TESS_CUDA(cudaMemsetAsync(out2w, 0, 2 * w * 4, s));
+    return;
+  }
+  dim3 g((unsigned)((w + kBlock - 1) / kBlock), (unsigned)nchunk);
+  TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX,
+      ln_params_partial_kernel<TD, TX><<<g, kBlock, 0, s>>>((const TD*)dy, (const TX*)x, mean,
+                                                            rstd, rows, w, scratch)));
+  colsum_finalize_kernel<<<(unsigned)((2 * w + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      scratch, nchunk, w, 2, out2w);
+  count_launch(2);
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cudaStream_t s) {
+  if (!rows) return;
+  const int warps = 8;
+  const unsigned g = (unsigned)((rows + warps - 1) / warps);
+  if (L % 4 == 0 && L <= 128 * 16) {
+    TESS_DISPATCH(t, T, softmax_fwd_reg_kernel<T, 16><<<g, 32 * warps, 0, s>>>(S, (T*)P, rows, L));
+  } else if (L % 4 == 0 && L <= 128 * 32) {
+    TESS_DISPATCH(t, T, softmax_fwd_reg_kernel<T, 32><<<g, 32 * warps, 0, s>>>(S, (T*)P, rows, L));
+  } else {
+    TESS_DISPATCH(t, T, softmax_fwd_generic_kernel<T><<<g, 32 * warps, 0, s>>>(S, (T*)P, rows, L));
+  }
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t rows, int64_t L,
+                   float scale, cudaStream_t s) {
+  if (!rows) return;
+  const int warps = 8;
+  const unsigned g = (unsigned)((rows + warps - 1) / warps);
+  TESS_DISPATCH(t, T, softmax_bwd_kernel<T><<<g, 32 * warps, 0, s>>>((const T*)P, dP, (T*)dS,
+                                                                       rows, L, scale));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+}  // namespace tess

@@ -33,7 +33,7 @@ enum class Epi : int {
   Gelu = 3,    // Z = v; C = gelu(v) with the exact erf GeLU
 };
 
-constexpr int kMaxSegments = 4;
+constexpr int kMaxSegments = 8;
 
 struct GemmSeg {
   const void* a = nullptr;  // A panel for this K range

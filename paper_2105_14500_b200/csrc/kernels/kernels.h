@@ -1,0 +1,63 @@
+// Memory-bound kernels of the Tesseract layers (HBM-bound; see DESIGN.md for
+// the algorithmic bytes each one moves). All launchers are stream-ordered.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "gemm.h"
+
+namespace tess {
+
+// ---- conversion / arithmetic --------------------------------------------
+// dst = (dst_type) src, elementwise (f64 <-> f32 <-> bf16).
+void k_convert(const void* src, DType st, void* dst, DType dt, size_t n, cudaStream_t s);
+// out[i] = a[i] + b[i]; a/out of type t, b of type tb.
+void k_add(const void* a, DType ta, const void* b, DType tb, void* out, DType to, size_t n,
+           cudaStream_t s);
+// out[r, c] = x[r, c] + bias[c] (bias fp32 [cols]); ref layers.cpp:491-503.
+void k_bias_add(const void* x, const float* bias, void* out, DType t, int64_t rows,
+                int64_t cols, cudaStream_t s);
+// dz = dh * gelu'(z) (exact erf derivative, ref layers.cpp:34-42, 365).
+void k_gelu_bwd(const float* dh, const void* z, void* dz, DType t, size_t n, cudaStream_t s);
+// Column sums of x [rows, cols] (type t) into out fp32 [cols]; deterministic
+// fixed-order two-stage reduction (ref layers.cpp:507-510 colsum).
+void k_colsum(const void* x, DType t, int64_t rows, int64_t cols, float* out, float* scratch,
+              cudaStream_t s);
+size_t k_colsum_scratch_floats(int64_t rows, int64_t cols);
+
+// ---- LayerNorm (ref layers.cpp:242-345) -----------------------------------
+// Local partial statistics per row for the row-group all-reduce:
+// stats[r] = {sum x, sum (x - mu_r)^2, w * mu_r^2} with mu_r the local mean.
+void k_ln_stats(const void* x, DType t, int64_t rows, int64_t w, float* stats, cudaStream_t s);
+// Normalise with the (all-reduced) statistics over hidden_total columns:
+// y = gain * (x - mean) * rstd + bias; writes mean/rstd per row (cache).
+void k_ln_apply(const void* x, DType t, const float* stats, int64_t rows, int64_t w,
+                double hidden_total, const float* gain, const float* bias, double eps,
+                void* y, float* mean, float* rstd, cudaStream_t s);
+// Backward partial row sums: stats[r] = {sum dxhat, sum xhat*dxhat},
+// dxhat = dy * gain, xhat = (x - mean) * rstd.
+void k_ln_bwd_stats(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                    const float* rstd, const float* gain, int64_t rows, int64_t w,
+                    float* stats, cudaStream_t s);
+// dx = rstd * (dxhat - s0/n - xhat * s1/n) (+ resid); out of type to.
+void k_ln_bwd_apply(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                    const float* rstd, const float* gain, const float* stats, int64_t rows,
+                    int64_t w, double hidden_total, const void* resid, DType tr, void* dx,
+                    DType to, cudaStream_t s);
+// Column partials for dgain/dbias: out[0][c] = sum_r dy*xhat, out[1][c] = sum_r dy.
+void k_ln_bwd_params(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                     const float* rstd, int64_t rows, int64_t w, float* out2w, float* scratch,
+                     cudaStream_t s);
+size_t k_ln_params_scratch_floats(int64_t rows, int64_t w);
+
+// ---- softmax (ref layers.cpp:44-74) ---------------------------------------
+// P = softmax_rows(S) with max subtraction; S fp32 [rows, L] (already scaled).
+void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cudaStream_t s);
+// dS = scale * P * (dP - sum_c P*dP); dP fp32.
+void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t rows, int64_t L,
+                   float scale, cudaStream_t s);
+
+}  // namespace tess

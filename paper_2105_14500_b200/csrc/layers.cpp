@@ -1,0 +1,423 @@
+// Rank-level Transformer layers on the Tesseract grid (reference
+// proj/src/layers.cpp:242-517), B200 version:
+//  * LayerNorm: per-row partial statistics (sum, centred M2, w*mu^2 -- a
+//    Chan-style combination that avoids E[x^2]-E[x]^2 cancellation in fp32)
+//    all-reduced over the row group, then normalise; the meter charges the
+//    reference's [rows, 2] payload (layers.cpp:258).
+//  * FF: FF1 GEMM with the exact-erf GeLU fused into its epilogue (stores the
+//    pre-activation z and h = gelu(z)); FF2 GEMM with the residual add fused.
+//  * Attention: batched tcgen05 GEMMs per local sample over the local heads
+//    (per-head interleaved Q|K|V columns addressed by TMA strides, no copies),
+//    row softmax, P kept for the backward like the reference (layers.cpp:403).
+//    No causal mask (reference semantics).
+//  * Residual adds are fused into GEMM epilogues (forward) or into the
+//    LayerNorm-backward apply kernel (backward).
+// Forward caches live in the context workspace under per-op names until the
+// matching backward.
+#include <cmath>
+#include <string>
+
+#include "kernels/kernels.h"
+#include "ops.h"
+
+namespace tess {
+
+RankDims rank_dims(const Ctx& c, const tess_layer_dims& d) {
+  // ref: layers.cpp:115-136 (divisibility), 230-238 (rank_dims)
+  const int q = c.grid.q, dd = c.grid.d;
+  auto req = [](bool ok, const std::string& what) {
+    if (!ok) fail(TESS_ERR_DIVISIBILITY, what);
+  };
+  req(d.batch % (dd * q) == 0, "batch (" + std::to_string(d.batch) + ") not divisible by d*q (" +
+                                   std::to_string(dd * q) + ")");
+  req(d.hidden % q == 0, "hidden (" + std::to_string(d.hidden) + ") not divisible by q (" +
+                             std::to_string(q) + ")");
+  req(d.heads > 0 && d.heads % q == 0, "heads (" + std::to_string(d.heads) +
+                                           ") not divisible by q (" + std::to_string(q) + ")");
+  req(d.hidden % d.heads == 0, "hidden (" + std::to_string(d.hidden) +
+                                   ") not divisible by heads (" + std::to_string(d.heads) + ")");
+  RankDims r;
+  r.seq = d.seq;
+  r.head_dim = d.hidden / d.heads;
+  r.heads_local = d.heads / q;
+  r.samples_local = d.batch / (dd * q);
+  r.hidden_total = d.hidden;
+  r.hq = d.hidden / q;
+  r.rows = r.samples_local * d.seq;
+  return r;
+}
+
+namespace {
+
+void* wsget(Ctx& c, const std::string& name, size_t bytes) { return c.ws->get(name, bytes); }
+
+Out out_to(void* p, DType t, int64_t ld = 0) {
+  Out o;
+  o.c = p;
+  o.t = t;
+  o.ldc = ld;
+  return o;
+}
+
+// ----------------------------------------------------------- LayerNorm
+struct LnCache {
+  const void* x;
+  float* mean;
+  float* rstd;
+};
+
+void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const void* x,
+            const float* gain, const float* bias, double eps, void* y, cudaStream_t s) {
+  const int64_t rows = rd.rows, w = rd.hq;
+  float* stats = static_cast<float*>(wsget(c, "ln.stats", rows * 3 * 4));
+  float* mean = static_cast<float*>(wsget(c, tag + ".mean", rows * 4));
+  float* rstd = static_cast<float*>(wsget(c, tag + ".rstd", rows * 4));
+  k_ln_stats(x, t, rows, w, stats, s);
+  // ref layers.cpp:258: row all-reduce of the [rows, 2] sums (metered as such)
+  c.meter.reduce(c.grid.group_size(ROW), c.grid.slot_in_group(c.coord, ROW), 0,
+                 (uint64_t)rows * 2, true);
+  if (c.trace_on) c.trace.push_back({c.rank, c.step, 2, ROW, 0, (uint64_t)rows * 2 * 8});
+  c.step++;
+  c.comm->allreduce(ROW, stats, rows * 3, s);
+  k_ln_apply(x, t, stats, rows, w, (double)rd.hidden_total, gain, bias, eps, y, mean, rstd, s);
+}
+
+// dx = LN'(dy) (+ resid); optional gain/bias grads (column + depth all-reduce,
+// ref layers.cpp:318-343, only when requested).
+void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const void* dy,
+            DType tdy, const void* x, const float* gain, const void* resid, DType tr, void* dx,
+            DType tdx, float* dgain, float* dbias, bool accumulate, cudaStream_t s) {
+  const int64_t rows = rd.rows, w = rd.hq;
+  const float* mean = static_cast<const float*>(wsget(c, tag + ".mean", rows * 4));
+  const float* rstd = static_cast<const float*>(wsget(c, tag + ".rstd", rows * 4));
+  float* stats = static_cast<float*>(wsget(c, "ln.bstats", rows * 2 * 4));
+  k_ln_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, s);
+  coll_allreduce(c, ROW, stats, rows * 2, s);  // ref layers.cpp:305
+  k_ln_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w, (double)rd.hidden_total,
+                 resid, tr, dx, tdx, s);
+  if (dgain || dbias) {
+    float* packed = static_cast<float*>(wsget(c, "ln.packed", 2 * w * 4));
+    float* scratch =
+        static_cast<float*>(wsget(c, "ln.pscratch", k_ln_params_scratch_floats(rows, w) * 4));
+    k_ln_bwd_params(dy, tdy, x, t, mean, rstd, rows, w, packed, scratch, s);
+    coll_allreduce(c, COL, packed, 2 * w, s);    // ref layers.cpp:331
+    coll_allreduce(c, DEPTH, packed, 2 * w, s);  // ref layers.cpp:332
+    for (int k = 0; k < 2; ++k) {
+      float* dst = k == 0 ? dgain : dbias;
+      if (!dst) continue;
+      if (accumulate)
+        k_add(dst, DType::F32, packed + k * w, DType::F32, dst, DType::F32, w, s);
+      else
+        TESS_CUDA(cudaMemcpyAsync(dst, packed + k * w, w * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+}
+
+Out grad_out(float* g, bool accumulate) {
+  Out o = out_to(g, DType::F32);
+  o.epi = accumulate ? Epi::Accum : Epi::Store;
+  return o;
+}
+
+// TN weight-gradient product; with no grads requested the collectives still
+// run into scratch (ref layers.cpp:372-377).
+void weight_grad(Ctx& c, DType t, const void* a, int64_t ar, int64_t an, const void* b,
+                 int64_t bn, float* g, bool accumulate, cudaStream_t s) {
+  float* dst = g ? g : static_cast<float*>(wsget(c, "wgrad.discard", (size_t)an * bn * 4));
+  tn_product(c, t, a, ar, an, b, bn, true, grad_out(dst, g && accumulate), s);
+}
+
+// ----------------------------------------------------------------- FF
+// ref layers.cpp:349-360. Cache: x (caller-owned), z, h.
+void ff_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
+            const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s) {
+  const int64_t rows = rd.rows, hq = rd.hq;
+  const size_t esz = dtype_size(t);
+  void* z = wsget(c, tag + ".z", rows * 4 * hq * esz);
+  void* h = wsget(c, tag + ".h", rows * 4 * hq * esz);
+  Out o1 = out_to(h, t);
+  o1.epi = Epi::Gelu;
+  o1.z = z;
+  nn_product(c, t, x, rows, hq, p.w_ff1, 4 * hq, o1, s);
+  nn_product(c, t, h, rows, 4 * hq, p.w_ff2, hq, yout, s);
+}
+
+// ref layers.cpp:362-379: NT, gelu', NT, TN, TN. dx written fp32.
+void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
+            const tess_block_shard& p, const void* x, const void* dy, float* dx_f32,
+            tess_block_grads* g, bool accumulate, cudaStream_t s) {
+  const int64_t rows = rd.rows, hq = rd.hq;
+  const size_t esz = dtype_size(t);
+  const void* z = wsget(c, tag + ".z", rows * 4 * hq * esz);
+  const void* h = wsget(c, tag + ".h", rows * 4 * hq * esz);
+  float* dh = static_cast<float*>(wsget(c, "ff.dh", rows * 4 * hq * 4));
+  void* dz = wsget(c, "ff.dz", rows * 4 * hq * esz);
+  nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s);
+  k_gelu_bwd(dh, z, dz, t, (size_t)rows * 4 * hq, s);  // ref layers.cpp:365
+  nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, hq, out_to(dx_f32, DType::F32), s);
+  weight_grad(c, t, h, rows, 4 * hq, dy, hq, g ? g->w_ff2 : nullptr, accumulate, s);
+  weight_grad(c, t, x, rows, hq, dz, 4 * hq, g ? g->w_ff1 : nullptr, accumulate, s);
+}
+
+// ----------------------------------------------------------- attention
+// ref layers.cpp:383-414.
+void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
+              const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s) {
+  const int64_t rows = rd.rows, hq = rd.hq, S = rd.seq, hd = rd.head_dim;
+  const int64_t H = rd.heads_local, ld = 3 * hq;
+  const size_t esz = dtype_size(t);
+  void* qkv = wsget(c, tag + ".qkv", rows * ld * esz);
+  void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
+  void* o = wsget(c, tag + ".o", rows * hq * esz);
+  float* Sbuf = static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
+  nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s);
+  const float scale = (float)(1.0 / std::sqrt((double)hd));
+  const char* base = static_cast<const char*>(qkv);
+  for (int64_t smp = 0; smp < rd.samples_local; ++smp) {
+    const char* q0 = base + (size_t)smp * S * ld * esz;
+    // scores = Q K^T / sqrt(hd) for every local head (batched over heads)
+    GemmDesc g;
+    g.M = S;
+    g.N = S;
+    g.nb0 = H;
+    g.in = t;
+    g.trans_b = true;
+    g.seg[0] = {q0, q0 + hd * esz, hd};
+    g.lda = ld;
+    g.as0 = 3 * hd;
+    g.ldb = ld;
+    g.bs0 = 3 * hd;
+    g.c = Sbuf;
+    g.c_type = DType::F32;
+    g.ldc = S;
+    g.cs0 = S * S;
+    g.alpha = scale;
+    TESS_CUDA(gemm(g, s));
+    count_launch();
+    char* Ps = static_cast<char*>(P) + (size_t)smp * H * S * S * esz;
+    k_softmax_fwd(Sbuf, Ps, t, H * S, S, s);
+    // O = P V
+    GemmDesc g2;
+    g2.M = S;
+    g2.N = hd;
+    g2.nb0 = H;
+    g2.in = t;
+    g2.seg[0] = {Ps, q0 + 2 * hd * esz, S};
+    g2.lda = S;
+    g2.as0 = S * S;
+    g2.ldb = ld;
+    g2.bs0 = 3 * hd;
+    g2.c = static_cast<char*>(o) + (size_t)smp * S * hq * esz;
+    g2.c_type = t;
+    g2.ldc = hq;
+    g2.cs0 = hd;
+    TESS_CUDA(gemm(g2, s));
+    count_launch();
+  }
+  nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s);
+}
+
+// ref layers.cpp:416-456: NT, TN, per-head local backward, NT, TN.
+void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
+              const tess_block_shard& p, const void* x, const void* dy, float* dx_f32,
+              tess_block_grads* g, bool accumulate, cudaStream_t s) {
+  const int64_t rows = rd.rows, hq = rd.hq, S = rd.seq, hd = rd.head_dim;
+  const int64_t H = rd.heads_local, ld = 3 * hq;
+  const size_t esz = dtype_size(t);
+  const void* qkv = wsget(c, tag + ".qkv", rows * ld * esz);
+  const void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
+  const void* o = wsget(c, tag + ".o", rows * hq * esz);
+  float* dout32 = static_cast<float*>(wsget(c, "attn.dout32", rows * hq * 4));
+  void* dout = t == DType::F32 ? dout32 : wsget(c, "attn.dout", rows * hq * esz);
+  void* dqkv = wsget(c, "attn.dqkv", rows * ld * esz);
+  float* dP = static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
+  void* dS = wsget(c, "attn.dS", (size_t)H * S * S * esz);
+  nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s);
+  if (t != DType::F32) k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
+  weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
+  const float scale = (float)(1.0 / std::sqrt((double)hd));
+  for (int64_t smp = 0; smp < rd.samples_local; ++smp) {
+    const char* q0 = static_cast<const char*>(qkv) + (size_t)smp * S * ld * esz;
+    const char* do0 = static_cast<const char*>(dout) + (size_t)smp * S * hq * esz;
+    char* dq0 = static_cast<char*>(dqkv) + (size_t)smp * S * ld * esz;
+    const char* Ps = static_cast<const char*>(P) + (size_t)smp * H * S * S * esz;
+    // dP = dO V^T
+    GemmDesc g1;
+    g1.M = S; g1.N = S; g1.nb0 = H; g1.in = t; g1.trans_b = true;
+    g1.seg[0] = {do0, q0 + 2 * hd * esz, hd};
+    g1.lda = hq; g1.as0 = hd; g1.ldb = ld; g1.bs0 = 3 * hd;
+    g1.c = dP; g1.c_type = DType::F32; g1.ldc = S; g1.cs0 = S * S;
+    TESS_CUDA(gemm(g1, s));
+    // dV = P^T dO
+    GemmDesc g2;
+    g2.M = S; g2.N = hd; g2.nb0 = H; g2.in = t; g2.trans_a = true;
+    g2.seg[0] = {Ps, do0, S};
+    g2.lda = S; g2.as0 = S * S; g2.ldb = hq; g2.bs0 = hd;
+    g2.c = dq0 + 2 * hd * esz; g2.c_type = t; g2.ldc = ld; g2.cs0 = 3 * hd;
+    TESS_CUDA(gemm(g2, s));
+    // dS = P * (dP - rowsum(P*dP)) / sqrt(hd)
+    k_softmax_bwd(Ps, dP, dS, t, H * S, S, scale, s);
+    // dQ = dS K
+    GemmDesc g3;
+    g3.M = S; g3.N = hd; g3.nb0 = H; g3.in = t;
+    g3.seg[0] = {dS, q0 + hd * esz, S};
+    g3.lda = S; g3.as0 = S * S; g3.ldb = ld; g3.bs0 = 3 * hd;
+    g3.c = dq0; g3.c_type = t; g3.ldc = ld; g3.cs0 = 3 * hd;
+    TESS_CUDA(gemm(g3, s));
+    // dK = dS^T Q
+    GemmDesc g4;
+    g4.M = S; g4.N = hd; g4.nb0 = H; g4.in = t; g4.trans_a = true;
+    g4.seg[0] = {dS, q0, S};
+    g4.lda = S; g4.as0 = S * S; g4.ldb = ld; g4.bs0 = 3 * hd;
+    g4.c = dq0 + hd * esz; g4.c_type = t; g4.ldc = ld; g4.cs0 = 3 * hd;
+    TESS_CUDA(gemm(g4, s));
+    count_launch(4);
+  }
+  nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s);
+  weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
+}
+
+// ------------------------------------------------------------- host staging
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
+                   const tess_block_shard& p, const float* bias_row0, const void* x_in,
+                   void* y_out, cudaStream_t s) {
+  const int64_t rows = rd.rows, hq = rd.hq;
+  const size_t act = (size_t)rows * hq * dtype_size(t);
+  const std::string tag = "op" + std::to_string((int)op);
+  // Host buffers are staged through the context (x kept until backward).
+  const void* x = x_in;
+  if (!is_device_ptr(x_in)) {
+    void* xs = wsget(c, tag + ".xstage", act);
+    TESS_CUDA(cudaMemcpyAsync(xs, x_in, act, cudaMemcpyHostToDevice, s));
+    x = xs;
+  }
+  void* y = is_device_ptr(y_out) ? y_out : wsget(c, "stage.y", act);
+  switch (op) {
+    case TESS_OP_LAYERNORM:
+      ln_fwd(c, t, rd, tag + ".ln", x, p.ln1_gain, p.ln1_bias, p.eps, y, s);
+      break;
+    case TESS_OP_FEEDFORWARD:
+      ff_fwd(c, t, rd, tag + ".ff", p, x, out_to(y, t), s);
+      break;
+    case TESS_OP_ATTENTION:
+      attn_fwd(c, t, rd, tag + ".attn", p, x, out_to(y, t), s);
+      break;
+    case TESS_OP_BIAS_ADD: {
+      // ref layers.cpp:491-503: bias lives at i == 0, column broadcast.
+      float* b = static_cast<float*>(wsget(c, "bias.row", hq * 4));
+      if (c.coord.i == 0) {
+        if (!bias_row0) fail(TESS_ERR_INVALID, "bias_add: bias_row0 required on i == 0 ranks");
+        TESS_CUDA(cudaMemcpyAsync(b, bias_row0, hq * 4, cudaMemcpyDefault, s));
+      }
+      coll_bcast(c, COL, 0, b, hq * 4, (uint64_t)hq, s);
+      k_bias_add(x, b, y, t, rows, hq, s);
+      break;
+    }
+    case TESS_OP_BLOCK: {
+      // ref layers.cpp:460-472 (pre-norm; residuals fused into epilogues)
+      void* ln1 = wsget(c, tag + ".ln1out", act);
+      void* r1 = wsget(c, tag + ".r1", act);
+      void* ln2 = wsget(c, tag + ".ln2out", act);
+      ln_fwd(c, t, rd, tag + ".ln1", x, p.ln1_gain, p.ln1_bias, p.eps, ln1, s);
+      Out ao = out_to(r1, t);
+      ao.epi = Epi::Resid;
+      ao.r = x;
+      attn_fwd(c, t, rd, tag + ".attn", p, ln1, ao, s);
+      ln_fwd(c, t, rd, tag + ".ln2", r1, p.ln2_gain, p.ln2_bias, p.eps, ln2, s);
+      Out fo = out_to(y, t);
+      fo.epi = Epi::Resid;
+      fo.r = r1;
+      ff_fwd(c, t, rd, tag + ".ff", p, ln2, fo, s);
+      break;
+    }
+    default:
+      fail(TESS_ERR_INVALID, "unknown layer op");
+  }
+  if (y != y_out) {
+    TESS_CUDA(cudaMemcpyAsync(y_out, y, act, cudaMemcpyDeviceToHost, s));
+  }
+  c.fwd_x[(int)op] = x;  // the backward needs the forward input
+}
+
+void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
+                    const tess_block_shard& p, const void* dy_in, void* dx_out,
+                    tess_block_grads* g, bool accumulate, float* dbias, cudaStream_t s) {
+  const int64_t rows = rd.rows, hq = rd.hq;
+  const size_t act = (size_t)rows * hq * dtype_size(t);
+  const std::string tag = "op" + std::to_string((int)op);
+  const void* x = c.fwd_x[(int)op];
+  if (!x) fail(TESS_ERR_SHAPE, "layer backward: missing forward cache");
+  const void* dy = dy_in;
+  if (!is_device_ptr(dy_in)) {
+    void* ds = wsget(c, "stage.dy", act);
+    TESS_CUDA(cudaMemcpyAsync(ds, dy_in, act, cudaMemcpyHostToDevice, s));
+    dy = ds;
+  }
+  void* dx = is_device_ptr(dx_out) ? dx_out : wsget(c, "stage.dx", act);
+  switch (op) {
+    case TESS_OP_LAYERNORM:
+      ln_bwd(c, t, rd, tag + ".ln", dy, t, x, p.ln1_gain, nullptr, t, dx, t,
+             g ? g->ln1_gain : nullptr, g ? g->ln1_bias : nullptr, accumulate, s);
+      break;
+    case TESS_OP_FEEDFORWARD: {
+      float* dxf = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
+      ff_bwd(c, t, rd, tag + ".ff", p, x, dy, dxf, g, accumulate, s);
+      k_convert(dxf, DType::F32, dx, t, (size_t)rows * hq, s);
+      break;
+    }
+    case TESS_OP_ATTENTION: {
+      float* dxf = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
+      attn_bwd(c, t, rd, tag + ".attn", p, x, dy, dxf, g, accumulate, s);
+      k_convert(dxf, DType::F32, dx, t, (size_t)rows * hq, s);
+      break;
+    }
+    case TESS_OP_BIAS_ADD: {
+      // ref layers.cpp:505-517
+      float* cs = static_cast<float*>(wsget(c, "bias.colsum", hq * 4));
+      float* scratch =
+          static_cast<float*>(wsget(c, "bias.scratch", k_colsum_scratch_floats(rows, hq) * 4));
+      k_colsum(dy, t, rows, hq, cs, scratch, s);
+      float* red = static_cast<float*>(wsget(c, "bias.red", hq * 4));
+      coll_reduce(c, COL, 0, cs, red, hq, s);
+      if (c.coord.i == 0) {
+        coll_allreduce(c, DEPTH, red, hq, s);
+        if (dbias) TESS_CUDA(cudaMemcpyAsync(dbias, red, hq * 4, cudaMemcpyDefault, s));
+      }
+      if (dx != dy) TESS_CUDA(cudaMemcpyAsync(dx, dy, act, cudaMemcpyDeviceToDevice, s));
+      break;
+    }
+    case TESS_OP_BLOCK: {
+      // ref layers.cpp:474-487
+      const void* r1 = wsget(c, tag + ".r1", act);
+      const void* ln1 = wsget(c, tag + ".ln1out", act);
+      const void* ln2 = wsget(c, tag + ".ln2out", act);
+      float* dff = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
+      ff_bwd(c, t, rd, tag + ".ff", p, ln2, dy, dff, g, accumulate, s);
+      void* dr1 = wsget(c, "blk.dr1", act);
+      ln_bwd(c, t, rd, tag + ".ln2", dff, DType::F32, r1, p.ln2_gain, dy, t, dr1, t,
+             g ? g->ln2_gain : nullptr, g ? g->ln2_bias : nullptr, accumulate, s);
+      float* dat = static_cast<float*>(wsget(c, "blk.dattn32", (size_t)rows * hq * 4));
+      attn_bwd(c, t, rd, tag + ".attn", p, ln1, dr1, dat, g, accumulate, s);
+      ln_bwd(c, t, rd, tag + ".ln1", dat, DType::F32, x, p.ln1_gain, dr1, t, dx, t,
+             g ? g->ln1_gain : nullptr, g ? g->ln1_bias : nullptr, accumulate, s);
+      break;
+    }
+    default:
+      fail(TESS_ERR_INVALID, "unknown layer op");
+  }
+  if (dx != dx_out) TESS_CUDA(cudaMemcpyAsync(dx_out, dx, act, cudaMemcpyDeviceToHost, s));
+}
+
+}  // namespace tess

@@ -1,0 +1,61 @@
+// Rank-level Tesseract operators (SUMMA-in-depth products and the layers
+// built on them). Reference counterparts:
+//   nn/nt/tn_product    proj/src/algorithms.cpp:34-76
+//   ln/ff/attn/block    proj/src/layers.cpp:242-487
+//   bias_add            proj/src/layers.cpp:491-517
+#pragma once
+
+#include "ctx.h"
+#include "kernels/gemm.h"
+
+namespace tess {
+
+// Where and how a product's result is written.
+struct Out {
+  void* c = nullptr;
+  DType t = DType::F32;
+  int64_t ldc = 0;
+  Epi epi = Epi::Store;
+  const void* r = nullptr;  // residual (Resid), same type/ld as c
+  int64_t ldr = 0;
+  void* z = nullptr;  // pre-activation (Gelu)
+  int64_t ldz = 0;
+  float alpha = 1.0f;
+};
+
+// C[ar, bn] (op)= sum_t A(h,t) B(t,j); A panels row-broadcast, B panels
+// column-broadcast, all q panels accumulated in one tensor-memory
+// accumulator (one GEMM with q K-segments).
+void nn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t ak, const void* b,
+                int64_t bn, const Out& out, cudaStream_t s);
+
+// C(h, j') = sum_j A(h,j) B(j',j)^T reduced over the row to slot j' (fp32).
+// out must be fp32 (Store or Accum) or bf16 Store.
+void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const void* b,
+                int64_t br, const Out& out, cudaStream_t s);
+
+// C(i', j) = sum A(h,i')^T B(h,j) reduced down the column to slot i' and, if
+// sum_over_depth, all-reduced over depth. out fp32 Store or Accum.
+void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const void* b,
+                int64_t bn, bool sum_over_depth, const Out& out, cudaStream_t s);
+
+// ------------------------------------------------------------------ layers
+struct RankDims {
+  int64_t rows = 0;       // local activation rows = samples_local * seq
+  int64_t hq = 0;         // hidden / q
+  int64_t seq = 0;
+  int64_t head_dim = 0;
+  int64_t heads_local = 0;
+  int64_t samples_local = 0;
+  int64_t hidden_total = 0;
+};
+RankDims rank_dims(const Ctx& c, const tess_layer_dims& d);
+
+void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
+                   const tess_block_shard& p, const float* bias_row0, const void* x, void* y,
+                   cudaStream_t s);
+void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
+                    const tess_block_shard& p, const void* dy, void* dx,
+                    tess_block_grads* g, bool accumulate, float* dbias, cudaStream_t s);
+
+}  // namespace tess

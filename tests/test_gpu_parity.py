@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle.
+
+Tolerances (north star + SURVEY App. C):
+  * partition / gather: bit-exact;
+  * fp32 mode: rel_diff (max|diff| / max|ref|, matrix.cpp:138-140) <= 1e-5
+    against the oracle run on the same fp32-rounded inputs;
+  * bf16 mode (tcgen05, fp32 accumulate, fp32 output before any cast):
+    relative Frobenius <= 1e-4 vs the oracle on identical bf16-rounded
+    inputs, <= 5e-3 vs the oracle on the original fp64 inputs;
+  * bf16 layers (intermediates stored in bf16): relative Frobenius <= 2e-2.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GRIDS = [(1, 1, False), (1, 2, True), (2, 1, False), (2, 2, False)]
+
+
+@pytest.fixture(scope="module")
+def tess():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2105_14500_b200 as t
+    return t
+
+
+def f32r(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def bf16r(a):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    # round-to-nearest-even to the top 16 bits
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def rel_diff(v, r):
+    return np.abs(v - r).max() / max(np.abs(r).max(), 1e-30)
+
+
+def frob(v, r):
+    return np.linalg.norm(v - r) / max(np.linalg.norm(r), 1e-30)
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS)
+def test_config1_nn_fp32(tess, orc, q, d, allow):
+    # BASELINE.json config 1: A, B 1024x1024, streams (42,0), (42,1), fp32.
+    a = f32r(orc.random_matrix(1024, 1024, 42, 0))
+    b = f32r(orc.random_matrix(1024, 1024, 42, 1))
+    want, sr, sk = orc.tesseract_matmul(a, b, q, d, "nn")
+    got = tess.tesseract_matmul(a, b, tess.GridSpec(q, d, allow), "nn", dtype="f32")
+    assert rel_diff(got.value, want) <= 1e-5
+    assert (got.stats.per_rank == sr).all() and (got.stats.per_kind == sk).all()
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS + [(3, 1, False)])
+@pytest.mark.parametrize("variant", ["nn", "nt", "tn"])
+def test_variants_fp32(tess, orc, q, d, allow, variant):
+    m, n, r = 48 * q * d, 40 * q, 24 * q
+    a = f32r(orc.random_matrix(m, n, 5, 0))
+    b = f32r(orc.random_matrix({"nn": n, "nt": r, "tn": m}[variant],
+                               {"nn": r, "nt": n, "tn": r}[variant], 5, 1))
+    want, sr, sk = orc.tesseract_matmul(a, b, q, d, variant)
+    got = tess.tesseract_matmul(a, b, tess.GridSpec(q, d, allow), variant, dtype="f32")
+    assert rel_diff(got.value, want) <= 1e-5
+    assert (got.stats.per_rank == sr).all() and (got.stats.per_kind == sk).all()
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS)
+@pytest.mark.parametrize("variant", ["nn", "nt", "tn"])
+def test_variants_bf16(tess, orc, q, d, allow, variant):
+    m, n, r = 256 * q * d, 256 * q, 128 * q
+    a0 = orc.random_matrix(m, n, 6, 0)
+    b0 = orc.random_matrix({"nn": n, "nt": r, "tn": m}[variant],
+                           {"nn": r, "nt": n, "tn": r}[variant], 6, 1)
+    a, b = bf16r(a0), bf16r(b0)
+    want, sr, sk = orc.tesseract_matmul(a, b, q, d, variant)
+    want0, _, _ = orc.tesseract_matmul(a0, b0, q, d, variant)
+    got = tess.tesseract_matmul(a0, b0, tess.GridSpec(q, d, allow), variant, dtype="bf16")
+    assert frob(got.value, want) <= 1e-4
+    assert frob(got.value, want0) <= 5e-3
+    assert (got.stats.per_rank == sr).all() and (got.stats.per_kind == sk).all()
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_backward(tess, orc, q, d, allow, dtype):
+    m, k, n = 128 * q * d, 64 * q, 96 * q
+    rnd = f32r if dtype == "f32" else bf16r
+    a = rnd(orc.random_matrix(m, k, 7, 0))
+    b = rnd(orc.random_matrix(k, n, 7, 1))
+    dc = rnd(orc.random_matrix(m, n, 7, 2))
+    da, db, sr, sk = orc.tesseract_backward(dc, a, b, q, d)
+    got = tess.tesseract_backward_dense(dc, a, b, tess.GridSpec(q, d, allow), dtype=dtype)
+    if dtype == "f32":
+        assert rel_diff(got.a_grad, da) <= 1e-5 and rel_diff(got.b_grad, db) <= 1e-5
+    else:
+        assert frob(got.a_grad, da) <= 1e-4 and frob(got.b_grad, db) <= 1e-4
+    assert (got.stats.per_rank == sr).all() and (got.stats.per_kind == sk).all()
+
+
+def test_partition_bit_exact(tess, orc):
+    import torch
+    q, d = 2, 2
+    grid = tess.GridSpec(q, d)
+    ctxs = tess.init_local(grid)
+    try:
+        m = orc.random_matrix(64, 48, 8, 0).astype(np.float32)
+        gdev = torch.from_numpy(m).cuda()
+        for scheme in (0, 1):
+            blocks = orc.partition(m.astype(np.float64), q, d, scheme)
+            back = torch.zeros_like(gdev)
+            for r, cx in enumerate(ctxs):
+                loc = torch.empty(blocks[r].shape, dtype=torch.float32, device="cuda")
+                cx.partition(scheme, "f32", gdev.data_ptr(), 64, 48, loc.data_ptr())
+                torch.cuda.synchronize()
+                assert (loc.cpu().numpy().astype(np.float64) == blocks[r]).all()
+                cx.unpartition(scheme, "f32", loc.data_ptr(), 64, 48, back.data_ptr())
+            torch.cuda.synchronize()
+            assert torch.equal(back, gdev)
+        # bf16 bytes round-trip bit-exactly too
+        gb = gdev.to(torch.bfloat16)
+        back = torch.zeros_like(gb)
+        for cx in ctxs:
+            loc = torch.empty((64 // 4, 48 // 2), dtype=torch.bfloat16, device="cuda")
+            cx.partition(0, "bf16", gb.data_ptr(), 64, 48, loc.data_ptr())
+            cx.unpartition(0, "bf16", loc.data_ptr(), 64, 48, back.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(back.view(torch.int16), gb.view(torch.int16))
+    finally:
+        for cx in ctxs:
+            cx.close()
+
+
+def _layer_inputs(orc, b, s, h, seed, rnd):
+    x = rnd(orc.random_matrix(b * s, h, seed, 0))
+    dy = rnd(orc.random_matrix(b * s, h, seed, 2))
+    P = orc.random_block_params(h, seed, 100)
+    P = {k: (rnd(v) if k.startswith("w_") else f32r(v)) for k, v in P.items()}
+    return x, dy, P
+
+
+def _compare_layer(res, want, tol, metric):
+    errs = {"y": metric(res.y, want["y"]), "dx": metric(res.dx, want["dx"])}
+    for k, v in want["grads"].items():
+        if np.abs(v).max() > 0:
+            errs[k] = metric(res.grads[k], v)
+        else:
+            assert np.abs(res.grads[k]).max() == 0, k
+    worst = max(errs.values())
+    assert worst <= tol, errs
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS)
+@pytest.mark.parametrize("op", ["feedforward", "attention", "layernorm", "bias_add", "block"])
+def test_layers_fp32(tess, orc, q, d, allow, op):
+    b, s, h, nh = 4, 8, 32, 4
+    x, dy, P = _layer_inputs(orc, b, s, h, 9, f32r)
+    want = orc.layer_run(op, x, dy, P, b, s, nh)
+    res = tess.layer_run(op, x, dy, P, tess.LayerDims(b, s, h, nh), tess.GridSpec(q, d, allow),
+                         dtype="f32")
+    _compare_layer(res, want, 1e-5, rel_diff)
+    if op == "bias_add":
+        assert rel_diff(res.dbias, want["dbias"]) <= 1e-5
+    sr, sk = orc.layer_stats(op, q, d, b, s, h)
+    assert (res.stats.per_rank == sr).all() and (res.stats.per_kind == sk).all()
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS)
+@pytest.mark.parametrize("op", ["feedforward", "attention", "layernorm", "block"])
+def test_layers_bf16(tess, orc, q, d, allow, op):
+    b, s, h, nh = 4, 64, 128, 4
+    x, dy, P = _layer_inputs(orc, b, s, h, 10, bf16r)
+    want = orc.layer_run(op, x, dy, P, b, s, nh)
+    res = tess.layer_run(op, x, dy, P, tess.LayerDims(b, s, h, nh), tess.GridSpec(q, d, allow),
+                         dtype="bf16")
+    _compare_layer(res, want, 2e-2, frob)
+    sr, sk = orc.layer_stats(op, q, d, b, s, h)
+    assert (res.stats.per_rank == sr).all() and (res.stats.per_kind == sk).all()
+
+
+def test_error_taxonomy(tess, orc):
+    a = orc.random_matrix(8, 6, 1, 0)
+    with pytest.raises(tess.ShapeError):
+        tess.tesseract_matmul(a, orc.random_matrix(5, 4, 1, 1), tess.GridSpec(1, 1))
+    with pytest.raises(tess.DivisibilityError, match="rows"):
+        tess.tesseract_matmul(orc.random_matrix(6, 4, 1, 0), orc.random_matrix(4, 4, 1, 1),
+                              tess.GridSpec(2, 2))
+    with pytest.raises(tess.DivisibilityError, match="batch"):
+        x = orc.random_matrix(3 * 2, 8, 1, 0)
+        P = orc.random_block_params(8, 1, 100)
+        tess.layer_run("block", x, x, P, tess.LayerDims(3, 2, 8, 2), tess.GridSpec(2, 1))
+
+
+def test_determinism_bitwise(tess, orc):
+    a = orc.random_matrix(256, 128, 3, 0)
+    b = orc.random_matrix(128, 192, 3, 1)
+    g = tess.GridSpec(2, 2)
+    r1 = tess.tesseract_matmul(a, b, g, "nn", dtype="bf16").value
+    r2 = tess.tesseract_matmul(a, b, g, "nn", dtype="bf16").value
+    assert (r1 == r2).all()
+
+
+def test_degeneracy_summa_equals_tesseract_d1(tess, orc):
+    # [q,q,1] Tesseract == SUMMA in values and CommStats.
+    a = f32r(orc.random_matrix(96, 64, 4, 0))
+    b = f32r(orc.random_matrix(64, 80, 4, 1))
+    got = tess.tesseract_matmul(a, b, tess.GridSpec(2, 1), "nn")
+    want, sr, sk = orc.tesseract_matmul(a, b, 2, 1, "nn")
+    assert rel_diff(got.value, want) <= 1e-5 and (got.stats.per_kind == sk).all()
+
+
+def test_per_rank_contexts_threaded_nn(tess, orc):
+    """Drive the per-rank C-ABI from one Python thread per rank (run_spmd)."""
+    import torch
+    q, d = 2, 2
+    grid = tess.GridSpec(q, d)
+    M, K, N = 128, 96, 64
+    a = f32r(orc.random_matrix(M, K, 12, 0))
+    b = f32r(orc.random_matrix(K, N, 12, 1))
+    want, _, sk = orc.tesseract_matmul(a, b, q, d, "nn")
+    ab = orc.partition(a, q, d, 0)
+    bb = orc.partition(b, q, d, 1)
+    ctxs = tess.init_local(grid)
+    outs = [None] * grid.size()
+    errs = []
+
+    def run(r):
+        try:
+            cx = ctxs[r]
+            la = torch.from_numpy(ab[r].astype(np.float32)).cuda()
+            lb = torch.from_numpy(bb[r].astype(np.float32)).cuda()
+            lc = torch.empty((la.shape[0], lb.shape[1]), dtype=torch.float32, device="cuda")
+            cx.matmul("nn", "f32", la.data_ptr(), *la.shape, lb.data_ptr(), *lb.shape,
+                      lc.data_ptr())
+            torch.cuda.synchronize()
+            outs[r] = lc.cpu().numpy().astype(np.float64)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(grid.size())]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    try:
+        assert not errs, errs
+        got = orc.combine(outs, M, N, q, d, 0)
+        assert rel_diff(got, want) <= 1e-5
+        assert sum(cx.stats()["by_kind"][0][0] for cx in ctxs) == int(sk[0, 0])
+    finally:
+        for cx in ctxs:
+            cx.close()
