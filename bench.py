@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark: Tesseract Transformer-layer fwd+bwd on B200 (BASELINE.json).
+
+Workload (BASELINE.json configs[3], weak scaling): one pre-norm Transformer
+block (LN -> QKV -> attention (no mask) -> proj -> +res -> LN -> FF1+GeLU ->
+FF2 -> +res), forward + backward with weight/LN gradients, h=12288, 96 heads,
+seq 2048, batch 4 per GPU-equivalent (b = 4 * p), bf16 storage with fp32
+accumulation, on the [q,q,d] grid for N GPUs:
+    N=1 [1,1,1]   N=2 [1,1,2]   N=4 [2,2,1]   N=8 [2,2,2]
+One process per GPU (torchrun for N>1), NCCL row/column/depth communicators
+inside libtess; torch.distributed (gloo) only for the unique-id exchange,
+barriers and the max-over-ranks timing reduction.
+
+Prints ONE JSON line on rank 0 (see the contract in the task statement).
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, the unmodified tesseract-sim) on a bounded sample instead.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Transformer-layer fwd+bwd TFLOP/s at [2,2,2] on 8×B200; step ms; exposed comm %"
+GRIDS = {1: (1, 1, True), 2: (1, 2, True), 4: (2, 1, False), 8: (2, 2, False)}
+HIDDEN, HEADS, SEQ, B_PER_GPU = 12288, 96, 2048, 4
+# CPU sample for the reference / cpu_baseline legs (bounded CPU work)
+SAMPLE = dict(batch=4, seq=128, hidden=512, heads=8)
+
+
+def layer_flops(batch, seq, hidden):
+    """Algorithmic flops of one block fwd+bwd (2*m*n*k of GEMMs + attention
+    contractions): 72*T*h^2 + 12*T*s*h, T = batch*seq."""
+    T = batch * seq
+    return 72.0 * T * hidden * hidden + 12.0 * T * seq * hidden
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops_sustained", 1434.2), "measured", d.get("hbm_gbs")
+    return 1400.0, "fallback", 6650.0
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------- CPU legs
+def cpu_sample_run(reps_min_s=10.0, reps_max_s=30.0, max_reps=None):
+    """Times the reference CPU implementation of layer_run(Block) on the
+    bounded SAMPLE; returns (tflops, seconds_per_call, kind, cores, desc)."""
+    import numpy as np
+    ncpu = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(ncpu))
+    import oracle
+    b, s, h, nh = SAMPLE["batch"], SAMPLE["seq"], SAMPLE["hidden"], SAMPLE["heads"]
+    orc = oracle.Oracle()
+    x = orc.random_matrix(b * s, h, 42, 0)
+    dy = orc.random_matrix(b * s, h, 42, 2)
+    P = orc.random_block_params(h, 42, 100)
+    if oracle.Reference.available():
+        ref = oracle.Reference()
+        kind, cores = "reference", int(os.environ.get("OMP_NUM_THREADS", ncpu))
+        call = lambda: ref.layer_run("block", x, dy, P, b, s, nh, q=1, d=1)  # noqa: E731
+    else:
+        kind, cores = "port", 1
+        call = lambda: orc.layer_run("block", x, dy, P, b, s, nh)  # noqa: E731
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+        el = time.perf_counter() - t_all
+        if max_reps is not None and len(times) >= max_reps:
+            break
+        if el >= reps_min_s or el + times[-1] > reps_max_s:
+            break
+    per = sum(times) / len(times)
+    fl = layer_flops(b, s, h)
+    desc = (f"layer_run(Block) fwd+bwd b={b} s={s} h={h} heads={nh} grid [1,1,1], "
+            f"{len(times)} calls, fp64")
+    return fl / per / 1e12, per, kind, cores, desc, np
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    fl = layer_flops(SAMPLE["batch"], SAMPLE["seq"], SAMPLE["hidden"])
+    # warmup + timed steps, one sample call per step
+    cpu_sample_run(max_reps=max(args.warmup, 1), reps_min_s=0, reps_max_s=1e9)
+    tf, per, kind, cores, desc, _ = cpu_sample_run(max_reps=args.steps, reps_min_s=0,
+                                                   reps_max_s=1e9)
+    line = {"metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "reference CPU layer_run(Block) sample", **SAMPLE},
+            "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                             "sample": desc},
+            "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tess", choices=["tess", "reference"])
+    ap.add_argument("--batch-per-gpu", type=int, default=B_PER_GPU)
+    ap.add_argument("--hidden", type=int, default=HIDDEN)
+    ap.add_argument("--heads", type=int, default=HEADS)
+    ap.add_argument("--seq", type=int, default=SEQ)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        if dist:
+            dist.barrier()
+        return
+
+    import torch
+    import paper_2105_14500_b200 as tess
+
+    if args.gpus not in GRIDS:
+        raise SystemExit(f"--gpus must be one of {sorted(GRIDS)}")
+    q, d, allow = GRIDS[args.gpus]
+    grid = tess.GridSpec(q, d, allow)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+
+    if world > 1:
+        obj = [tess.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = tess.init_nccl(grid, rank, local_rank, obj[0])
+    else:
+        ctx = tess.init_local(grid)[0]
+
+    p = grid.size()
+    h, nh, s = args.hidden, args.heads, args.seq
+    batch = args.batch_per_gpu * p
+    dims = tess.LayerDims(batch, s, h, nh)
+    rows = batch * s // (d * q)
+    hq = h // q
+    bf = torch.bfloat16
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+
+    def rnd(shape, scale, dtype=bf):
+        return (torch.rand(shape, device=dev, generator=g) * 2 - 1).mul_(scale).to(dtype)
+
+    # synthetic inputs of the named shapes; random-init weights (TesseractB blocks)
+    ws = 1.0 / (h ** 0.5)
+    W = {"w_qkv": rnd((hq, 3 * hq), ws), "w_proj": rnd((hq, hq), ws),
+         "w_ff1": rnd((hq, 4 * hq), ws), "w_ff2": rnd((4 * hq, hq), ws)}
+    LN = {"ln1_gain": 1 + rnd((hq,), 0.1, torch.float32), "ln1_bias": rnd((hq,), 0.1, torch.float32),
+          "ln2_gain": 1 + rnd((hq,), 0.1, torch.float32), "ln2_bias": rnd((hq,), 0.1, torch.float32)}
+    x = rnd((rows, hq), 1.0)
+    dy = rnd((rows, hq), 1.0)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in {**W, **LN}.items()}
+    shard = tess.BlockShardC(*[W[k].data_ptr() for k in ("w_qkv", "w_proj", "w_ff1", "w_ff2")],
+                             *[LN[k].data_ptr() for k in ("ln1_gain", "ln1_bias", "ln2_gain",
+                                                          "ln2_bias")], 1e-5)
+    grads = tess.BlockGradsC(*[G[k].data_ptr() for k in tess.PARAM_NAMES])
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step(xp, yp, dyp, dxp):
+        ctx.layer_forward("block", "bf16", dims, shard, xp, yp, stream=sh)
+        ctx.layer_backward("block", "bf16", dims, shard, dyp, dxp, grads, accumulate=False,
+                           stream=sh)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = tess.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = tess.kernel_launches() - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    flops = layer_flops(batch, s, h)
+    value = flops / (ms * 1e-3) / 1e12
+
+    # dominant kernel: the tcgen05 GEMM, timed per launch with events on its stream
+    tess.profile_enable(True)
+    step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
+    torch.cuda.synchronize(dev)
+    gemm_ms, gemm_flops, gemm_n = tess.profile_read()
+    tess.profile_enable(False)
+    peak, peak_src, _ = read_peaks()
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # end to end through the C-ABI with host (pinned) buffers, copies inside
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        dyh = dy.cpu().pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        dxh = torch.empty_like(xh).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            step(xh.data_ptr(), yh.data_ptr(), dyh.data_ptr(), dxh.data_ptr())
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(xh.data_ptr(), yh.data_ptr(), dyh.data_ptr(), dxh.data_ptr())
+        e1.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        nbytes = xh.numel() * xh.element_size()
+        e2e = {"value": flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": ms_e2e, "h2d_bytes_per_step": 2 * nbytes * p,
+               "d2h_bytes_per_step": 2 * nbytes * p}
+
+    cpu = None
+    if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
+        tf, per, kind, cores, desc, _ = cpu_sample_run()
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": kind, "sample": desc,
+               "seconds_per_call": per}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random inputs and random-init weights of the named shapes)",
+            "config": {
+                "workload": "cfg4: Tesseract Transformer block fwd+bwd (attention, no mask, + "
+                            "MLP + distributed LayerNorm), weak scaling b=4*p",
+                "grid": grid.to_string(), "global_batch": batch, "seq_len": s, "hidden": h,
+                "heads": nh, "rows_per_rank": rows, "parallelism": f"tesseract{grid}",
+                "l2": "inputs larger than L2 (per-GPU weights+activations >> 126 MB)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained", "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "tess::sm100::gemm_bf16_kernel (all launches of one step)",
+                         "gemm_ms_per_step": gemm_ms, "gemm_launches_per_step": gemm_n,
+                         "gemm_share_of_step": gemm_ms / ms if ms else None},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

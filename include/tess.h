@@ -256,6 +256,13 @@ tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q,
  * load (for the bench's gpu_launches claim). */
 uint64_t tess_kernel_launches(void);
 
+/* GEMM launch profiling: when enabled, every local GEMM launch is bracketed
+ * by CUDA events on its own stream; tess_profile_read synchronises them and
+ * returns the summed device time (ms), algorithmic flops (2*M*N*K per
+ * launch) and launch count since the last tess_profile_enable. */
+tess_status tess_profile_enable(int on);
+tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
+
 #ifdef __cplusplus
 }
 #endif

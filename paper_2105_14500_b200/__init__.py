@@ -120,6 +120,8 @@ def _load() -> C.CDLL:
         "tess_last_error": ([], C.c_char_p),
         "tess_version": ([], C.c_char_p),
         "tess_kernel_launches": ([], C.c_uint64),
+        "tess_profile_enable": ([i], i),
+        "tess_profile_read": ([dp, dp, u64p], i),
         "tess_grid_check": ([i, i, i], i),
         "tess_grid_parse": ([C.c_char_p, i, ip, ip], i),
         "tess_grid_rank_of": ([i, i, i, i, i, ip], i),
@@ -548,3 +550,15 @@ def init_nccl(grid: GridSpec, rank: int, device: int, unique_id: bytes) -> RankC
 
 def kernel_launches() -> int:
     return int(lib.tess_kernel_launches())
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every local GEMM launch with CUDA events on its stream."""
+    _check(lib.tess_profile_enable(int(on)))
+
+
+def profile_read():
+    """(gemm_ms, gemm_flops, gemm_launches) since profile_enable."""
+    ms, fl, n = C.c_double(), C.c_double(), C.c_uint64()
+    _check(lib.tess_profile_read(C.byref(ms), C.byref(fl), C.byref(n)))
+    return ms.value, fl.value, n.value

@@ -70,6 +70,14 @@ const char* tess_last_error(void) { return g_last_error.c_str(); }
 const char* tess_version(void) { return "tess-b200 0.1 (sm_100a, tcgen05)"; }
 uint64_t tess_kernel_launches(void) { return g_launches.load(); }
 
+tess_status tess_profile_enable(int on) {
+  return guarded([&] { profile_enable(on != 0); });
+}
+
+tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches) {
+  return guarded([&] { profile_read(gemm_ms, gemm_flops, gemm_launches); });
+}
+
 tess_status tess_grid_check(int q, int d, int allow) {
   return guarded([&] { Grid g(q, d, allow != 0); });
 }

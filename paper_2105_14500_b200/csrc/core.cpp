@@ -1,5 +1,6 @@
 // Grid geometry (reference proj/src/grid.cpp), workspace, metered collectives.
 #include <charconv>
+#include <mutex>
 
 #include "ctx.h"
 
@@ -106,6 +107,68 @@ size_t Workspace::bytes_held() const {
   size_t t = 0;
   for (auto& kv : bufs_) t += kv.second.bytes;
   return t;
+}
+
+// ------------------------------------------------------------ local GEMM
+namespace {
+struct ProfRec {
+  cudaEvent_t a, b;
+  double flops;
+  int device;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+void run_gemm(const GemmDesc& g, cudaStream_t s) {
+  ProfRec rec{nullptr, nullptr, 0.0, 0};
+  const bool prof = g_prof_on;
+  if (prof) {
+    cudaGetDevice(&rec.device);
+    TESS_CUDA(cudaEventCreate(&rec.a));
+    TESS_CUDA(cudaEventCreate(&rec.b));
+    TESS_CUDA(cudaEventRecord(rec.a, s));
+    double k = 0;
+    for (int i = 0; i < g.nseg; ++i) k += (double)g.seg[i].k;
+    rec.flops = 2.0 * (double)g.M * (double)g.N * k * (double)g.nb0 * (double)g.nb1;
+  }
+  cudaError_t e = gemm(g, s);
+  count_launch();
+  if (e == cudaErrorInvalidValue) fail(TESS_ERR_UNSUPPORTED, gemm_last_error());
+  if (e != cudaSuccess)
+    fail(TESS_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e) + " " + gemm_last_error());
+  if (prof) {
+    TESS_CUDA(cudaEventRecord(rec.b, s));
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(rec);
+  }
+}
+
+void profile_enable(bool on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  g_prof_on = on;
+}
+
+void profile_read(double* ms, double* flops, uint64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double t = 0, f = 0;
+  for (auto& r : g_prof) {
+    cudaSetDevice(r.device);
+    TESS_CUDA(cudaEventSynchronize(r.b));
+    float m = 0;
+    TESS_CUDA(cudaEventElapsedTime(&m, r.a, r.b));
+    t += m;
+    f += r.flops;
+  }
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (launches) *launches = g_prof.size();
 }
 
 // ------------------------------------------------------- collectives

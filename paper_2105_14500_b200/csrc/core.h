@@ -40,6 +40,10 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 enum Family { ROW = 0, COL = 1, DEPTH = 2 };
 
+// GEMM launch profiling (CUDA events around every local GEMM launch).
+void profile_enable(bool on);
+void profile_read(double* ms, double* flops, uint64_t* launches);
+
 struct Coord {
   int i = 0, j = 0, k = 0;
 };

@@ -60,12 +60,6 @@ Out out_to(void* p, DType t, int64_t ld = 0) {
 }
 
 // ----------------------------------------------------------- LayerNorm
-struct LnCache {
-  const void* x;
-  float* mean;
-  float* rstd;
-};
-
 void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const void* x,
             const float* gain, const float* bias, double eps, void* y, cudaStream_t s) {
   const int64_t rows = rd.rows, w = rd.hq;
@@ -192,8 +186,7 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g.ldc = S;
     g.cs0 = S * S;
     g.alpha = scale;
-    TESS_CUDA(gemm(g, s));
-    count_launch();
+    run_gemm(g, s);
     char* Ps = static_cast<char*>(P) + (size_t)smp * H * S * S * esz;
     k_softmax_fwd(Sbuf, Ps, t, H * S, S, s);
     // O = P V
@@ -211,8 +204,7 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g2.c_type = t;
     g2.ldc = hq;
     g2.cs0 = hd;
-    TESS_CUDA(gemm(g2, s));
-    count_launch();
+    run_gemm(g2, s);
   }
   nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s);
 }
@@ -247,14 +239,14 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g1.seg[0] = {do0, q0 + 2 * hd * esz, hd};
     g1.lda = hq; g1.as0 = hd; g1.ldb = ld; g1.bs0 = 3 * hd;
     g1.c = dP; g1.c_type = DType::F32; g1.ldc = S; g1.cs0 = S * S;
-    TESS_CUDA(gemm(g1, s));
+    run_gemm(g1, s);
     // dV = P^T dO
     GemmDesc g2;
     g2.M = S; g2.N = hd; g2.nb0 = H; g2.in = t; g2.trans_a = true;
     g2.seg[0] = {Ps, do0, S};
     g2.lda = S; g2.as0 = S * S; g2.ldb = hq; g2.bs0 = hd;
     g2.c = dq0 + 2 * hd * esz; g2.c_type = t; g2.ldc = ld; g2.cs0 = 3 * hd;
-    TESS_CUDA(gemm(g2, s));
+    run_gemm(g2, s);
     // dS = P * (dP - rowsum(P*dP)) / sqrt(hd)
     k_softmax_bwd(Ps, dP, dS, t, H * S, S, scale, s);
     // dQ = dS K
@@ -263,15 +255,14 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g3.seg[0] = {dS, q0 + hd * esz, S};
     g3.lda = S; g3.as0 = S * S; g3.ldb = ld; g3.bs0 = 3 * hd;
     g3.c = dq0; g3.c_type = t; g3.ldc = ld; g3.cs0 = 3 * hd;
-    TESS_CUDA(gemm(g3, s));
+    run_gemm(g3, s);
     // dK = dS^T Q
     GemmDesc g4;
     g4.M = S; g4.N = hd; g4.nb0 = H; g4.in = t; g4.trans_a = true;
     g4.seg[0] = {dS, q0, S};
     g4.lda = S; g4.as0 = S * S; g4.ldb = ld; g4.bs0 = 3 * hd;
     g4.c = dq0 + hd * esz; g4.c_type = t; g4.ldc = ld; g4.cs0 = 3 * hd;
-    TESS_CUDA(gemm(g4, s));
-    count_launch(4);
+    run_gemm(g4, s);
   }
   nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s);
   weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);

@@ -23,6 +23,11 @@ struct Out {
   float alpha = 1.0f;
 };
 
+// Launches one local GEMM (tcgen05 for bf16, CUDA cores for fp32); failures
+// become tess::Error. When profiling is on, the launch is bracketed by CUDA
+// events on its stream (tess_profile_*).
+void run_gemm(const GemmDesc& g, cudaStream_t s);
+
 // C[ar, bn] (op)= sum_t A(h,t) B(t,j); A panels row-broadcast, B panels
 // column-broadcast, all q panels accumulated in one tensor-memory
 // accumulator (one GEMM with q K-segments).

@@ -36,14 +36,6 @@ GemmDesc base_desc(DType in, int64_t M, int64_t N, const Out& out) {
   return g;
 }
 
-void run_gemm(const GemmDesc& g, cudaStream_t s) {
-  cudaError_t e = gemm(g, s);
-  count_launch();
-  if (e == cudaErrorInvalidValue) fail(TESS_ERR_UNSUPPORTED, gemm_last_error());
-  if (e != cudaSuccess)
-    fail(TESS_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e) + " " + gemm_last_error());
-}
-
 void check_q(const Ctx& c) {
   if (c.grid.q > kMaxSegments)
     fail(TESS_ERR_UNSUPPORTED, "q > " + std::to_string(kMaxSegments) + " not supported");
