@@ -128,8 +128,10 @@ def cpu_sample_run(reps_min_s=10.0, reps_max_s=30.0, max_reps=None):
         call()
         times.append(time.perf_counter() - t0)
         el = time.perf_counter() - t_all
-        if max_reps is not None and len(times) >= max_reps:
-            break
+        if max_reps is not None:
+            if len(times) >= max_reps:
+                break
+            continue
         if el >= reps_min_s or el + times[-1] > reps_max_s:
             break
     per = sum(times) / len(times)
