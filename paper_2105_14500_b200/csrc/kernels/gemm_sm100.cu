@@ -31,6 +31,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -478,6 +479,250 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================ 2-CTA kernel
+// CTA pair (cluster of 2 on one TPC) computing a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16): each CTA stages its own 128
+// rows of A and its 128-column half of B per k-block (32 KB/stage instead of
+// 48 KB for the 1-CTA 128x256 tile), so shared-memory and L2 operand traffic
+// per flop drop by a third. Only the leader CTA (rank 0) issues MMAs; both
+// producers' TMA loads signal the leader's full barrier (peer bit cleared),
+// MMA commits multicast to both CTAs' empty / tmem-full barriers, and both
+// CTAs' epilogue warps release the accumulator on the leader's tmem-empty
+// barrier with remote arrives.
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
+struct Cfg2 {
+  static constexpr int HALF = 128;  // rows of A / columns of B per CTA
+  static constexpr int A_BYTES = HALF * BK * 2;
+  static constexpr int B_BYTES = HALF * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+// Pair-tile index -> (batch0, batch1, m0 (multiple of 256), n0 (multiple of 256)).
+__device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int& b0, int& b1,
+                                                 int& m0, int& n0) {
+  const int b = tile / p.tiles_per_batch;
+  const int r = tile - b * p.tiles_per_batch;
+  b0 = b % p.nb0;
+  b1 = b / p.nb0;
+  const int width = p.group_m * p.tiles_n;
+  const int g = r / width;
+  const int first_m = g * p.group_m;
+  const int gm = min(p.tiles_m - first_m, p.group_m);
+  const int in = r - g * width;
+  m0 = (first_m + in % gm) * 256;
+  n0 = (in / gm) * 256;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
+  using C = Cfg2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t cta = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < p.nseg; ++s) {
+      prefetch_tmap(&p.tma_a[s]);
+      prefetch_tmap(&p.tma_b[s]);
+    }
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(tmem_slot)),
+        "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // -------------------------------------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+        int b0, b1, m0, n0;
+        decode_pair_tile(p, tile, b0, b1, m0, n0);
+        const int mr = m0 + (int)cta * C::HALF;
+        const int nr = n0 + (int)cta * C::HALF;
+        for (int s = 0; s < p.nseg; ++s) {
+          const CUtensorMap* ma = &p.tma_a[s];
+          const CUtensorMap* mb = &p.tma_b[s];
+          for (int kb = 0; kb < p.seg_kb[s]; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * C::STAGE_BYTES;
+            uint8_t* sb = sa + C::A_BYTES;
+            if (cta == 0) mbar_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+            const int k = kb * BK;
+            if (!A_MN) {
+              tma_load_4d_2sm(sa, ma, &full_bar[stage], k, mr, b0, b1);
+            } else {
+#pragma unroll
+              for (int c = 0; c < C::HALF / 64; ++c)
+                tma_load_4d_2sm(sa + c * 8192, ma, &full_bar[stage], mr + c * 64, k, b0, b1);
+            }
+            if (!B_MN) {
+              tma_load_4d_2sm(sb, mb, &full_bar[stage], k, nr, b0, b1);
+            } else {
+#pragma unroll
+              for (int c = 0; c < C::HALF / 64; ++c)
+                tma_load_4d_2sm(sb + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0, b1);
+            }
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && cta == 0) {
+      // ------------------------------------------ MMA issuer (leader CTA)
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < p.total_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc(sa + k * 2048, 8192, 1024)
+                                     : make_sdesc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc(sb + k * 2048, 8192, 1024)
+                                     : make_sdesc(sb + k * 32, 16, 1024);
+            mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit_2sm(&empty_bar[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2sm(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------- epilogue warps (both CTAs)
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+      int b0, b1, m0, n0;
+      decode_pair_tile(p, tile, b0, b1, m0, n0);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int m = m0 + (int)cta * C::HALF + quad * 32 + lane;
+      const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int c = 0; c < 256 / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(trow + c * 32, r);
+        const int n = n0 + c * 32;
+        if (m < p.M && n < p.N) epilogue_row_chunk(p, b0, b1, m, n, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -561,6 +806,38 @@ cudaError_t launch(const Params& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+template <bool A_MN, bool B_MN>
+cudaError_t launch_2cta(const Params& p, cudaStream_t stream) {
+  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg2::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int pairs = std::max(1, num_sms() / 2);
+  const int grid = 2 * std::min(p.num_tiles, pairs);
+  kern<<<grid, kThreads, Cfg2::SMEM_BYTES, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
+  if (!a_mn && b_mn) return launch_2cta<false, true>(p, s);
+  if (!a_mn && !b_mn) return launch_2cta<false, false>(p, s);
+  if (a_mn && b_mn) return launch_2cta<true, true>(p, s);
+  return launch_2cta<true, false>(p, s);
+}
+
+bool use_pair_kernel(int64_t M, int64_t N) {
+  static int mode = -1;  // TESS_GEMM_2CTA=0 forces the 1-CTA kernel (A/B testing)
+  if (mode < 0) {
+    const char* e = std::getenv("TESS_GEMM_2CTA");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return mode == 1 && M > 128 && N > 128;
+}
+
 template <int BN>
 cudaError_t launch_bn(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
   if (!a_mn && b_mn) return launch<BN, false, true>(p, s);
@@ -589,7 +866,11 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   }
   Params p;
   std::memset(&p, 0, sizeof(p));
+  const bool pair = use_pair_kernel(d.M, d.N);
   const int BN = d.N > 128 ? 256 : 128;
+  // TMA box rows for K-major operands: 128 (A, and B in the pair kernel) or BN.
+  const int a_box = BM;
+  const int b_box = pair ? 128 : BN;
   const bool a_mn = d.trans_a;   // A stored [K, M]: M contiguous
   const bool b_mn = !d.trans_b;  // B stored [K, N]: N contiguous
   int total_kb = 0;
@@ -603,14 +884,14 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
     bool ok;
     if (!a_mn)
       ok = encode_view(&p.tma_a[s], d.seg[s].a, K, d.M, d.lda, d.nb0, d.as0, d.nb1,
-                       d.as1, BM, &err);
+                       d.as1, a_box, &err);
     else
       ok = encode_view(&p.tma_a[s], d.seg[s].a, d.M, K, d.lda, d.nb0, d.as0, d.nb1,
                        d.as1, 64, &err);
     if (ok) {
       if (!b_mn)
         ok = encode_view(&p.tma_b[s], d.seg[s].b, K, d.N, d.ldb, d.nb0, d.bs0, d.nb1,
-                         d.bs1, BN, &err);
+                         d.bs1, b_box, &err);
       else
         ok = encode_view(&p.tma_b[s], d.seg[s].b, d.N, K, d.ldb, d.nb0, d.bs0, d.nb1,
                          d.bs1, 64, &err);
@@ -639,8 +920,9 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.M = static_cast<int>(d.M);
   p.N = static_cast<int>(d.N);
   p.nb0 = static_cast<int>(d.nb0);
-  p.tiles_m = static_cast<int>((d.M + BM - 1) / BM);
-  p.tiles_n = static_cast<int>((d.N + BN - 1) / BN);
+  const int tile_m = pair ? 256 : BM, tile_n = pair ? 256 : BN;
+  p.tiles_m = static_cast<int>((d.M + tile_m - 1) / tile_m);
+  p.tiles_n = static_cast<int>((d.N + tile_n - 1) / tile_n);
   p.tiles_per_batch = p.tiles_m * p.tiles_n;
   const long long nt = (long long)p.tiles_per_batch * d.nb0 * d.nb1;
   if (nt > (1ll << 31) - 1) {
@@ -648,7 +930,7 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   }
   p.num_tiles = static_cast<int>(nt);
-  p.group_m = 16;
+  p.group_m = pair ? 8 : 16;
   p.c = d.c;
   p.c_bf16 = d.c_type == DType::BF16;
   p.ldc = d.ldc;
@@ -664,8 +946,9 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.zs1 = d.zs1;
   p.alpha = d.alpha;
   p.epi = static_cast<int>(d.epi);
-  cudaError_t e = BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
-                            : launch_bn<128>(p, a_mn, b_mn, stream);
+  cudaError_t e = pair        ? launch_pair(p, a_mn, b_mn, stream)
+                  : BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
+                              : launch_bn<128>(p, a_mn, b_mn, stream);
   if (e != cudaSuccess) g_gemm_err = std::string("gemm_bf16_sm100 launch: ") +
                                      cudaGetErrorString(e);
   return e;
