@@ -369,6 +369,34 @@ __global__ void softmax_bwd_kernel(const T* __restrict__ P, const float* __restr
   }
 }
 
+__global__ void lse_combine_kernel(const float2* __restrict__ stats, int64_t rows, int nst,
+                                   float* __restrict__ lse) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float2* s = stats + r * nst;
+  float m = -INFINITY;
+  for (int i = 0; i < nst; ++i) m = fmaxf(m, s[i].x);
+  float sum = 0.f;
+  for (int i = 0; i < nst; ++i) sum += s[i].y * __expf(s[i].x - m);
+  lse[r] = m + __logf(sum);
+}
+
+// one warp per (row, head)
+template <typename T>
+__global__ void attn_delta_kernel(const T* __restrict__ dO, const T* __restrict__ O, int64_t ld,
+                                  int64_t S, int64_t H, int64_t hd, float* __restrict__ delta) {
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (w >= S * H) return;
+  const int64_t r = w / H, h = w % H;
+  const T* a = dO + r * ld + h * hd;
+  const T* b = O + r * ld + h * hd;
+  float acc = 0.f;
+  for (int64_t d = lane; d < hd; d += 32) acc += ldf<T>(a, d) * ldf<T>(b, d);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) delta[h * S + r] = acc;
+}
+
 // ------------------------------------------------------- comm helper
 struct SumArgs {
   const float* in[8];
@@ -530,6 +558,25 @@ void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cu
   } else {
     TESS_DISPATCH(t, T, softmax_fwd_generic_kernel<T><<<g, 32 * warps, 0, s>>>(S, (T*)P, rows, L));
   }
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_lse_combine(const float* stats, int64_t rows, int nst, float* lse, cudaStream_t s) {
+  if (!rows) return;
+  lse_combine_kernel<<<(unsigned)((rows + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      reinterpret_cast<const float2*>(stats), rows, nst, lse);
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_attn_delta(const void* dO, const void* O, DType t, int64_t ld, int64_t S, int64_t H,
+                  int64_t hd, float* delta, cudaStream_t s) {
+  if (!S || !H) return;
+  const int warps = 8;
+  const unsigned g = (unsigned)((S * H + warps - 1) / warps);
+  TESS_DISPATCH(t, T, attn_delta_kernel<T><<<g, 32 * warps, 0, s>>>((const T*)dO, (const T*)O, ld,
+                                                                      S, H, hd, delta));
   count_launch();
   TESS_CUDA(cudaGetLastError());
 }

@@ -27,10 +27,15 @@ inline int dtype_size(DType t) {
 
 // Epilogue applied to v = alpha * acc (fp32) for every output element.
 enum class Epi : int {
-  Store = 0,   // C = v
-  Accum = 1,   // C += v            (C fp32; weight-gradient accumulation)
-  Resid = 2,   // C = v + R         (residual add fused into the producer)
-  Gelu = 3,    // Z = v; C = gelu(v) with the exact erf GeLU
+  Store = 0,       // C = v
+  Accum = 1,       // C += v            (C fp32; weight-gradient accumulation)
+  Resid = 2,       // C = v + R         (residual add fused into the producer)
+  Gelu = 3,        // Z = v; C = gelu(v) with the exact erf GeLU
+  // The following are tcgen05-kernel only (bf16 inputs).
+  DGelu = 4,       // C = v * gelu'(R)  (R = FF1 pre-activation z; ref layers.cpp:365)
+  SoftmaxFwd = 5,  // C = exp(v - vec[row])   (vec = row log-sum-exp)
+  SoftmaxBwd = 6,  // C = R * (v - alpha*vec[row]) (R = P, vec = rowsum(dO*O))
+  RowStats = 7,    // no C: stats[row][tile] = (max_c v, sum_c exp(v - max))
 };
 
 constexpr int kMaxSegments = 8;
@@ -60,7 +65,21 @@ struct GemmDesc {
   int64_t ldz = 0, zs0 = 0, zs1 = 0;
   float alpha = 1.0f;
   Epi epi = Epi::Store;
+  // Per-row vector (SoftmaxFwd / SoftmaxBwd): vec[b0*vs0 + b1*vs1 + m].
+  const float* vec = nullptr;
+  int64_t vs0 = 0, vs1 = 0;
+  // RowStats output: float2 at stats[(b0*ss0 + b1*ss1 + m*nst + tile)*2],
+  // nst = gemm_bf16_stat_tiles(d) tiles per row.
+  float* stats = nullptr;
+  int64_t ss0 = 0, ss1 = 0;
 };
+
+// Column-tile width the tcgen05 dispatcher uses for d (RowStats layout).
+int gemm_bf16_tile_n(const GemmDesc& d);
+inline int gemm_bf16_stat_tiles(const GemmDesc& d) {
+  const int t = gemm_bf16_tile_n(d);
+  return static_cast<int>((d.N + t - 1) / t);
+}
 
 // bf16 inputs on 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
 cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream);

@@ -62,6 +62,11 @@ struct Params {
   long long ldz, zs0, zs1;
   float alpha;
   int epi;
+  const float* vec;
+  long long vs0, vs1;
+  float* stats;
+  long long ss0, ss1;
+  int nst, tile_n;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -175,6 +180,30 @@ __device__ __forceinline__ float gelu_erf(float v) {
   return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
 }
 
+// d/dz of the exact-erf GeLU (ref layers.cpp:34-42)
+__device__ __forceinline__ float gelu_erf_grad(float v) {
+  return 0.5f * (1.0f + erff(v * 0.70710678118654752f)) +
+         v * 0.39894228040143268f * __expf(-0.5f * v * v);
+}
+
+// Online (max, sum-exp) of the valid values of one 32-column chunk merged
+// into the running pair of the row (RowStats epilogue).
+__device__ __forceinline__ void row_stats_chunk(const uint32_t (&acc)[32], float alpha,
+                                                int nvalid, float& rmax, float& rsum) {
+  float cm = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < nvalid) cm = fmaxf(cm, __uint_as_float(acc[j]) * alpha);
+  if (cm == -INFINITY) return;
+  const float nm = fmaxf(rmax, cm);
+  float s = rsum * __expf(rmax - nm);
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j < nvalid) s += __expf(__uint_as_float(acc[j]) * alpha - nm);
+  rmax = nm;
+  rsum = s;
+}
+
 // Tile index -> (batch0, batch1, m0, n0). Within a batch, tiles are grouped
 // group_m tiles tall so that one wave of CTAs shares A and B panels in L2.
 __device__ __forceinline__ void decode_tile(const Params& p, int tile, int& b0,
@@ -239,6 +268,36 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0,
       } else {
         for (int j = 0; j < nvalid; ++j) v[j] += __bfloat162float(rrow[j]);
       }
+    } else if (epi == (int)Epi::DGelu || epi == (int)Epi::SoftmaxBwd) {
+      // R = z (DGelu) or P (SoftmaxBwd), bf16 with C's layout
+      const __nv_bfloat16* rrow =
+          batch_ptr<__nv_bfloat16>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
+          (long long)m * p.ldr + n;
+      float rv[32];
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = *reinterpret_cast<const uint4*>(rrow + q * 8);
+          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) rv[q * 8 + e] = __bfloat162float(rb[e]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) rv[j] = j < nvalid ? __bfloat162float(rrow[j]) : 0.f;
+      }
+      if (epi == (int)Epi::DGelu) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= gelu_erf_grad(rv[j]);
+      } else {
+        const float d = p.alpha * p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = rv[j] * (v[j] - d);
+      }
+    } else if (epi == (int)Epi::SoftmaxFwd) {
+      const float lse = p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __expf(v[j] - lse);
     } else if (epi == (int)Epi::Gelu) {
       __nv_bfloat16* zrow = batch_ptr<__nv_bfloat16>(p.z, p.zs0, p.zs1, b0, b1) +
                             (long long)m * p.ldz + n;
@@ -315,6 +374,32 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0,
     } else {
       for (int j = 0; j < nvalid; ++j) crow[j] = v[j];
     }
+  }
+}
+
+// Epilogue of one accumulator tile row (this thread's row m, columns
+// [n0, n0 + width)): tcgen05.ld 32 columns at a time, then either the
+// elementwise epilogue or the RowStats reduction.
+__device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, int m, int n0,
+                                              int width, uint32_t trow) {
+  const bool stats = p.epi == (int)Epi::RowStats;
+  float rmax = -INFINITY, rsum = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < width / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(trow + c * 32, r);  // warp-collective: executed by every lane
+    const int n = n0 + c * 32;
+    if (m < p.M && n < p.N) {
+      if (stats)
+        row_stats_chunk(r, p.alpha, min(32, p.N - n), rmax, rsum);
+      else
+        epilogue_row_chunk(p, b0, b1, m, n, r);
+    }
+  }
+  if (stats && m < p.M && n0 < p.N) {
+    float* dst = p.stats + (p.ss0 * b0 + p.ss1 * b1 + (long long)m * p.nst + n0 / p.tile_n) * 2;
+    dst[0] = rmax;
+    dst[1] = rsum;
   }
 }
 
@@ -454,13 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(trow + c * 32, r);
-        const int n = n0 + c * 32;
-        if (m < p.M && n < p.N) epilogue_row_chunk(p, b0, b1, m, n, r);
-      }
+      epilogue_tile(p, b0, b1, m, n0, BN, trow);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -699,13 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int m = m0 + (int)cta * C::HALF + quad * 32 + lane;
       const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
-#pragma unroll 1
-      for (int c = 0; c < 256 / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(trow + c * 32, r);
-        const int n = n0 + c * 32;
-        if (m < p.M && n < p.N) epilogue_row_chunk(p, b0, b1, m, n, r);
-      }
+      epilogue_tile(p, b0, b1, m, n0, 256, trow);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
@@ -854,6 +927,10 @@ thread_local std::string g_gemm_err;
 
 const char* gemm_last_error() { return g_gemm_err.c_str(); }
 
+int gemm_bf16_tile_n(const GemmDesc& d) {
+  return (sm100::use_pair_kernel(d.M, d.N) || d.N > 128) ? 256 : 128;
+}
+
 cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   using namespace sm100;
   if (d.in != DType::BF16) {
@@ -910,8 +987,14 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
     g_gemm_err = "gemm_bf16_sm100: output rows must be 16-byte aligned";
     return cudaErrorInvalidValue;
   }
-  if ((d.epi == Epi::Resid && !d.r) || (d.epi == Epi::Gelu && !d.z) ||
-      (d.epi == Epi::Accum && d.c_type != DType::F32)) {
+  const bool needs_r = d.epi == Epi::Resid || d.epi == Epi::DGelu || d.epi == Epi::SoftmaxBwd;
+  const bool bf16_only = d.epi == Epi::DGelu || d.epi == Epi::SoftmaxFwd ||
+                         d.epi == Epi::SoftmaxBwd;
+  const bool needs_vec = d.epi == Epi::SoftmaxFwd || d.epi == Epi::SoftmaxBwd;
+  if ((needs_r && !d.r) || (d.epi == Epi::Gelu && !d.z) ||
+      (d.epi == Epi::Accum && d.c_type != DType::F32) ||
+      (bf16_only && d.c_type != DType::BF16) || (needs_vec && !d.vec) ||
+      (d.epi == Epi::RowStats && !d.stats)) {
     g_gemm_err = "gemm_bf16_sm100: epilogue operands missing or wrong type";
     return cudaErrorInvalidValue;
   }
@@ -946,6 +1029,14 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.zs1 = d.zs1;
   p.alpha = d.alpha;
   p.epi = static_cast<int>(d.epi);
+  p.vec = d.vec;
+  p.vs0 = d.vs0;
+  p.vs1 = d.vs1;
+  p.stats = d.stats;
+  p.ss0 = d.ss0;
+  p.ss1 = d.ss1;
+  p.tile_n = tile_n;
+  p.nst = static_cast<int>((d.N + tile_n - 1) / tile_n);
   cudaError_t e = pair        ? launch_pair(p, a_mn, b_mn, stream)
                   : BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
                               : launch_bn<128>(p, a_mn, b_mn, stream);

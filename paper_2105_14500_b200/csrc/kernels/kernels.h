@@ -56,6 +56,12 @@ size_t k_ln_params_scratch_floats(int64_t rows, int64_t w);
 // ---- softmax (ref layers.cpp:44-74) ---------------------------------------
 // P = softmax_rows(S) with max subtraction; S fp32 [rows, L] (already scaled).
 void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cudaStream_t s);
+// lse[r] = log-sum-exp over the nst RowStats partials (max, sumexp) of row r.
+void k_lse_combine(const float* stats, int64_t rows, int nst, float* lse, cudaStream_t s);
+// delta[h][r] = sum_d dO[r, h*hd + d] * O[r, h*hd + d]  (= rowsum(P * dP),
+// the softmax-backward row term; rows S, heads H, row stride ld).
+void k_attn_delta(const void* dO, const void* O, DType t, int64_t ld, int64_t S, int64_t H,
+                  int64_t hd, float* delta, cudaStream_t s);
 // dS = scale * P * (dP - sum_c P*dP); dP fp32.
 void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t rows, int64_t L,
                    float scale, cudaStream_t s);

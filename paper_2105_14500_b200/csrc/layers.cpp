@@ -144,10 +144,18 @@ void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   const size_t esz = dtype_size(t);
   const void* z = wsget(c, tag + ".z", rows * 4 * hq * esz);
   const void* h = wsget(c, tag + ".h", rows * 4 * hq * esz);
-  float* dh = static_cast<float*>(wsget(c, "ff.dh", rows * 4 * hq * 4));
   void* dz = wsget(c, "ff.dz", rows * 4 * hq * esz);
-  nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s);
-  k_gelu_bwd(dh, z, dz, t, (size_t)rows * 4 * hq, s);  // ref layers.cpp:365
+  if (t == DType::BF16 && c.grid.q == 1) {
+    // no row reduce: fuse dz = dh * gelu'(z) into the NT epilogue
+    Out od = out_to(dz, t);
+    od.epi = Epi::DGelu;
+    od.r = z;
+    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, od, s);
+  } else {
+    float* dh = static_cast<float*>(wsget(c, "ff.dh", rows * 4 * hq * 4));
+    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s);
+    k_gelu_bwd(dh, z, dz, t, (size_t)rows * 4 * hq, s);  // ref layers.cpp:365
+  }
   nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, hq, out_to(dx_f32, DType::F32), s);
   weight_grad(c, t, h, rows, 4 * hq, dy, hq, g ? g->w_ff2 : nullptr, accumulate, s);
   weight_grad(c, t, x, rows, hq, dz, 4 * hq, g ? g->w_ff1 : nullptr, accumulate, s);
@@ -163,12 +171,48 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   void* qkv = wsget(c, tag + ".qkv", rows * ld * esz);
   void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
   void* o = wsget(c, tag + ".o", rows * hq * esz);
-  float* Sbuf = static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
+  const bool fused = t == DType::BF16;
+  float* Sbuf = fused ? nullptr : static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
   nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s);
   const float scale = (float)(1.0 / std::sqrt((double)hd));
   const char* base = static_cast<const char*>(qkv);
   for (int64_t smp = 0; smp < rd.samples_local; ++smp) {
     const char* q0 = base + (size_t)smp * S * ld * esz;
+    char* Ps = static_cast<char*>(P) + (size_t)smp * H * S * S * esz;
+    if (fused) {
+      // Two passes of the score GEMM, no fp32 S in HBM: (1) per-row
+      // (max, sum-exp) partials per column tile -> log-sum-exp; (2) the
+      // epilogue writes P = exp(scale*QK^T - lse) in bf16.
+      GemmDesc g;
+      g.M = S;
+      g.N = S;
+      g.nb0 = H;
+      g.in = t;
+      g.trans_b = true;
+      g.seg[0] = {q0, q0 + hd * esz, hd};
+      g.lda = ld;
+      g.as0 = 3 * hd;
+      g.ldb = ld;
+      g.bs0 = 3 * hd;
+      g.c_type = DType::BF16;
+      g.alpha = scale;
+      const int nst = gemm_bf16_stat_tiles(g);
+      float* st = static_cast<float*>(wsget(c, "attn.stats", (size_t)H * S * nst * 8));
+      float* lse = static_cast<float*>(wsget(c, "attn.lse", (size_t)H * S * 4));
+      g.epi = Epi::RowStats;
+      g.stats = st;
+      g.ss0 = S * nst;
+      run_gemm(g, s);
+      k_lse_combine(st, H * S, nst, lse, s);
+      g.epi = Epi::SoftmaxFwd;
+      g.stats = nullptr;
+      g.vec = lse;
+      g.vs0 = S;
+      g.c = Ps;
+      g.ldc = S;
+      g.cs0 = S * S;
+      run_gemm(g, s);
+    }
     // scores = Q K^T / sqrt(hd) for every local head (batched over heads)
     GemmDesc g;
     g.M = S;
@@ -186,9 +230,10 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g.ldc = S;
     g.cs0 = S * S;
     g.alpha = scale;
-    run_gemm(g, s);
-    char* Ps = static_cast<char*>(P) + (size_t)smp * H * S * S * esz;
-    k_softmax_fwd(Sbuf, Ps, t, H * S, S, s);
+    if (!fused) {
+      run_gemm(g, s);
+      k_softmax_fwd(Sbuf, Ps, t, H * S, S, s);
+    }
     // O = P V
     GemmDesc g2;
     g2.M = S;
@@ -222,7 +267,9 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   float* dout32 = static_cast<float*>(wsget(c, "attn.dout32", rows * hq * 4));
   void* dout = t == DType::F32 ? dout32 : wsget(c, "attn.dout", rows * hq * esz);
   void* dqkv = wsget(c, "attn.dqkv", rows * ld * esz);
-  float* dP = static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
+  const bool fused = t == DType::BF16;
+  float* dP = fused ? nullptr : static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
+  float* delta = fused ? static_cast<float*>(wsget(c, "attn.delta", (size_t)H * S * 4)) : nullptr;
   void* dS = wsget(c, "attn.dS", (size_t)H * S * S * esz);
   nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s);
   if (t != DType::F32) k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
@@ -233,12 +280,21 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     const char* do0 = static_cast<const char*>(dout) + (size_t)smp * S * hq * esz;
     char* dq0 = static_cast<char*>(dqkv) + (size_t)smp * S * ld * esz;
     const char* Ps = static_cast<const char*>(P) + (size_t)smp * H * S * S * esz;
-    // dP = dO V^T
+    // dP = dO V^T (fused path: straight to dS = scale * P * (dP - delta) with
+    // delta = rowsum(dO * O) = rowsum(P * dP), no fp32 dP in HBM)
     GemmDesc g1;
     g1.M = S; g1.N = S; g1.nb0 = H; g1.in = t; g1.trans_b = true;
     g1.seg[0] = {do0, q0 + 2 * hd * esz, hd};
     g1.lda = hq; g1.as0 = hd; g1.ldb = ld; g1.bs0 = 3 * hd;
-    g1.c = dP; g1.c_type = DType::F32; g1.ldc = S; g1.cs0 = S * S;
+    if (fused) {
+      const char* o0 = static_cast<const char*>(o) + (size_t)smp * S * hq * esz;
+      k_attn_delta(do0, o0, t, hq, S, H, hd, delta, s);
+      g1.c = dS; g1.c_type = t; g1.ldc = S; g1.cs0 = S * S;
+      g1.epi = Epi::SoftmaxBwd; g1.r = Ps; g1.ldr = S; g1.rs0 = S * S;
+      g1.vec = delta; g1.vs0 = S; g1.alpha = scale;
+    } else {
+      g1.c = dP; g1.c_type = DType::F32; g1.ldc = S; g1.cs0 = S * S;
+    }
     run_gemm(g1, s);
     // dV = P^T dO
     GemmDesc g2;
@@ -248,7 +304,7 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g2.c = dq0 + 2 * hd * esz; g2.c_type = t; g2.ldc = ld; g2.cs0 = 3 * hd;
     run_gemm(g2, s);
     // dS = P * (dP - rowsum(P*dP)) / sqrt(hd)
-    k_softmax_bwd(Ps, dP, dS, t, H * S, S, scale, s);
+    if (!fused) k_softmax_bwd(Ps, dP, dS, t, H * S, S, scale, s);
     // dQ = dS K
     GemmDesc g3;
     g3.M = S; g3.N = hd; g3.nb0 = H; g3.in = t;
