@@ -12,6 +12,7 @@
 // non-zero return code with the message available from ref_last_error().
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -160,6 +161,27 @@ __attribute__((visibility("default"))) int ref_tesseract_matmul(
     AlgoResult r = tesseract_matmul(to_matrix(a, ar, ac), to_matrix(b, br, bc), g, v);
     from_matrix(r.value, c);
     export_stats(r.stats, g.size(), stats_rank, stats_kind);
+  });
+}
+
+// tesseract_matmul with TesseractOptions::record_trace, trace rendered by
+// write_trace (runtime.cpp:90-96) into buf.
+__attribute__((visibility("default"))) int ref_tesseract_matmul_trace(
+    int variant, int q, int d, int allow, const double* a, int64_t ar, int64_t ac,
+    const double* b, int64_t br, int64_t bc, char* buf, int64_t cap) {
+  return guarded([&] {
+    GridSpec g(q, d, allow != 0);
+    MatmulVariant v = variant == 0 ? MatmulVariant::NN
+                      : variant == 1 ? MatmulVariant::NT
+                                     : MatmulVariant::TN;
+    TesseractOptions opt;
+    opt.record_trace = true;
+    AlgoResult r = tesseract_matmul(to_matrix(a, ar, ac), to_matrix(b, br, bc), g, v, opt);
+    std::ostringstream os;
+    write_trace(r.trace, os);
+    const std::string s = os.str();
+    std::strncpy(buf, s.c_str(), cap - 1);
+    buf[cap - 1] = 0;
   });
 }
 
