@@ -222,6 +222,12 @@ tess_status tess_layer_backward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtyp
                                 const void* dy, void* dx, tess_block_grads* grads,
                                 int accumulate, float* dbias, void* stream);
 
+/* Selects the forward-cache slot used by subsequent tess_layer_forward /
+ * tess_layer_backward calls on this context, so a stack of layers can keep
+ * one outstanding forward each (the reference keeps caller-owned
+ * BlockCacheRank objects, layers.hpp:114-119). Default 0. */
+tess_status tess_set_cache_slot(tess_ctx* ctx, int slot);
+
 /* ---------------------------------------------------------- global level
  * Whole-matrix operators with host fp64 buffers, mirroring the reference's
  * value-semantics API: partition -> per-rank SPMD (one host thread per rank,
@@ -251,6 +257,17 @@ tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q,
 /* ref: layers.hpp:195-197 layer_run; params/grads: 8 host fp64 arrays in
  * BlockParams order (w_qkv, w_proj, w_ff1, w_ff2, ln1_gain, ln1_bias,
  * ln2_gain, ln2_bias); grads may be NULL; dbias [hidden] for BiasAdd. */
+
+/* ref: layers.hpp:245-267 train_toy (the sharded half): `layers` Transformer
+ * blocks trained with MSE loss against `target` and plain SGD (learning rate
+ * lr) for `steps` steps on the [q,q,d] grid; the loss of every step (before
+ * its update) is written to losses[steps]. params: layers*8 host fp64 arrays
+ * (BlockParams order per layer). */
+tess_status tess_train_toy(const tess_layer_dims* dims, int layers, int steps, double lr, int q,
+                           int d, int allow_d_gt_q, tess_dtype compute, const double* x,
+                           const double* target, const double* const* params, double eps,
+                           double* losses, const int* devices, uint64_t* stats_rank,
+                           uint64_t* stats_kind);
 
 /* Number of kernels launched by this library on the calling process since
  * load (for the bench's gpu_launches claim). */

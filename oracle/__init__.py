@@ -214,6 +214,16 @@ class Oracle:
             raise ValueError("layer_run: bad dims")
         return {"y": y, "dx": dx, "grads": dict(zip(PARAM_NAMES, grads)), "dbias": dbias}
 
+    def train_toy(self, batch, seq, hidden, heads, layers, steps, lr, seed, eps=1e-5):
+        """Serial losses of train_toy (layers.cpp:947-1004)."""
+        L = self.L
+        L.tor_train_toy.argtypes = [C.c_int64] * 4 + [C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                                      C.c_double, _dp]
+        out = np.zeros(steps)
+        if L.tor_train_toy(batch, seq, hidden, heads, layers, steps, lr, seed, eps, _ptr(out)):
+            raise ValueError("train_toy: bad dims")
+        return out
+
     def layer_stats(self, op: str, q: int, d: int, batch: int, seq: int, hidden: int):
         p = d * q * q
         sr = np.zeros((p, 4), dtype=np.uint64)
@@ -250,6 +260,29 @@ class Reference:
              _u64p]
         L.ref_verify_suite.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.POINTER(C.c_double)]
+        L.ref_tesseract_matmul_trace.argtypes = [C.c_int] * 4 + [_dp, C.c_int64, C.c_int64,
+                                                                _dp, C.c_int64, C.c_int64,
+                                                                C.c_char_p, C.c_int64]
+
+    def train_toy(self, batch, seq, hidden, heads, layers, steps, lr, seed, q, d, allow=False):
+        """(serial_losses, dist_losses, max_divergence) of the reference train_toy."""
+        L = self.L
+        L.ref_train_toy.argtypes = [C.c_int64] * 4 + [C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                                      C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
+        s1, s2 = np.zeros(steps), np.zeros(steps)
+        md = C.c_double()
+        self._check(L.ref_train_toy(batch, seq, hidden, heads, layers, steps, lr, seed, q, d,
+                                    int(allow), _ptr(s1), _ptr(s2), C.byref(md)))
+        return s1, s2, md.value
+
+    def tesseract_matmul_trace(self, a, b, q, d, variant="nn", allow=False) -> str:
+        """write_trace() text of tesseract_matmul with record_trace."""
+        a, b = _f64(a), _f64(b)
+        buf = C.create_string_buffer(1 << 20)
+        self._check(self.L.ref_tesseract_matmul_trace(
+            {"nn": 0, "nt": 1, "tn": 2}[variant], q, d, int(allow), _ptr(a), a.shape[0],
+            a.shape[1], _ptr(b), b.shape[0], b.shape[1], buf, 1 << 20))
+        return buf.value.decode()
 
     @staticmethod
     def available() -> bool:

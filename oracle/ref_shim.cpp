@@ -185,6 +185,31 @@ __attribute__((visibility("default"))) int ref_tesseract_matmul_trace(
   });
 }
 
+// train_toy (layers.cpp:947-1036): paired serial / sharded SGD training.
+__attribute__((visibility("default"))) int ref_train_toy(
+    int64_t batch, int64_t seq, int64_t hidden, int64_t heads, int layers, int steps,
+    double lr, uint64_t seed, int q, int d, int allow, double* serial_losses,
+    double* dist_losses, double* max_div) {
+  return guarded([&] {
+    ToyConfig c;
+    c.dims = LayerDims{static_cast<int>(batch), static_cast<int>(seq), static_cast<int>(hidden),
+                       static_cast<int>(heads)};
+    c.layers = layers;
+    c.steps = steps;
+    c.lr = lr;
+    c.seed = seed;
+    c.q = q;
+    c.d = d;
+    c.allow_d_gt_q = allow != 0;
+    ToyTrainResult r = train_toy(c);
+    for (int i = 0; i < steps; ++i) {
+      serial_losses[i] = r.serial_loss[i];
+      dist_losses[i] = r.dist_loss[i];
+    }
+    *max_div = r.max_divergence;
+  });
+}
+
 __attribute__((visibility("default"))) int ref_tesseract_backward(
     int q, int d, int allow, const double* dc, const double* a, const double* b,
     int64_t m, int64_t k, int64_t n, double* da, double* db, uint64_t* stats_rank,

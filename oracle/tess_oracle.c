@@ -944,3 +944,112 @@ TOR_EXPORT void tor_layer_stats(int op, int q, int d, int64_t batch, int64_t seq
 #undef ATB
   meter_finish(mt, stats_kind);
 }
+
+/* ------------------------------------------------------------ toy training */
+/* Serial half of train_toy (layers.cpp:947-1004): `layers` pre-norm blocks,
+ * MSE loss sum(diff^2)/(rows*hidden) against a random target, dy =
+ * 2*diff/denom, plain SGD on every parameter (including LayerNorm vectors),
+ * seeds: x = stream(seed,0), target = stream(seed,1), block l params =
+ * stream(seed,100+l). Writes the loss of every step (before its update). */
+typedef struct {
+  double *xh1, *isv1, *ln1, *r1, *xh2, *isv2, *ln2, *y;
+  attc_t ac;
+  ffc_t fc;
+} blkc_t;
+
+static void block_fwd(const double* x, int64_t b, int64_t s, int64_t h, int64_t nh,
+                      const params_t* p, blkc_t* c) {
+  const int64_t T = b * s;
+  c->xh1 = dalloc(T * h); c->isv1 = dalloc(T); c->ln1 = dalloc(T * h);
+  c->r1 = dalloc(T * h); c->xh2 = dalloc(T * h); c->isv2 = dalloc(T);
+  c->ln2 = dalloc(T * h); c->y = dalloc(T * h);
+  double* att = dalloc(T * h);
+  double* ff = dalloc(T * h);
+  layernorm(x, T, h, p->ln1g, p->ln1b, p->eps, c->ln1, c->xh1, c->isv1);
+  attention(c->ln1, b, s, h, nh, p, att, &c->ac);
+  for (int64_t i = 0; i < T * h; ++i) c->r1[i] = x[i] + att[i];
+  layernorm(c->r1, T, h, p->ln2g, p->ln2b, p->eps, c->ln2, c->xh2, c->isv2);
+  feedforward(c->ln2, T, h, p, ff, &c->fc);
+  for (int64_t i = 0; i < T * h; ++i) c->y[i] = c->r1[i] + ff[i];
+  free(att);
+  free(ff);
+}
+
+static void block_bwd(const double* dy, int64_t b, int64_t s, int64_t h, int64_t nh,
+                      const params_t* p, blkc_t* c, double* dx, grads_t* g) {
+  const int64_t T = b * s;
+  double *dff = dalloc(T * h), *dln2 = dalloc(T * h), *dr1 = dalloc(T * h);
+  double *dat = dalloc(T * h), *dln1 = dalloc(T * h);
+  feedforward_backward(dy, T, h, p, &c->fc, dff, g);
+  layernorm_backward(dff, T, h, c->xh2, c->isv2, p->ln2g, dln2, g->ln2g, g->ln2b);
+  for (int64_t i = 0; i < T * h; ++i) dr1[i] = dy[i] + dln2[i];
+  attention_backward(dr1, b, s, h, nh, p, &c->ac, dat, g);
+  layernorm_backward(dat, T, h, c->xh1, c->isv1, p->ln1g, dln1, g->ln1g, g->ln1b);
+  for (int64_t i = 0; i < T * h; ++i) dx[i] = dr1[i] + dln1[i];
+  free(dff); free(dln2); free(dr1); free(dat); free(dln1);
+  free(c->xh1); free(c->isv1); free(c->ln1); free(c->r1); free(c->xh2); free(c->isv2);
+  free(c->ln2); free(c->y);
+  free(c->ac.x); free(c->ac.qkv); free(c->ac.o); free(c->ac.probs);
+  free(c->fc.x); free(c->fc.z); free(c->fc.h);
+}
+
+TOR_EXPORT int tor_train_toy(int64_t batch, int64_t seq, int64_t hidden, int64_t heads,
+                             int layers, int steps, double lr, uint64_t seed, double eps,
+                             double* losses) {
+  const int64_t T = batch * seq, h = hidden;
+  if (heads <= 0 || h % heads || layers < 1) return -1;
+  const double denom = (double)(T * h);
+  double* x = dalloc(T * h);
+  double* target = dalloc(T * h);
+  tor_random_matrix(seed, 0, T, h, x);
+  tor_random_matrix(seed, 1, T, h, target);
+  const int64_t sz[8] = {h * 3 * h, h * h, h * 4 * h, 4 * h * h, h, h, h, h};
+  double** W = (double**)calloc((size_t)layers * 8, sizeof(double*));
+  double** G = (double**)calloc((size_t)layers * 8, sizeof(double*));
+  for (int l = 0; l < layers; ++l) {
+    for (int k = 0; k < 8; ++k) {
+      W[l * 8 + k] = dalloc(sz[k]);
+      G[l * 8 + k] = dalloc(sz[k]);
+    }
+    tor_random_block_params(h, seed, 100 + (uint64_t)l, W[l * 8 + 0], W[l * 8 + 1],
+                            W[l * 8 + 2], W[l * 8 + 3], W[l * 8 + 4], W[l * 8 + 5],
+                            W[l * 8 + 6], W[l * 8 + 7]);
+  }
+  blkc_t* cache = (blkc_t*)calloc((size_t)layers, sizeof(blkc_t));
+  double* dy = dalloc(T * h);
+  double* dxb = dalloc(T * h);
+  for (int st = 0; st < steps; ++st) {
+    const double* cur = x;
+    for (int l = 0; l < layers; ++l) {
+      params_t p = {W[l * 8 + 0], W[l * 8 + 1], W[l * 8 + 2], W[l * 8 + 3], W[l * 8 + 4],
+                    W[l * 8 + 5], W[l * 8 + 6], W[l * 8 + 7], eps};
+      block_fwd(cur, batch, seq, h, heads, &p, &cache[l]);
+      cur = cache[l].y;
+    }
+    double loss = 0.0;
+    for (int64_t i = 0; i < T * h; ++i) {
+      const double dv = cur[i] - target[i];
+      loss += dv * dv;
+      dy[i] = 2.0 / denom * dv;
+    }
+    losses[st] = loss / denom;
+    for (int l = layers - 1; l >= 0; --l) {
+      params_t p = {W[l * 8 + 0], W[l * 8 + 1], W[l * 8 + 2], W[l * 8 + 3], W[l * 8 + 4],
+                    W[l * 8 + 5], W[l * 8 + 6], W[l * 8 + 7], eps};
+      for (int k = 0; k < 8; ++k) memset(G[l * 8 + k], 0, (size_t)sz[k] * sizeof(double));
+      grads_t g = {G[l * 8 + 0], G[l * 8 + 1], G[l * 8 + 2], G[l * 8 + 3],
+                   G[l * 8 + 4], G[l * 8 + 5], G[l * 8 + 6], G[l * 8 + 7]};
+      block_bwd(dy, batch, seq, h, heads, &p, &cache[l], dxb, &g);
+      memcpy(dy, dxb, (size_t)(T * h) * sizeof(double));
+    }
+    for (int l = 0; l < layers; ++l)
+      for (int k = 0; k < 8; ++k)
+        for (int64_t i = 0; i < sz[k]; ++i) W[l * 8 + k][i] -= lr * G[l * 8 + k][i];
+  }
+  for (int i = 0; i < layers * 8; ++i) {
+    free(W[i]);
+    free(G[i]);
+  }
+  free(W); free(G); free(cache); free(x); free(target); free(dy); free(dxb);
+  return 0;
+}

@@ -120,6 +120,9 @@ def _load() -> C.CDLL:
         "tess_last_error": ([], C.c_char_p),
         "tess_version": ([], C.c_char_p),
         "tess_kernel_launches": ([], C.c_uint64),
+        "tess_set_cache_slot": ([vp, i], i),
+        "tess_train_toy": ([C.POINTER(_LayerDimsC), i, i, C.c_double, i, i, i, i, dp, dp,
+                            C.POINTER(dp), C.c_double, dp, ip, u64p, u64p], i),
         "tess_profile_enable": ([i], i),
         "tess_profile_read": ([dp, dp, u64p], i),
         "tess_grid_check": ([i, i, i], i),
@@ -442,6 +445,32 @@ def layer_run(op: str, x, dy, params: Dict[str, np.ndarray], dims: LayerDims, gr
                               _dptr(y), _dptr(dx), G, _dptr(dbias),
                               _devices(devices, grid.size()), _u64(sr), _u64(sk)))
     return LayerRunResult(y, dx, dict(zip(PARAM_NAMES, grads)), dbias, CommStats(sr, sk))
+
+
+@dataclasses.dataclass
+class ToyTrainResult:
+    dist_loss: np.ndarray
+    stats: CommStats
+
+
+def train_toy(dims: LayerDims, layers: int, steps: int, lr: float, grid: GridSpec, x, target,
+              params: Sequence[Dict[str, np.ndarray]], dtype="f32", eps: float = 1e-5,
+              devices: Optional[Sequence[int]] = None) -> ToyTrainResult:
+    """Sharded half of train_toy (layers.cpp:947-1036): `layers` blocks, MSE
+    loss, SGD; returns the loss of every step (before its update)."""
+    x, target = _f64(x), _f64(target)
+    if len(params) != layers:
+        raise ValueError("one parameter dict per layer")
+    prm = [_f64(p[n]) for p in params for n in PARAM_NAMES]
+    P = (C.POINTER(C.c_double) * len(prm))(*[_dptr(t) for t in prm])
+    losses = np.zeros(steps)
+    sr, sk = _stats_bufs(grid.size())
+    dc = dims.c()
+    _check(lib.tess_train_toy(C.byref(dc), layers, steps, lr, grid.q(), grid.d(),
+                              int(grid.allow_d_gt_q), _dtype(dtype), _dptr(x), _dptr(target), P,
+                              eps, _dptr(losses), _devices(devices, grid.size()), _u64(sr),
+                              _u64(sk)))
+    return ToyTrainResult(losses, CommStats(sr, sk))
 
 
 # ------------------------------------------------------- per-rank contexts

@@ -221,6 +221,14 @@ tess_status tess_reset_comm_stats(tess_ctx* c) {
   });
 }
 
+tess_status tess_set_cache_slot(tess_ctx* c, int slot) {
+  return guarded([&] {
+    if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
+    if (slot < 0) fail(TESS_ERR_INVALID, "cache slot must be >= 0");
+    c->cache_slot = slot;
+  });
+}
+
 tess_status tess_set_trace(tess_ctx* c, int enable) {
   return guarded([&] {
     if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");

@@ -22,7 +22,11 @@ struct tess_ctx {
   uint64_t step = 0;  // collective sequence number (RankCtx::step_)
   std::vector<tess::TraceEvent> trace;
   std::unique_ptr<tess::Workspace> ws;
-  const void* fwd_x[5] = {};  // forward input per layer op, for the backward
+  // Forward caches are named by (cache slot, layer op); the slot lets several
+  // layers keep outstanding forwards (tess_set_cache_slot). The forward input
+  // of each (slot, op) is remembered for the backward.
+  int cache_slot = 0;
+  std::map<int, const void*> fwd_x;
 };
 
 namespace tess {

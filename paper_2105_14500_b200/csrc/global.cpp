@@ -6,6 +6,7 @@
 // in-process backend (the SpmdRunner of runtime.cpp:534-554) -> combine with
 // the reference's replica checks (shard.cpp:139-183, layers.cpp:184-228).
 // Inputs are rounded once to the compute dtype on the device.
+#include <array>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -424,6 +425,130 @@ tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q,
     if (dbias && op == TESS_OP_BIAS_ADD)
       for (int j = 0; j < q; ++j)
         for (int64_t cc = 0; cc < hq; ++cc) dbias[j * hq + cc] = dbs[g.rank_of({0, j, 0})][cc];
+    R.stats(sr, sk);
+  });
+}
+
+// ref layers.cpp:947-1036 (the sharded half of train_toy): `layers` blocks,
+// MSE loss with global_sum_rank (row, column, depth all-reduce of the local
+// sum, layers.cpp:519-526), backward through every block, plain SGD on every
+// parameter shard. In bf16 mode weights keep an fp32 master copy.
+tess_status tess_train_toy(const tess_layer_dims* dims, int layers, int steps, double lr, int q,
+                           int d, int allow, tess_dtype compute, const double* x,
+                           const double* target, const double* const* params, double eps,
+                           double* losses, const int* devices, uint64_t* sr, uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    if (!dims || !x || !target || !params || !losses || layers < 1 || steps < 0)
+      fail(TESS_ERR_INVALID, "train_toy: bad arguments");
+    Grid g(q, d, allow != 0);
+    const tess_layer_dims D = *dims;
+    Runner R(q, d, allow != 0, devices);
+    tess::RankDims rd0 = rank_dims(*R.ctx[0], D);
+    const int64_t h = D.hidden, T = (int64_t)D.batch * D.seq, hq = rd0.hq, rows = rd0.rows;
+    const double denom = (double)(T * h);
+    const int64_t wshape[4][2] = {{h, 3 * h}, {h, h}, {h, 4 * h}, {4 * h, h}};
+    DevMat dX, dT;
+    upload(dX, R.unique_devices(), x, (size_t)T * h, t);
+    upload(dT, R.unique_devices(), target, (size_t)T * h, t);
+    std::vector<std::unique_ptr<DevMat>> W32, LN;  // fp32 uploads of every parameter
+    for (int l = 0; l < layers; ++l) {
+      for (int i = 0; i < 4; ++i) {
+        W32.push_back(std::make_unique<DevMat>());
+        upload(*W32.back(), R.unique_devices(), params[l * 8 + i],
+               (size_t)(wshape[i][0] * wshape[i][1]), DType::F32);
+      }
+      for (int i = 0; i < 4; ++i) {
+        LN.push_back(std::make_unique<DevMat>());
+        upload(*LN.back(), R.unique_devices(), params[l * 8 + 4 + i], (size_t)h, DType::F32);
+      }
+    }
+    std::vector<double> rank0_losses(steps, 0.0);
+    R.run([&](Ctx& c, cudaStream_t s) {
+      const tess::RankDims rd = rank_dims(c, D);
+      const tess_dtype td = t == DType::F32 ? TESS_F32 : TESS_BF16;
+      const size_t act = (size_t)rows * hq * dtype_size(t);
+      void* lx = take_block(c, TESS_SCHEME_A, t, dX.on(c.device), T, h, "toy.x", s);
+      void* lt = take_block(c, TESS_SCHEME_A, t, dT.on(c.device), T, h, "toy.t", s);
+      const int64_t gsz[8] = {hq * 3 * hq, hq * hq, hq * 4 * hq, 4 * hq * hq, hq, hq, hq, hq};
+      std::vector<tess_block_shard> sh(layers);
+      std::vector<tess_block_grads> gr(layers);
+      std::vector<std::array<void*, 8>> wptr(layers);
+      std::vector<std::array<float*, 8>> master(layers);
+      for (int l = 0; l < layers; ++l) {
+        const std::string L = "toy.l" + std::to_string(l);
+        for (int i = 0; i < 4; ++i) {
+          float* m32 = static_cast<float*>(take_block(c, TESS_SCHEME_B, DType::F32,
+                                                      W32[l * 4 + i]->on(c.device), wshape[i][0],
+                                                      wshape[i][1], L + ".m" + std::to_string(i), s));
+          master[l][i] = m32;
+          if (t == DType::F32) {
+            wptr[l][i] = m32;
+            master[l][i] = nullptr;
+          } else {
+            wptr[l][i] = c.ws->get(L + ".w" + std::to_string(i), (size_t)gsz[i] * 2);
+            k_convert(m32, DType::F32, wptr[l][i], t, (size_t)gsz[i], s);
+          }
+        }
+        for (int i = 0; i < 4; ++i) {
+          float* v = static_cast<float*>(c.ws->get(L + ".ln" + std::to_string(i), hq * 4));
+          TESS_CUDA(cudaMemcpyAsync(v, static_cast<const float*>(LN[l * 4 + i]->on(c.device)) +
+                                           (int64_t)c.coord.j * hq,
+                                    hq * 4, cudaMemcpyDeviceToDevice, s));
+          wptr[l][4 + i] = v;
+          master[l][4 + i] = nullptr;
+        }
+        sh[l] = {wptr[l][0], wptr[l][1], wptr[l][2], wptr[l][3],
+                 static_cast<float*>(wptr[l][4]), static_cast<float*>(wptr[l][5]),
+                 static_cast<float*>(wptr[l][6]), static_cast<float*>(wptr[l][7]), eps};
+        float* gp[8];
+        for (int i = 0; i < 8; ++i)
+          gp[i] = static_cast<float*>(c.ws->get(L + ".g" + std::to_string(i), (size_t)gsz[i] * 4));
+        gr[l] = {gp[0], gp[1], gp[2], gp[3], gp[4], gp[5], gp[6], gp[7]};
+      }
+      double* dsum = static_cast<double*>(c.ws->get("toy.sum", 8));
+      double* scratch =
+          static_cast<double*>(c.ws->get("toy.scr", k_mse_scratch_doubles(rows * hq) * 8));
+      float* fsum = static_cast<float*>(c.ws->get("toy.fsum", 4));
+      void* dyb[2] = {c.ws->get("toy.dy0", act), c.ws->get("toy.dy1", act)};
+      for (int st = 0; st < steps; ++st) {
+        const void* cur = lx;
+        for (int l = 0; l < layers; ++l) {
+          c.cache_slot = l;
+          void* y = c.ws->get("toy.y" + std::to_string(l), act);
+          call(tess_layer_forward(&c, TESS_OP_BLOCK, td, &D, &sh[l], nullptr, cur, y, s));
+          cur = y;
+        }
+        k_mse_grad(cur, lt, t, (size_t)rows * hq, denom, dyb[0], dsum, scratch, s);
+        double local = 0;
+        TESS_CUDA(cudaMemcpyAsync(&local, dsum, 8, cudaMemcpyDeviceToHost, s));
+        TESS_CUDA(cudaStreamSynchronize(s));
+        const float lf = (float)local;
+        TESS_CUDA(cudaMemcpyAsync(fsum, &lf, 4, cudaMemcpyHostToDevice, s));
+        coll_allreduce(c, ROW, fsum, 1, s);  // global_sum_rank, layers.cpp:519-526
+        coll_allreduce(c, COL, fsum, 1, s);
+        coll_allreduce(c, DEPTH, fsum, 1, s);
+        float total = 0;
+        TESS_CUDA(cudaMemcpyAsync(&total, fsum, 4, cudaMemcpyDeviceToHost, s));
+        TESS_CUDA(cudaStreamSynchronize(s));
+        if (c.rank == 0) rank0_losses[st] = (double)total / denom;
+        int cur_dy = 0;
+        for (int l = layers - 1; l >= 0; --l) {
+          c.cache_slot = l;
+          call(tess_layer_backward(&c, TESS_OP_BLOCK, td, &D, &sh[l], dyb[cur_dy],
+                                   dyb[1 - cur_dy], &gr[l], 0, nullptr, s));
+          cur_dy = 1 - cur_dy;
+        }
+        for (int l = 0; l < layers; ++l) {
+          const float* gp[8] = {gr[l].w_qkv, gr[l].w_proj, gr[l].w_ff1, gr[l].w_ff2,
+                                gr[l].ln1_gain, gr[l].ln1_bias, gr[l].ln2_gain, gr[l].ln2_bias};
+          for (int i = 0; i < 8; ++i)
+            k_sgd(wptr[l][i], i < 4 ? t : DType::F32, master[l][i], gp[i], lr, (size_t)gsz[i], s);
+        }
+      }
+      c.cache_slot = 0;
+    });
+    for (int st = 0; st < steps; ++st) losses[st] = rank0_losses[st];
     R.stats(sr, sk);
   });
 }

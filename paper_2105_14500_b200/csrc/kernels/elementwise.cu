@@ -397,6 +397,50 @@ __global__ void attn_delta_kernel(const T* __restrict__ dO, const T* __restrict_
   if (lane == 0) delta[h * S + r] = acc;
 }
 
+// --------------------------------------------------------- toy training
+constexpr int kMseBlocks = 1024;
+
+template <typename T>
+__global__ void mse_grad_kernel(const T* __restrict__ y, const T* __restrict__ t, size_t n,
+                                float scale, T* __restrict__ dy, double* __restrict__ part) {
+  __shared__ double red[kBlock];
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float d = ldf<T>(y, i) - ldf<T>(t, i);
+    acc += (double)d * d;
+    stf<T>(dy, i, scale * d);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void sum_doubles_kernel(const double* part, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];  // fixed order: deterministic
+    *out = s;
+  }
+}
+
+template <typename T>
+__global__ void sgd_kernel(T* w, float* master, const float* g, float lr, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    if (master) {
+      master[i] -= lr * g[i];
+      stf<T>(w, i, master[i]);
+    } else {
+      stf<T>(w, i, ldf<T>(w, i) - lr * g[i]);
+    }
+  }
+}
+
 // ------------------------------------------------------- comm helper
 struct SumArgs {
   const float* in[8];
@@ -558,6 +602,25 @@ void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cu
   } else {
     TESS_DISPATCH(t, T, softmax_fwd_generic_kernel<T><<<g, 32 * warps, 0, s>>>(S, (T*)P, rows, L));
   }
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+size_t k_mse_scratch_doubles(size_t) { return kMseBlocks; }
+
+void k_mse_grad(const void* y, const void* target, DType t, size_t n, double denom, void* dy,
+                double* sum, double* scratch, cudaStream_t s) {
+  const float scale = (float)(2.0 / denom);
+  TESS_DISPATCH(t, T, mse_grad_kernel<T><<<kMseBlocks, kBlock, 0, s>>>(
+                          (const T*)y, (const T*)target, n, scale, (T*)dy, scratch));
+  sum_doubles_kernel<<<1, 32, 0, s>>>(scratch, kMseBlocks, sum);
+  count_launch(2);
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_sgd(void* w, DType t, float* master, const float* g, double lr, size_t n, cudaStream_t s) {
+  if (!n) return;
+  TESS_DISPATCH(t, T, sgd_kernel<T><<<grid_for(n), kBlock, 0, s>>>((T*)w, master, g, (float)lr, n));
   count_launch();
   TESS_CUDA(cudaGetLastError());
 }

@@ -615,12 +615,13 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
+template <int ST>
 struct Cfg2 {
   static constexpr int HALF = 128;  // rows of A / columns of B per CTA
   static constexpr int A_BYTES = HALF * BK * 2;
   static constexpr int B_BYTES = HALF * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = ST;
   static constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -641,10 +642,10 @@ __device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int&
   n0 = (in / gm) * 256;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int ST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
-  using C = Cfg2;
+  using C = Cfg2<ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -879,27 +880,37 @@ cudaError_t launch(const Params& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int ST>
 cudaError_t launch_2cta(const Params& p, cudaStream_t stream) {
-  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN>;
+  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg2::SMEM_BYTES);
+                                         Cfg2<ST>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int pairs = std::max(1, num_sms() / 2);
   const int grid = 2 * std::min(p.num_tiles, pairs);
-  kern<<<grid, kThreads, Cfg2::SMEM_BYTES, stream>>>(p);
+  kern<<<grid, kThreads, Cfg2<ST>::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 
+template <int ST>
+cudaError_t launch_pair_st(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
+  if (!a_mn && b_mn) return launch_2cta<false, true, ST>(p, s);
+  if (!a_mn && !b_mn) return launch_2cta<false, false, ST>(p, s);
+  if (a_mn && b_mn) return launch_2cta<true, true, ST>(p, s);
+  return launch_2cta<true, false, ST>(p, s);
+}
+
 cudaError_t launch_pair(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
-  if (!a_mn && b_mn) return launch_2cta<false, true>(p, s);
-  if (!a_mn && !b_mn) return launch_2cta<false, false>(p, s);
-  if (a_mn && b_mn) return launch_2cta<true, true>(p, s);
-  return launch_2cta<true, false>(p, s);
+  static int stages = 0;  // TESS_GEMM_STAGES=6|7 (smem ring depth of the pair kernel)
+  if (!stages) {
+    const char* e = std::getenv("TESS_GEMM_STAGES");
+    stages = (e && e[0] == '6') ? 6 : 7;
+  }
+  return stages == 6 ? launch_pair_st<6>(p, a_mn, b_mn, s) : launch_pair_st<7>(p, a_mn, b_mn, s);
 }
 
 bool use_pair_kernel(int64_t M, int64_t N) {

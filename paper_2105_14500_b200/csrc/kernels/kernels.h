@@ -28,6 +28,16 @@ void k_colsum(const void* x, DType t, int64_t rows, int64_t cols, float* out, fl
               cudaStream_t s);
 size_t k_colsum_scratch_floats(int64_t rows, int64_t cols);
 
+// ---- toy training (ref layers.cpp:947-1036) --------------------------------
+// dy = (2/denom) * (y - target); partial[b] = per-block sums of (y - target)^2
+// (fixed-order two-stage sum into *sum, fp64). y/target of type t.
+void k_mse_grad(const void* y, const void* target, DType t, size_t n, double denom, void* dy,
+                double* sum, double* scratch, cudaStream_t s);
+size_t k_mse_scratch_doubles(size_t n);
+// w -= lr * g (w of type t, g fp32; when master != nullptr the fp32 master copy
+// is updated and w is rewritten from it).
+void k_sgd(void* w, DType t, float* master, const float* g, double lr, size_t n, cudaStream_t s);
+
 // ---- LayerNorm (ref layers.cpp:242-345) -----------------------------------
 // Local partial statistics per row for the row-group all-reduce:
 // stats[r] = {sum x, sum (x - mu_r)^2, w * mu_r^2} with mu_r the local mean.

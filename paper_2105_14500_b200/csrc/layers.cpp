@@ -324,6 +324,10 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
 }
 
+std::string cache_tag(const Ctx& c, tess_layer_op op) {
+  return "s" + std::to_string(c.cache_slot) + ".op" + std::to_string((int)op);
+}
+
 // ------------------------------------------------------------- host staging
 bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -342,7 +346,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                    void* y_out, cudaStream_t s) {
   const int64_t rows = rd.rows, hq = rd.hq;
   const size_t act = (size_t)rows * hq * dtype_size(t);
-  const std::string tag = "op" + std::to_string((int)op);
+  const std::string tag = cache_tag(c, op);
   // Host buffers are staged through the context (x kept until backward).
   const void* x = x_in;
   if (!is_device_ptr(x_in)) {
@@ -395,7 +399,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   if (y != y_out) {
     TESS_CUDA(cudaMemcpyAsync(y_out, y, act, cudaMemcpyDeviceToHost, s));
   }
-  c.fwd_x[(int)op] = x;  // the backward needs the forward input
+  c.fwd_x[c.cache_slot * 8 + (int)op] = x;  // the backward needs the forward input
 }
 
 void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
@@ -403,9 +407,11 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                     tess_block_grads* g, bool accumulate, float* dbias, cudaStream_t s) {
   const int64_t rows = rd.rows, hq = rd.hq;
   const size_t act = (size_t)rows * hq * dtype_size(t);
-  const std::string tag = "op" + std::to_string((int)op);
-  const void* x = c.fwd_x[(int)op];
-  if (!x) fail(TESS_ERR_SHAPE, "layer backward: missing forward cache");
+  const std::string tag = cache_tag(c, op);
+  const auto it = c.fwd_x.find(c.cache_slot * 8 + (int)op);
+  if (it == c.fwd_x.end() || !it->second)
+    fail(TESS_ERR_SHAPE, "layer backward: missing forward cache");
+  const void* x = it->second;
   const void* dy = dy_in;
   if (!is_device_ptr(dy_in)) {
     void* ds = wsget(c, "stage.dy", act);

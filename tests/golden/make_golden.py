@@ -65,3 +65,23 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def traces():
+    """Reference write_trace() text for NN/NT/TN (record_trace), small shapes."""
+    import json
+    ref = oracle.Reference()
+    out = {}
+    for q, d, allow in [(2, 1, False), (2, 2, False), (1, 2, True)]:
+        m, n, r = 4 * q * d, 4 * q, 6 * q
+        a = ref.random_matrix(m, n, 14, 0)
+        for v, b in (("nn", ref.random_matrix(n, r, 14, 1)), ("nt", ref.random_matrix(r, n, 14, 1)),
+                     ("tn", ref.random_matrix(m, r, 14, 1))):
+            out[f"{v}_{q}{q}{d}"] = ref.tesseract_matmul_trace(a, b, q, d, v, allow=allow)
+    with open(os.path.join(HERE, "reference_traces.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("wrote", len(out), "traces")
+
+
+if __name__ == "__main__" and "--traces" in sys.argv:
+    traces()

@@ -255,3 +255,29 @@ def test_per_rank_contexts_threaded_nn(tess, orc):
     finally:
         for cx in ctxs:
             cx.close()
+
+
+@pytest.mark.parametrize("q,d,allow", [(2, 2, False), (1, 2, True), (1, 1, False)])
+def test_train_toy_fp32_tracks_reference(tess, orc, q, d, allow):
+    # ToyConfig defaults (layers.hpp:256): dims {4,4,8,2}, 2 layers, lr 0.05, seed 1234
+    b, s, h, nh, L, steps, lr, seed = 4, 4, 8, 2, 2, 12, 0.05, 1234
+    want = orc.train_toy(b, s, h, nh, L, steps, lr, seed)
+    x = f32r(orc.random_matrix(b * s, h, seed, 0))
+    tgt = f32r(orc.random_matrix(b * s, h, seed, 1))
+    P = [{k: f32r(v) for k, v in orc.random_block_params(h, seed, 100 + l).items()}
+         for l in range(L)]
+    res = tess.train_toy(tess.LayerDims(b, s, h, nh), L, steps, lr, tess.GridSpec(q, d, allow),
+                         x, tgt, P, dtype="f32")
+    assert np.abs(res.dist_loss - want).max() / want.max() <= 1e-5, (res.dist_loss, want)
+    assert res.dist_loss[-1] < res.dist_loss[0]  # it trains
+
+
+def test_train_toy_bf16(tess, orc):
+    b, s, h, nh, L, steps, lr, seed = 4, 64, 128, 4, 2, 4, 0.05, 99
+    want = orc.train_toy(b, s, h, nh, L, steps, lr, seed)
+    x = orc.random_matrix(b * s, h, seed, 0)
+    tgt = orc.random_matrix(b * s, h, seed, 1)
+    P = [orc.random_block_params(h, seed, 100 + l) for l in range(L)]
+    res = tess.train_toy(tess.LayerDims(b, s, h, nh), L, steps, lr, tess.GridSpec(2, 2), x, tgt,
+                         P, dtype="bf16")
+    assert np.abs(res.dist_loss - want).max() / want.max() <= 2e-2, (res.dist_loss, want)
