@@ -25,7 +25,9 @@ def main():
     dev = torch.device("cuda", 0)
     ctx = tess.init_local(tess.GridSpec(1, 1))[0]
     iters = int(os.environ.get("ITERS", "5"))
+    print("init ok", flush=True, file=sys.stderr)
     for name, v, sa, sb in SHAPES:
+        print("shape", name, flush=True, file=sys.stderr)
         a = torch.randn(sa, device=dev, dtype=torch.bfloat16)
         b = torch.randn(sb, device=dev, dtype=torch.bfloat16)
         if v == "nn":
@@ -55,6 +57,9 @@ def main():
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / iters
 
+        ours()
+        torch.cuda.synchronize()
+        print("first ours ok", flush=True, file=sys.stderr)
         res = {"shape": name, "M": M, "N": N, "K": K}
         for rnd in range(2):
             for label, fn in (("tess", ours), ("cublas", ref)):
@@ -62,8 +67,11 @@ def main():
                 res[f"{label}_tflops_{rnd}"] = 2.0 * M * N * K / ms / 1e9
         ours()
         torch.cuda.synchronize()
-        err = ((c.float() - ref().float()).norm() / ref().float().norm()).item()
-        res["rel_frob_vs_cublas"] = err
+        r = ref().float()
+        cf = c.float()
+        res["rel_frob_vs_cublas"] = ((cf - r).norm() / r.norm()).item()
+        res["max_abs_diff"] = (cf - r).abs().max().item()
+        res["frac_elems_differ"] = (cf != r).float().mean().item()
         print(json.dumps(res), flush=True)
         del a, b, c
         torch.cuda.empty_cache()
