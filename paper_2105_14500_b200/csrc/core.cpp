@@ -171,11 +171,38 @@ void profile_read(double* ms, double* flops, uint64_t* launches) {
   if (launches) *launches = g_prof.size();
 }
 
+// ------------------------------------------------------- comm stream
+cudaStream_t comm_stream(Ctx& c, cudaStream_t s) {
+  if (c.grid.size() == 1) return s;
+  if (!c.comm_s) {
+    int lo = 0, hi = 0;
+    TESS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    TESS_CUDA(cudaStreamCreateWithPriority(&c.comm_s, cudaStreamNonBlocking, hi));
+  }
+  return c.comm_s;
+}
+
+void stream_dep(Ctx& c, cudaStream_t from, cudaStream_t to) {
+  if (from == to) return;
+  if (c.ev_ring.empty()) {
+    c.ev_ring.resize(64);
+    for (auto& e : c.ev_ring) TESS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t e = c.ev_ring[c.ev_next++ % c.ev_ring.size()];
+  TESS_CUDA(cudaEventRecord(e, from));
+  TESS_CUDA(cudaStreamWaitEvent(to, e, 0));
+}
+
 // ------------------------------------------------------- collectives
 static void trace_event(Ctx& c, int kind, Family f, int root, uint64_t elements) {
   const uint64_t step = c.step++;
   if (c.trace_on)
     c.trace.push_back({c.rank, step, kind, static_cast<int>(f), root, elements * 8});
+}
+
+void coll_note_single(Ctx& c, int kind, Family f, int root, uint64_t elements) {
+  if (c.grid.group_size(f) != 1) fail(TESS_ERR_SPMD, "coll_note_single on a multi-rank group");
+  trace_event(c, kind, f, root, elements);
 }
 
 void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t elements,
@@ -199,3 +226,12 @@ void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s) {
 }
 
 }  // namespace tess
+
+tess_ctx::~tess_ctx() {
+  cudaSetDevice(device);
+  if (comm_s) {
+    cudaStreamSynchronize(comm_s);
+    cudaStreamDestroy(comm_s);
+  }
+  for (auto e : ev_ring) cudaEventDestroy(e);
+}

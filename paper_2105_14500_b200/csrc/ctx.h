@@ -27,6 +27,13 @@ struct tess_ctx {
   // of each (slot, op) is remembered for the backward.
   int cache_slot = 0;
   std::map<int, const void*> fwd_x;
+  // High-priority stream carrying this rank's collectives so they overlap
+  // the compute stream (created on first use; the compute stream itself when
+  // the grid has a single rank). Cross-stream ordering uses a ring of events.
+  cudaStream_t comm_s = nullptr;
+  std::vector<cudaEvent_t> ev_ring;
+  size_t ev_next = 0;
+  ~tess_ctx();
 };
 
 namespace tess {
@@ -41,5 +48,14 @@ void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t el
 void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, size_t n,
                  cudaStream_t s);
 void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s);
+
+// Records a collective whose group has a single member (no data moves): the
+// reference still counts the call in its trace step sequence.
+void coll_note_single(Ctx& c, int kind, Family f, int root, uint64_t elements);
+
+// The rank's comm stream (== s when the grid has one rank).
+cudaStream_t comm_stream(Ctx& c, cudaStream_t s);
+// Makes `to` wait for everything enqueued on `from` so far (no-op if equal).
+void stream_dep(Ctx& c, cudaStream_t from, cudaStream_t to);
 
 }  // namespace tess

@@ -72,7 +72,10 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
                  (uint64_t)rows * 2, true);
   if (c.trace_on) c.trace.push_back({c.rank, c.step, 2, ROW, 0, (uint64_t)rows * 2 * 8});
   c.step++;
-  c.comm->allreduce(ROW, stats, rows * 3, s);
+  cudaStream_t cs = comm_stream(c, s);
+  stream_dep(c, s, cs);
+  c.comm->allreduce(ROW, stats, rows * 3, cs);
+  stream_dep(c, cs, s);
   k_ln_apply(x, t, stats, rows, w, (double)rd.hidden_total, gain, bias, eps, y, mean, rstd, s);
 }
 
@@ -86,23 +89,29 @@ void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   const float* rstd = static_cast<const float*>(wsget(c, tag + ".rstd", rows * 4));
   float* stats = static_cast<float*>(wsget(c, "ln.bstats", rows * 2 * 4));
   k_ln_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, s);
-  coll_allreduce(c, ROW, stats, rows * 2, s);  // ref layers.cpp:305
+  cudaStream_t cs = comm_stream(c, s);
+  stream_dep(c, s, cs);
+  coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305
+  stream_dep(c, cs, s);
   k_ln_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w, (double)rd.hidden_total,
                  resid, tr, dx, tdx, s);
   if (dgain || dbias) {
-    float* packed = static_cast<float*>(wsget(c, "ln.packed", 2 * w * 4));
+    // per-LN buffers: the all-reduces and the gradient update stay on the
+    // comm stream (joined at the end of the layer backward)
+    float* packed = static_cast<float*>(wsget(c, tag + ".packed", 2 * w * 4));
     float* scratch =
         static_cast<float*>(wsget(c, "ln.pscratch", k_ln_params_scratch_floats(rows, w) * 4));
     k_ln_bwd_params(dy, tdy, x, t, mean, rstd, rows, w, packed, scratch, s);
-    coll_allreduce(c, COL, packed, 2 * w, s);    // ref layers.cpp:331
-    coll_allreduce(c, DEPTH, packed, 2 * w, s);  // ref layers.cpp:332
+    stream_dep(c, s, cs);
+    coll_allreduce(c, COL, packed, 2 * w, cs);    // ref layers.cpp:331
+    coll_allreduce(c, DEPTH, packed, 2 * w, cs);  // ref layers.cpp:332
     for (int k = 0; k < 2; ++k) {
       float* dst = k == 0 ? dgain : dbias;
       if (!dst) continue;
       if (accumulate)
-        k_add(dst, DType::F32, packed + k * w, DType::F32, dst, DType::F32, w, s);
+        k_add(dst, DType::F32, packed + k * w, DType::F32, dst, DType::F32, w, cs);
       else
-        TESS_CUDA(cudaMemcpyAsync(dst, packed + k * w, w * 4, cudaMemcpyDeviceToDevice, s));
+        TESS_CUDA(cudaMemcpyAsync(dst, packed + k * w, w * 4, cudaMemcpyDeviceToDevice, cs));
     }
   }
 }
@@ -118,13 +127,39 @@ Out grad_out(float* g, bool accumulate) {
 void weight_grad(Ctx& c, DType t, const void* a, int64_t ar, int64_t an, const void* b,
                  int64_t bn, float* g, bool accumulate, cudaStream_t s) {
   float* dst = g ? g : static_cast<float*>(wsget(c, "wgrad.discard", (size_t)an * bn * 4));
-  tn_product(c, t, a, ar, an, b, bn, true, grad_out(dst, g && accumulate), s);
+  // deferred: reduce + depth all-reduce + gradient write hide under the rest
+  // of the backward (layer_backward joins the comm stream before returning)
+  tn_product(c, t, a, ar, an, b, bn, true, grad_out(dst, g && accumulate), s, /*defer=*/true);
+}
+
+// Weight panels of a layer broadcast over the column group up front (they do
+// not depend on activations), for the NN (forward) / NT (backward) products.
+struct WeightPanels {
+  Panels qkv, proj, ff1, ff2;
+};
+
+WeightPanels prefetch_weights(Ctx& c, DType t, const RankDims& rd, const tess_block_shard& p,
+                              bool attn, bool ff, cudaStream_t s) {
+  WeightPanels w;
+  if (c.grid.q == 1) return w;
+  const int64_t hq = rd.hq;
+  const size_t e = dtype_size(t);
+  if (attn) {
+    w.qkv = prefetch_panels(c, COL, p.w_qkv, hq, 3 * hq, e, "pf.qkv", s);
+    w.proj = prefetch_panels(c, COL, p.w_proj, hq, hq, e, "pf.proj", s);
+  }
+  if (ff) {
+    w.ff1 = prefetch_panels(c, COL, p.w_ff1, hq, 4 * hq, e, "pf.ff1", s);
+    w.ff2 = prefetch_panels(c, COL, p.w_ff2, 4 * hq, hq, e, "pf.ff2", s);
+  }
+  return w;
 }
 
 // ----------------------------------------------------------------- FF
 // ref layers.cpp:349-360. Cache: x (caller-owned), z, h.
 void ff_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
-            const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s) {
+            const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s,
+            const WeightPanels& wp) {
   const int64_t rows = rd.rows, hq = rd.hq;
   const size_t esz = dtype_size(t);
   void* z = wsget(c, tag + ".z", rows * 4 * hq * esz);
@@ -132,14 +167,14 @@ void ff_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   Out o1 = out_to(h, t);
   o1.epi = Epi::Gelu;
   o1.z = z;
-  nn_product(c, t, x, rows, hq, p.w_ff1, 4 * hq, o1, s);
-  nn_product(c, t, h, rows, 4 * hq, p.w_ff2, hq, yout, s);
+  nn_product(c, t, x, rows, hq, p.w_ff1, 4 * hq, o1, s, &wp.ff1);
+  nn_product(c, t, h, rows, 4 * hq, p.w_ff2, hq, yout, s, &wp.ff2);
 }
 
 // ref layers.cpp:362-379: NT, gelu', NT, TN, TN. dx written fp32.
 void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
             const tess_block_shard& p, const void* x, const void* dy, float* dx_f32,
-            tess_block_grads* g, bool accumulate, cudaStream_t s) {
+            tess_block_grads* g, bool accumulate, cudaStream_t s, const WeightPanels& wp) {
   const int64_t rows = rd.rows, hq = rd.hq;
   const size_t esz = dtype_size(t);
   const void* z = wsget(c, tag + ".z", rows * 4 * hq * esz);
@@ -150,13 +185,13 @@ void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     Out od = out_to(dz, t);
     od.epi = Epi::DGelu;
     od.r = z;
-    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, od, s);
+    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, od, s, &wp.ff2);
   } else {
     float* dh = static_cast<float*>(wsget(c, "ff.dh", rows * 4 * hq * 4));
-    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s);
+    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s, &wp.ff2);
     k_gelu_bwd(dh, z, dz, t, (size_t)rows * 4 * hq, s);  // ref layers.cpp:365
   }
-  nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, hq, out_to(dx_f32, DType::F32), s);
+  nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, hq, out_to(dx_f32, DType::F32), s, &wp.ff1);
   weight_grad(c, t, h, rows, 4 * hq, dy, hq, g ? g->w_ff2 : nullptr, accumulate, s);
   weight_grad(c, t, x, rows, hq, dz, 4 * hq, g ? g->w_ff1 : nullptr, accumulate, s);
 }
@@ -164,7 +199,8 @@ void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
 // ----------------------------------------------------------- attention
 // ref layers.cpp:383-414.
 void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
-              const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s) {
+              const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s,
+              const WeightPanels& wp) {
   const int64_t rows = rd.rows, hq = rd.hq, S = rd.seq, hd = rd.head_dim;
   const int64_t H = rd.heads_local, ld = 3 * hq;
   const size_t esz = dtype_size(t);
@@ -173,7 +209,7 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   void* o = wsget(c, tag + ".o", rows * hq * esz);
   const bool fused = t == DType::BF16;
   float* Sbuf = fused ? nullptr : static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
-  nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s);
+  nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
   const float scale = (float)(1.0 / std::sqrt((double)hd));
   const char* base = static_cast<const char*>(qkv);
   for (int64_t smp = 0; smp < rd.samples_local; ++smp) {
@@ -251,13 +287,13 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g2.cs0 = hd;
     run_gemm(g2, s);
   }
-  nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s);
+  nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s, &wp.proj);
 }
 
 // ref layers.cpp:416-456: NT, TN, per-head local backward, NT, TN.
 void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
               const tess_block_shard& p, const void* x, const void* dy, float* dx_f32,
-              tess_block_grads* g, bool accumulate, cudaStream_t s) {
+              tess_block_grads* g, bool accumulate, cudaStream_t s, const WeightPanels& wp) {
   const int64_t rows = rd.rows, hq = rd.hq, S = rd.seq, hd = rd.head_dim;
   const int64_t H = rd.heads_local, ld = 3 * hq;
   const size_t esz = dtype_size(t);
@@ -271,7 +307,7 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   float* dP = fused ? nullptr : static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
   float* delta = fused ? static_cast<float*>(wsget(c, "attn.delta", (size_t)H * S * 4)) : nullptr;
   void* dS = wsget(c, "attn.dS", (size_t)H * S * S * esz);
-  nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s);
+  nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
   if (t != DType::F32) k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
   weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
   const float scale = (float)(1.0 / std::sqrt((double)hd));
@@ -320,7 +356,7 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g4.c = dq0 + hd * esz; g4.c_type = t; g4.ldc = ld; g4.cs0 = 3 * hd;
     run_gemm(g4, s);
   }
-  nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s);
+  nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s, &wp.qkv);
   weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
 }
 
@@ -355,15 +391,19 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     x = xs;
   }
   void* y = is_device_ptr(y_out) ? y_out : wsget(c, "stage.y", act);
+  // weight panels of the whole layer go out on the comm stream first
+  const WeightPanels wp =
+      prefetch_weights(c, t, rd, p, op == TESS_OP_ATTENTION || op == TESS_OP_BLOCK,
+                       op == TESS_OP_FEEDFORWARD || op == TESS_OP_BLOCK, s);
   switch (op) {
     case TESS_OP_LAYERNORM:
       ln_fwd(c, t, rd, tag + ".ln", x, p.ln1_gain, p.ln1_bias, p.eps, y, s);
       break;
     case TESS_OP_FEEDFORWARD:
-      ff_fwd(c, t, rd, tag + ".ff", p, x, out_to(y, t), s);
+      ff_fwd(c, t, rd, tag + ".ff", p, x, out_to(y, t), s, wp);
       break;
     case TESS_OP_ATTENTION:
-      attn_fwd(c, t, rd, tag + ".attn", p, x, out_to(y, t), s);
+      attn_fwd(c, t, rd, tag + ".attn", p, x, out_to(y, t), s, wp);
       break;
     case TESS_OP_BIAS_ADD: {
       // ref layers.cpp:491-503: bias lives at i == 0, column broadcast.
@@ -372,7 +412,10 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
         if (!bias_row0) fail(TESS_ERR_INVALID, "bias_add: bias_row0 required on i == 0 ranks");
         TESS_CUDA(cudaMemcpyAsync(b, bias_row0, hq * 4, cudaMemcpyDefault, s));
       }
-      coll_bcast(c, COL, 0, b, hq * 4, (uint64_t)hq, s);
+      cudaStream_t cs = comm_stream(c, s);
+      stream_dep(c, s, cs);
+      coll_bcast(c, COL, 0, b, hq * 4, (uint64_t)hq, cs);
+      stream_dep(c, cs, s);
       k_bias_add(x, b, y, t, rows, hq, s);
       break;
     }
@@ -385,17 +428,18 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       Out ao = out_to(r1, t);
       ao.epi = Epi::Resid;
       ao.r = x;
-      attn_fwd(c, t, rd, tag + ".attn", p, ln1, ao, s);
+      attn_fwd(c, t, rd, tag + ".attn", p, ln1, ao, s, wp);
       ln_fwd(c, t, rd, tag + ".ln2", r1, p.ln2_gain, p.ln2_bias, p.eps, ln2, s);
       Out fo = out_to(y, t);
       fo.epi = Epi::Resid;
       fo.r = r1;
-      ff_fwd(c, t, rd, tag + ".ff", p, ln2, fo, s);
+      ff_fwd(c, t, rd, tag + ".ff", p, ln2, fo, s, wp);
       break;
     }
     default:
       fail(TESS_ERR_INVALID, "unknown layer op");
   }
+  join_comm(c, s);
   if (y != y_out) {
     TESS_CUDA(cudaMemcpyAsync(y_out, y, act, cudaMemcpyDeviceToHost, s));
   }
@@ -419,6 +463,9 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     dy = ds;
   }
   void* dx = is_device_ptr(dx_out) ? dx_out : wsget(c, "stage.dx", act);
+  const WeightPanels wp =
+      prefetch_weights(c, t, rd, p, op == TESS_OP_ATTENTION || op == TESS_OP_BLOCK,
+                       op == TESS_OP_FEEDFORWARD || op == TESS_OP_BLOCK, s);
   switch (op) {
     case TESS_OP_LAYERNORM:
       ln_bwd(c, t, rd, tag + ".ln", dy, t, x, p.ln1_gain, nullptr, t, dx, t,
@@ -426,27 +473,29 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       break;
     case TESS_OP_FEEDFORWARD: {
       float* dxf = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
-      ff_bwd(c, t, rd, tag + ".ff", p, x, dy, dxf, g, accumulate, s);
+      ff_bwd(c, t, rd, tag + ".ff", p, x, dy, dxf, g, accumulate, s, wp);
       k_convert(dxf, DType::F32, dx, t, (size_t)rows * hq, s);
       break;
     }
     case TESS_OP_ATTENTION: {
       float* dxf = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
-      attn_bwd(c, t, rd, tag + ".attn", p, x, dy, dxf, g, accumulate, s);
+      attn_bwd(c, t, rd, tag + ".attn", p, x, dy, dxf, g, accumulate, s, wp);
       k_convert(dxf, DType::F32, dx, t, (size_t)rows * hq, s);
       break;
     }
     case TESS_OP_BIAS_ADD: {
       // ref layers.cpp:505-517
-      float* cs = static_cast<float*>(wsget(c, "bias.colsum", hq * 4));
+      float* csum = static_cast<float*>(wsget(c, "bias.colsum", hq * 4));
       float* scratch =
           static_cast<float*>(wsget(c, "bias.scratch", k_colsum_scratch_floats(rows, hq) * 4));
-      k_colsum(dy, t, rows, hq, cs, scratch, s);
+      k_colsum(dy, t, rows, hq, csum, scratch, s);
       float* red = static_cast<float*>(wsget(c, "bias.red", hq * 4));
-      coll_reduce(c, COL, 0, cs, red, hq, s);
+      cudaStream_t cs = comm_stream(c, s);
+      stream_dep(c, s, cs);
+      coll_reduce(c, COL, 0, csum, red, hq, cs);
       if (c.coord.i == 0) {
-        coll_allreduce(c, DEPTH, red, hq, s);
-        if (dbias) TESS_CUDA(cudaMemcpyAsync(dbias, red, hq * 4, cudaMemcpyDefault, s));
+        coll_allreduce(c, DEPTH, red, hq, cs);
+        if (dbias) TESS_CUDA(cudaMemcpyAsync(dbias, red, hq * 4, cudaMemcpyDefault, cs));
       }
       if (dx != dy) TESS_CUDA(cudaMemcpyAsync(dx, dy, act, cudaMemcpyDeviceToDevice, s));
       break;
@@ -457,12 +506,12 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       const void* ln1 = wsget(c, tag + ".ln1out", act);
       const void* ln2 = wsget(c, tag + ".ln2out", act);
       float* dff = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
-      ff_bwd(c, t, rd, tag + ".ff", p, ln2, dy, dff, g, accumulate, s);
+      ff_bwd(c, t, rd, tag + ".ff", p, ln2, dy, dff, g, accumulate, s, wp);
       void* dr1 = wsget(c, "blk.dr1", act);
       ln_bwd(c, t, rd, tag + ".ln2", dff, DType::F32, r1, p.ln2_gain, dy, t, dr1, t,
              g ? g->ln2_gain : nullptr, g ? g->ln2_bias : nullptr, accumulate, s);
       float* dat = static_cast<float*>(wsget(c, "blk.dattn32", (size_t)rows * hq * 4));
-      attn_bwd(c, t, rd, tag + ".attn", p, ln1, dr1, dat, g, accumulate, s);
+      attn_bwd(c, t, rd, tag + ".attn", p, ln1, dr1, dat, g, accumulate, s, wp);
       ln_bwd(c, t, rd, tag + ".ln1", dat, DType::F32, x, p.ln1_gain, dr1, t, dx, t,
              g ? g->ln1_gain : nullptr, g ? g->ln1_bias : nullptr, accumulate, s);
       break;
@@ -470,6 +519,8 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     default:
       fail(TESS_ERR_INVALID, "unknown layer op");
   }
+  // deferred weight/LN-gradient communication completes before we return
+  join_comm(c, s);
   if (dx != dx_out) TESS_CUDA(cudaMemcpyAsync(dx_out, dx, act, cudaMemcpyDeviceToHost, s));
 }
 

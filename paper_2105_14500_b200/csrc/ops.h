@@ -28,21 +28,38 @@ struct Out {
 // events on its stream (tess_profile_*).
 void run_gemm(const GemmDesc& g, cudaStream_t s);
 
+// The q panels of one operand after a family broadcast (slot t -> ptr[t]).
+struct Panels {
+  bool valid = false;
+  void* ptr[kMaxSegments] = {};
+};
+
+// Broadcasts every slot's panel of a weight-style operand over family f on
+// the comm stream ahead of its use (the weight panels of a whole layer do
+// not depend on activations), into workspace buffers named tag<t>.
+Panels prefetch_panels(Ctx& c, Family f, const void* local, int64_t rows, int64_t cols,
+                       size_t esz, const std::string& tag, cudaStream_t s);
+
+// Makes the compute stream wait for all collectives issued so far.
+void join_comm(Ctx& c, cudaStream_t s);
+
 // C[ar, bn] (op)= sum_t A(h,t) B(t,j); A panels row-broadcast, B panels
-// column-broadcast, all q panels accumulated in one tensor-memory
-// accumulator (one GEMM with q K-segments).
+// column-broadcast (or prefetched: bp), all q panels accumulated in one
+// tensor-memory accumulator (one GEMM with q K-segments).
 void nn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t ak, const void* b,
-                int64_t bn, const Out& out, cudaStream_t s);
+                int64_t bn, const Out& out, cudaStream_t s, const Panels* bp = nullptr);
 
 // C(h, j') = sum_j A(h,j) B(j',j)^T reduced over the row to slot j' (fp32).
 // out must be fp32 (Store or Accum) or bf16 Store.
 void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const void* b,
-                int64_t br, const Out& out, cudaStream_t s);
+                int64_t br, const Out& out, cudaStream_t s, const Panels* bp = nullptr);
 
 // C(i', j) = sum A(h,i')^T B(h,j) reduced down the column to slot i' and, if
-// sum_over_depth, all-reduced over depth. out fp32 Store or Accum.
+// sum_over_depth, all-reduced over depth. out fp32 Store or Accum. With
+// defer, the result is completed on the comm stream only (join_comm later).
 void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const void* b,
-                int64_t bn, bool sum_over_depth, const Out& out, cudaStream_t s);
+                int64_t bn, bool sum_over_depth, const Out& out, cudaStream_t s,
+                bool defer = false);
 
 // ------------------------------------------------------------------ layers
 struct RankDims {

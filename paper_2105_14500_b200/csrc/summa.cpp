@@ -1,15 +1,24 @@
 // SUMMA-in-depth products on the [q,q,d] grid (reference
 // proj/src/algorithms.cpp:34-76), re-expressed for B200:
+//  * every collective runs on the rank's high-priority comm stream, ordered
+//    against the compute stream with events, so communication overlaps the
+//    GEMMs around it;
 //  * NN: the q row/column panel broadcasts land in per-step panel buffers
-//    (a rank's own panel is used in place), then ONE GEMM with q K-segments
-//    accumulates every step in the same tensor-memory accumulator, instead of
-//    q GEMMs plus q-1 fp32 read-modify-writes of C (reference `add`,
-//    algorithms.cpp:42).
-//  * NT/TN: the fp32 partial of step t is reduced to its owner slot t; with
-//    q == 1 the GEMM writes straight into the caller's output with the
-//    caller's epilogue.
-// The collective sequence (kind, family, root, payload elements) is exactly
-// the reference's, so the host meter reproduces its CommStats.
+//    (a rank's own panel is used in place; weight panels may be prefetched
+//    for a whole layer, see prefetch_panels), then ONE GEMM with q
+//    K-segments accumulates every step in the same tensor-memory accumulator
+//    instead of q GEMMs plus q-1 fp32 read-modify-writes of C (reference
+//    `add`, algorithms.cpp:42);
+//  * NT/TN: the fp32 partial of step t is reduced to its owner slot t on the
+//    comm stream while the GEMM of step t+1 fills the other partial buffer
+//    (double buffering); with q == 1 the GEMM writes straight into the
+//    caller's output with the caller's epilogue;
+//  * TN with `defer`: the column reduce, depth all-reduce and the final
+//    write into the gradient stay on the comm stream; the caller joins the
+//    streams later (join_comm), so weight-gradient communication hides under
+//    the remaining backward compute.
+// The collective sequence (kind, family, root, payload elements) is the
+// reference's, so the host meter reproduces its CommStats.
 #include <string>
 
 #include "kernels/kernels.h"
@@ -41,7 +50,7 @@ void check_q(const Ctx& c) {
     fail(TESS_ERR_UNSUPPORTED, "q > " + std::to_string(kMaxSegments) + " not supported");
 }
 
-// Final write of an fp32 owned result into `out`.
+// Final write of an fp32 owned result into `out` (on stream s).
 void finish(const float* res, int64_t rows, int64_t cols, const Out& out, cudaStream_t s) {
   const int64_t ldc = out.ldc ? out.ldc : cols;
   if (ldc != cols) fail(TESS_ERR_UNSUPPORTED, "strided product outputs need q == 1");
@@ -57,93 +66,140 @@ void finish(const float* res, int64_t rows, int64_t cols, const Out& out, cudaSt
 
 }  // namespace
 
+void join_comm(Ctx& c, cudaStream_t s) { stream_dep(c, comm_stream(c, s), s); }
+
+Panels prefetch_panels(Ctx& c, Family f, const void* local, int64_t rows, int64_t cols,
+                       size_t esz, const std::string& tag, cudaStream_t s) {
+  Panels p;
+  const int q = c.grid.q;
+  check_q(c);
+  cudaStream_t cs = comm_stream(c, s);
+  stream_dep(c, s, cs);
+  const int mine = c.grid.slot_in_group(c.coord, f);
+  for (int t = 0; t < q; ++t) {
+    void* buf = t == mine ? const_cast<void*>(local)
+                          : c.ws->get(tag + std::to_string(t), rows * cols * esz);
+    coll_bcast(c, f, t, buf, rows * cols * esz, (uint64_t)(rows * cols), cs);
+    p.ptr[t] = buf;
+  }
+  p.valid = true;
+  return p;
+}
+
 void nn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t ak, const void* b,
-                int64_t bn, const Out& out, cudaStream_t s) {
+                int64_t bn, const Out& out, cudaStream_t s, const Panels* bp) {
   check_q(c);
   const int q = c.grid.q;
   const size_t esz = dtype_size(in);
+  cudaStream_t cs = comm_stream(c, s);
   GemmDesc g = base_desc(in, ar, bn, out);
   g.nseg = q;
   g.lda = ak;
   g.ldb = bn;
+  stream_dep(c, s, cs);  // A (and B) produced on the compute stream
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:39: row broadcast of A(h, t) from slot t
     void* at = c.coord.j == t ? const_cast<void*>(a)
                               : c.ws->get("nn.a" + std::to_string(t), ar * ak * esz);
-    coll_bcast(c, ROW, t, at, ar * ak * esz, (uint64_t)(ar * ak), s);
+    coll_bcast(c, ROW, t, at, ar * ak * esz, (uint64_t)(ar * ak), cs);
     // ref algorithms.cpp:40: column broadcast of B(t, j) from slot t
-    void* bt = c.coord.i == t ? const_cast<void*>(b)
-                              : c.ws->get("nn.b" + std::to_string(t), ak * bn * esz);
-    coll_bcast(c, COL, t, bt, ak * bn * esz, (uint64_t)(ak * bn), s);
+    void* bt;
+    if (bp && bp->valid) {
+      bt = bp->ptr[t];
+    } else {
+      bt = c.coord.i == t ? const_cast<void*>(b)
+                          : c.ws->get("nn.b" + std::to_string(t), ak * bn * esz);
+      coll_bcast(c, COL, t, bt, ak * bn * esz, (uint64_t)(ak * bn), cs);
+    }
     g.seg[t] = {at, bt, ak};
   }
+  stream_dep(c, cs, s);  // panels landed
   if (ar > 0 && bn > 0) run_gemm(g, s);
+  stream_dep(c, s, cs);  // panel buffers free for the next broadcasts
 }
 
 void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const void* b,
-                int64_t br, const Out& out, cudaStream_t s) {
+                int64_t br, const Out& out, cudaStream_t s, const Panels* bp) {
   check_q(c);
   const int q = c.grid.q;
   const size_t esz = dtype_size(in);
   const size_t n = (size_t)ar * br;
+  cudaStream_t cs = comm_stream(c, s);
   const bool direct = q == 1;
   const bool into_out = out.t == DType::F32 && out.epi == Epi::Store &&
                         (out.ldc == 0 || out.ldc == br);
   float* result = direct ? nullptr
                          : (into_out ? static_cast<float*>(out.c)
                                      : static_cast<float*>(c.ws->get("nt.r", n * 4)));
+  stream_dep(c, s, cs);
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:53: column broadcast of B(t, j)
-    void* bt = c.coord.i == t ? const_cast<void*>(b)
-                              : c.ws->get("nt.b", br * an * esz);
-    coll_bcast(c, COL, t, bt, br * an * esz, (uint64_t)(br * an), s);
-    if (direct) {
-      GemmDesc g = base_desc(in, ar, br, out);
-      g.trans_b = true;
-      g.lda = an;
-      g.ldb = an;
-      g.seg[0] = {a, bt, an};
-      if (ar > 0 && br > 0) run_gemm(g, s);
-      continue;
+    void* bt;
+    if (bp && bp->valid) {
+      bt = bp->ptr[t];
+    } else {
+      bt = c.coord.i == t ? const_cast<void*>(b)
+                          : c.ws->get("nt.b" + std::to_string(t & 1), br * an * esz);
+      coll_bcast(c, COL, t, bt, br * an * esz, (uint64_t)(br * an), cs);
     }
-    // ref algorithms.cpp:54-56: partial, then row reduce to slot t
-    float* partial = static_cast<float*>(c.ws->get("nt.p", n * 4));
-    Out po;
-    po.c = partial;
-    po.t = DType::F32;
-    GemmDesc g = base_desc(in, ar, br, po);
+    stream_dep(c, cs, s);  // B(t) landed; partial buffer t&1 released by reduce t-2
+    GemmDesc g;
+    if (direct) {
+      g = base_desc(in, ar, br, out);
+    } else {
+      Out po;
+      po.c = c.ws->get("nt.p" + std::to_string(t & 1), n * 4);
+      po.t = DType::F32;
+      g = base_desc(in, ar, br, po);
+    }
     g.trans_b = true;
     g.lda = an;
     g.ldb = an;
     g.seg[0] = {a, bt, an};
     if (ar > 0 && br > 0) run_gemm(g, s);
-    coll_reduce(c, ROW, t, partial, result, n, s);
+    if (direct) {
+      coll_note_single(c, 1, ROW, t, n);  // the reference's 1-member row reduce
+      continue;
+    }
+    stream_dep(c, s, cs);
+    // ref algorithms.cpp:55-56: row reduce of the partial to slot t (on the
+    // comm stream, overlapping the next step's GEMM)
+    coll_reduce(c, ROW, t, static_cast<float*>(g.c), result, n, cs);
   }
-  if (!direct && !into_out) finish(result, ar, br, out, s);
+  if (direct) return;
+  if (!into_out) finish(result, ar, br, out, cs);
+  stream_dep(c, cs, s);  // owned result ready for the consumer
 }
 
 void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const void* b,
-                int64_t bn, bool sum_over_depth, const Out& out, cudaStream_t s) {
+                int64_t bn, bool sum_over_depth, const Out& out, cudaStream_t s, bool defer) {
   check_q(c);
   const int q = c.grid.q;
   const size_t esz = dtype_size(in);
   const size_t n = (size_t)an * bn;
+  cudaStream_t cs = comm_stream(c, s);
   const bool depth = sum_over_depth;
   const bool direct = q == 1 && (!depth || c.grid.d == 1);
   const bool into_out = out.t == DType::F32 && out.epi == Epi::Store &&
                         (out.ldc == 0 || out.ldc == bn);
+  // A deferred result outlives this call on the comm stream: give it a buffer
+  // of its own (keyed by the destination) so the next product cannot race it.
+  const std::string rname = defer ? "tn.r." + std::to_string(reinterpret_cast<uintptr_t>(out.c))
+                                  : std::string("tn.r");
   float* result = direct ? nullptr
                          : (into_out ? static_cast<float*>(out.c)
-                                     : static_cast<float*>(c.ws->get("tn.r", n * 4)));
+                                     : static_cast<float*>(c.ws->get(rname, n * 4)));
+  stream_dep(c, s, cs);
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:67: row broadcast of A(h, t)
     void* at = c.coord.j == t ? const_cast<void*>(a)
-                              : c.ws->get("tn.a", ar * an * esz);
-    coll_bcast(c, ROW, t, at, ar * an * esz, (uint64_t)(ar * an), s);
+                              : c.ws->get("tn.a" + std::to_string(t & 1), ar * an * esz);
+    coll_bcast(c, ROW, t, at, ar * an * esz, (uint64_t)(ar * an), cs);
+    stream_dep(c, cs, s);
     Out po = out;
     if (!direct) {
       po = Out();
-      po.c = q == 1 ? result : c.ws->get("tn.p", n * 4);
+      po.c = q == 1 ? result : c.ws->get("tn.p" + std::to_string(t & 1), n * 4);
       po.t = DType::F32;
     }
     GemmDesc g = base_desc(in, an, bn, po);
@@ -158,13 +214,20 @@ void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
         TESS_CUDA(cudaMemsetAsync(po.c, 0, n * dtype_size(po.t), s));
       }
     }
+    if (q == 1) {
+      coll_note_single(c, 1, COL, t, n);  // the reference's 1-member column reduce
+      continue;
+    }
+    stream_dep(c, s, cs);
     // ref algorithms.cpp:69-70: column reduce of the partial to slot t
-    if (!direct && q > 1) coll_reduce(c, COL, t, static_cast<float*>(po.c), result, n, s);
+    coll_reduce(c, COL, t, static_cast<float*>(po.c), result, n, cs);
   }
   if (direct) return;
+  stream_dep(c, s, cs);  // (q == 1) the GEMM wrote `result` on the compute stream
   // ref algorithms.cpp:72-74: depth all-reduce of the layer partial
-  if (depth) coll_allreduce(c, DEPTH, result, n, s);
-  if (!into_out) finish(result, an, bn, out, s);
+  if (depth) coll_allreduce(c, DEPTH, result, n, cs);
+  if (!into_out) finish(result, an, bn, out, cs);
+  if (!defer) stream_dep(c, cs, s);
 }
 
 }  // namespace tess
