@@ -279,6 +279,9 @@ uint64_t tess_kernel_launches(void);
  * launch) and launch count since the last tess_profile_enable. */
 tess_status tess_profile_enable(int on);
 tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
+/* Per kernel instantiation since tess_profile_enable, as JSON text
+ * {"<kernel>": [device_ms, algorithmic_flops, launches], ...}. */
+tess_status tess_profile_json(char* buf, size_t cap, size_t* needed);
 
 #ifdef __cplusplus
 }

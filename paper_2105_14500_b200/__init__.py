@@ -124,6 +124,7 @@ def _load() -> C.CDLL:
         "tess_train_toy": ([C.POINTER(_LayerDimsC), i, i, C.c_double, i, i, i, i, dp, dp,
                             C.POINTER(dp), C.c_double, dp, ip, u64p, u64p], i),
         "tess_profile_enable": ([i], i),
+        "tess_profile_json": ([C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], i),
         "tess_profile_read": ([dp, dp, u64p], i),
         "tess_grid_check": ([i, i, i], i),
         "tess_grid_parse": ([C.c_char_p, i, ip, ip], i),
@@ -584,6 +585,16 @@ def kernel_launches() -> int:
 def profile_enable(on: bool = True) -> None:
     """Bracket every local GEMM launch with CUDA events on its stream."""
     _check(lib.tess_profile_enable(int(on)))
+
+
+def profile_kernels() -> dict:
+    """{kernel: (device_ms, flops, launches)} per GEMM kernel instantiation."""
+    import json
+    need = C.c_size_t()
+    _check(lib.tess_profile_json(None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _check(lib.tess_profile_json(buf, need.value, None))
+    return {k: tuple(v) for k, v in json.loads(buf.value.decode()).items()}
 
 
 def profile_read():

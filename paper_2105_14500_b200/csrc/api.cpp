@@ -74,6 +74,18 @@ tess_status tess_profile_enable(int on) {
   return guarded([&] { profile_enable(on != 0); });
 }
 
+tess_status tess_profile_json(char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    const std::string s = profile_json();
+    if (needed) *needed = s.size() + 1;
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
 tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches) {
   return guarded([&] { profile_read(gemm_ms, gemm_flops, gemm_launches); });
 }

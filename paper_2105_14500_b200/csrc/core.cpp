@@ -1,5 +1,7 @@
 // Grid geometry (reference proj/src/grid.cpp), workspace, metered collectives.
+#include <array>
 #include <charconv>
+#include <cstdio>
 #include <mutex>
 
 #include "ctx.h"
@@ -115,6 +117,7 @@ struct ProfRec {
   cudaEvent_t a, b;
   double flops;
   int device;
+  std::string kernel;
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
@@ -122,9 +125,10 @@ std::vector<ProfRec> g_prof;
 }  // namespace
 
 void run_gemm(const GemmDesc& g, cudaStream_t s) {
-  ProfRec rec{nullptr, nullptr, 0.0, 0};
+  ProfRec rec{nullptr, nullptr, 0.0, 0, std::string()};
   const bool prof = g_prof_on;
   if (prof) {
+    rec.kernel = gemm_kernel_name(g);
     cudaGetDevice(&rec.device);
     TESS_CUDA(cudaEventCreate(&rec.a));
     TESS_CUDA(cudaEventCreate(&rec.b));
@@ -169,6 +173,31 @@ void profile_read(double* ms, double* flops, uint64_t* launches) {
   if (ms) *ms = t;
   if (flops) *flops = f;
   if (launches) *launches = g_prof.size();
+}
+
+// Per kernel instantiation: {"name": [ms, flops, launches], ...}
+std::string profile_json() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  std::map<std::string, std::array<double, 3>> agg;
+  for (auto& r : g_prof) {
+    cudaSetDevice(r.device);
+    TESS_CUDA(cudaEventSynchronize(r.b));
+    float m = 0;
+    TESS_CUDA(cudaEventElapsedTime(&m, r.a, r.b));
+    auto& a = agg[r.kernel];
+    a[0] += m;
+    a[1] += r.flops;
+    a[2] += 1;
+  }
+  std::string s = "{";
+  for (auto& kv : agg) {
+    if (s.size() > 1) s += ", ";
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "\"%s\": [%.6f, %.6e, %.0f]", kv.first.c_str(), kv.second[0],
+                  kv.second[1], kv.second[2]);
+    s += buf;
+  }
+  return s + "}";
 }
 
 // ------------------------------------------------------- comm stream

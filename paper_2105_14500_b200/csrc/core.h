@@ -43,6 +43,7 @@ enum Family { ROW = 0, COL = 1, DEPTH = 2 };
 // GEMM launch profiling (CUDA events around every local GEMM launch).
 void profile_enable(bool on);
 void profile_read(double* ms, double* flops, uint64_t* launches);
+std::string profile_json();
 
 struct Coord {
   int i = 0, j = 0, k = 0;

@@ -17,6 +17,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <string>
+
 namespace tess {
 
 enum class DType : int { F32 = 0, BF16 = 1, F64 = 2 };
@@ -73,6 +75,9 @@ struct GemmDesc {
   float* stats = nullptr;
   int64_t ss0 = 0, ss1 = 0;
 };
+
+// Name of the kernel instantiation gemm() launches for d (profiling).
+std::string gemm_kernel_name(const GemmDesc& d);
 
 // Column-tile width the tcgen05 dispatcher uses for d (RowStats layout).
 int gemm_bf16_tile_n(const GemmDesc& d);

@@ -938,6 +938,17 @@ thread_local std::string g_gemm_err;
 
 const char* gemm_last_error() { return g_gemm_err.c_str(); }
 
+std::string gemm_kernel_name(const GemmDesc& d) {
+  const int am = d.trans_a ? 1 : 0, bm = d.trans_b ? 0 : 1;
+  if (d.in == DType::F32)
+    return "gemm_f32_kernel<" + std::to_string((int)d.trans_a) + "," +
+           std::to_string((int)d.trans_b) + ">";
+  if (sm100::use_pair_kernel(d.M, d.N))
+    return "gemm_bf16_2cta_kernel<" + std::to_string(am) + "," + std::to_string(bm) + ">";
+  return "gemm_bf16_kernel<" + std::to_string(d.N > 128 ? 256 : 128) + "," + std::to_string(am) +
+         "," + std::to_string(bm) + ">";
+}
+
 int gemm_bf16_tile_n(const GemmDesc& d) {
   return (sm100::use_pair_kernel(d.M, d.N) || d.N > 128) ? 256 : 128;
 }
