@@ -269,6 +269,25 @@ tess_status tess_train_toy(const tess_layer_dims* dims, int layers, int steps, d
                            double* losses, const int* devices, uint64_t* stats_rank,
                            uint64_t* stats_kind);
 
+/* ref: algorithms.hpp:82-85 megatron_1d_linear -- the 1-D tensor-parallel
+ * comparator (config 5): on a [1,1,p] line grid W1 [xc, w1c] is column-split,
+ * W2 [w1c, w2c] row-split, every rank computes X W1_k W2_k and one all-reduce
+ * sums the partials; out [xr, w2c] (fp32 result before any cast). */
+tess_status tess_megatron_1d_linear(int p, tess_dtype compute, const double* x, int64_t xr,
+                                    int64_t xc, const double* w1, int64_t w1r, int64_t w1c,
+                                    const double* w2, int64_t w2r, int64_t w2c, double* out,
+                                    const int* devices, uint64_t* stats_rank,
+                                    uint64_t* stats_kind);
+
+/* ref: matrix.cpp:352-370 checksum (FNV-1a over rows, cols and the
+ * little-endian doubles; printed by the reference as "fnv1a:%x"). */
+uint64_t tess_checksum(int64_t rows, int64_t cols, const double* values);
+/* ref: matrix.cpp:244-350 save_matrix / load_matrix: ".csv" paths are CSV
+ * (shortest round-trip text), anything else is the "TMX1" binary format.
+ * tess_load_matrix with values == NULL returns only the shape. */
+tess_status tess_save_matrix(const char* path, int64_t rows, int64_t cols, const double* values);
+tess_status tess_load_matrix(const char* path, int64_t* rows, int64_t* cols, double* values);
+
 /* Number of kernels launched by this library on the calling process since
  * load (for the bench's gpu_launches claim). */
 uint64_t tess_kernel_launches(void);

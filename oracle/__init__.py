@@ -214,6 +214,18 @@ class Oracle:
             raise ValueError("layer_run: bad dims")
         return {"y": y, "dx": dx, "grads": dict(zip(PARAM_NAMES, grads)), "dbias": dbias}
 
+    def megatron_1d_linear(self, x, w1, w2, p):
+        """megatron_1d_linear (algorithms.cpp:244-265)."""
+        x, w1, w2 = _f64(x), _f64(w1), _f64(w2)
+        L = self.L
+        L.tor_megatron_1d_linear.argtypes = [C.c_int, _dp, C.c_int64, C.c_int64, _dp, C.c_int64,
+                                             _dp, C.c_int64, _dp]
+        out = np.zeros((x.shape[0], w2.shape[1]))
+        if L.tor_megatron_1d_linear(p, _ptr(x), x.shape[0], x.shape[1], _ptr(w1), w1.shape[1],
+                                    _ptr(w2), w2.shape[1], _ptr(out)):
+            raise ValueError("megatron_1d_linear: divisibility")
+        return out
+
     def train_toy(self, batch, seq, hidden, heads, layers, steps, lr, seed, eps=1e-5):
         """Serial losses of train_toy (layers.cpp:947-1004)."""
         L = self.L
@@ -274,6 +286,25 @@ class Reference:
         self._check(L.ref_train_toy(batch, seq, hidden, heads, layers, steps, lr, seed, q, d,
                                     int(allow), _ptr(s1), _ptr(s2), C.byref(md)))
         return s1, s2, md.value
+
+    def megatron_1d_linear(self, x, w1, w2, p):
+        x, w1, w2 = _f64(x), _f64(w1), _f64(w2)
+        self.L.ref_megatron_1d_linear.argtypes = [C.c_int, _dp, C.c_int64, C.c_int64, _dp,
+                                                  C.c_int64, _dp, C.c_int64, _dp, _u64p, _u64p]
+        out = np.zeros((x.shape[0], w2.shape[1]))
+        sr = np.zeros((p, 4), dtype=np.uint64)
+        sk = np.zeros((5, 2), dtype=np.uint64)
+        self._check(self.L.ref_megatron_1d_linear(p, _ptr(x), x.shape[0], x.shape[1], _ptr(w1),
+                                                  w1.shape[1], _ptr(w2), w2.shape[1], _ptr(out),
+                                                  sr.ctypes.data_as(_u64p),
+                                                  sk.ctypes.data_as(_u64p)))
+        return out, sr, sk
+
+    def file_checksum(self, path: str) -> str:
+        self.L.ref_file_checksum.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        buf = C.create_string_buffer(64)
+        self._check(self.L.ref_file_checksum(path.encode(), buf, 64))
+        return buf.value.decode()
 
     def tesseract_matmul_trace(self, a, b, q, d, variant="nn", allow=False) -> str:
         """write_trace() text of tesseract_matmul with record_trace."""

@@ -185,6 +185,27 @@ __attribute__((visibility("default"))) int ref_tesseract_matmul_trace(
   });
 }
 
+__attribute__((visibility("default"))) int ref_megatron_1d_linear(
+    int p, const double* x, int64_t xr, int64_t xc, const double* w1, int64_t w1c,
+    const double* w2, int64_t w2c, double* out, uint64_t* stats_rank, uint64_t* stats_kind) {
+  return guarded([&] {
+    AlgoResult r = megatron_1d_linear(to_matrix(x, xr, xc), to_matrix(w1, xc, w1c),
+                                      to_matrix(w2, w1c, w2c), p);
+    from_matrix(r.value, out);
+    export_stats(r.stats, p, stats_rank, stats_kind);
+  });
+}
+
+// load_matrix + checksum of a file written by the B200 library
+__attribute__((visibility("default"))) int ref_file_checksum(const char* path, char* out,
+                                                             int cap) {
+  return guarded([&] {
+    std::string s = checksum(load_matrix(path));
+    std::strncpy(out, s.c_str(), cap - 1);
+    out[cap - 1] = 0;
+  });
+}
+
 // train_toy (layers.cpp:947-1036): paired serial / sharded SGD training.
 __attribute__((visibility("default"))) int ref_train_toy(
     int64_t batch, int64_t seq, int64_t hidden, int64_t heads, int layers, int steps,

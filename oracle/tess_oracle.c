@@ -1053,3 +1053,30 @@ TOR_EXPORT int tor_train_toy(int64_t batch, int64_t seq, int64_t hidden, int64_t
   free(W); free(G); free(cache); free(x); free(target); free(dy); free(dxb);
   return 0;
 }
+
+/* megatron_1d_linear, algorithms.cpp:244-265: line grid [1,1,p]; W1 split by
+ * column blocks (Column1D, shard.cpp:110-118), W2 by row blocks (Row1D,
+ * shard.cpp:119-127); out = sum_k (X W1_k) W2_k with the slot-ascending sum of
+ * the depth all-reduce. Returns -1 on shape / divisibility errors. */
+TOR_EXPORT int tor_megatron_1d_linear(int p, const double* x, int64_t xr, int64_t xc,
+                                      const double* w1, int64_t w1c, const double* w2,
+                                      int64_t w2c, double* out) {
+  if (p < 1 || w1c % p) return -1;
+  const int64_t kb = w1c / p;
+  double* b1 = dalloc(xc * kb);
+  double* h = dalloc(xr * kb);
+  double* part = dalloc(xr * w2c);
+  memset(out, 0, (size_t)(xr * w2c) * sizeof(double));
+  for (int k = 0; k < p; ++k) {
+    for (int64_t r = 0; r < xc; ++r)
+      memcpy(b1 + r * kb, w1 + r * w1c + (int64_t)k * kb, (size_t)kb * sizeof(double));
+    tor_matmul(x, xr, xc, b1, kb, h);
+    tor_matmul(h, xr, kb, w2 + (int64_t)k * kb * w2c, w2c, part);
+    if (k == 0) memcpy(out, part, (size_t)(xr * w2c) * sizeof(double));
+    else vadd(out, part, xr * w2c);
+  }
+  free(b1);
+  free(h);
+  free(part);
+  return 0;
+}

@@ -121,6 +121,11 @@ def _load() -> C.CDLL:
         "tess_version": ([], C.c_char_p),
         "tess_kernel_launches": ([], C.c_uint64),
         "tess_set_cache_slot": ([vp, i], i),
+        "tess_megatron_1d_linear": ([i, i, dp, i64, i64, dp, i64, i64, dp, i64, i64, dp, ip, u64p,
+                                     u64p], i),
+        "tess_checksum": ([i64, i64, dp], C.c_uint64),
+        "tess_save_matrix": ([C.c_char_p, i64, i64, dp], i),
+        "tess_load_matrix": ([C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), dp], i),
         "tess_train_toy": ([C.POINTER(_LayerDimsC), i, i, C.c_double, i, i, i, i, dp, dp,
                             C.POINTER(dp), C.c_double, dp, ip, u64p, u64p], i),
         "tess_profile_enable": ([i], i),
@@ -446,6 +451,47 @@ def layer_run(op: str, x, dy, params: Dict[str, np.ndarray], dims: LayerDims, gr
                               _dptr(y), _dptr(dx), G, _dptr(dbias),
                               _devices(devices, grid.size()), _u64(sr), _u64(sk)))
     return LayerRunResult(y, dx, dict(zip(PARAM_NAMES, grads)), dbias, CommStats(sr, sk))
+
+
+def summa_matmul(a, b, q: int, dtype="f32", devices=None) -> AlgoResult:
+    """SUMMA on a [q,q] mesh (algorithms.cpp:105-118) = the [q,q,1] Tesseract NN."""
+    return tesseract_matmul(a, b, GridSpec(q, 1), "nn", dtype=dtype, devices=devices)
+
+
+def megatron_1d_linear(x, w1, w2, p: int, dtype="f32",
+                       devices: Optional[Sequence[int]] = None) -> AlgoResult:
+    """1-D TP pair of linear layers (algorithms.cpp:244-265): X W1_k W2_k, all-reduce."""
+    x, w1, w2 = _f64(x), _f64(w1), _f64(w2)
+    out = np.zeros((x.shape[0], w2.shape[1]))
+    sr, sk = _stats_bufs(p)
+    _check(lib.tess_megatron_1d_linear(p, _dtype(dtype), _dptr(x), *x.shape, _dptr(w1), *w1.shape,
+                                       _dptr(w2), *w2.shape, _dptr(out), _devices(devices, p),
+                                       _u64(sr), _u64(sk)))
+    return AlgoResult(out, CommStats(sr, sk))
+
+
+def checksum(m) -> str:
+    """FNV-1a fingerprint in the reference's format (matrix.cpp:352-370)."""
+    m = _f64(m)
+    if m.ndim == 1:
+        m = m.reshape(1, -1)
+    return "fnv1a:%x" % lib.tess_checksum(m.shape[0], m.shape[1], _dptr(m))
+
+
+def save_matrix(m, path: str) -> None:
+    """TMX1 binary, or CSV for '.csv' paths (matrix.cpp:244-350)."""
+    m = _f64(m)
+    if m.ndim == 1:
+        m = m.reshape(1, -1)
+    _check(lib.tess_save_matrix(path.encode(), m.shape[0], m.shape[1], _dptr(m)))
+
+
+def load_matrix(path: str) -> np.ndarray:
+    r, c = C.c_int64(), C.c_int64()
+    _check(lib.tess_load_matrix(path.encode(), C.byref(r), C.byref(c), None))
+    out = np.zeros((r.value, c.value))
+    _check(lib.tess_load_matrix(path.encode(), C.byref(r), C.byref(c), _dptr(out)))
+    return out
 
 
 @dataclasses.dataclass

@@ -2,6 +2,7 @@
 #include <array>
 #include <charconv>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "ctx.h"
@@ -129,6 +130,17 @@ void run_gemm(const GemmDesc& g, cudaStream_t s) {
   const bool prof = g_prof_on;
   if (prof) {
     rec.kernel = gemm_kernel_name(g);
+    static const bool detail = [] {
+      const char* e = std::getenv("TESS_PROFILE_DETAIL");
+      return e && e[0] == '1';
+    }();
+    if (detail) {
+      double kk = 0;
+      for (int i = 0; i < g.nseg; ++i) kk += (double)g.seg[i].k;
+      rec.kernel += " M=" + std::to_string(g.M) + " N=" + std::to_string(g.N) +
+                    " K=" + std::to_string((long long)kk) +
+                    " b=" + std::to_string(g.nb0 * g.nb1) + " epi=" + std::to_string((int)g.epi);
+    }
     cudaGetDevice(&rec.device);
     TESS_CUDA(cudaEventCreate(&rec.a));
     TESS_CUDA(cudaEventCreate(&rec.b));

@@ -553,4 +553,63 @@ tess_status tess_train_toy(const tess_layer_dims* dims, int layers, int steps, d
   });
 }
 
+// ref algorithms.cpp:244-265 (megatron_1d_linear): the 1-D tensor-parallel
+// pair of linear layers on a [1,1,p] line grid -- W1 column-split (Column1D),
+// W2 row-split (Row1D), every rank computes X W1_k W2_k (two local GEMMs) and
+// one all-reduce over the single depth group sums the partial outputs. The
+// 1-D comparator of BASELINE config 5.
+tess_status tess_megatron_1d_linear(int p, tess_dtype compute, const double* x, int64_t xr,
+                                    int64_t xc, const double* w1, int64_t w1r, int64_t w1c,
+                                    const double* w2, int64_t w2r, int64_t w2c, double* out,
+                                    const int* devices, uint64_t* sr, uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    if (xc != w1r)
+      fail(TESS_ERR_SHAPE, "megatron_1d_linear: A.cols (" + std::to_string(xc) +
+                               ") != B.rows (" + std::to_string(w1r) + ")");
+    if (w1c != w2r)
+      fail(TESS_ERR_SHAPE, "megatron_1d_linear: A.cols (" + std::to_string(w1c) +
+                               ") != B.rows (" + std::to_string(w2r) + ")");
+    if (p < 1 || w1c % p != 0)
+      fail(TESS_ERR_DIVISIBILITY, "megatron_1d_linear: inner width (" + std::to_string(w1c) +
+                                      ") not divisible by p (" + std::to_string(p) + ")");
+    const int64_t kb = w1c / p;
+    Runner R(1, p, true, devices);
+    DevMat dX, dW1, dW2;
+    upload(dX, R.unique_devices(), x, (size_t)(xr * xc), t);
+    upload(dW1, R.unique_devices(), w1, (size_t)(w1r * w1c), t);
+    upload(dW2, R.unique_devices(), w2, (size_t)(w2r * w2c), t);
+    std::vector<float> res;
+    R.run([&](Ctx& c, cudaStream_t s) {
+      const size_t e = dtype_size(t);
+      const int k = c.coord.k;  // line grid: the rank index is the depth slot
+      void* b1 = c.ws->get("mg.w1", (size_t)w1r * kb * e);
+      TESS_CUDA(cudaMemcpy2DAsync(b1, kb * e,
+                                  static_cast<const char*>(dW1.on(c.device)) + (size_t)k * kb * e,
+                                  w1c * e, kb * e, w1r, cudaMemcpyDeviceToDevice, s));
+      void* b2 = c.ws->get("mg.w2", (size_t)kb * w2c * e);
+      TESS_CUDA(cudaMemcpyAsync(b2,
+                                static_cast<const char*>(dW2.on(c.device)) + (size_t)k * kb * w2c * e,
+                                (size_t)kb * w2c * e, cudaMemcpyDeviceToDevice, s));
+      void* h = c.ws->get("mg.h", (size_t)xr * kb * e);
+      float* part = static_cast<float*>(c.ws->get("mg.part", (size_t)xr * w2c * 4));
+      GemmDesc g1;
+      g1.M = xr; g1.N = kb; g1.in = t; g1.seg[0] = {dX.on(c.device), b1, xc};
+      g1.lda = xc; g1.ldb = kb; g1.c = h; g1.c_type = t; g1.ldc = kb;
+      run_gemm(g1, s);
+      GemmDesc g2;
+      g2.M = xr; g2.N = w2c; g2.in = t; g2.seg[0] = {h, b2, kb};
+      g2.lda = kb; g2.ldb = w2c; g2.c = part; g2.c_type = DType::F32; g2.ldc = w2c;
+      run_gemm(g2, s);
+      cudaStream_t cs = comm_stream(c, s);
+      stream_dep(c, s, cs);
+      coll_allreduce(c, DEPTH, part, (size_t)xr * w2c, cs);  // ref algorithms.cpp:261
+      stream_dep(c, cs, s);
+      if (c.rank == 0) res = fetch(part, (size_t)xr * w2c, DType::F32, s);
+    });
+    for (size_t i = 0; i < res.size(); ++i) out[i] = res[i];
+    R.stats(sr, sk);
+  });
+}
+
 }  // extern "C"

@@ -281,3 +281,29 @@ def test_train_toy_bf16(tess, orc):
     res = tess.train_toy(tess.LayerDims(b, s, h, nh), L, steps, lr, tess.GridSpec(2, 2), x, tgt,
                          P, dtype="bf16")
     assert np.abs(res.dist_loss - want).max() / want.max() <= 2e-2, (res.dist_loss, want)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_megatron_1d_linear(tess, orc, p, dtype):
+    rnd = f32r if dtype == "f32" else bf16r
+    x = rnd(orc.random_matrix(64, 128, 15, 0))
+    w1 = rnd(orc.random_matrix(128, 256, 15, 1))
+    w2 = rnd(orc.random_matrix(256, 96, 15, 2))
+    want = orc.megatron_1d_linear(x, w1, w2, p)
+    got = tess.megatron_1d_linear(x, w1, w2, p, dtype=dtype)
+    if dtype == "f32":
+        assert rel_diff(got.value, want) <= 1e-5
+    else:  # the X W1_k intermediate is stored in bf16 between the two GEMMs
+        assert frob(got.value, want) <= 1e-2
+    # one all-reduce of [64, 96] over the p-rank line (flat counting)
+    assert got.stats.by_kind("all_reduce") == ((2 * (p - 1), 2 * (p - 1) * 64 * 96) if p > 1
+                                               else (0, 0))
+
+
+def test_summa_is_tesseract_d1(tess, orc):
+    a = f32r(orc.random_matrix(96, 64, 16, 0))
+    b = f32r(orc.random_matrix(64, 80, 16, 1))
+    want, _, sk = orc.tesseract_matmul(a, b, 2, 1, "nn")
+    got = tess.summa_matmul(a, b, 2)
+    assert rel_diff(got.value, want) <= 1e-5 and (got.stats.per_kind == sk).all()
