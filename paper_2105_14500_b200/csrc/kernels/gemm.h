@@ -81,10 +81,8 @@ std::string gemm_kernel_name(const GemmDesc& d);
 
 // Column-tile width the tcgen05 dispatcher uses for d (RowStats layout).
 int gemm_bf16_tile_n(const GemmDesc& d);
-inline int gemm_bf16_stat_tiles(const GemmDesc& d) {
-  const int t = gemm_bf16_tile_n(d);
-  return static_cast<int>((d.N + t - 1) / t);
-}
+// RowStats partials per row (column tiles x epilogue warps per lane quadrant).
+int gemm_bf16_stat_tiles(const GemmDesc& d);
 
 // bf16 inputs on 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
 cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream);

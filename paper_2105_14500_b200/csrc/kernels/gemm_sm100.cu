@@ -41,7 +41,8 @@ namespace sm100 {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 2 non-epilogue + 8 epilogue warps
+constexpr int kEpiHalves = 2;   // epilogue warps per TMEM lane quadrant
 
 struct Params {
   CUtensorMap tma_a[kMaxSegments];
@@ -239,165 +240,163 @@ __device__ __forceinline__ T* batch_ptr(void* base, long long s0, long long s1,
   return reinterpret_cast<T*>(base) + s0 * b0 + s1 * b1;
 }
 
-// Writes 32 consecutive columns [n, n+32) of one output row.
-__device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0,
-                                                   int b1, int m, int n,
-                                                   const uint32_t (&acc)[32]) {
+// ---- epilogue ---------------------------------------------------------------
+// Every loop runs over exactly 32 columns with compile-time indices (tail
+// columns are predicated), so the per-thread chunk arrays stay in registers.
+__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* row, int nvalid, float (&o)[32]) {
+  if (nvalid == 32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = *reinterpret_cast<const uint4*>(row + q * 8);
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[q * 8 + e] = __bfloat162float(b[e]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = j < nvalid ? __bfloat162float(row[j]) : 0.f;
+  }
+}
+
+__device__ __forceinline__ void load32_f32(const float* row, int nvalid, float (&o)[32]) {
+  if (nvalid == 32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 f = *reinterpret_cast<const float4*>(row + q * 4);
+      o[q * 4 + 0] = f.x;
+      o[q * 4 + 1] = f.y;
+      o[q * 4 + 2] = f.z;
+      o[q * 4 + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = j < nvalid ? row[j] : 0.f;
+  }
+}
+
+__device__ __forceinline__ void store32_bf16(__nv_bfloat16* row, int nvalid, const float (&v)[32]) {
+  if (nvalid == 32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 out;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        o2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(row + q * 8) = out;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) row[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+__device__ __forceinline__ void store32_f32(float* row, int nvalid, const float (&v)[32]) {
+  if (nvalid == 32) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(row + q * 4) =
+          make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) row[j] = v[j];
+  }
+}
+
+// Epilogue input other than the accumulator: R (Resid / DGelu / SoftmaxBwd)
+// or the old C (Accum). Loaded BEFORE the tcgen05.ld of the chunk so the
+// global-memory latency overlaps the TMEM read.
+__device__ __forceinline__ bool epi_needs_aux(int epi) {
+  return epi == (int)Epi::Resid || epi == (int)Epi::DGelu || epi == (int)Epi::SoftmaxBwd ||
+         epi == (int)Epi::Accum;
+}
+
+__device__ __forceinline__ void epilogue_load_aux(const Params& p, int b0, int b1, int m, int n,
+                                                  int nvalid, float (&aux)[32]) {
+  if (p.epi == (int)Epi::Accum) {
+    load32_f32(batch_ptr<float>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n, nvalid,
+               aux);
+  } else if (p.c_bf16) {
+    load32_bf16(batch_ptr<__nv_bfloat16>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
+                    (long long)m * p.ldr + n,
+                nvalid, aux);
+  } else {
+    load32_f32(batch_ptr<float>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
+                   (long long)m * p.ldr + n,
+               nvalid, aux);
+  }
+}
+
+// Writes 32 consecutive columns [n, n + nvalid) of one output row.
+__device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int b1, int m, int n,
+                                                   int nvalid, const uint32_t (&acc)[32],
+                                                   const float (&aux)[32]) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * p.alpha;
   const int epi = p.epi;
-  const bool full = (n + 32 <= p.N);
-  const int nvalid = full ? 32 : max(0, p.N - n);
-
-  if (p.c_bf16) {
-    __nv_bfloat16* crow =
-        batch_ptr<__nv_bfloat16>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n;
-    if (epi == (int)Epi::Resid) {
-      const __nv_bfloat16* rrow =
-          batch_ptr<__nv_bfloat16>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
-          (long long)m * p.ldr + n;
-      if (full) {
+  if (epi == (int)Epi::Resid || epi == (int)Epi::Accum) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 rv = *reinterpret_cast<const uint4*>(rrow + q * 8);
-          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+    for (int j = 0; j < 32; ++j) v[j] += aux[j];
+  } else if (epi == (int)Epi::DGelu) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[q * 8 + e] += __bfloat162float(rb[e]);
-        }
-      } else {
-        for (int j = 0; j < nvalid; ++j) v[j] += __bfloat162float(rrow[j]);
-      }
-    } else if (epi == (int)Epi::DGelu || epi == (int)Epi::SoftmaxBwd) {
-      // R = z (DGelu) or P (SoftmaxBwd), bf16 with C's layout
-      const __nv_bfloat16* rrow =
-          batch_ptr<__nv_bfloat16>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
-          (long long)m * p.ldr + n;
-      float rv[32];
-      if (full) {
+    for (int j = 0; j < 32; ++j) v[j] *= gelu_erf_grad(aux[j]);
+  } else if (epi == (int)Epi::SoftmaxBwd) {
+    const float d = p.alpha * p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u = *reinterpret_cast<const uint4*>(rrow + q * 8);
-          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&u);
+    for (int j = 0; j < 32; ++j) v[j] = aux[j] * (v[j] - d);
+  } else if (epi == (int)Epi::SoftmaxFwd) {
+    const float lse = p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) rv[q * 8 + e] = __bfloat162float(rb[e]);
-        }
-      } else {
+    for (int j = 0; j < 32; ++j) v[j] = __expf(v[j] - lse);
+  } else if (epi == (int)Epi::Gelu) {
+    if (p.c_bf16)
+      store32_bf16(batch_ptr<__nv_bfloat16>(p.z, p.zs0, p.zs1, b0, b1) + (long long)m * p.ldz + n,
+                   nvalid, v);
+    else
+      store32_f32(batch_ptr<float>(p.z, p.zs0, p.zs1, b0, b1) + (long long)m * p.ldz + n, nvalid,
+                  v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) rv[j] = j < nvalid ? __bfloat162float(rrow[j]) : 0.f;
-      }
-      if (epi == (int)Epi::DGelu) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= gelu_erf_grad(rv[j]);
-      } else {
-        const float d = p.alpha * p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = rv[j] * (v[j] - d);
-      }
-    } else if (epi == (int)Epi::SoftmaxFwd) {
-      const float lse = p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __expf(v[j] - lse);
-    } else if (epi == (int)Epi::Gelu) {
-      __nv_bfloat16* zrow = batch_ptr<__nv_bfloat16>(p.z, p.zs0, p.zs1, b0, b1) +
-                            (long long)m * p.ldz + n;
-      if (full) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 out;
-          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            o2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
-          *reinterpret_cast<uint4*>(zrow + q * 8) = out;
-        }
-      } else {
-        for (int j = 0; j < nvalid; ++j) zrow[j] = __float2bfloat16_rn(v[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-    }
-    if (full) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 out;
-        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&out);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          o2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
-        *reinterpret_cast<uint4*>(crow + q * 8) = out;
-      }
-    } else {
-      for (int j = 0; j < nvalid; ++j) crow[j] = __float2bfloat16_rn(v[j]);
-    }
-  } else {
-    float* crow = batch_ptr<float>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n;
-    if (epi == (int)Epi::Accum) {
-      if (full) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = *reinterpret_cast<const float4*>(crow + q * 4);
-          v[q * 4 + 0] += o.x;
-          v[q * 4 + 1] += o.y;
-          v[q * 4 + 2] += o.z;
-          v[q * 4 + 3] += o.w;
-        }
-      } else {
-        for (int j = 0; j < nvalid; ++j) v[j] += crow[j];
-      }
-    } else if (epi == (int)Epi::Resid) {
-      const float* rrow = batch_ptr<float>(const_cast<void*>(p.r), p.rs0, p.rs1, b0, b1) +
-                          (long long)m * p.ldr + n;
-      if (full) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = *reinterpret_cast<const float4*>(rrow + q * 4);
-          v[q * 4 + 0] += o.x;
-          v[q * 4 + 1] += o.y;
-          v[q * 4 + 2] += o.z;
-          v[q * 4 + 3] += o.w;
-        }
-      } else {
-        for (int j = 0; j < nvalid; ++j) v[j] += rrow[j];
-      }
-    } else if (epi == (int)Epi::Gelu) {
-      float* zrow = batch_ptr<float>(p.z, p.zs0, p.zs1, b0, b1) + (long long)m * p.ldz + n;
-      for (int j = 0; j < nvalid; ++j) zrow[j] = v[j];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-    }
-    if (full) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<float4*>(crow + q * 4) =
-            make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
-    } else {
-      for (int j = 0; j < nvalid; ++j) crow[j] = v[j];
-    }
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
   }
+  if (p.c_bf16)
+    store32_bf16(batch_ptr<__nv_bfloat16>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n,
+                 nvalid, v);
+  else
+    store32_f32(batch_ptr<float>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n, nvalid, v);
 }
 
-// Epilogue of one accumulator tile row (this thread's row m, columns
-// [n0, n0 + width)): tcgen05.ld 32 columns at a time, then either the
-// elementwise epilogue or the RowStats reduction.
+// Epilogue of this thread's accumulator row m over the 32-column chunks
+// half, half + kEpiHalves, ... of the tile [n0, n0 + width): two epilogue
+// warps share each TMEM lane quadrant and split its chunks. RowStats writes
+// one (max, sum-exp) partial per (tile, half).
 __device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, int m, int n0,
-                                              int width, uint32_t trow) {
+                                              int width, uint32_t trow, int half) {
   const bool stats = p.epi == (int)Epi::RowStats;
+  const bool aux_in = epi_needs_aux(p.epi);
   float rmax = -INFINITY, rsum = 0.f;
 #pragma unroll 1
-  for (int c = 0; c < width / 32; ++c) {
+  for (int c = half; c < width / 32; c += kEpiHalves) {
+    const int n = n0 + c * 32;
+    const bool valid = m < p.M && n < p.N;
+    const int nvalid = valid ? min(32, p.N - n) : 0;
+    float aux[32];
+    if (aux_in && valid) epilogue_load_aux(p, b0, b1, m, n, nvalid, aux);
     uint32_t r[32];
     tmem_ld32(trow + c * 32, r);  // warp-collective: executed by every lane
-    const int n = n0 + c * 32;
-    if (m < p.M && n < p.N) {
+    if (valid) {
       if (stats)
-        row_stats_chunk(r, p.alpha, min(32, p.N - n), rmax, rsum);
+        row_stats_chunk(r, p.alpha, nvalid, rmax, rsum);
       else
-        epilogue_row_chunk(p, b0, b1, m, n, r);
+        epilogue_row_chunk(p, b0, b1, m, n, nvalid, r, aux);
     }
   }
   if (stats && m < p.M && n0 < p.N) {
-    float* dst = p.stats + (p.ss0 * b0 + p.ss1 * b1 + (long long)m * p.nst + n0 / p.tile_n) * 2;
+    float* dst = p.stats +
+                 (p.ss0 * b0 + p.ss1 * b1 + (long long)m * p.nst + (n0 / p.tile_n) * kEpiHalves +
+                  half) * 2;
     dst[0] = rmax;
     dst[1] = rsum;
   }
@@ -426,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], 4 * kEpiHalves);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < p.nseg; ++s) {
@@ -539,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      epilogue_tile(p, b0, b1, m, n0, BN, trow);
+      epilogue_tile(p, b0, b1, m, n0, BN, trow, (warp - 2) / 4);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -668,7 +667,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy used)
+      mbar_init(&tempty_bar[a], 8 * kEpiHalves);  // epilogue warps of both CTAs (leader's copy used)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < p.nseg; ++s) {
@@ -779,7 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int m = m0 + (int)cta * C::HALF + quad * 32 + lane;
       const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
-      epilogue_tile(p, b0, b1, m, n0, 256, trow);
+      epilogue_tile(p, b0, b1, m, n0, 256, trow, (warp - 2) / 4);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
@@ -949,6 +948,11 @@ std::string gemm_kernel_name(const GemmDesc& d) {
          "," + std::to_string(bm) + ">";
 }
 
+int gemm_bf16_stat_tiles(const GemmDesc& d) {
+  const int t = gemm_bf16_tile_n(d);
+  return static_cast<int>((d.N + t - 1) / t) * sm100::kEpiHalves;
+}
+
 int gemm_bf16_tile_n(const GemmDesc& d) {
   return (sm100::use_pair_kernel(d.M, d.N) || d.N > 128) ? 256 : 128;
 }
@@ -1058,7 +1062,7 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.ss0 = d.ss0;
   p.ss1 = d.ss1;
   p.tile_n = tile_n;
-  p.nst = static_cast<int>((d.N + tile_n - 1) / tile_n);
+  p.nst = static_cast<int>((d.N + tile_n - 1) / tile_n) * kEpiHalves;
   cudaError_t e = pair        ? launch_pair(p, a_mn, b_mn, stream)
                   : BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
                               : launch_bn<128>(p, a_mn, b_mn, stream);
