@@ -274,5 +274,9 @@ tess_ctx::~tess_ctx() {
     cudaStreamSynchronize(comm_s);
     cudaStreamDestroy(comm_s);
   }
+  if (copy_s) {
+    cudaStreamSynchronize(copy_s);
+    cudaStreamDestroy(copy_s);
+  }
   for (auto e : ev_ring) cudaEventDestroy(e);
 }

@@ -31,6 +31,9 @@ struct tess_ctx {
   // the compute stream (created on first use; the compute stream itself when
   // the grid has a single rank). Cross-stream ordering uses a ring of events.
   cudaStream_t comm_s = nullptr;
+  // Side stream for host copies of layer outputs (overlaps the next call).
+  cudaStream_t copy_s = nullptr;
+  bool copy_pending = false;
   std::vector<cudaEvent_t> ev_ring;
   size_t ev_next = 0;
   ~tess_ctx();

@@ -373,12 +373,14 @@ __global__ void lse_combine_kernel(const float2* __restrict__ stats, int64_t row
                                    float* __restrict__ lse) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
+  // partials are (max, sum) in log2 units (RowStats epilogue); so is lse
   const float2* s = stats + r * nst;
   float m = -INFINITY;
   for (int i = 0; i < nst; ++i) m = fmaxf(m, s[i].x);
   float sum = 0.f;
-  for (int i = 0; i < nst; ++i) sum += s[i].y * __expf(s[i].x - m);
-  lse[r] = m + __logf(sum);
+  for (int i = 0; i < nst; ++i)
+    if (s[i].x != -INFINITY) sum += s[i].y * exp2f(s[i].x - m);
+  lse[r] = m + log2f(sum);
 }
 
 // one warp per (row, head)

@@ -35,9 +35,9 @@ enum class Epi : int {
   Gelu = 3,        // Z = v; C = gelu(v) with the exact erf GeLU
   // The following are tcgen05-kernel only (bf16 inputs).
   DGelu = 4,       // C = v * gelu'(R)  (R = FF1 pre-activation z; ref layers.cpp:365)
-  SoftmaxFwd = 5,  // C = exp(v - vec[row])   (vec = row log-sum-exp)
+  SoftmaxFwd = 5,  // C = 2^(v*log2e - vec[row])  (vec = row log-sum-exp in log2 units)
   SoftmaxBwd = 6,  // C = R * (v - alpha*vec[row]) (R = P, vec = rowsum(dO*O))
-  RowStats = 7,    // no C: stats[row][tile] = (max_c v, sum_c exp(v - max))
+  RowStats = 7,    // no C: stats[row][part] = (max v*log2e, sum 2^(v*log2e - max))
 };
 
 constexpr int kMaxSegments = 8;

@@ -189,18 +189,38 @@ __device__ __forceinline__ float gelu_erf_grad(float v) {
 
 // Online (max, sum-exp) of the valid values of one 32-column chunk merged
 // into the running pair of the row (RowStats epilogue).
+// Works in the log2 domain: v*alpha*log2(e) via one FFMA per element feeding
+// ex2.approx; the running pair is kept as (max in log2 units, sum).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void row_stats_chunk(const uint32_t (&acc)[32], float alpha,
                                                 int nvalid, float& rmax, float& rsum) {
+  const float a2 = alpha * 1.4426950408889634f;  // alpha * log2(e)
   float cm = -INFINITY;
+  if (nvalid == 32) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j < nvalid) cm = fmaxf(cm, __uint_as_float(acc[j]) * alpha);
+    for (int j = 0; j < 32; ++j) cm = fmaxf(cm, __uint_as_float(acc[j]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) cm = fmaxf(cm, __uint_as_float(acc[j]));
+  }
   if (cm == -INFINITY) return;
+  cm *= a2;  // alpha > 0: max commutes with the scaling
   const float nm = fmaxf(rmax, cm);
-  float s = rsum * __expf(rmax - nm);
+  float s = rsum * ex2_approx(rmax - nm);
+  if (nvalid == 32) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j < nvalid) s += __expf(__uint_as_float(acc[j]) * alpha - nm);
+    for (int j = 0; j < 32; ++j) s += ex2_approx(fmaf(__uint_as_float(acc[j]), a2, -nm));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) s += ex2_approx(fmaf(__uint_as_float(acc[j]), a2, -nm));
+  }
   rmax = nm;
   rsum = s;
 }
@@ -348,9 +368,9 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int 
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = aux[j] * (v[j] - d);
   } else if (epi == (int)Epi::SoftmaxFwd) {
-    const float lse = p.vec[p.vs0 * b0 + p.vs1 * b1 + m];
+    const float lse2 = p.vec[p.vs0 * b0 + p.vs1 * b1 + m];  // log2 units
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __expf(v[j] - lse);
+    for (int j = 0; j < 32; ++j) v[j] = ex2_approx(fmaf(v[j], 1.4426950408889634f, -lse2));
   } else if (epi == (int)Epi::Gelu) {
     if (p.c_bf16)
       store32_bf16(batch_ptr<__nv_bfloat16>(p.z, p.zs0, p.zs1, b0, b1) + (long long)m * p.ldz + n,
@@ -377,20 +397,33 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, i
   const bool stats = p.epi == (int)Epi::RowStats;
   const bool aux_in = epi_needs_aux(p.epi);
   float rmax = -INFINITY, rsum = 0.f;
+  // aux operand of chunk c is fetched one chunk ahead (software pipeline) so
+  // its global-load latency hides under the previous chunk's work
+  float aux[32], aux_next[32];
+  auto nvalid_of = [&](int c) {
+    const int n = n0 + c * 32;
+    return (m < p.M && n < p.N) ? min(32, p.N - n) : 0;
+  };
+  if (aux_in && nvalid_of(half) > 0)
+    epilogue_load_aux(p, b0, b1, m, n0 + half * 32, nvalid_of(half), aux);
 #pragma unroll 1
   for (int c = half; c < width / 32; c += kEpiHalves) {
     const int n = n0 + c * 32;
-    const bool valid = m < p.M && n < p.N;
-    const int nvalid = valid ? min(32, p.N - n) : 0;
-    float aux[32];
-    if (aux_in && valid) epilogue_load_aux(p, b0, b1, m, n, nvalid, aux);
+    const int nvalid = nvalid_of(c);
+    const int cn = c + kEpiHalves;
+    if (aux_in && cn < width / 32 && nvalid_of(cn) > 0)
+      epilogue_load_aux(p, b0, b1, m, n0 + cn * 32, nvalid_of(cn), aux_next);
     uint32_t r[32];
     tmem_ld32(trow + c * 32, r);  // warp-collective: executed by every lane
-    if (valid) {
+    if (nvalid > 0) {
       if (stats)
         row_stats_chunk(r, p.alpha, nvalid, rmax, rsum);
       else
         epilogue_row_chunk(p, b0, b1, m, n, nvalid, r, aux);
+    }
+    if (aux_in) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) aux[j] = aux_next[j];
     }
   }
   if (stats && m < p.M && n0 < p.N) {
@@ -610,7 +643,10 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+  // relaxed: the arrive only publishes "TMEM drained" (tcgen05.wait::ld has
+  // completed the reads); a release would add a GPU-scope MEMBAR that waits
+  // for every outstanding epilogue store of this thread.
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
 }
 

@@ -66,7 +66,8 @@ size_t k_ln_params_scratch_floats(int64_t rows, int64_t w);
 // ---- softmax (ref layers.cpp:44-74) ---------------------------------------
 // P = softmax_rows(S) with max subtraction; S fp32 [rows, L] (already scaled).
 void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cudaStream_t s);
-// lse[r] = log-sum-exp over the nst RowStats partials (max, sumexp) of row r.
+// lse[r] = log-sum-exp (log2 units) over the nst RowStats partials
+// (max, sum-exp2) of row r.
 void k_lse_combine(const float* stats, int64_t rows, int nst, float* lse, cudaStream_t s);
 // delta[h][r] = sum_d dO[r, h*hd + d] * O[r, h*hd + d]  (= rowsum(P * dP),
 // the softmax-backward row term; rows S, heads H, row stride ld).

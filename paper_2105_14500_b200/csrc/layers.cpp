@@ -360,6 +360,17 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
 }
 
+cudaStream_t copy_stream(Ctx& c) {
+  if (!c.copy_s) TESS_CUDA(cudaStreamCreateWithFlags(&c.copy_s, cudaStreamNonBlocking));
+  return c.copy_s;
+}
+
+void join_copies(Ctx& c, cudaStream_t s) {
+  if (!c.copy_pending) return;
+  stream_dep(c, c.copy_s, s);
+  c.copy_pending = false;
+}
+
 std::string cache_tag(const Ctx& c, tess_layer_op op) {
   return "s" + std::to_string(c.cache_slot) + ".op" + std::to_string((int)op);
 }
@@ -383,6 +394,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   const int64_t rows = rd.rows, hq = rd.hq;
   const size_t act = (size_t)rows * hq * dtype_size(t);
   const std::string tag = cache_tag(c, op);
+  join_copies(c, s);  // a previous host copy of the staging buffer must be done
   // Host buffers are staged through the context (x kept until backward).
   const void* x = x_in;
   if (!is_device_ptr(x_in)) {
@@ -441,7 +453,13 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   }
   join_comm(c, s);
   if (y != y_out) {
-    TESS_CUDA(cudaMemcpyAsync(y_out, y, act, cudaMemcpyDeviceToHost, s));
+    // The host copy of y runs on a copy stream, overlapping whatever the
+    // caller enqueues next (normally the backward); the next layer call joins
+    // it before reusing the staging buffer.
+    cudaStream_t cp = copy_stream(c);
+    stream_dep(c, s, cp);
+    TESS_CUDA(cudaMemcpyAsync(y_out, y, act, cudaMemcpyDeviceToHost, cp));
+    c.copy_pending = true;
   }
   c.fwd_x[c.cache_slot * 8 + (int)op] = x;  // the backward needs the forward input
 }
@@ -521,6 +539,7 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   }
   // deferred weight/LN-gradient communication completes before we return
   join_comm(c, s);
+  join_copies(c, s);  // the forward's host copy of y completes within this call
   if (dx != dx_out) TESS_CUDA(cudaMemcpyAsync(dx_out, dx, act, cudaMemcpyDeviceToHost, s));
 }
 
