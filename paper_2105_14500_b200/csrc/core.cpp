@@ -125,40 +125,54 @@ bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 }  // namespace
 
+ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s) {
+  ProfToken t;
+  if (!g_prof_on) return t;
+  auto* rec = new ProfRec{nullptr, nullptr, flops, 0, kernel};
+  cudaGetDevice(&rec->device);
+  TESS_CUDA(cudaEventCreate(&rec->a));
+  TESS_CUDA(cudaEventCreate(&rec->b));
+  TESS_CUDA(cudaEventRecord(rec->a, s));
+  t.rec = rec;
+  return t;
+}
+
+void prof_end(ProfToken& t, cudaStream_t s) {
+  if (!t.rec) return;
+  auto* rec = static_cast<ProfRec*>(t.rec);
+  t.rec = nullptr;
+  TESS_CUDA(cudaEventRecord(rec->b, s));
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.push_back(*rec);
+  delete rec;
+}
+
+bool prof_detail() {
+  static const bool detail = [] {
+    const char* e = std::getenv("TESS_PROFILE_DETAIL");
+    return e && e[0] == '1';
+  }();
+  return detail;
+}
+
 void run_gemm(const GemmDesc& g, cudaStream_t s) {
-  ProfRec rec{nullptr, nullptr, 0.0, 0, std::string()};
-  const bool prof = g_prof_on;
-  if (prof) {
-    rec.kernel = gemm_kernel_name(g);
-    static const bool detail = [] {
-      const char* e = std::getenv("TESS_PROFILE_DETAIL");
-      return e && e[0] == '1';
-    }();
-    if (detail) {
-      double kk = 0;
-      for (int i = 0; i < g.nseg; ++i) kk += (double)g.seg[i].k;
-      rec.kernel += " M=" + std::to_string(g.M) + " N=" + std::to_string(g.N) +
-                    " K=" + std::to_string((long long)kk) +
-                    " b=" + std::to_string(g.nb0 * g.nb1) + " epi=" + std::to_string((int)g.epi);
-    }
-    cudaGetDevice(&rec.device);
-    TESS_CUDA(cudaEventCreate(&rec.a));
-    TESS_CUDA(cudaEventCreate(&rec.b));
-    TESS_CUDA(cudaEventRecord(rec.a, s));
-    double k = 0;
-    for (int i = 0; i < g.nseg; ++i) k += (double)g.seg[i].k;
-    rec.flops = 2.0 * (double)g.M * (double)g.N * k * (double)g.nb0 * (double)g.nb1;
+  ProfToken tok;
+  if (g_prof_on) {
+    std::string name = gemm_kernel_name(g);
+    double kk = 0;
+    for (int i = 0; i < g.nseg; ++i) kk += (double)g.seg[i].k;
+    if (prof_detail())
+      name += " M=" + std::to_string(g.M) + " N=" + std::to_string(g.N) +
+              " K=" + std::to_string((long long)kk) + " b=" + std::to_string(g.nb0 * g.nb1) +
+              " epi=" + std::to_string((int)g.epi);
+    tok = prof_begin(name, 2.0 * (double)g.M * (double)g.N * kk * (double)g.nb0 * (double)g.nb1, s);
   }
   cudaError_t e = gemm(g, s);
   count_launch();
   if (e == cudaErrorInvalidValue) fail(TESS_ERR_UNSUPPORTED, gemm_last_error());
   if (e != cudaSuccess)
     fail(TESS_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e) + " " + gemm_last_error());
-  if (prof) {
-    TESS_CUDA(cudaEventRecord(rec.b, s));
-    std::lock_guard<std::mutex> lk(g_prof_mu);
-    g_prof.push_back(rec);
-  }
+  prof_end(tok, s);
 }
 
 void profile_enable(bool on) {

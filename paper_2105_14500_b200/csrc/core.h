@@ -40,7 +40,14 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 enum Family { ROW = 0, COL = 1, DEPTH = 2 };
 
-// GEMM launch profiling (CUDA events around every local GEMM launch).
+// Launch profiling (CUDA events around every local GEMM / attention launch
+// while enabled; tess_profile_*).
+struct ProfToken {
+  void* rec = nullptr;
+};
+ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s);
+void prof_end(ProfToken& t, cudaStream_t s);
+bool prof_detail();
 void profile_enable(bool on);
 void profile_read(double* ms, double* flops, uint64_t* launches);
 std::string profile_json();

@@ -1,0 +1,832 @@
+// Fused attention forward / backward for sm_100a (tcgen05 + TMEM + TMA).
+//
+// Replaces, for bf16, the per-(sample, head) loop of the reference's
+// attn_forward_rank / attn_backward_rank (proj/src/layers.cpp:383-456):
+//   S = Q K^T / sqrt(hd), P = softmax_rows(S) (layers.cpp:44-58, no mask),
+//   O = P V; backward dV = P^T dO, dP = dO V^T, dS = P * (dP - rowsum(dP*P))
+//   / sqrt(hd) (layers.cpp:60-74), dQ = dS K, dK = dS^T Q.
+// Neither S nor P reaches HBM: the forward keeps one log2-sum-exp per query
+// row, the backward recomputes P from it.
+//
+// ---------------------------------------------------------------- forward
+// One CTA = one (sample, head) and two 128-query tiles A and B that share
+// every K/V tile (halving K/V traffic). 320 threads:
+//   warp 0      TMA producer: Q_A, Q_B once, then K_j, V_j into a ring of
+//               KV_STAGES 128-key tiles (128B-swizzled boxes {64, 128}).
+//   warp 1      MMA issuer + TMEM owner. Per key tile j:
+//                 S_A(j+1) = Q_A K_{j+1}^T, S_B(j+1) = Q_B K_{j+1}^T
+//                 O_A += P_A(j) V_j,         O_B += P_B(j) V_j
+//               interleaved so the tensor core works on one tile's MMAs
+//               while the other tile's softmax runs.
+//   warps 2-5   softmax of tile A (warp w owns TMEM lanes 32*(w%4)..+31:
+//               thread = query row), warps 6-9 tile B. Row max / exp2 /
+//               row sum in registers; P (bf16) written to shared memory in
+//               the UMMA K-major 128B-swizzled layout; lazy rescaling of O
+//               (only when the running max grows by more than 2^8, exact
+//               because the final normalisation uses the same max).
+// TMEM: S_A [0,128), S_B [128,256), O_A [256,256+hd), O_B [384,384+hd).
+#include "attention.h"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "sm100_ptx.cuh"
+
+namespace tess {
+
+namespace {
+thread_local std::string g_attn_err;
+}
+
+const char* attn_last_error() { return g_attn_err.c_str(); }
+
+namespace sm100 {
+namespace attn {
+
+constexpr int kThreads = 320;
+constexpr int BQ = 128;   // query rows per tile (UMMA M)
+constexpr int BKV = 128;  // keys per tile (UMMA N of S, K of P V)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct FwdParams {
+  CUtensorMap tm_qkv;  // 3-D view [cols, S, samples] of qkv, box {64, 128, 1}
+  int S, H, n_pairs, n_kv;
+  int hd;
+  float c;  // scale * log2(e)
+  __nv_bfloat16* o;
+  long long ld_o;
+  float* lse;
+};
+
+template <int HD>
+struct FwdCfg {
+  static constexpr int Q_BYTES = BQ * HD * 2;    // one 128-row tile of Q (or K, V)
+  static constexpr int KV_BYTES = BKV * HD * 2;
+  static constexpr int P_BYTES = BQ * BKV * 2;
+  static constexpr int KV_STAGES = HD == 128 ? 3 : 6;
+  static constexpr int OFF_QA = 0;
+  static constexpr int OFF_QB = Q_BYTES;
+  static constexpr int OFF_PA = 2 * Q_BYTES;
+  static constexpr int OFF_PB = OFF_PA + P_BYTES;
+  static constexpr int OFF_KV = OFF_PB + P_BYTES;
+  static constexpr int OFF_BAR = OFF_KV + KV_STAGES * KV_BYTES;
+  static constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;  // + barriers + alignment slack
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int TM_S0 = 0, TM_O0 = 256;
+};
+
+// P (bf16, row r of this thread, 128 keys) -> shared memory, UMMA K-major
+// SWIZZLE_128B layout: [key chunk kc (64 keys)][row][128 B], 16-byte unit u of
+// a row stored at unit u ^ (row % 8).
+__device__ __forceinline__ void store_p_row(uint32_t p_base, int r, const float (&p)[BKV]) {
+  const uint32_t row_base = p_base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k0 = kc * 64 + u * 8;
+      st_shared_v4(row_base + kc * 16384u + (uint32_t)((u ^ (r & 7)) << 4),
+                   pack_bf16x2(p[k0 + 0], p[k0 + 1]), pack_bf16x2(p[k0 + 2], p[k0 + 3]),
+                   pack_bf16x2(p[k0 + 4], p[k0 + 5]), pack_bf16x2(p[k0 + 6], p[k0 + 7]));
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ FwdParams p) {
+  using C = FwdCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;                        // 1
+  uint64_t* kv_full = bars + 1;                   // KV_STAGES
+  uint64_t* kv_empty = kv_full + C::KV_STAGES;    // KV_STAGES
+  uint64_t* s_full = kv_empty + C::KV_STAGES;     // 2 (tile A, B)
+  uint64_t* p_full = s_full + 2;                  // 2
+  uint64_t* o_full = p_full + 2;                  // 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int pair = blockIdx.x % p.n_pairs;
+  const int head = (blockIdx.x / p.n_pairs) % p.H;
+  const int smp = blockIdx.x / (p.n_pairs * p.H);
+  const int q0 = pair * 2 * BQ;
+  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::KV_STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);
+    }
+    mbar_init(o_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&p.tm_qkv);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------ TMA producer
+      mbar_expect_tx(q_full, 2 * C::Q_BYTES);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_3d(smem + C::OFF_QA + c * 16384, &p.tm_qkv, q_full, col_q + c * 64, q0, smp);
+        tma_load_3d(smem + C::OFF_QB + c * 16384, &p.tm_qkv, q_full, col_q + c * 64, q0 + BQ,
+                    smp);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < p.n_kv; ++j) {
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {  // K_j then V_j
+          mbar_wait(&kv_empty[stage], phase ^ 1);
+          uint8_t* dst = smem + C::OFF_KV + stage * C::KV_BYTES;
+          mbar_expect_tx(&kv_full[stage], C::KV_BYTES);
+          const int col = which == 0 ? col_k : col_v;
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_3d(dst + c * 16384, &p.tm_qkv, &kv_full[stage], col + c * 64, j * BKV, smp);
+          if (++stage == C::KV_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16(BQ, BKV, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(BQ, HD, false, true);
+      const uint32_t sq0 = smem_u32(smem + C::OFF_QA);  // Q_B, P_B follow at fixed offsets
+      const uint32_t sp0 = smem_u32(smem + C::OFF_PA);
+      int stage = 0;
+      uint32_t phase = 0;
+      auto next_kv = [&]() {
+        const int s = stage;
+        mbar_wait(&kv_full[s], phase);
+        tc_fence_after();
+        if (++stage == C::KV_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+        return s;
+      };
+      auto issue_s = [&](int t, uint32_t skv) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
+          mma_bf16(tmem + C::TM_S0 + t * BKV, make_sdesc(sq0 + t * C::Q_BYTES + off, 16, 1024),
+                   make_sdesc(skv + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, uint32_t skv, bool acc) {
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint32_t aoff = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
+          mma_bf16(tmem + C::TM_O0 + t * 128, make_sdesc(sp0 + t * C::P_BYTES + aoff, 16, 1024),
+                   make_sdesc(skv + (uint32_t)kk * 2048u, 16384, 1024), idesc_pv,
+                   (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      int ks = next_kv();
+      const uint32_t sk0 = smem_u32(smem + C::OFF_KV + ks * C::KV_BYTES);
+      issue_s(0, sk0);
+      issue_s(1, sk0);
+      mma_commit(&kv_empty[ks]);
+      for (int j = 0; j < p.n_kv; ++j) {
+        const int vs = next_kv();
+        const uint32_t sv = smem_u32(smem + C::OFF_KV + vs * C::KV_BYTES);
+        const bool more = j + 1 < p.n_kv;
+        uint32_t skn = 0;
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, sv, j > 0);
+        if (more) {
+          ks = next_kv();
+          skn = smem_u32(smem + C::OFF_KV + ks * C::KV_BYTES);
+          issue_s(0, skn);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, sv, j > 0);
+        mma_commit(&kv_empty[vs]);
+        if (more) {
+          issue_s(1, skn);
+          mma_commit(&kv_empty[ks]);
+        }
+      }
+      mma_commit(o_full);
+    }
+  } else {
+    // --------------------------------------------------- softmax warps
+    const int t = (warp - 2) >> 2;   // tile A (0) or B (1)
+    const int quad = warp & 3;       // TMEM lane quadrant
+    const int r = quad * 32 + lane;  // query row within the tile
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + C::TM_S0 + t * BKV;
+    const uint32_t t_o = tmem + lane_off + C::TM_O0 + t * 128;
+    const uint32_t p_base = smem_u32(smem + (t == 0 ? C::OFF_PA : C::OFF_PB));
+    const float cl2 = p.c;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < p.n_kv; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      float s[BKV];
+      {
+        uint32_t a0[32], a1[32], a2[32], a3[32];
+        tmem_ld32_nowait(t_s + 0, a0);
+        tmem_ld32_nowait(t_s + 32, a1);
+        tmem_ld32_nowait(t_s + 64, a2);
+        tmem_ld32_nowait(t_s + 96, a3);
+        tmem_wait_ld();
+        reg_fence32(a0);
+        reg_fence32(a1);
+        reg_fence32(a2);
+        reg_fence32(a3);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          s[e] = __uint_as_float(a0[e]);
+          s[32 + e] = __uint_as_float(a1[e]);
+          s[64 + e] = __uint_as_float(a2[e]);
+          s[96 + e] = __uint_as_float(a3[e]);
+        }
+      }
+      const int nvalid = p.S - j * BKV;  // keys of this tile inside the sequence
+      if (nvalid < BKV) {
+#pragma unroll
+        for (int e = 0; e < BKV; ++e)
+          if (e >= nvalid) s[e] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int e = 1; e < BKV; ++e) mx = fmaxf(mx, s[e]);
+      const float m_new = fmaxf(m_used, mx * cl2);
+      const bool need = m_new > m_used + kRescaleThreshold;
+      if (__any_sync(0xffffffffu, need)) {
+        // lazy rescale: whole warp moves to the new max (factor <= 1)
+        const float f = ex2_approx(m_used - m_new);  // 0 on the first tile
+        if (j > 0) {
+          l *= f;
+#pragma unroll 1
+          for (int c = 0; c < HD / 16; ++c) {
+            uint32_t ov[16];
+            tmem_ld16_nowait(t_o + c * 16, ov);
+            tmem_wait_ld();
+            reg_fence16(ov);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * f);
+            tmem_st16(t_o + c * 16, ov);
+          }
+          tmem_wait_st();
+        }
+        m_used = m_new;
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int e = 0; e < BKV; ++e) {
+        s[e] = ex2_approx(fmaf(s[e], cl2, -m_used));
+        rs += s[e];
+      }
+      l += rs;
+      store_p_row(p_base, r, s);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const int qrow = q0 + t * BQ + r;
+    const float inv = 1.0f / l;
+    __nv_bfloat16* orow = p.o + ((long long)smp * p.S + qrow) * p.ld_o + (long long)head * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t ov[32];
+      tmem_ld32_nowait(t_o + c * 32, ov);
+      tmem_wait_ld();
+      reg_fence32(ov);
+      if (qrow < p.S) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(ov[u * 8 + 0]) * inv, __uint_as_float(ov[u * 8 + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(ov[u * 8 + 2]) * inv, __uint_as_float(ov[u * 8 + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(ov[u * 8 + 4]) * inv, __uint_as_float(ov[u * 8 + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(ov[u * 8 + 6]) * inv, __uint_as_float(ov[u * 8 + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = w;
+        }
+      }
+    }
+    if (qrow < p.S) p.lse[((long long)smp * p.H + head) * p.S + qrow] = m_used + __log2f(l);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+
+// --------------------------------------------------------------- backward
+// One CTA = one (sample, head, 128-key tile); it walks the 64-query tiles
+// i of the sequence. 320 threads:
+//   warp 0      TMA producer: K, V of the key tile once; then Q_i, dO_i
+//               (64 x hd, boxes {64, 64}) through a RING-slot FIFO.
+//   warp 1      MMA issuer + TMEM owner. Per query tile:
+//                 S^T(i+1) = K Q_{i+1}^T, dP^T(i+1) = V dO_{i+1}^T  (M=128, N=64)
+//                 dV += P^T(i) dO_i, dK += dS^T(i) Q_i                (M=128, N=hd)
+//               with S^T / dP^T double buffered in TMEM, so the next
+//               tile's scores run under this tile's softmax.
+//   warps 2-9   thread = key row (TMEM lane), two warps per lane quadrant
+//               (32 query columns each): P^T = 2^(c*S^T - lse[q]),
+//               dS^T = P^T (dP^T - delta[q]) / sqrt(hd), both bf16 into
+//               shared memory (UMMA K-major SW128) for the dV/dK MMAs; dS^T
+//               also leaves by TMA store for dQ = dS K (one batched GEMM).
+// Q_i and dO_i tiles are used twice with different majorness: K-major B of
+// the score MMAs ([N=q][K=hd]) and MN-major B of dV/dK ([K=q][N=hd]) -- the
+// same bytes under two descriptors.
+// TMEM: S^T bufs [0,64) [64,128), dP^T bufs [128,192) [192,256),
+//       dV [256, 256+hd), dK [384, 384+hd).
+constexpr int BQB = 64;  // queries per backward tile
+
+struct BwdParams {
+  CUtensorMap tm_kv;   // qkv view, box {64, 128}: K, V of the key tile
+  CUtensorMap tm_q;    // qkv view, box {64, 64}: Q_i
+  CUtensorMap tm_do;   // dO view [hq cols, S, samples], box {64, 64}
+  CUtensorMap tm_dst;  // dS^T view [S q, S k, samples*H], box {64, 128} (store)
+  int S, H, n_kt, n_qt;
+  float c;      // scale * log2(e)
+  float scale;  // 1/sqrt(hd)
+  const float* lse;
+  const float* delta;
+  __nv_bfloat16* dqkv;
+  long long ld_qkv;
+};
+
+template <int HD>
+struct BwdCfg {
+  static constexpr int KV_BYTES = 128 * HD * 2;   // K or V tile
+  static constexpr int SLOT_BYTES = BQB * HD * 2;  // Q_i or dO_i
+  static constexpr int RING = HD == 128 ? 6 : 10;
+  static constexpr int PD_BYTES = 128 * BQB * 2;   // P^T or dS^T tile
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = KV_BYTES;
+  static constexpr int OFF_RING = 2 * KV_BYTES;
+  static constexpr int OFF_P = OFF_RING + RING * SLOT_BYTES;  // 2 buffers
+  static constexpr int OFF_DS = OFF_P + 2 * PD_BYTES;         // 2 buffers
+  static constexpr int OFF_BAR = OFF_DS + 2 * PD_BYTES;
+  static constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int TM_ST = 0, TM_DPT = 128, TM_DV = 256, TM_DK = 384;
+};
+
+// 32 bf16 values of row r (columns [u0*8, u0*8+32) of a 64-column K-major
+// SW128 tile) -> shared memory.
+__device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const float (&v)[32]) {
+  const uint32_t row_base = base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k0 = u * 8;
+    st_shared_v4(row_base + (uint32_t)(((u0 + u) ^ (r & 7)) << 4), pack_bf16x2(v[k0], v[k0 + 1]),
+                 pack_bf16x2(v[k0 + 2], v[k0 + 3]), pack_bf16x2(v[k0 + 4], v[k0 + 5]),
+                 pack_bf16x2(v[k0 + 6], v[k0 + 7]));
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
+  using C = BwdCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bars;                   // 1
+  uint64_t* r_full = bars + 1;                // RING
+  uint64_t* r_empty = r_full + C::RING;       // RING
+  uint64_t* sdp_full = r_empty + C::RING;     // 2
+  uint64_t* sdp_free = sdp_full + 2;          // 2
+  uint64_t* pds_full = sdp_free + 2;          // 2
+  uint64_t* pds_free = pds_full + 2;          // 2
+  uint64_t* fin = pds_free + 2;               // 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int kt = blockIdx.x % p.n_kt;
+  const int head = (blockIdx.x / p.n_kt) % p.H;
+  const int smp = blockIdx.x / (p.n_kt * p.H);
+  const int k0 = kt * 128;
+  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < C::RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sdp_full[b], 1);
+      mbar_init(&sdp_free[b], 8);
+      mbar_init(&pds_full[b], 1);
+      mbar_init(&pds_free[b], 1);
+    }
+    mbar_init(fin, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&p.tm_kv);
+    prefetch_tmap(&p.tm_q);
+    prefetch_tmap(&p.tm_do);
+    prefetch_tmap(&p.tm_dst);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------ TMA producer
+      mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_3d(smem + C::OFF_K + c * 16384, &p.tm_kv, kv_full, col_k + c * 64, k0, smp);
+        tma_load_3d(smem + C::OFF_V + c * 16384, &p.tm_kv, kv_full, col_v + c * 64, k0, smp);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < p.n_qt; ++i) {
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {  // Q_i then dO_i
+          mbar_wait(&r_empty[stage], phase ^ 1);
+          uint8_t* dst = smem + C::OFF_RING + stage * C::SLOT_BYTES;
+          mbar_expect_tx(&r_full[stage], C::SLOT_BYTES);
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            if (which == 0)
+              tma_load_3d(dst + c * 8192, &p.tm_q, &r_full[stage], col_q + c * 64, i * BQB, smp);
+            else
+              tma_load_3d(dst + c * 8192, &p.tm_do, &r_full[stage], head * HD + c * 64, i * BQB,
+                          smp);
+          }
+          if (++stage == C::RING) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16(128, BQB, false, false);
+      constexpr uint32_t idesc_g = idesc_bf16(128, HD, false, true);
+      const uint32_t sk = smem_u32(smem + C::OFF_K), sv = smem_u32(smem + C::OFF_V);
+      const uint32_t ring = smem_u32(smem + C::OFF_RING);
+      int stage = 0;
+      uint32_t phase = 0;
+      auto next_slot = [&]() {
+        const int s = stage;
+        mbar_wait(&r_full[s], phase);
+        tc_fence_after();
+        if (++stage == C::RING) {
+          stage = 0;
+          phase ^= 1;
+        }
+        return s;
+      };
+      // A [128 x HD] K-major (chunk stride 16 KB) times B [64 x HD] K-major
+      // (chunk stride 8 KB) -> TMEM columns [d, d + 64).
+      auto issue_scores = [&](uint32_t d, uint32_t a, uint32_t b) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t ko = (uint32_t)(kk & 3) * 32u;
+          mma_bf16(d, make_sdesc(a + (uint32_t)(kk >> 2) * 16384u + ko, 16, 1024),
+                   make_sdesc(b + (uint32_t)(kk >> 2) * 8192u + ko, 16, 1024), idesc_s,
+                   kk > 0 ? 1u : 0u);
+        }
+      };
+      // A [128 x 64] K-major (P^T or dS^T) times B [64 x HD] MN-major.
+      auto issue_grad = [&](uint32_t d, uint32_t a, uint32_t b, bool acc) {
+#pragma unroll
+        for (int kk = 0; kk < BQB / 16; ++kk)
+          mma_bf16(d, make_sdesc(a + (uint32_t)kk * 32u, 16, 1024),
+                   make_sdesc(b + (uint32_t)kk * 2048u, 8192, 1024), idesc_g,
+                   (acc || kk > 0) ? 1u : 0u);
+      };
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      int qs = next_slot();
+      int ds = next_slot();
+      issue_scores(tmem + C::TM_ST, sk, ring + qs * C::SLOT_BYTES);
+      issue_scores(tmem + C::TM_DPT, sv, ring + ds * C::SLOT_BYTES);
+      mma_commit(&sdp_full[0]);
+      for (int i = 0; i < p.n_qt; ++i) {
+        const int b = i & 1;
+        int qn = 0, dn = 0;
+        if (i + 1 < p.n_qt) {
+          mbar_wait(&sdp_free[b ^ 1], (((i + 1) >> 1) & 1) ^ 1);
+          tc_fence_after();
+          qn = next_slot();
+          dn = next_slot();
+          issue_scores(tmem + C::TM_ST + (b ^ 1) * 64, sk, ring + qn * C::SLOT_BYTES);
+          issue_scores(tmem + C::TM_DPT + (b ^ 1) * 64, sv, ring + dn * C::SLOT_BYTES);
+          mma_commit(&sdp_full[b ^ 1]);
+        }
+        mbar_wait(&pds_full[b], (i >> 1) & 1);
+        tc_fence_after();
+        issue_grad(tmem + C::TM_DV, smem_u32(smem + C::OFF_P + b * C::PD_BYTES),
+                   ring + ds * C::SLOT_BYTES, i > 0);
+        mma_commit(&r_empty[ds]);
+        issue_grad(tmem + C::TM_DK, smem_u32(smem + C::OFF_DS + b * C::PD_BYTES),
+                   ring + qs * C::SLOT_BYTES, i > 0);
+        mma_commit(&r_empty[qs]);
+        mma_commit(&pds_free[b]);
+        qs = qn;
+        ds = dn;
+      }
+      mma_commit(fin);
+    }
+  } else {
+    // ------------------------------------------ softmax-gradient warps
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;  // query columns [half*32, half*32+32)
+    const int r = quad * 32 + lane;    // key row within the tile
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float cl2 = p.c, scale = p.scale;
+    const bool storer = warp == 2 && lane == 0;
+    const float* lse_h = p.lse + ((long long)smp * p.H + head) * p.S;
+    const float* dlt_h = p.delta + ((long long)smp * p.H + head) * p.S;
+    for (int i = 0; i < p.n_qt; ++i) {
+      const int b = i & 1;
+      const int qc = i * BQB + half * 32;  // first query column of this thread
+      float lv[32], dv[32];
+      if (qc + 32 <= p.S) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(lse_h + qc) + e);
+          const float4 d = __ldg(reinterpret_cast<const float4*>(dlt_h + qc) + e);
+          lv[4 * e] = a.x; lv[4 * e + 1] = a.y; lv[4 * e + 2] = a.z; lv[4 * e + 3] = a.w;
+          dv[4 * e] = d.x; dv[4 * e + 1] = d.y; dv[4 * e + 2] = d.z; dv[4 * e + 3] = d.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const bool ok = qc + e < p.S;
+          lv[e] = ok ? lse_h[qc + e] : INFINITY;  // 2^(x - inf) = 0: no contribution
+          dv[e] = ok ? dlt_h[qc + e] : 0.f;
+        }
+      }
+      mbar_wait(&sdp_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tmem_ld32_nowait(tmem + lane_off + C::TM_ST + b * 64 + half * 32, sr);
+      tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + b * 64 + half * 32, dr);
+      tmem_wait_ld();
+      reg_fence32(sr);
+      reg_fence32(dr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sdp_free[b]);
+      float pv[32], gv[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        pv[e] = ex2_approx(fmaf(__uint_as_float(sr[e]), cl2, -lv[e]));
+        gv[e] = pv[e] * (__uint_as_float(dr[e]) - dv[e]) * scale;
+      }
+      // P^T / dS^T buffer b is free once dV/dK of tile i-2 completed and the
+      // TMA store of dS^T(i-2) has read it.
+      mbar_wait(&pds_free[b], ((i >> 1) & 1) ^ 1);
+      if (storer) bulk_wait_read<1>();
+      named_bar_sync(1, 256);
+      store_row32(smem_u32(smem + C::OFF_P + b * C::PD_BYTES), r, half * 4, pv);
+      store_row32(smem_u32(smem + C::OFF_DS + b * C::PD_BYTES), r, half * 4, gv);
+      fence_proxy_async_smem();
+      named_bar_sync(1, 256);
+      if (storer) {
+        tma_store_3d(&p.tm_dst, smem + C::OFF_DS + b * C::PD_BYTES, i * BQB, k0,
+                     smp * p.H + head);
+        bulk_commit();
+        mbar_arrive(&pds_full[b]);
+      }
+    }
+    // ------------------------------------------------- dK, dV epilogue
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const int krow = k0 + r;
+    __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + krow) * p.ld_qkv + col_k;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {  // dK then dV
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        const int col = half * (HD / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld32_nowait(tmem + lane_off + (which == 0 ? C::TM_DK : C::TM_DV) + col, v);
+        tmem_wait_ld();
+        reg_fence32(v);
+        if (krow < p.S) {
+          __nv_bfloat16* dst = drow + which * HD + col;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]), __uint_as_float(v[u * 8 + 1]));
+            w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]), __uint_as_float(v[u * 8 + 3]));
+            w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]), __uint_as_float(v[u * 8 + 5]));
+            w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]), __uint_as_float(v[u * 8 + 7]));
+            *reinterpret_cast<uint4*>(dst + u * 8) = w;
+          }
+        }
+      }
+    }
+    if (storer) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------- host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 3-D bf16 view [cols, seq, samples] (row stride ld, sample stride seq*ld),
+// box {64, box_rows, 1}, 128B swizzle; rows past seq read as zero.
+bool encode_3d(CUtensorMap* map, const void* base, int64_t cols, int64_t seq, int64_t samples,
+               int64_t ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    g_attn_err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)seq, (cuuint64_t)samples};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)(seq * ld) * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_attn_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
+template <int HD>
+cudaError_t launch_fwd(const FwdParams& p, int grid, cudaStream_t s) {
+  using C = FwdCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<HD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  attn_fwd_kernel<HD><<<grid, kThreads, C::SMEM_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int HD>
+cudaError_t launch_bwd(const BwdParams& p, int grid, cudaStream_t s) {
+  using C = BwdCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<HD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  attn_bwd_kernel<HD><<<grid, kThreads, C::SMEM_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace attn
+}  // namespace sm100
+
+bool attn_fused_supported(const AttnDesc& d) {
+  if (!(d.head_dim == 64 || d.head_dim == 128)) return false;
+  if (d.seq <= 0 || d.seq % 8 != 0 || d.heads <= 0 || d.samples <= 0) return false;
+  if (d.ld_qkv % 8 != 0 || d.ld_o % 8 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(d.qkv) % 16 || reinterpret_cast<uintptr_t>(d.o) % 16)
+    return false;
+  if (d.seq > (1 << 30) / 2 || d.samples > 65535) return false;
+  return true;
+}
+
+cudaError_t attn_fwd_sm100(const AttnDesc& d, cudaStream_t s) {
+  using namespace sm100::attn;
+  if (!attn_fused_supported(d)) {
+    g_attn_err = "attn_fwd_sm100: unsupported shape (head_dim must be 64 or 128, rows 16-byte aligned)";
+    return cudaErrorInvalidValue;
+  }
+  FwdParams p;
+  std::memset(&p, 0, sizeof(p));
+  if (!encode_3d(&p.tm_qkv, d.qkv, 3 * d.heads * d.head_dim, d.seq, d.samples, d.ld_qkv, 128))
+    return cudaErrorInvalidValue;
+  p.S = (int)d.seq;
+  p.H = (int)d.heads;
+  p.hd = (int)d.head_dim;
+  p.n_pairs = (int)((d.seq + 2 * BQ - 1) / (2 * BQ));
+  p.n_kv = (int)((d.seq + BKV - 1) / BKV);
+  p.c = d.scale * kLog2e;
+  p.o = static_cast<__nv_bfloat16*>(d.o);
+  p.ld_o = d.ld_o;
+  p.lse = d.lse;
+  const long long grid = (long long)p.n_pairs * d.heads * d.samples;
+  if (grid > 0x7fffffffLL) {
+    g_attn_err = "attn_fwd_sm100: grid too large";
+    return cudaErrorInvalidValue;
+  }
+  cudaError_t e = d.head_dim == 128 ? launch_fwd<128>(p, (int)grid, s) : launch_fwd<64>(p, (int)grid, s);
+  if (e != cudaSuccess) g_attn_err = std::string("attn_fwd_sm100 launch: ") + cudaGetErrorString(e);
+  return e;
+}
+
+cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s) {
+  using namespace sm100::attn;
+  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !d.dst || !d.lse ||
+      d.ld_o % 8 != 0 || reinterpret_cast<uintptr_t>(d.dout) % 16 ||
+      reinterpret_cast<uintptr_t>(d.dqkv) % 16 || reinterpret_cast<uintptr_t>(d.dst) % 16) {
+    g_attn_err = "attn_bwd_sm100: unsupported shape or missing operand";
+    return cudaErrorInvalidValue;
+  }
+  BwdParams p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t cols = 3 * d.heads * d.head_dim;
+  if (!encode_3d(&p.tm_kv, d.qkv, cols, d.seq, d.samples, d.ld_qkv, 128) ||
+      !encode_3d(&p.tm_q, d.qkv, cols, d.seq, d.samples, d.ld_qkv, BQB) ||
+      !encode_3d(&p.tm_do, d.dout, d.heads * d.head_dim, d.seq, d.samples, d.ld_o, BQB) ||
+      !encode_3d(&p.tm_dst, d.dst, d.seq, d.seq, d.samples * d.heads, d.seq, 128))
+    return cudaErrorInvalidValue;
+  p.S = (int)d.seq;
+  p.H = (int)d.heads;
+  p.n_kt = (int)((d.seq + 127) / 128);
+  p.n_qt = (int)((d.seq + BQB - 1) / BQB);
+  p.c = d.scale * kLog2e;
+  p.scale = d.scale;
+  p.lse = d.lse;
+  p.delta = d.delta;
+  p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
+  p.ld_qkv = d.ld_qkv;
+  const long long grid = (long long)p.n_kt * d.heads * d.samples;
+  if (grid > 0x7fffffffLL) {
+    g_attn_err = "attn_bwd_sm100: grid too large";
+    return cudaErrorInvalidValue;
+  }
+  cudaError_t e = d.head_dim == 128 ? launch_bwd<128>(p, (int)grid, s) : launch_bwd<64>(p, (int)grid, s);
+  if (e != cudaSuccess) g_attn_err = std::string("attn_bwd_sm100 launch: ") + cudaGetErrorString(e);
+  return e;
+}
+
+}  // namespace tess

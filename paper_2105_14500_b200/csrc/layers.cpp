@@ -15,8 +15,10 @@
 // Forward caches live in the context workspace under per-op names until the
 // matching backward.
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
+#include "kernels/attention.h"
 #include "kernels/kernels.h"
 #include "ops.h"
 
@@ -197,6 +199,52 @@ void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
 }
 
 // ----------------------------------------------------------- attention
+// The fused tcgen05 attention kernels (kernels/attention_sm100.cu) serve the
+// bf16 mode when the head shape allows (head_dim 64 / 128, seq % 8 == 0);
+// TESS_ATTN_FUSED=0 selects the unfused GEMM + softmax path (A/B checks).
+// Forward and backward make the same choice, so the forward caches what the
+// backward reads: the row log-sum-exp (fused) or P (unfused).
+AttnDesc attn_desc(const RankDims& rd, const void* qkv, void* o, float* lse) {
+  AttnDesc a;
+  a.qkv = qkv;
+  a.ld_qkv = 3 * rd.hq;
+  a.o = o;
+  a.ld_o = rd.hq;
+  a.lse = lse;
+  a.samples = rd.samples_local;
+  a.heads = rd.heads_local;
+  a.seq = rd.seq;
+  a.head_dim = rd.head_dim;
+  a.scale = (float)(1.0 / std::sqrt((double)rd.head_dim));
+  return a;
+}
+
+bool use_fused_attn(DType t, const RankDims& rd) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("TESS_ATTN_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || t != DType::BF16) return false;
+  AttnDesc a = attn_desc(rd, reinterpret_cast<void*>(256), reinterpret_cast<void*>(256), nullptr);
+  return attn_fused_supported(a);
+}
+
+void run_attn(bool fwd, const AttnDesc& a, cudaStream_t s) {
+  ProfToken tok;
+  // algorithmic flops: 2 (fwd) or 4 (bwd: dV, dP, dK; dQ is its own GEMM)
+  // contractions of 2*S*S*hd per (sample, head)
+  const double unit = 2.0 * (double)a.seq * a.seq * a.head_dim * a.heads * a.samples;
+  tok = prof_begin(fwd ? (a.head_dim == 128 ? "attn_fwd_kernel<128>" : "attn_fwd_kernel<64>")
+                       : (a.head_dim == 128 ? "attn_bwd_kernel<128>" : "attn_bwd_kernel<64>"),
+                   (fwd ? 2.0 : 3.0) * unit, s);
+  cudaError_t e = fwd ? attn_fwd_sm100(a, s) : attn_bwd_sm100(a, s);
+  count_launch();
+  if (e == cudaErrorInvalidValue) fail(TESS_ERR_UNSUPPORTED, attn_last_error());
+  if (e != cudaSuccess)
+    fail(TESS_ERR_CUDA, std::string("attention: ") + cudaGetErrorString(e) + " " + attn_last_error());
+  prof_end(tok, s);
+}
+
 // ref layers.cpp:383-414.
 void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
               const tess_block_shard& p, const void* x, const Out& yout, cudaStream_t s,
@@ -205,6 +253,14 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   const int64_t H = rd.heads_local, ld = 3 * hq;
   const size_t esz = dtype_size(t);
   void* qkv = wsget(c, tag + ".qkv", rows * ld * esz);
+  if (use_fused_attn(t, rd)) {
+    void* o = wsget(c, tag + ".o", rows * hq * esz);
+    float* lse = static_cast<float*>(wsget(c, tag + ".lse", (size_t)rd.samples_local * H * S * 4));
+    nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
+    run_attn(true, attn_desc(rd, qkv, o, lse), s);
+    nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s, &wp.proj);
+    return;
+  }
   void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
   void* o = wsget(c, tag + ".o", rows * hq * esz);
   const bool fused = t == DType::BF16;
@@ -298,6 +354,39 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   const int64_t H = rd.heads_local, ld = 3 * hq;
   const size_t esz = dtype_size(t);
   const void* qkv = wsget(c, tag + ".qkv", rows * ld * esz);
+  if (use_fused_attn(t, rd)) {
+    void* o = wsget(c, tag + ".o", rows * hq * esz);
+    float* lse = static_cast<float*>(wsget(c, tag + ".lse", (size_t)rd.samples_local * H * S * 4));
+    float* dout32 = static_cast<float*>(wsget(c, "attn.dout32", rows * hq * 4));
+    void* dout = wsget(c, "attn.dout", rows * hq * esz);
+    void* dqkv = wsget(c, "attn.dqkv", rows * ld * esz);
+    float* delta = static_cast<float*>(wsget(c, "attn.delta", (size_t)rd.samples_local * H * S * 4));
+    void* dst = wsget(c, "attn.dst", (size_t)rd.samples_local * H * S * S * esz);
+    nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
+    k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
+    weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
+    for (int64_t smp = 0; smp < rd.samples_local; ++smp)
+      k_attn_delta(static_cast<const char*>(dout) + (size_t)smp * S * hq * esz,
+                   static_cast<const char*>(o) + (size_t)smp * S * hq * esz, t, hq, S, H, hd,
+                   delta + (size_t)smp * H * S, s);
+    AttnDesc a = attn_desc(rd, qkv, o, lse);
+    a.dout = dout;
+    a.delta = delta;
+    a.dqkv = dqkv;
+    a.dst = dst;
+    run_attn(false, a, s);  // dK, dV -> dqkv; dS^T -> dst
+    // dQ = dS K for every (sample, head): A = dS^T stored [keys, queries]
+    GemmDesc gq;
+    gq.M = S; gq.N = hd; gq.nb0 = H; gq.nb1 = rd.samples_local; gq.in = t; gq.trans_a = true;
+    gq.seg[0] = {dst, static_cast<const char*>(qkv) + hd * esz, S};
+    gq.lda = S; gq.as0 = S * S; gq.as1 = H * S * S;
+    gq.ldb = ld; gq.bs0 = 3 * hd; gq.bs1 = S * ld;
+    gq.c = dqkv; gq.c_type = t; gq.ldc = ld; gq.cs0 = 3 * hd; gq.cs1 = S * ld;
+    run_gemm(gq, s);
+    nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s, &wp.qkv);
+    weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
+    return;
+  }
   const void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
   const void* o = wsget(c, tag + ".o", rows * hq * esz);
   float* dout32 = static_cast<float*>(wsget(c, "attn.dout32", rows * hq * 4));
