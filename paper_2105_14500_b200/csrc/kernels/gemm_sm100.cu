@@ -49,6 +49,10 @@ constexpr int kEpiHalves = 2;   // epilogue warps per TMEM lane quadrant
 struct Params {
   CUtensorMap tma_a[kMaxSegments];
   CUtensorMap tma_b[kMaxSegments];
+  // TMA-store epilogue (pair kernel): C and Z views [N, M, nb0, nb1], box
+  // {32 bf16 | 16 f32 columns, 32 rows}, SWIZZLE_64B (64-byte box rows)
+  CUtensorMap tma_c, tma_z;
+  int tma_epi;
   int seg_kb[kMaxSegments];
   int nseg;
   int total_kb;
@@ -56,6 +60,10 @@ struct Params {
   int nb0;
   int tiles_m, tiles_n, tiles_per_batch, num_tiles;
   int group_m;
+  int skip_store;               // experiment: epilogue computes but does not store
+  int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch) or null
+  int raster_n;                 // pair kernel: 1 = groups of group_m N-tiles, N fastest
+  unsigned long long hint_a, hint_b;  // pair kernel: L2 cache policy of the A / B TMA loads
   void* c;
   int c_bf16;
   long long ldc, cs0, cs1;
@@ -278,14 +286,114 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int 
     store32_f32(batch_ptr<float>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n, nvalid, v);
 }
 
+// v = epilogue(alpha * acc) for one 32-column chunk of row m, without
+// storing (TMA-store path); for Gelu v is the pre-activation (the GeLU is
+// applied after Z is staged). Rows past M (partial tiles) compute garbage
+// that the TMA store clips.
+__device__ __forceinline__ void epilogue_values(const Params& p, int b0, int b1, int m,
+                                                const uint32_t (&acc)[32], const float (&aux)[32],
+                                                float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * p.alpha;
+  const int epi = p.epi;
+  const bool in_m = m < p.M;
+  if (epi == (int)Epi::Resid) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += aux[j];
+  } else if (epi == (int)Epi::DGelu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= gelu_erf_grad(aux[j]);
+  } else if (epi == (int)Epi::SoftmaxBwd) {
+    const float d = in_m ? p.alpha * p.vec[p.vs0 * b0 + p.vs1 * b1 + m] : 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = aux[j] * (v[j] - d);
+  } else if (epi == (int)Epi::SoftmaxFwd) {
+    const float lse2 = in_m ? p.vec[p.vs0 * b0 + p.vs1 * b1 + m] : 0.f;  // log2 units
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = ex2_approx(fmaf(v[j], 1.4426950408889634f, -lse2));
+  }
+}
+
+// Per-warp double-buffered staging of 32 rows x 64 bytes for the TMA store
+// epilogue (SWIZZLE_64B: 16-byte unit u of row r at u ^ ((r >> 1) & 3), which
+// keeps the 8-lane phases of st.shared.v4 conflict-free).
+struct EpiStage {
+  uint32_t buf;  // two 2 KB buffers
+  int bi;
+};
+
+__device__ __forceinline__ void stage_store(const CUtensorMap* map, EpiStage& st, int lane,
+                                            const float* v, bool bf16, bool reduce, int n,
+                                            int mrow0, int b0, int b1) {
+  const uint32_t dst = st.buf + (uint32_t)st.bi * 2048u;
+  if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 units ago
+  __syncwarp();
+  const uint32_t row = dst + (uint32_t)lane * 64u;
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint32_t a, b, c, d;
+    if (bf16) {
+      a = pack_bf16x2(v[u * 8 + 0], v[u * 8 + 1]);
+      b = pack_bf16x2(v[u * 8 + 2], v[u * 8 + 3]);
+      c = pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]);
+      d = pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]);
+    } else {
+      a = __float_as_uint(v[u * 4 + 0]);
+      b = __float_as_uint(v[u * 4 + 1]);
+      c = __float_as_uint(v[u * 4 + 2]);
+      d = __float_as_uint(v[u * 4 + 3]);
+    }
+    st_shared_v4(row + (uint32_t)((u ^ sw) << 4), a, b, c, d);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (reduce)
+      tma_reduce_add_4d(map, dst, n, mrow0, b0, b1);
+    else
+      tma_store_4d(map, dst, n, mrow0, b0, b1);
+    bulk_commit();
+  }
+  st.bi ^= 1;
+}
+
+// One 32-column chunk through the TMA path: bf16 = one 32-column box, f32 =
+// two 16-column boxes; Gelu stores Z first; Accum is a TMA reduce-add into C.
+__device__ __forceinline__ void epilogue_chunk_tma(const Params& p, EpiStage& st, int lane,
+                                                   int b0, int b1, int n, int mrow0,
+                                                   float (&v)[32]) {
+  const bool bf16 = p.c_bf16;
+  const bool reduce = p.epi == (int)Epi::Accum;
+  if (p.epi == (int)Epi::Gelu) {
+    if (bf16) {
+      stage_store(&p.tma_z, st, lane, v, true, false, n, mrow0, b0, b1);
+    } else {
+      stage_store(&p.tma_z, st, lane, v, false, false, n, mrow0, b0, b1);
+      stage_store(&p.tma_z, st, lane, v + 16, false, false, n + 16, mrow0, b0, b1);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  }
+  if (bf16) {
+    stage_store(&p.tma_c, st, lane, v, true, reduce, n, mrow0, b0, b1);
+  } else {
+    stage_store(&p.tma_c, st, lane, v, false, reduce, n, mrow0, b0, b1);
+    stage_store(&p.tma_c, st, lane, v + 16, false, reduce, n + 16, mrow0, b0, b1);
+  }
+}
+
 // Epilogue of this thread's accumulator row m over the 32-column chunks
 // half, half + kEpiHalves, ... of the tile [n0, n0 + width): two epilogue
 // warps share each TMEM lane quadrant and split its chunks. RowStats writes
 // one (max, sum-exp) partial per (tile, half).
 __device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, int m, int n0,
-                                              int width, uint32_t trow, int half) {
+                                              int width, uint32_t trow, int half,
+                                              EpiStage* st = nullptr, int lane = 0,
+                                              int mrow0 = 0) {
   const bool stats = p.epi == (int)Epi::RowStats;
-  const bool aux_in = epi_needs_aux(p.epi);
+  // Accum through TMA is a reduce-add: the old C is not read by the SM
+  const bool aux_in = epi_needs_aux(p.epi) && !(st && p.epi == (int)Epi::Accum);
   float rmax = -INFINITY, rsum = 0.f;
   // aux operand of chunk c is fetched one chunk ahead (software pipeline) so
   // its global-load latency hides under the previous chunk's work
@@ -305,7 +413,14 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, i
       epilogue_load_aux(p, b0, b1, m, n0 + cn * 32, nvalid_of(cn), aux_next);
     uint32_t r[32];
     tmem_ld32(trow + c * 32, r);  // warp-collective: executed by every lane
-    if (nvalid > 0) {
+    if (st) {
+      // warp-uniform: every lane stages its row, the store clips rows >= M
+      if (n < p.N && !p.skip_store) {
+        float v[32];
+        epilogue_values(p, b0, b1, m, r, aux, v);
+        epilogue_chunk_tma(p, *st, lane, b0, b1, n, mrow0, v);
+      }
+    } else if (nvalid > 0 && !p.skip_store) {
       if (stats)
         row_stats_chunk(r, p.alpha, nvalid, rmax, rsum);
       else
@@ -504,12 +619,13 @@ __device__ __forceinline__ void cluster_sync() {
 }
 
 __device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                                int c0, int c1, int c2, int c3) {
+                                                int c0, int c1, int c2, int c3,
+                                                unsigned long long policy) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1),
-      "r"(c2), "r"(c3)
+      "r"(c2), "r"(c3), "l"(policy)
       : "memory");
 }
 
@@ -540,51 +656,158 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
-template <int ST>
+// NH = 256-column accumulator halves per pair tile: NH = 1 is a 256 x 256
+// tile with two TMEM accumulators (the epilogue of tile i overlaps the MMAs
+// of tile i+1); NH = 2 is a 256 x 512 tile (A staged once for 512 output
+// columns: a quarter less L2->SM traffic and fewer DRAM re-reads per flop,
+// the cuBLAS sm_100 tile shape) whose two halves fill all 512 TMEM columns;
+// each half has its own empty barrier, so the next tile's half-0 MMAs start
+// while the epilogue still drains half 1.
+// ---- dynamic tile order for the persistent pair kernel ----------------------
+// A statically strided persistent schedule lets clusters drift apart over
+// their ~40 tiles until tiles that share A/B panels no longer run together,
+// and the L2 reuse between them collapses (2-3x the DRAM reads, measured).
+// Instead the pair leader's producer takes tiles from a global atomic
+// counter (first wave static), so running tiles stay contiguous in tile
+// order like a hardware-scheduled grid, and broadcasts each tile id through
+// a small shared-memory queue to every role of both CTAs.
+constexpr int kTQ = 4;
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC;\n\t"
+      "bra LAB_WAITC;\n"
+      "DONEC:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct TileQ {
+  int* ids;
+  uint64_t* full;
+  uint64_t* empty;  // the leader CTA's copy counts every consumer
+  int slot;
+  uint32_t ph;
+  __device__ __forceinline__ void advance() {
+    if (++slot == kTQ) {
+      slot = 0;
+      ph ^= 1;
+    }
+  }
+  // Consumer: next tile id (-1 = done). A single thread (whole_warp false)
+  // or all 32 lanes of a warp (whole_warp true: every lane reads, then lane 0
+  // releases the slot) to the leader CTA's empty barrier.
+  __device__ __forceinline__ int pop(uint32_t cta, bool whole_warp) {
+    mbar_wait_cluster(&full[slot], ph);
+    const int t = *reinterpret_cast<volatile int*>(&ids[slot]);
+    bool arrive = true;
+    if (whole_warp) {
+      __syncwarp();
+      arrive = (threadIdx.x % 32) == 0;
+    }
+    if (arrive) {
+      if (cta == 0)
+        mbar_arrive(&empty[slot]);
+      else
+        mbar_arrive_cluster(mapa_u32(smem_u32(&empty[slot]), 0));
+    }
+    advance();
+    return t;
+  }
+  // Leader producer: publish t to both CTAs of the pair.
+  __device__ __forceinline__ void push(int t) {
+    mbar_wait(&empty[slot], ph ^ 1);
+    ids[slot] = t;
+    st_cluster_u32(mapa_u32(smem_u32(&ids[slot]), 1), t);
+    mbar_arrive(&full[slot]);
+    mbar_arrive_cluster(mapa_u32(smem_u32(&full[slot]), 1));
+    advance();
+  }
+};
+// consumers per tile: leader MMA thread + 8 epilogue warps per CTA + peer producer
+constexpr int kTQConsumers = 1 + 8 + 1 + 8;
+
+template <int ST, int NH>
 struct Cfg2 {
-  static constexpr int HALF = 128;  // rows of A / columns of B per CTA
+  static constexpr int HALF = 128;  // rows of A / columns of B per CTA and half
   static constexpr int A_BYTES = HALF * BK * 2;
-  static constexpr int B_BYTES = HALF * BK * 2;
+  static constexpr int B_BYTES = NH * HALF * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = ST;
-  static constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 512;  // 2 x 256 fp32 columns
+  // NH = 2: per-epilogue-warp TMA-store staging (2 x 2 KB per warp)
+  static constexpr int EPI_BYTES = NH == 2 ? 8 * 4096 : 0;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
-// Pair-tile index -> (batch0, batch1, m0 (multiple of 256), n0 (multiple of 256)).
+// Pair-tile index -> (batch0, batch1, m0 (multiple of 256), n0 (multiple of
+// p.tile_n)).
 __device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int& b0, int& b1,
                                                  int& m0, int& n0) {
   const int b = tile / p.tiles_per_batch;
   const int r = tile - b * p.tiles_per_batch;
   b0 = b % p.nb0;
   b1 = b / p.nb0;
-  const int width = p.group_m * p.tiles_n;
-  const int g = r / width;
-  const int first_m = g * p.group_m;
-  const int gm = min(p.tiles_m - first_m, p.group_m);
-  const int in = r - g * width;
-  m0 = (first_m + in % gm) * 256;
-  n0 = (in / gm) * 256;
+  if (!p.raster_n) {
+    const int width = p.group_m * p.tiles_n;
+    const int g = r / width;
+    const int first_m = g * p.group_m;
+    const int gm = min(p.tiles_m - first_m, p.group_m);
+    const int in = r - g * width;
+    m0 = (first_m + in % gm) * 256;
+    n0 = (in / gm) * p.tile_n;
+  } else {
+    const int width = p.group_m * p.tiles_m;
+    const int g = r / width;
+    const int first_n = g * p.group_m;
+    const int gn = min(p.tiles_n - first_n, p.group_m);
+    const int in = r - g * width;
+    n0 = (first_n + in % gn) * p.tile_n;
+    m0 = (in / gn) * 256;
+  }
 }
 
-template <bool A_MN, bool B_MN, int ST>
+template <bool A_MN, bool B_MN, int ST, int NH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
-  using C = Cfg2<ST>;
+  using C = Cfg2<ST, NH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi_smem + C::EPI_BYTES);
   uint64_t* empty_bar = full_bar + C::STAGES;
-  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;  // per 256-column accumulator slot
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* tq_full = tempty_bar + 2;
+  uint64_t* tq_empty = tq_full + kTQ;
+  int* tq_ids = reinterpret_cast<int*>(tq_empty + kTQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_ids + kTQ);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t cta = cluster_ctarank();
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
+  TileQ tq{tq_ids, tq_full, tq_empty, 0, 0};
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -594,6 +817,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 8 * kEpiHalves);  // epilogue warps of both CTAs (leader's copy used)
+    }
+    for (int q = 0; q < kTQ; ++q) {
+      mbar_init(&tq_full[q], 1);
+      mbar_init(&tq_empty[q], kTQConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < p.nseg; ++s) {
@@ -618,11 +845,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // -------------------------------------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+      int next = cluster;  // first wave static
+      for (;;) {
+        int tile;
+        if (cta == 0) {
+          tile = next < p.num_tiles ? next : -1;
+          tq.push(tile);
+          if (tile < 0) break;
+          // fetch the following tile now: the atomic's latency hides under this tile's loads
+          next = p.tile_counter ? nclusters + atomicAdd(p.tile_counter, 1) : tile + nclusters;
+        } else {
+          tile = tq.pop(cta, false);
+          if (tile < 0) break;
+        }
         int b0, b1, m0, n0;
         decode_pair_tile(p, tile, b0, b1, m0, n0);
         const int mr = m0 + (int)cta * C::HALF;
-        const int nr = n0 + (int)cta * C::HALF;
         for (int s = 0; s < p.nseg; ++s) {
           const CUtensorMap* ma = &p.tma_a[s];
           const CUtensorMap* mb = &p.tma_b[s];
@@ -633,18 +871,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (cta == 0) mbar_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
             const int k = kb * BK;
             if (!A_MN) {
-              tma_load_4d_2sm(sa, ma, &full_bar[stage], k, mr, b0, b1);
+              tma_load_4d_2sm(sa, ma, &full_bar[stage], k, mr, b0, b1, p.hint_a);
             } else {
 #pragma unroll
               for (int c = 0; c < C::HALF / 64; ++c)
-                tma_load_4d_2sm(sa + c * 8192, ma, &full_bar[stage], mr + c * 64, k, b0, b1);
+                tma_load_4d_2sm(sa + c * 8192, ma, &full_bar[stage], mr + c * 64, k, b0, b1,
+                                p.hint_a);
             }
-            if (!B_MN) {
-              tma_load_4d_2sm(sb, mb, &full_bar[stage], k, nr, b0, b1);
-            } else {
 #pragma unroll
-              for (int c = 0; c < C::HALF / 64; ++c)
-                tma_load_4d_2sm(sb + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0, b1);
+            for (int h = 0; h < NH; ++h) {
+              // the pair's columns [n0 + 256h, +256): this CTA stages its 128
+              const int nr = n0 + h * 256 + (int)cta * C::HALF;
+              uint8_t* sbh = sb + h * (C::HALF * BK * 2);
+              if (!B_MN) {
+                tma_load_4d_2sm(sbh, mb, &full_bar[stage], k, nr, b0, b1, p.hint_b);
+              } else {
+#pragma unroll
+                for (int c = 0; c < C::HALF / 64; ++c)
+                  tma_load_4d_2sm(sbh + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0, b1,
+                                  p.hint_b);
+              }
             }
             if (++stage == C::STAGES) {
               stage = 0;
@@ -662,24 +908,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                              ((uint32_t)(256 >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * 256;
+      int acc = 0;  // NH == 1: alternating slot; NH == 2: both slots every tile
+      uint32_t slot_phase = 0;  // bit s = phase of slot s
+      for (;;) {
+        if (tq.pop(cta, false) < 0) break;
         for (int kb = 0; kb < p.total_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? make_sdesc(sa + k * 2048, 8192, 1024)
-                                     : make_sdesc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_sdesc(sb + k * 2048, 8192, 1024)
-                                     : make_sdesc(sb + k * 32, 16, 1024);
-            mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          for (int h = 0; h < NH; ++h) {
+            const int slot = NH == 1 ? acc : h;
+            if (kb == 0) {
+              // the accumulator slot must have been drained by the epilogue
+              mbar_wait(&tempty_bar[slot], ((slot_phase >> slot) & 1) ^ 1);
+              tc_fence_after();
+            }
+            const uint32_t d_tmem = tmem_base + slot * 256;
+            const uint32_t sbh = sb + h * (C::HALF * BK * 2);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = A_MN ? make_sdesc(sa + k * 2048, 8192, 1024)
+                                       : make_sdesc(sa + k * 32, 16, 1024);
+              const uint64_t bd = B_MN ? make_sdesc(sbh + k * 2048, 8192, 1024)
+                                       : make_sdesc(sbh + k * 32, 16, 1024);
+              mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
           }
           mma_commit_2sm(&empty_bar[stage]);
           if (++stage == C::STAGES) {
@@ -687,30 +942,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        mma_commit_2sm(&tfull_bar[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int slot = NH == 1 ? acc : h;
+          mma_commit_2sm(&tfull_bar[slot]);
+          slot_phase ^= 1u << slot;
+        }
+        if (NH == 1) acc ^= 1;
       }
     }
   } else {
     // ------------------------------------------- epilogue warps (both CTAs)
     const int quad = warp & 3;
     int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = cluster; tile < p.num_tiles; tile += nclusters) {
+    uint32_t slot_phase = 0;
+    EpiStage st{smem_u32(epi_smem) + (uint32_t)(warp - 2) * 4096u, 0};
+    const bool tma_epi = NH == 2 && p.tma_epi;
+    for (;;) {
+      const int tile = tq.pop(cta, true);
+      if (tile < 0) break;
       int b0, b1, m0, n0;
       decode_pair_tile(p, tile, b0, b1, m0, n0);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const int m = m0 + (int)cta * C::HALF + quad * 32 + lane;
-      const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * 256;
-      epilogue_tile(p, b0, b1, m, n0, 256, trow, (warp - 2) / 4);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(&tempty_bar[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      const int mrow0 = m0 + (int)cta * C::HALF + quad * 32;
+      const int m = mrow0 + lane;
+#pragma unroll 1
+      for (int h = 0; h < NH; ++h) {
+        const int slot = NH == 1 ? acc : h;
+        mbar_wait(&tfull_bar[slot], (slot_phase >> slot) & 1);
+        tc_fence_after();
+        const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + slot * 256;
+        epilogue_tile(p, b0, b1, m, n0 + h * 256, 256, trow, (warp - 2) / 4,
+                      tma_epi ? &st : nullptr, lane, mrow0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty_bar[slot]);
+        slot_phase ^= 1u << slot;
+      }
+      if (NH == 1) acc ^= 1;
     }
+    if (tma_epi && lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -736,6 +1006,40 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     }
   });
   return fn;
+}
+
+CUtensorMapL2promotion l2_promotion() {
+  static const CUtensorMapL2promotion v = [] {
+    const char* e = std::getenv("TESS_GEMM_PROMO");  // 0 none, 1 64B, 2 128B, 3 256B
+    const int k = e ? std::atoi(e) : 3;
+    return k == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+           : k == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+           : k == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
+  return v;
+}
+
+// Output view for the TMA-store epilogue: [N, M, nb0, nb1] of bf16 / f32
+// with a {32 | 16, 32, 1, 1} box (64-byte rows) and SWIZZLE_64B.
+bool encode_out(CUtensorMap* map, const void* ptr, bool bf16, int64_t N, int64_t M, int64_t ld,
+                int64_t nb0, int64_t s0, int64_t nb1, int64_t s1) {
+  auto fn = encode_fn();
+  if (!fn || !ptr) return false;
+  const int64_t esz = bf16 ? 2 : 4;
+  if (nb0 <= 1) s0 = ld * M;
+  if (nb1 <= 1) s1 = s0 * (nb0 > 1 ? nb0 : 1);
+  cuuint64_t dims[4] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)nb0, (cuuint64_t)nb1};
+  cuuint64_t strides[3] = {(cuuint64_t)(ld * esz), (cuuint64_t)(s0 * esz), (cuuint64_t)(s1 * esz)};
+  for (int i = 0; i < 3; ++i)
+    if (strides[i] % 16 != 0) return false;
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) return false;
+  cuuint32_t box[4] = {(cuuint32_t)(bf16 ? 32 : 16), 32, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+            const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Encodes a 4-D bf16 view [inner, outer, nb0, nb1] with a {64, box_outer}
@@ -769,7 +1073,7 @@ bool encode_view(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer
   }
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr),
                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
@@ -805,37 +1109,83 @@ cudaError_t launch(const Params& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-template <bool A_MN, bool B_MN, int ST>
-cudaError_t launch_2cta(const Params& p, cudaStream_t stream) {
-  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST>;
+// Per-device ring of tile counters for the pair kernel's dynamic schedule;
+// each launch takes the next slot and zeroes it on its stream.
+int* tile_counter_slot(cudaStream_t stream) {
+  constexpr int kSlots = 4096;
+  static std::mutex mu;
+  static int* bufs[64] = {};
+  static unsigned next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  int* slot;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!bufs[dev] && cudaMalloc(&bufs[dev], kSlots * sizeof(int)) != cudaSuccess) {
+      bufs[dev] = nullptr;
+      return nullptr;
+    }
+    slot = bufs[dev] + (next[dev]++ % kSlots);
+  }
+  if (cudaMemsetAsync(slot, 0, sizeof(int), stream) != cudaSuccess) return nullptr;
+  return slot;
+}
+
+template <bool A_MN, bool B_MN, int ST, int NH>
+cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
+  Params p = p_in;
+  static const bool static_order = std::getenv("TESS_GEMM_STATIC") != nullptr;
+  p.tile_counter = static_order ? nullptr : tile_counter_slot(stream);
+  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg2<ST>::SMEM_BYTES);
+                                         Cfg2<ST, NH>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  static const bool nonpersist = std::getenv("TESS_GEMM_NONPERSIST") != nullptr;
   const int pairs = std::max(1, num_sms() / 2);
-  const int grid = 2 * std::min(p.num_tiles, pairs);
-  kern<<<grid, kThreads, Cfg2<ST>::SMEM_BYTES, stream>>>(p);
+  const int grid = 2 * (nonpersist ? p.num_tiles : std::min(p.num_tiles, pairs));
+  kern<<<grid, kThreads, Cfg2<ST, NH>::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <int ST>
+template <int ST, int NH>
 cudaError_t launch_pair_st(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
-  if (!a_mn && b_mn) return launch_2cta<false, true, ST>(p, s);
-  if (!a_mn && !b_mn) return launch_2cta<false, false, ST>(p, s);
-  if (a_mn && b_mn) return launch_2cta<true, true, ST>(p, s);
-  return launch_2cta<true, false, ST>(p, s);
+  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH>(p, s);
+  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH>(p, s);
+  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH>(p, s);
+  return launch_2cta<true, false, ST, NH>(p, s);
 }
 
-cudaError_t launch_pair(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
-  static int stages = 0;  // TESS_GEMM_STAGES=6|7 (smem ring depth of the pair kernel)
-  if (!stages) {
-    const char* e = std::getenv("TESS_GEMM_STAGES");
-    stages = (e && e[0] == '6') ? 6 : 7;
-  }
-  return stages == 6 ? launch_pair_st<6>(p, a_mn, b_mn, s) : launch_pair_st<7>(p, a_mn, b_mn, s);
+cudaError_t launch_pair(const Params& p, int nh, bool a_mn, bool b_mn, cudaStream_t s) {
+  // smem ring depth: 7 x 32 KB stages for 256 x 256 tiles, 4 x 48 KB for 256 x 512
+  if (nh == 2) return launch_pair_st<4, 2>(p, a_mn, b_mn, s);
+  return launch_pair_st<7, 1>(p, a_mn, b_mn, s);
+}
+
+// 256-column halves per pair tile (see Cfg2): 2 when the wider tile does not
+// cost a partial extra wave over the 148 SMs (74 pairs) and the epilogue has
+// no per-256-column-tile layout (RowStats partials, attention epilogues).
+int pair_halves(const GemmDesc& d) {
+  static const int env = [] {
+    const char* e = std::getenv("TESS_GEMM_NH");  // 1 forces 256 x 256 tiles
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env == 1) return 1;
+  if (d.epi == Epi::RowStats || d.epi == Epi::SoftmaxFwd || d.epi == Epi::SoftmaxBwd) return 1;
+  // GeLU' reads z row-per-thread: cheaper hidden under the next tile's MMAs
+  // (NH = 1 double-buffers TMEM) than exposed (measured 1280 vs 1160 TF/s)
+  if (d.epi == Epi::DGelu && env != 2) return 1;
+  if (d.N <= 256) return 1;
+  const long long pairs = std::max(1, num_sms() / 2);
+  const long long tm = (d.M + 255) / 256, b = d.nb0 * d.nb1;
+  const long long t1 = tm * ((d.N + 255) / 256) * b, t2 = tm * ((d.N + 511) / 512) * b;
+  const long long w1 = (t1 + pairs - 1) / pairs, w2 = (t2 + pairs - 1) / pairs;
+  if (env == 2) return 2;
+  return (2 * w2 * 100 <= 103 * w1) ? 2 : 1;
 }
 
 bool use_pair_kernel(int64_t M, int64_t N) {
@@ -869,7 +1219,8 @@ std::string gemm_kernel_name(const GemmDesc& d) {
     return "gemm_f32_kernel<" + std::to_string((int)d.trans_a) + "," +
            std::to_string((int)d.trans_b) + ">";
   if (sm100::use_pair_kernel(d.M, d.N))
-    return "gemm_bf16_2cta_kernel<" + std::to_string(am) + "," + std::to_string(bm) + ">";
+    return "gemm_bf16_2cta_kernel<" + std::to_string(am) + "," + std::to_string(bm) + "," +
+           std::to_string(256 * sm100::pair_halves(d)) + ">";
   return "gemm_bf16_kernel<" + std::to_string(d.N > 128 ? 256 : 128) + "," + std::to_string(am) +
          "," + std::to_string(bm) + ">";
 }
@@ -896,6 +1247,7 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   Params p;
   std::memset(&p, 0, sizeof(p));
   const bool pair = use_pair_kernel(d.M, d.N);
+  const int nh = pair ? pair_halves(d) : 1;
   const int BN = d.N > 128 ? 256 : 128;
   // TMA box rows for K-major operands: 128 (A, and B in the pair kernel) or BN.
   const int a_box = BM;
@@ -955,7 +1307,7 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.M = static_cast<int>(d.M);
   p.N = static_cast<int>(d.N);
   p.nb0 = static_cast<int>(d.nb0);
-  const int tile_m = pair ? 256 : BM, tile_n = pair ? 256 : BN;
+  const int tile_m = pair ? 256 : BM, tile_n = pair ? 256 * nh : BN;
   p.tiles_m = static_cast<int>((d.M + tile_m - 1) / tile_m);
   p.tiles_n = static_cast<int>((d.N + tile_n - 1) / tile_n);
   p.tiles_per_batch = p.tiles_m * p.tiles_n;
@@ -966,6 +1318,32 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   }
   p.num_tiles = static_cast<int>(nt);
   p.group_m = pair ? 8 : 16;
+  if (pair) {
+    // experiment knobs (TESS_GEMM_GROUP / _RASTER / _HINT_A / _HINT_B)
+    static const int env_group = [] {
+      const char* e = std::getenv("TESS_GEMM_GROUP");
+      return e ? std::atoi(e) : 0;
+    }();
+    static const int env_raster = [] {
+      const char* e = std::getenv("TESS_GEMM_RASTER");
+      return e ? std::atoi(e) : 0;
+    }();
+    auto hint = [](const char* name) -> unsigned long long {
+      const char* e = std::getenv(name);
+      const int v = e ? std::atoi(e) : 0;
+      return v == 1 ? 0x12F0000000000000ull    // EVICT_FIRST
+             : v == 2 ? 0x14F0000000000000ull  // EVICT_LAST
+                      : 0x1000000000000000ull; // EVICT_NORMAL
+    };
+    static const unsigned long long env_ha = hint("TESS_GEMM_HINT_A");
+    static const unsigned long long env_hb = hint("TESS_GEMM_HINT_B");
+    if (env_group > 0) p.group_m = env_group;
+    static const int env_skip = std::getenv("TESS_GEMM_SKIP_STORE") ? 1 : 0;
+    p.skip_store = env_skip;
+    p.raster_n = env_raster;
+    p.hint_a = env_ha;
+    p.hint_b = env_hb;
+  }
   p.c = d.c;
   p.c_bf16 = d.c_type == DType::BF16;
   p.ldc = d.ldc;
@@ -988,8 +1366,17 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.ss0 = d.ss0;
   p.ss1 = d.ss1;
   p.tile_n = tile_n;
+  if (pair && nh == 2 && d.epi != Epi::RowStats) {
+    static const bool env_off = std::getenv("TESS_GEMM_TMA_EPI") &&
+                                std::getenv("TESS_GEMM_TMA_EPI")[0] == '0';
+    const bool bf = d.c_type == DType::BF16;
+    p.tma_epi = !env_off &&
+                encode_out(&p.tma_c, d.c, bf, d.N, d.M, d.ldc, d.nb0, d.cs0, d.nb1, d.cs1) &&
+                (d.epi != Epi::Gelu ||
+                 encode_out(&p.tma_z, d.z, bf, d.N, d.M, d.ldz, d.nb0, d.zs0, d.nb1, d.zs1));
+  }
   p.nst = static_cast<int>((d.N + tile_n - 1) / tile_n) * kEpiHalves;
-  cudaError_t e = pair        ? launch_pair(p, a_mn, b_mn, stream)
+  cudaError_t e = pair        ? launch_pair(p, nh, a_mn, b_mn, stream)
                   : BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
                               : launch_bn<128>(p, a_mn, b_mn, stream);
   if (e != cudaSuccess) g_gemm_err = std::string("gemm_bf16_sm100 launch: ") +
