@@ -288,11 +288,18 @@ def main():
     # achieved = its algorithmic flops per launch / its mean launch duration
     top, (top_ms, top_flops, top_n) = max(per_kernel.items(), key=lambda kv: kv[1][0])
     achieved = top_flops / (top_ms * 1e-3) / 1e12 if top_ms > 0 else None
+    # DRAM bytes per launch of that kernel from the committed `ncu --set full`
+    # capture of one step (tools/ncu_step.py -> tools/ncu_digest.py)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "ncu_kernel_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            traffic = json.load(f).get(top, {}).get("dram_bytes_per_launch")
+    burst = None
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        with open(pk) as f:
+            burst = json.load(f).get("bf16_tflops")
 
     # end to end through the C-ABI with host (pinned) buffers, copies inside
     e2e = None
@@ -340,9 +347,13 @@ def main():
                          "kernel_flops_per_launch": top_flops / top_n,
                          "kernel_ms_per_launch": top_ms / top_n,
                          "kernel_share_of_step": top_ms / ms if ms else None,
-                         "all_gemm_tflops": gemm_flops / (gemm_ms * 1e-3) / 1e12,
-                         "all_gemm_ms_per_step": gemm_ms, "all_gemm_launches_per_step": gemm_n,
-                         "all_gemm_share_of_step": gemm_ms / ms if ms else None},
+                         "frac_of_burst_peak": (achieved / burst) if achieved and burst else None,
+                         # every tensor-core launch of the step (GEMMs + fused attention)
+                         "tensor_kernels_tflops": gemm_flops / (gemm_ms * 1e-3) / 1e12,
+                         "tensor_kernels_ms_per_step": gemm_ms,
+                         "tensor_kernels_launches_per_step": gemm_n,
+                         "tensor_kernels_share_of_step": gemm_ms / ms if ms else None,
+                         "per_kernel_ms_flops_launches": per_kernel},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
         }

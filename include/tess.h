@@ -302,6 +302,11 @@ tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gem
  * {"<kernel>": [device_ms, algorithmic_flops, launches], ...}. */
 tess_status tess_profile_json(char* buf, size_t cap, size_t* needed);
 
+/* Debug: with TESS_ATTN_TRACE set, the fused attention backward records
+ * per-phase clock64 stamps of its CTA 0 ([5 events][64 tiles]); copies the
+ * last trace into out (320 values). No reference counterpart. */
+tess_status tess_debug_attn_trace(long long* out, int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "kernels/kernels.h"
+#include "kernels/attention.h"
 #include "ops.h"
 
 using namespace tess;
@@ -72,6 +73,18 @@ uint64_t tess_kernel_launches(void) { return g_launches.load(); }
 
 tess_status tess_profile_enable(int on) {
   return guarded([&] { profile_enable(on != 0); });
+}
+
+tess_status tess_debug_attn_trace(long long* out, int n) {
+  if (!out || n <= 0) return TESS_ERR_INVALID;
+  long long* tr = tess::attn_debug_trace();
+  if (!tr) return TESS_ERR_INVALID;
+  cudaDeviceSynchronize();
+  const int m = n < 320 ? n : 320;
+  return cudaMemcpy(out, tr, m * sizeof(long long), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? TESS_OK
+             : TESS_ERR_CUDA;
 }
 
 tess_status tess_profile_json(char* buf, size_t cap, size_t* needed) {

@@ -48,4 +48,7 @@ cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s);
 
 const char* attn_last_error();
 
+// Debug (TESS_ATTN_TRACE): device buffer of the last traced backward, or null.
+long long* attn_debug_trace();
+
 }  // namespace tess

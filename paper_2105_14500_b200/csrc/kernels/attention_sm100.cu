@@ -32,6 +32,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -43,8 +44,10 @@ namespace tess {
 namespace {
 thread_local std::string g_attn_err;
 }
+long long* g_attn_trace = nullptr;  // debug: device buffer of the last traced backward
 
 const char* attn_last_error() { return g_attn_err.c_str(); }
+long long* attn_debug_trace() { return g_attn_trace; }
 
 namespace sm100 {
 namespace attn {
@@ -392,7 +395,15 @@ struct BwdParams {
   const float* delta;
   __nv_bfloat16* dqkv;
   long long ld_qkv;
+  long long* trace;  // debug (TESS_ATTN_TRACE): per-phase clock64 of CTA 0, [event][tile]
 };
+
+// trace events (CTA 0 only): MMA issue of S^T(i), MMA pds_full(i) seen,
+// softmax (quad-0 warp of the owning group) sdp_full(i) seen, math done, pds_full(i) arrive
+enum { TR_MMA_S = 0, TR_MMA_P = 1, TR_SM_IN = 2, TR_SM_MATH = 3, TR_SM_OUT = 4, TR_N = 5 };
+__device__ __forceinline__ void trace_ev(const BwdParams& p, int ev, int tile) {
+  if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
+}
 
 template <int HD>
 struct BwdCfg {
@@ -405,8 +416,12 @@ struct BwdCfg {
   static constexpr int OFF_RING = 2 * KV_BYTES;
   static constexpr int OFF_P = OFF_RING + RING * SLOT_BYTES;  // 2 buffers
   static constexpr int OFF_DS = OFF_P + 2 * PD_BYTES;         // 2 buffers
-  static constexpr int OFF_BAR = OFF_DS + 2 * PD_BYTES;
-  static constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;
+  static constexpr int OFF_LD = OFF_DS + 2 * PD_BYTES;  // per group x 2 bufs: lse 64 | delta 64
+  static constexpr int OFF_BAR = OFF_LD + 2 * 2 * 128 * 4;
+  static constexpr int USED = OFF_BAR + 256;
+  // the dynamic window is 1024-aligned in practice; the kernel checks and
+  // traps if the slack we could afford does not cover its misalignment
+  static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
   static constexpr int TMEM_COLS = 512;
   static constexpr int TM_ST = 0, TM_DPT = 128, TM_DV = 256, TM_DK = 384;
 };
@@ -427,9 +442,10 @@ __device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HD>;
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if ((smem - smem_raw) + C::USED > C::SMEM_BYTES) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars;                   // 1
   uint64_t* r_full = bars + 1;                // RING
@@ -438,7 +454,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* sdp_free = sdp_full + 2;          // 2
   uint64_t* pds_full = sdp_free + 2;          // 2
   uint64_t* pds_free = pds_full + 2;          // 2
-  uint64_t* fin = pds_free + 2;               // 1
+  uint64_t* ds_free = pds_free + 2;           // 2: TMA store of dS^T buffer done reading
+  uint64_t* fin = ds_free + 2;                // 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
   const int warp = threadIdx.x / 32;
@@ -457,9 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sdp_full[b], 1);
-      mbar_init(&sdp_free[b], 8);
-      mbar_init(&pds_full[b], 1);
+      mbar_init(&sdp_free[b], 4);  // the 4 warps of the group owning buffer b
+      mbar_init(&pds_full[b], 4);  // one arrive per warp of the owning group
       mbar_init(&pds_free[b], 1);
+      mbar_init(&ds_free[b], 1);
     }
     mbar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -553,6 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tc_fence_after();
       int qs = next_slot();
       int ds = next_slot();
+      trace_ev(p, TR_MMA_S, 0);
       issue_scores(tmem + C::TM_ST, sk, ring + qs * C::SLOT_BYTES);
       issue_scores(tmem + C::TM_DPT, sv, ring + ds * C::SLOT_BYTES);
       mma_commit(&sdp_full[0]);
@@ -564,12 +583,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           tc_fence_after();
           qn = next_slot();
           dn = next_slot();
+          trace_ev(p, TR_MMA_S, i + 1);
           issue_scores(tmem + C::TM_ST + (b ^ 1) * 64, sk, ring + qn * C::SLOT_BYTES);
           issue_scores(tmem + C::TM_DPT + (b ^ 1) * 64, sv, ring + dn * C::SLOT_BYTES);
           mma_commit(&sdp_full[b ^ 1]);
         }
         mbar_wait(&pds_full[b], (i >> 1) & 1);
         tc_fence_after();
+        trace_ev(p, TR_MMA_P, i);
         issue_grad(tmem + C::TM_DV, smem_u32(smem + C::OFF_P + b * C::PD_BYTES),
                    ring + ds * C::SLOT_BYTES, i > 0);
         mma_commit(&r_empty[ds]);
@@ -584,66 +605,119 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     }
   } else {
     // ------------------------------------------ softmax-gradient warps
+    // Two groups of 4 warps alternate query tiles (group g takes tiles
+    // i = g, g+2, ...), so one group's TMEM reads / math / smem writes overlap
+    // the other's; group g owns S^T/dP^T TMEM buffer g and P^T/dS^T smem
+    // buffer g. Warp (g, quad): key rows quad*32.., all 64 query columns of
+    // its tiles in two 32-column chunks.
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;  // query columns [half*32, half*32+32)
+    const int g = (warp - 2) >> 2;
+    const int half = g;                // dK/dV epilogue column half
     const int r = quad * 32 + lane;    // key row within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float cl2 = p.c, scale = p.scale;
-    const bool storer = warp == 2 && lane == 0;
+    const bool storer = quad == 0 && lane == 0;  // one TMA-store thread per group
     const float* lse_h = p.lse + ((long long)smp * p.H + head) * p.S;
     const float* dlt_h = p.delta + ((long long)smp * p.H + head) * p.S;
-    for (int i = 0; i < p.n_qt; ++i) {
-      const int b = i & 1;
-      const int qc = i * BQB + half * 32;  // first query column of this thread
-      float lv[32], dv[32];
-      if (qc + 32 <= p.S) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(lse_h + qc) + e);
-          const float4 d = __ldg(reinterpret_cast<const float4*>(dlt_h + qc) + e);
-          lv[4 * e] = a.x; lv[4 * e + 1] = a.y; lv[4 * e + 2] = a.z; lv[4 * e + 3] = a.w;
-          dv[4 * e] = d.x; dv[4 * e + 1] = d.y; dv[4 * e + 2] = d.z; dv[4 * e + 3] = d.w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const bool ok = qc + e < p.S;
-          lv[e] = ok ? lse_h[qc + e] : INFINITY;  // 2^(x - inf) = 0: no contribution
-          dv[e] = ok ? dlt_h[qc + e] : 0.f;
-        }
-      }
-      mbar_wait(&sdp_full[b], (i >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[32], dr[32];
-      tmem_ld32_nowait(tmem + lane_off + C::TM_ST + b * 64 + half * 32, sr);
-      tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + b * 64 + half * 32, dr);
-      tmem_wait_ld();
-      reg_fence32(sr);
-      reg_fence32(dr);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sdp_free[b]);
-      float pv[32], gv[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        pv[e] = ex2_approx(fmaf(__uint_as_float(sr[e]), cl2, -lv[e]));
-        gv[e] = pv[e] * (__uint_as_float(dr[e]) - dv[e]) * scale;
-      }
-      // P^T / dS^T buffer b is free once dV/dK of tile i-2 completed and the
-      // TMA store of dS^T(i-2) has read it.
-      mbar_wait(&pds_free[b], ((i >> 1) & 1) ^ 1);
-      if (storer) bulk_wait_read<1>();
-      named_bar_sync(1, 256);
-      store_row32(smem_u32(smem + C::OFF_P + b * C::PD_BYTES), r, half * 4, pv);
-      store_row32(smem_u32(smem + C::OFF_DS + b * C::PD_BYTES), r, half * 4, gv);
-      fence_proxy_async_smem();
-      named_bar_sync(1, 256);
+    // (lse, delta) of the group's tiles staged through shared memory, double
+    // buffered per group: the quad-0 warp loads tile i+2's 64 + 64 values
+    // while tile i is processed (L2 latency hidden), a 128-thread named
+    // barrier at the start of each tile orders them against the readers.
+    const uint32_t ldg_base = smem_u32(smem + C::OFF_LD) + (uint32_t)g * 1024u;  // [buf][lse|delta]
+    const bool ld_writer = quad == 0;
+    auto gload = [&](int i, float (&v)[4]) {
+      const int q0 = i * BQB + lane;
+      const bool ok0 = i < p.n_qt && q0 < p.S, ok1 = i < p.n_qt && q0 + 32 < p.S;
+      v[0] = ok0 ? __ldg(lse_h + q0) : INFINITY;  // 2^(x - inf) = 0: no contribution
+      v[1] = ok1 ? __ldg(lse_h + q0 + 32) : INFINITY;
+      v[2] = ok0 ? __ldg(dlt_h + q0) : 0.f;
+      v[3] = ok1 ? __ldg(dlt_h + q0 + 32) : 0.f;
+    };
+    auto sstore = [&](int i, const float (&v)[4]) {
+      const uint32_t a = ldg_base + (uint32_t)((i >> 1) & 1) * 512u + lane * 4;
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[0]) : "memory");
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 128), "f"(v[1]) : "memory");
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 256), "f"(v[2]) : "memory");
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 384), "f"(v[3]) : "memory");
+    };
+    if (ld_writer) {
+      float v[4];
+      gload(g, v);
+      sstore(g, v);
+    }
+    const int b = g;
+    const uint32_t p_buf = smem_u32(smem + C::OFF_P + b * C::PD_BYTES);
+    const uint32_t ds_buf = smem_u32(smem + C::OFF_DS + b * C::PD_BYTES);
+    for (int i = g; i < p.n_qt; i += 2) {
+      const uint32_t k = (uint32_t)(i >> 1) & 1u;  // phase of this buffer's k-th use
+      const uint32_t ldw = ldg_base + k * 512u;    // this tile's (lse, delta)
+      named_bar_sync(1 + g, 128);  // tile i's staging written; tile i-2's readers done
+      float nv[4];
+      if (ld_writer) gload(i + 2, nv);
       if (storer) {
+        // dS^T buffer b was last stored at tile i-2 by this thread: wait for
+        // that TMA store to finish reading, then release the buffer
+        bulk_wait_read<0>();
+        mbar_arrive(&ds_free[b]);
+      }
+      mbar_wait(&sdp_full[b], k);
+      tc_fence_after();
+      if (quad == 0 && lane == 0) trace_ev(p, TR_SM_IN, i);
+      bool waited = false;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32_nowait(tmem + lane_off + C::TM_ST + b * 64 + c * 32, sr);
+        tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + b * 64 + c * 32, dr);
+        tmem_wait_ld();
+        reg_fence32(sr);
+        reg_fence32(dr);
+        if (c == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sdp_free[b]);
+        }
+        float pv[32], gv[32];
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          float4 l4, d4;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w)
+                       : "r"(ldw + (uint32_t)(c * 32 + 4 * e4) * 4u));
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
+                       : "r"(ldw + 256u + (uint32_t)(c * 32 + 4 * e4) * 4u));
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = 4 * e4 + u;
+            pv[e] = ex2_approx(fmaf(__uint_as_float(sr[e]), cl2, -lv[u]));
+            gv[e] = pv[e] * (__uint_as_float(dr[e]) - dv[u]) * scale;
+          }
+        }
+        if (!waited) {
+          if (quad == 0 && lane == 0) trace_ev(p, TR_SM_MATH, i);
+          // buffer b: dV/dK of tile i-2 done and its dS^T TMA store has read it
+          mbar_wait(&pds_free[b], k ^ 1u);
+          mbar_wait(&ds_free[b], k);
+          waited = true;
+        }
+        store_row32(p_buf, r, c * 4, pv);
+        store_row32(ds_buf, r, c * 4, gv);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pds_full[b]);
+      if (quad == 0 && lane == 0) trace_ev(p, TR_SM_OUT, i);
+      if (storer) {
+        mbar_wait(&pds_full[b], k);  // the group's 4 warps wrote their rows
         tma_store_3d(&p.tm_dst, smem + C::OFF_DS + b * C::PD_BYTES, i * BQB, k0,
                      smp * p.H + head);
         bulk_commit();
-        mbar_arrive(&pds_full[b]);
       }
+      // tile i+2's (lse, delta) into the other staging buffer (last read at tile i-2)
+      if (ld_writer) sstore(i + 2, nv);
     }
     // ------------------------------------------------- dK, dV epilogue
     mbar_wait(fin, 0);
@@ -819,6 +893,14 @@ cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s) {
   p.delta = d.delta;
   p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
   p.ld_qkv = d.ld_qkv;
+  p.trace = nullptr;
+  if (std::getenv("TESS_ATTN_TRACE")) {
+    static long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, TR_N * 64 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, TR_N * 64 * sizeof(long long), s);
+    p.trace = tr;
+    g_attn_trace = tr;
+  }
   const long long grid = (long long)p.n_kt * d.heads * d.samples;
   if (grid > 0x7fffffffLL) {
     g_attn_err = "attn_bwd_sm100: grid too large";
@@ -830,3 +912,7 @@ cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s) {
 }
 
 }  // namespace tess
+// shared-memory budgets (227 KB opt-in per CTA)
+static_assert(tess::sm100::attn::FwdCfg<128>::SMEM_BYTES <= 232448, "attn fwd smem");
+static_assert(tess::sm100::attn::BwdCfg<128>::USED <= 232448, "attn bwd smem");
+static_assert(tess::sm100::attn::BwdCfg<64>::USED <= 232448, "attn bwd smem");
