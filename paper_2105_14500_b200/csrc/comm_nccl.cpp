@@ -107,6 +107,18 @@ class NcclComm : public Comm {
     ncclUniqueId id;
     std::memcpy(&id, uid128, sizeof(id));
     TESS_NCCL(nccl().CommInitRank(&world_, g.size(), id, rank));
+    // The row/column/depth communicators run their kernels on at most
+    // `budget` CTAs, and the persistent GEMMs leave that many SMs free, so the
+    // comm stream's broadcasts / reductions overlap the GEMMs instead of
+    // queueing behind them (TESS_NCCL_SMS, default 8; 0 = NCCL defaults).
+    const char* env = std::getenv("TESS_NCCL_SMS");
+    const int budget = env ? std::atoi(env) : 8;
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (budget > 0) {
+      cfg.minCTAs = 1;
+      cfg.maxCTAs = budget;
+      if (g.size() > 1) gemm_set_sm_reserve(budget);
+    }
     for (int f = 0; f < 3; ++f) {
       const Family fam = Family(f);
       if (g.group_size(fam) == 1) {
@@ -117,7 +129,7 @@ class NcclComm : public Comm {
         continue;
       }
       TESS_NCCL(nccl().CommSplit(world_, g.group_index(c_, fam), g.slot_in_group(c_, fam),
-                              &comm_[f], nullptr));
+                              &comm_[f], budget > 0 ? &cfg : nullptr));
       int nr = 0, me = 0;
       TESS_NCCL(nccl().CommCount(comm_[f], &nr));
       TESS_NCCL(nccl().CommUserRank(comm_[f], &me));

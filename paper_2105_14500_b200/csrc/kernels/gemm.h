@@ -95,6 +95,10 @@ cudaError_t gemm_f32_simt(const GemmDesc& d, cudaStream_t stream);
 // (e.g. bf16 rows that are not 16-byte aligned, which TMA cannot address).
 cudaError_t gemm(const GemmDesc& d, cudaStream_t stream);
 
+// Leave `sms` SMs free of the persistent GEMM grids (process-wide maximum of
+// all requests): set by the NCCL backend so its kernels overlap the GEMMs.
+void gemm_set_sm_reserve(int sms);
+
 // Last dispatch-level error text (thread local), for the C-ABI's
 // tess_last_error.
 const char* gemm_last_error();

@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -1110,6 +1111,11 @@ bool encode_view(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer
   return true;
 }
 
+std::atomic<int> g_sm_reserve{0};
+
+// SMs the persistent GEMMs may occupy: all of them, minus the ones left for
+// NCCL kernels when this process has peers (gemm_set_sm_reserve), so that
+// collectives on the comm stream run concurrently with the GEMMs.
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1118,7 +1124,8 @@ int num_sms() {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }
-  return n;
+  const int r = g_sm_reserve.load(std::memory_order_relaxed);
+  return (r > 0 && r < n - 2) ? ((n - r) & ~1) : n;
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -1241,6 +1248,12 @@ thread_local std::string g_gemm_err;
 }
 
 const char* gemm_last_error() { return g_gemm_err.c_str(); }
+
+void gemm_set_sm_reserve(int sms) {
+  int cur = sm100::g_sm_reserve.load();
+  while (sms > cur && !sm100::g_sm_reserve.compare_exchange_weak(cur, sms)) {
+  }
+}
 
 std::string gemm_kernel_name(const GemmDesc& d) {
   const int am = d.trans_a ? 1 : 0, bm = d.trans_b ? 0 : 1;

@@ -307,3 +307,43 @@ def test_summa_is_tesseract_d1(tess, orc):
     want, _, sk = orc.tesseract_matmul(a, b, 2, 1, "nn")
     got = tess.summa_matmul(a, b, 2)
     assert rel_diff(got.value, want) <= 1e-5 and (got.stats.per_kind == sk).all()
+
+
+def test_nccl_backend_world1_matches_local(tess, orc):
+    """The NCCL backend (dlopen'd libnccl, world communicator + the three
+    ncclCommSplits with NCCL_SPLIT_NOCOLOR for single-member groups) on a
+    [1,1,1] grid runs a bf16 Transformer block bitwise like the in-process
+    backend. (NCCL refuses two ranks on one GPU, so N>1 data movement is
+    covered by the in-process backend on every grid instead.)"""
+    import torch
+    b, s, h, nh = 2, 64, 128, 2
+    x, dy, P = _layer_inputs(orc, b, s, h, 11, bf16r)
+    dev = torch.device("cuda", 0)
+    bf = torch.bfloat16
+    names = ("w_qkv", "w_proj", "w_ff1", "w_ff2")
+    W = [torch.tensor(P[k], dtype=torch.float32, device=dev).to(bf).contiguous() for k in names]
+    LN = [torch.tensor(P[k], dtype=torch.float32, device=dev).contiguous()
+          for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")]
+    xt = torch.tensor(x, dtype=torch.float32, device=dev).to(bf)
+    dyt = torch.tensor(dy, dtype=torch.float32, device=dev).to(bf)
+    shard = tess.BlockShardC(*[t.data_ptr() for t in W + LN], 1e-5)
+    dims = tess.LayerDims(b, s, h, nh)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for kind in ("local", "nccl"):
+        ctx = (tess.init_local(tess.GridSpec(1, 1))[0] if kind == "local" else
+               tess.init_nccl(tess.GridSpec(1, 1), 0, 0, tess.nccl_unique_id()))
+        try:
+            y, dx = torch.empty_like(xt), torch.empty_like(xt)
+            G = [torch.zeros(t.shape, device=dev) for t in W + LN]
+            grads = tess.BlockGradsC(*[t.data_ptr() for t in G])
+            ctx.layer_forward("block", "bf16", dims, shard, xt.data_ptr(), y.data_ptr(), stream=st)
+            ctx.layer_backward("block", "bf16", dims, shard, dyt.data_ptr(), dx.data_ptr(), grads,
+                               stream=st)
+            torch.cuda.synchronize()
+            ctx.barrier()
+            outs.append([y.clone(), dx.clone()] + [g.clone() for g in G])
+        finally:
+            ctx.close()
+    for a, c in zip(*outs):
+        assert torch.equal(a, c)
