@@ -74,7 +74,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, which):
+        """Host time bounds of the timed region (samples outside are dropped)."""
+        setattr(self, which, time.time())
 
     def stop(self):
         if self.proc:
@@ -85,7 +89,10 @@ class ClockSampler:
                 self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        for ts, ln in self.lines:
+            if t0 is not None and t1 is not None and not (t0 <= ts <= t1 + 0.15):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -257,24 +264,47 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # the sampler starts before the warm-up (nvidia-smi needs ~0.5 s to come
+    # up) and keeps only the samples taken inside the timed region
+    clocks = ClockSampler(local_rank)
+    clocks.start()
     for _ in range(args.warmup):
         step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
     barrier()
-    clocks = ClockSampler(local_rank)
-    clocks.start()
     launches0 = tess.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    clocks.mark("t0")
     e0.record(stream)
     for _ in range(args.steps):
         step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
     e1.record(stream)
     barrier()
+    clocks.mark("t1")
     clk = clocks.stop()
     launches = tess.kernel_launches() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     flops = layer_flops(batch, s, h)
     value = flops / (ms * 1e-3) / 1e12
+
+    # exposed communication: the same step with every collective
+    # metered but moving no data; exposed = (t - t_noop) / t, max over ranks.
+    # A one-rank grid has no collectives at all: exposed is 0 by construction.
+    if p == 1:
+        ms_noop, exposed = ms, 0.0
+    else:
+        ctx.set_comm_noop(True)
+        for _ in range(2):
+            step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
+        e1.record(stream)
+        barrier()
+        ctx.set_comm_noop(False)
+        ms_noop = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        exposed = max(0.0, (ms - ms_noop) / ms) if ms else None
 
     # dominant kernel: the tcgen05 GEMM, timed per launch with events on its stream
     tess.profile_enable(True)
@@ -354,6 +384,8 @@ def main():
                          "tensor_kernels_launches_per_step": gemm_n,
                          "tensor_kernels_share_of_step": gemm_ms / ms if ms else None,
                          "per_kernel_ms_flops_launches": per_kernel},
+            "exposed_comm_pct": 100.0 * exposed if exposed is not None else None,
+            "ms_per_step_without_comm": ms_noop,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
         }

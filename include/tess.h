@@ -228,6 +228,13 @@ tess_status tess_layer_backward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtyp
  * BlockCacheRank objects, layers.hpp:114-119). Default 0. */
 tess_status tess_set_cache_slot(tess_ctx* ctx, int slot);
 
+/* Measurement switch (no reference counterpart): with enable != 0 every
+ * collective of this context is metered and traced as usual but moves no
+ * data, so a step timed this way is the step without communication; the
+ * exposed-communication share of the step is (t - t_noop) / t.
+ * Results computed while it is on are meaningless. */
+tess_status tess_set_comm_noop(tess_ctx* ctx, int enable);
+
 /* ---------------------------------------------------------- global level
  * Whole-matrix operators with host fp64 buffers, mirroring the reference's
  * value-semantics API: partition -> per-rank SPMD (one host thread per rank,
@@ -303,8 +310,8 @@ tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gem
 tess_status tess_profile_json(char* buf, size_t cap, size_t* needed);
 
 /* Debug: with TESS_ATTN_TRACE set, the fused attention backward records
- * per-phase clock64 stamps of its CTA 0 ([5 events][64 tiles]); copies the
- * last trace into out (320 values). No reference counterpart. */
+ * per-phase clock64 stamps of its CTA 0 ([8 events][64 tiles]); copies the
+ * last trace into out (up to 512 values). No reference counterpart. */
 tess_status tess_debug_attn_trace(long long* out, int n);
 
 #ifdef __cplusplus

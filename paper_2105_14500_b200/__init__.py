@@ -147,6 +147,7 @@ def _load() -> C.CDLL:
         "tess_get_comm_stats": ([vp, C.POINTER(CommStatsC)], i),
         "tess_reset_comm_stats": ([vp], i),
         "tess_set_trace": ([vp, i], i),
+        "tess_set_comm_noop": ([vp, i], i),
         "tess_trace_text": ([vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], i),
         "tess_broadcast": ([vp, i, i, vp, C.c_size_t, C.c_size_t, vp], i),
         "tess_reduce": ([vp, i, i, vp, vp, C.c_size_t, vp], i),
@@ -547,6 +548,11 @@ class RankContext:
 
     def reset_stats(self):
         _check(lib.tess_reset_comm_stats(self.h))
+
+    def set_comm_noop(self, on=True):
+        """Collectives metered but moving no data (timing the step without
+        communication: exposed comm = (t - t_noop) / t)."""
+        _check(lib.tess_set_comm_noop(self.h, int(on)))
 
     def set_trace(self, on=True):
         _check(lib.tess_set_trace(self.h, int(on)))

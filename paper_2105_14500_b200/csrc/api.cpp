@@ -80,7 +80,7 @@ tess_status tess_debug_attn_trace(long long* out, int n) {
   long long* tr = tess::attn_debug_trace();
   if (!tr) return TESS_ERR_INVALID;
   cudaDeviceSynchronize();
-  const int m = n < 320 ? n : 320;
+  const int m = n < 512 ? n : 512;
   return cudaMemcpy(out, tr, m * sizeof(long long), cudaMemcpyDeviceToHost) ==
                  cudaSuccess
              ? TESS_OK
@@ -251,6 +251,13 @@ tess_status tess_set_cache_slot(tess_ctx* c, int slot) {
     if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
     if (slot < 0) fail(TESS_ERR_INVALID, "cache slot must be >= 0");
     c->cache_slot = slot;
+  });
+}
+
+tess_status tess_set_comm_noop(tess_ctx* c, int enable) {
+  return guarded([&] {
+    if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
+    c->comm_noop = enable != 0;
   });
 }
 

@@ -264,20 +264,20 @@ void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t el
                 cudaStream_t s) {
   c.meter.bcast(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, elements);
   trace_event(c, 0, f, root, elements);
-  c.comm->bcast(f, root, buf, bytes, s);
+  if (!c.comm_noop) c.comm->bcast(f, root, buf, bytes, s);
 }
 
 void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, size_t n,
                  cudaStream_t s) {
   c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, n, false);
   trace_event(c, 1, f, root, n);
-  c.comm->reduce(f, root, send, recv, n, s);
+  if (!c.comm_noop) c.comm->reduce(f, root, send, recv, n, s);
 }
 
 void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s) {
   c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), 0, n, true);
   trace_event(c, 2, f, 0, n);
-  c.comm->allreduce(f, buf, n, s);
+  if (!c.comm_noop) c.comm->allreduce(f, buf, n, s);
 }
 
 }  // namespace tess

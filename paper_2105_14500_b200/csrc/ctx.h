@@ -19,6 +19,9 @@ struct tess_ctx {
   std::shared_ptr<tess::LocalWorld> world;  // in-process backend only
   tess::Meter meter;
   bool trace_on = false;
+  // Measurement only (tess_set_comm_noop): collectives are metered and traced
+  // but move no data, to time the step without communication (exposed comm).
+  bool comm_noop = false;
   uint64_t step = 0;  // collective sequence number (RankCtx::step_)
   std::vector<tess::TraceEvent> trace;
   std::unique_ptr<tess::Workspace> ws;

@@ -400,7 +400,10 @@ struct BwdParams {
 
 // trace events (CTA 0 only): MMA issue of S^T(i), MMA pds_full(i) seen,
 // softmax (quad-0 warp of the owning group) sdp_full(i) seen, math done, pds_full(i) arrive
-enum { TR_MMA_S = 0, TR_MMA_P = 1, TR_SM_IN = 2, TR_SM_MATH = 3, TR_SM_OUT = 4, TR_N = 5 };
+enum {
+  TR_MMA_S = 0, TR_MMA_P = 1, TR_SM_IN = 2, TR_SM_MATH = 3, TR_SM_OUT = 4,
+  TR_SM_LOADED = 5, TR_MMA_FREE = 6, TR_MMA_GDONE = 7, TR_N = 8
+};
 __device__ __forceinline__ void trace_ev(const BwdParams& p, int ev, int tile) {
   if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
 }
@@ -591,6 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         mbar_wait(&pds_full[b], (i >> 1) & 1);
         tc_fence_after();
         trace_ev(p, TR_MMA_P, i);
+        // (TR_MMA_FREE / TR_MMA_GDONE bracket this tile's gradient issue)
         issue_grad(tmem + C::TM_DV, smem_u32(smem + C::OFF_P + b * C::PD_BYTES),
                    ring + ds * C::SLOT_BYTES, i > 0);
         mma_commit(&r_empty[ds]);
@@ -598,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
                    ring + qs * C::SLOT_BYTES, i > 0);
         mma_commit(&r_empty[qs]);
         mma_commit(&pds_free[b]);
+        trace_ev(p, TR_MMA_GDONE, i);
         qs = qn;
         ds = dn;
       }
@@ -676,6 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sdp_free[b]);
+          if (quad == 0 && lane == 0) trace_ev(p, TR_SM_LOADED, i);
         }
         float pv[32], gv[32];
 #pragma unroll
@@ -896,8 +902,8 @@ cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s) {
   p.trace = nullptr;
   if (std::getenv("TESS_ATTN_TRACE")) {
     static long long* tr = nullptr;
-    if (!tr) cudaMalloc(&tr, TR_N * 64 * sizeof(long long));
-    cudaMemsetAsync(tr, 0, TR_N * 64 * sizeof(long long), s);
+    if (!tr) cudaMalloc(&tr, 8 * 64 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), s);
     p.trace = tr;
     g_attn_trace = tr;
   }

@@ -347,3 +347,52 @@ def test_nccl_backend_world1_matches_local(tess, orc):
             ctx.close()
     for a, c in zip(*outs):
         assert torch.equal(a, c)
+
+
+def test_comm_noop_keeps_schedule_and_meter(tess, orc):
+    """tess_set_comm_noop (bench.py's exposed-communication measurement): the
+    [2,2,2] NN product runs through the same schedule with no data moved --
+    identical CommStats, and switching it off restores the exact result."""
+    import torch
+    q, d = 2, 2
+    grid = tess.GridSpec(q, d)
+    M, K, N = 128, 96, 64
+    a = f32r(orc.random_matrix(M, K, 13, 0))
+    b = f32r(orc.random_matrix(K, N, 13, 1))
+    want, _, _ = orc.tesseract_matmul(a, b, q, d, "nn")
+    ab = orc.partition(a, q, d, 0)
+    bb = orc.partition(b, q, d, 1)
+    ctxs = tess.init_local(grid)
+    outs = [None] * grid.size()
+    stats = {}
+    errs = []
+
+    def run(r, noop):
+        try:
+            cx = ctxs[r]
+            cx.set_comm_noop(noop)
+            cx.reset_stats()
+            la = torch.from_numpy(ab[r].astype(np.float32)).cuda()
+            lb = torch.from_numpy(bb[r].astype(np.float32)).cuda()
+            lc = torch.zeros((la.shape[0], lb.shape[1]), dtype=torch.float32, device="cuda")
+            cx.matmul("nn", "f32", la.data_ptr(), *la.shape, lb.data_ptr(), *lb.shape,
+                      lc.data_ptr())
+            torch.cuda.synchronize()
+            outs[r] = lc.cpu().numpy().astype(np.float64)
+            stats[(noop, r)] = cx.stats()["by_kind"]
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    try:
+        for noop in (True, False):
+            th = [threading.Thread(target=run, args=(r, noop)) for r in range(grid.size())]
+            [t.start() for t in th]
+            [t.join() for t in th]
+            assert not errs, errs
+        got = orc.combine(outs, M, N, q, d, 0)
+        assert rel_diff(got, want) <= 1e-5
+        for r in range(grid.size()):
+            assert stats[(True, r)] == stats[(False, r)]
+    finally:
+        for cx in ctxs:
+            cx.close()
