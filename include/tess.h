@@ -213,7 +213,10 @@ tess_status tess_matmul(tess_ctx* ctx, tess_variant v, tess_dtype in, const void
  * grads may be NULL (the collective sequence is unchanged, ref:
  * layers.cpp:372-377); with accumulate=0 gradients are overwritten, else
  * added (ref: layers.cpp:368-371 add()). dbias (BiasAdd) is fp32 [hidden/q],
- * valid on i == 0 ranks (ref: layers.cpp:507-517). */
+ * valid on i == 0 ranks (ref: layers.cpp:507-517).
+ * Host outputs (y, dx in host memory) leave on the context's copy stream so
+ * they overlap the caller's next work; order a stream after them with
+ * tess_stream_join before reading them (the global operators do). */
 tess_status tess_layer_forward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
                                const tess_layer_dims* dims, const tess_block_shard* shard,
                                const void* bias_row0, const void* x, void* y, void* stream);
@@ -221,6 +224,12 @@ tess_status tess_layer_backward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtyp
                                 const tess_layer_dims* dims, const tess_block_shard* shard,
                                 const void* dy, void* dx, tess_block_grads* grads,
                                 int accumulate, float* dbias, void* stream);
+
+/* Makes `stream` wait for everything the context still has in flight on its
+ * side streams: pending host copies of layer outputs and deferred
+ * collectives (the reference's calls return completed values; this is the
+ * completion point of the asynchronous C-ABI). */
+tess_status tess_stream_join(tess_ctx* ctx, void* stream);
 
 /* Selects the forward-cache slot used by subsequent tess_layer_forward /
  * tess_layer_backward calls on this context, so a stack of layers can keep

@@ -148,6 +148,7 @@ def _load() -> C.CDLL:
         "tess_reset_comm_stats": ([vp], i),
         "tess_set_trace": ([vp, i], i),
         "tess_set_comm_noop": ([vp, i], i),
+        "tess_stream_join": ([vp, vp], i),
         "tess_trace_text": ([vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], i),
         "tess_broadcast": ([vp, i, i, vp, C.c_size_t, C.c_size_t, vp], i),
         "tess_reduce": ([vp, i, i, vp, vp, C.c_size_t, vp], i),
@@ -548,6 +549,11 @@ class RankContext:
 
     def reset_stats(self):
         _check(lib.tess_reset_comm_stats(self.h))
+
+    def stream_join(self, stream=0):
+        """Order `stream` after the context's in-flight host copies of layer
+        outputs and deferred collectives (read host outputs after this)."""
+        _check(lib.tess_stream_join(self.h, C.c_void_p(stream)))
 
     def set_comm_noop(self, on=True):
         """Collectives metered but moving no data (timing the step without

@@ -254,6 +254,14 @@ tess_status tess_set_cache_slot(tess_ctx* c, int slot) {
   });
 }
 
+tess_status tess_stream_join(tess_ctx* c, void* stream) {
+  return guarded([&] {
+    if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
+    TESS_CUDA(cudaSetDevice(c->device));
+    ctx_join(*c, static_cast<cudaStream_t>(stream));
+  });
+}
+
 tess_status tess_set_comm_noop(tess_ctx* c, int enable) {
   return guarded([&] {
     if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");

@@ -292,5 +292,6 @@ tess_ctx::~tess_ctx() {
     cudaStreamSynchronize(copy_s);
     cudaStreamDestroy(copy_s);
   }
+  for (auto& kv : copy_ev) cudaEventDestroy(kv.second);
   for (auto e : ev_ring) cudaEventDestroy(e);
 }

@@ -34,9 +34,11 @@ struct tess_ctx {
   // the compute stream (created on first use; the compute stream itself when
   // the grid has a single rank). Cross-stream ordering uses a ring of events.
   cudaStream_t comm_s = nullptr;
-  // Side stream for host copies of layer outputs (overlaps the next call).
+  // Side stream for host copies of layer outputs (overlaps the next call);
+  // pending device->host copies per staging buffer, joined before the buffer
+  // is rewritten or by tess_stream_join.
   cudaStream_t copy_s = nullptr;
-  bool copy_pending = false;
+  std::map<std::string, cudaEvent_t> copy_ev;
   std::vector<cudaEvent_t> ev_ring;
   size_t ev_next = 0;
   ~tess_ctx();
@@ -58,6 +60,10 @@ void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s);
 // Records a collective whose group has a single member (no data moves): the
 // reference still counts the call in its trace step sequence.
 void coll_note_single(Ctx& c, int kind, Family f, int root, uint64_t elements);
+
+// Makes s wait for everything this context still has in flight on its side
+// streams (collectives, host copies of layer outputs): tess_stream_join.
+void ctx_join(Ctx& c, cudaStream_t s);
 
 // The rank's comm stream (== s when the grid has one rank).
 cudaStream_t comm_stream(Ctx& c, cudaStream_t s);

@@ -67,6 +67,7 @@ struct Runner {
           TESS_CUDA(cudaSetDevice(c.device));
           TESS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
           fn(c, s);
+          ctx_join(c, s);  // host copies of layer outputs + deferred collectives
           TESS_CUDA(cudaStreamSynchronize(s));
         } catch (const tess::Error& e) {
           local_world_fail(c.world.get(), e.what());

@@ -454,10 +454,28 @@ cudaStream_t copy_stream(Ctx& c) {
   return c.copy_s;
 }
 
-void join_copies(Ctx& c, cudaStream_t s) {
-  if (!c.copy_pending) return;
-  stream_dep(c, c.copy_s, s);
-  c.copy_pending = false;
+// s waits for the pending host copy out of staging buffer `name` (if any).
+void join_copy(Ctx& c, const std::string& name, cudaStream_t s) {
+  auto it = c.copy_ev.find(name);
+  if (it == c.copy_ev.end()) return;
+  TESS_CUDA(cudaStreamWaitEvent(s, it->second, 0));
+  cudaEventDestroy(it->second);
+  c.copy_ev.erase(it);
+}
+
+// Device staging buffer -> host on the context's copy stream, after the work
+// enqueued on s so far: the copy overlaps whatever the caller enqueues next
+// (the backward, or the next step's input upload: PCIe is full duplex).
+void async_d2h(Ctx& c, const std::string& name, void* host, const void* dev, size_t bytes,
+               cudaStream_t s) {
+  join_copy(c, name, s);
+  cudaStream_t cp = copy_stream(c);
+  stream_dep(c, s, cp);
+  TESS_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, cp));
+  cudaEvent_t ev;
+  TESS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  TESS_CUDA(cudaEventRecord(ev, cp));
+  c.copy_ev[name] = ev;
 }
 
 std::string cache_tag(const Ctx& c, tess_layer_op op) {
@@ -483,7 +501,6 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   const int64_t rows = rd.rows, hq = rd.hq;
   const size_t act = (size_t)rows * hq * dtype_size(t);
   const std::string tag = cache_tag(c, op);
-  join_copies(c, s);  // a previous host copy of the staging buffer must be done
   // Host buffers are staged through the context (x kept until backward).
   const void* x = x_in;
   if (!is_device_ptr(x_in)) {
@@ -492,6 +509,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     x = xs;
   }
   void* y = is_device_ptr(y_out) ? y_out : wsget(c, "stage.y", act);
+  if (y != y_out) join_copy(c, "stage.y", s);  // its previous host copy must be done
   // weight panels of the whole layer go out on the comm stream first
   const WeightPanels wp =
       prefetch_weights(c, t, rd, p, op == TESS_OP_ATTENTION || op == TESS_OP_BLOCK,
@@ -541,15 +559,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       fail(TESS_ERR_INVALID, "unknown layer op");
   }
   join_comm(c, s);
-  if (y != y_out) {
-    // The host copy of y runs on a copy stream, overlapping whatever the
-    // caller enqueues next (normally the backward); the next layer call joins
-    // it before reusing the staging buffer.
-    cudaStream_t cp = copy_stream(c);
-    stream_dep(c, s, cp);
-    TESS_CUDA(cudaMemcpyAsync(y_out, y, act, cudaMemcpyDeviceToHost, cp));
-    c.copy_pending = true;
-  }
+  if (y != y_out) async_d2h(c, "stage.y", y_out, y, act, s);
   c.fwd_x[c.cache_slot * 8 + (int)op] = x;  // the backward needs the forward input
 }
 
@@ -570,6 +580,7 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     dy = ds;
   }
   void* dx = is_device_ptr(dx_out) ? dx_out : wsget(c, "stage.dx", act);
+  if (dx != dx_out) join_copy(c, "stage.dx", s);  // its previous host copy must be done
   const WeightPanels wp =
       prefetch_weights(c, t, rd, p, op == TESS_OP_ATTENTION || op == TESS_OP_BLOCK,
                        op == TESS_OP_FEEDFORWARD || op == TESS_OP_BLOCK, s);
@@ -628,8 +639,16 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   }
   // deferred weight/LN-gradient communication completes before we return
   join_comm(c, s);
-  join_copies(c, s);  // the forward's host copy of y completes within this call
-  if (dx != dx_out) TESS_CUDA(cudaMemcpyAsync(dx_out, dx, act, cudaMemcpyDeviceToHost, s));
+  if (dx != dx_out) async_d2h(c, "stage.dx", dx_out, dx, act, s);
+}
+
+void ctx_join(Ctx& c, cudaStream_t s) {
+  join_comm(c, s);
+  for (auto& kv : c.copy_ev) {
+    TESS_CUDA(cudaStreamWaitEvent(s, kv.second, 0));
+    cudaEventDestroy(kv.second);
+  }
+  c.copy_ev.clear();
 }
 
 }  // namespace tess
