@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 
 #include "../core.h"
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace tess {
@@ -283,6 +285,167 @@ __global__ void ln_params_partial_kernel(const TD* dy, const TX* x, const float*
   }
   part[((int64_t)blockIdx.y * 2 + 0) * w + c] = dg;
   part[((int64_t)blockIdx.y * 2 + 1) * w + c] = db;
+}
+
+// ---- fused single-pass LayerNorm for a one-member row group (q == 1) -------
+// With q == 1 the row all-reduce between the statistics and the apply moves
+// nothing, so a block keeps its rows in registers and does stats + apply
+// (forward) or stats + dx + dgain/dbias partials (backward) in ONE pass over
+// HBM with 16-byte vector accesses. Thread t owns columns
+// [t*8 + v*4096, +8) for v < NV (block 512 threads, w = NV * 4096).
+constexpr int kLnThreads = 512;
+constexpr int kLnSpan = kLnThreads * 8;  // columns per vector pass
+
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void ld8(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// Deterministic block sums of two values (fixed-order combine of warp sums).
+__device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();  // red is reused row after row
+  if (lane == 0) red[warp] = make_float2(a, b);
+  __syncthreads();
+  float2 t = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int w = 0; w < kLnThreads / 32; ++w) {
+    t.x += red[w].x;
+    t.y += red[w].y;
+  }
+  return t;
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(kLnThreads) ln_fused_fwd_kernel(
+    const T* __restrict__ x, int64_t rows, const float* __restrict__ gain,
+    const float* __restrict__ bias, float eps, T* __restrict__ y, float* __restrict__ mean_out,
+    float* __restrict__ rstd_out) {
+  __shared__ float2 red[kLnThreads / 32];
+  constexpr int w = NV * kLnSpan;
+  const int c0 = threadIdx.x * 8;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    float v[NV][8];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      ld8(x + r * w + c0 + k * kLnSpan, v[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += v[k][e];
+    }
+    const float mu = block_sum2(s, 0.f, red).x / (float)w;
+    float m2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = v[k][e] - mu;
+        m2 += d * d;
+      }
+    const float var = block_sum2(m2, 0.f, red).x / (float)w;
+    const float rstd = 1.0f / sqrtf(var + eps);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float g[8], b[8], o[8];
+      ld8(gain + c0 + k * kLnSpan, g);
+      ld8(bias + c0 + k * kLnSpan, b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = g[e] * ((v[k][e] - mu) * rstd) + b[e];
+      st8(y + r * w + c0 + k * kLnSpan, o);
+    }
+    if (threadIdx.x == 0) {
+      mean_out[r] = mu;
+      rstd_out[r] = rstd;
+    }
+  }
+}
+
+// dx = rstd * (dxhat - mean(dxhat) - xhat * mean(xhat*dxhat)) (+ resid), with
+// per-block column partials of dgain = sum dy*xhat, dbias = sum dy into
+// part[block][2][w] (summed over blocks in fixed order afterwards).
+template <typename TD, typename TX, typename TR, typename TO, int NV>
+__global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
+    const TD* __restrict__ dy, const TX* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ gain, int64_t rows,
+    const TR* __restrict__ resid, TO* __restrict__ dx, float* __restrict__ part) {
+  __shared__ float2 red[kLnThreads / 32];
+  constexpr int w = NV * kLnSpan;
+  const int c0 = threadIdx.x * 8;
+  float dg[NV][8], db[NV][8];  // gain is re-read per row (L1-resident) to save registers
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dg[k][e] = db[k][e] = 0.f;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float mu = mean[r], rs = rstd[r];
+    float d[NV][8], xh[NV][8];
+    float a = 0.f, b = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float g[8];
+      ld8(dy + r * w + c0 + k * kLnSpan, d[k]);
+      ld8(x + r * w + c0 + k * kLnSpan, xh[k]);
+      ld8(gain + c0 + k * kLnSpan, g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xh[k][e] = (xh[k][e] - mu) * rs;
+        const float dxh = d[k][e] * g[e];
+        a += dxh;
+        b += xh[k][e] * dxh;
+        dg[k][e] += d[k][e] * xh[k][e];
+        db[k][e] += d[k][e];
+      }
+    }
+    const float2 t = block_sum2(a, b, red);
+    const float md = t.x / (float)w, mxd = t.y / (float)w;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float o[8], g[8];
+      ld8(gain + c0 + k * kLnSpan, g);
+      if (resid) ld8(resid + r * w + c0 + k * kLnSpan, o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = rs * (d[k][e] * g[e] - md - xh[k][e] * mxd);
+        o[e] = resid ? o[e] + v : v;
+      }
+      st8(dx + r * w + c0 + k * kLnSpan, o);
+    }
+  }
+  if (part) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      st8(part + ((int64_t)blockIdx.x * 2 + 0) * w + c0 + k * kLnSpan, dg[k]);
+      st8(part + ((int64_t)blockIdx.x * 2 + 1) * w + c0 + k * kLnSpan, db[k]);
+    }
+  }
 }
 
 // ------------------------------------------------------------- softmax
@@ -655,6 +818,92 @@ void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t ro
                                                                        rows, L, scale));
   count_launch();
   TESS_CUDA(cudaGetLastError());
+}
+
+
+// ---- fused LayerNorm launchers (q == 1) -----------------------------------
+int ln_fused_nv(int64_t w) {
+  if (w % kLnSpan != 0) return 0;
+  const int64_t nv = w / kLnSpan;
+  return (nv >= 1 && nv <= 4) ? (int)nv : 0;
+}
+
+// fwd: 4 blocks per SM; bwd: 2 (each block's dgain/dbias partials are summed
+// afterwards, so fewer blocks = less partial traffic)
+int ln_fused_blocks(int64_t rows, int per_sm = 2) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t b = std::min<int64_t>(rows, (int64_t)sms * per_sm);
+  return (int)std::max<int64_t>(b, 1);
+}
+
+bool k_ln_fused_supported(int64_t w) { return ln_fused_nv(w) > 0; }
+
+size_t k_ln_fused_scratch_floats(int64_t rows, int64_t w) {
+  return (size_t)ln_fused_blocks(rows) * 2 * w;
+}
+
+template <int NV>
+void ln_fwd_nv(const void* x, DType t, int64_t rows, const float* gain, const float* bias,
+               float eps, void* y, float* mean, float* rstd, cudaStream_t s) {
+  const int g = ln_fused_blocks(rows, 4);
+  TESS_DISPATCH(t, T, ln_fused_fwd_kernel<T, NV><<<g, kLnThreads, 0, s>>>(
+      (const T*)x, rows, gain, bias, eps, (T*)y, mean, rstd));
+}
+
+void k_ln_fused_fwd(const void* x, DType t, int64_t rows, int64_t w, const float* gain,
+                    const float* bias, double eps, void* y, float* mean, float* rstd,
+                    cudaStream_t s) {
+  if (!rows) return;
+  const float e = (float)eps;
+  switch (ln_fused_nv(w)) {
+    case 1: ln_fwd_nv<1>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
+    case 2: ln_fwd_nv<2>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
+    case 3: ln_fwd_nv<3>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
+    case 4: ln_fwd_nv<4>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
+    default: fail(TESS_ERR_UNSUPPORTED, "fused LayerNorm: hidden/q must be a multiple of 4096");
+  }
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+template <int NV>
+void ln_bwd_nv(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+               const float* rstd, const float* gain, int64_t rows, const void* resid, DType tr,
+               void* dx, DType tdx, float* part, cudaStream_t s) {
+  const int g = ln_fused_blocks(rows);
+  TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR, TESS_DISPATCH(tdx, TO,
+      ln_fused_bwd_kernel<TD, TX, TR, TO, NV><<<g, kLnThreads, 0, s>>>(
+          (const TD*)dy, (const TX*)x, mean, rstd, gain, rows, (const TR*)resid, (TO*)dx,
+          part)))));
+}
+
+void k_ln_fused_bwd(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                    const float* rstd, const float* gain, int64_t rows, int64_t w,
+                    const void* resid, DType tr, void* dx, DType tdx, float* out2w,
+                    float* scratch, cudaStream_t s) {
+  if (!rows) {
+    if (out2w) TESS_CUDA(cudaMemsetAsync(out2w, 0, 2 * w * 4, s));
+    return;
+  }
+  float* part = out2w ? scratch : nullptr;
+  switch (ln_fused_nv(w)) {
+    case 1: ln_bwd_nv<1>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
+    case 2: ln_bwd_nv<2>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
+    case 3: ln_bwd_nv<3>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
+    case 4: ln_bwd_nv<4>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
+    default: fail(TESS_ERR_UNSUPPORTED, "fused LayerNorm: hidden/q must be a multiple of 4096");
+  }
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+  if (out2w) {
+    const int64_t nb = ln_fused_blocks(rows);
+    colsum_finalize_kernel<<<(unsigned)((2 * w + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+        scratch, nb, w, 2, out2w);
+    count_launch();
+    TESS_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace tess

@@ -63,6 +63,22 @@ void k_ln_bwd_params(const void* dy, DType tdy, const void* x, DType tx, const f
                      cudaStream_t s);
 size_t k_ln_params_scratch_floats(int64_t rows, int64_t w);
 
+// Fused single-pass LayerNorm for a one-member row group (q == 1: the row
+// all-reduce between statistics and apply moves nothing). Supported when
+// w % 4096 == 0 and w <= 16384; bitwise-deterministic.
+bool k_ln_fused_supported(int64_t w);
+// y = gain * (x - mean) * rstd + bias over the local w columns (= hidden).
+void k_ln_fused_fwd(const void* x, DType t, int64_t rows, int64_t w, const float* gain,
+                    const float* bias, double eps, void* y, float* mean, float* rstd,
+                    cudaStream_t s);
+// dx (+ resid) and, if out2w, [dgain | dbias] column sums (fixed-order
+// two-stage reduction through scratch).
+void k_ln_fused_bwd(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                    const float* rstd, const float* gain, int64_t rows, int64_t w,
+                    const void* resid, DType tr, void* dx, DType tdx, float* out2w,
+                    float* scratch, cudaStream_t s);
+size_t k_ln_fused_scratch_floats(int64_t rows, int64_t w);
+
 // ---- softmax (ref layers.cpp:44-74) ---------------------------------------
 // P = softmax_rows(S) with max subtraction; S fp32 [rows, L] (already scaled).
 void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cudaStream_t s);

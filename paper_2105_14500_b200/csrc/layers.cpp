@@ -68,6 +68,15 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   float* stats = static_cast<float*>(wsget(c, "ln.stats", rows * 3 * 4));
   float* mean = static_cast<float*>(wsget(c, tag + ".mean", rows * 4));
   float* rstd = static_cast<float*>(wsget(c, tag + ".rstd", rows * 4));
+  if (c.grid.q == 1 && k_ln_fused_supported(w)) {
+    // one-member row group: the [rows, 2] all-reduce moves nothing (still
+    // metered and traced like the reference), so stats + apply is one pass
+    c.meter.reduce(1, 0, 0, (uint64_t)rows * 2, true);
+    if (c.trace_on) c.trace.push_back({c.rank, c.step, 2, ROW, 0, (uint64_t)rows * 2 * 8});
+    c.step++;
+    k_ln_fused_fwd(x, t, rows, w, gain, bias, eps, y, mean, rstd, s);
+    return;
+  }
   k_ln_stats(x, t, rows, w, stats, s);
   // ref layers.cpp:258: row all-reduce of the [rows, 2] sums (metered as such)
   c.meter.reduce(c.grid.group_size(ROW), c.grid.slot_in_group(c.coord, ROW), 0,
@@ -90,20 +99,34 @@ void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   const float* mean = static_cast<const float*>(wsget(c, tag + ".mean", rows * 4));
   const float* rstd = static_cast<const float*>(wsget(c, tag + ".rstd", rows * 4));
   float* stats = static_cast<float*>(wsget(c, "ln.bstats", rows * 2 * 4));
-  k_ln_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, s);
   cudaStream_t cs = comm_stream(c, s);
-  stream_dep(c, s, cs);
-  coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305
-  stream_dep(c, cs, s);
-  k_ln_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w, (double)rd.hidden_total,
-                 resid, tr, dx, tdx, s);
-  if (dgain || dbias) {
-    // per-LN buffers: the all-reduces and the gradient update stay on the
-    // comm stream (joined at the end of the layer backward)
-    float* packed = static_cast<float*>(wsget(c, tag + ".packed", 2 * w * 4));
-    float* scratch =
-        static_cast<float*>(wsget(c, "ln.pscratch", k_ln_params_scratch_floats(rows, w) * 4));
-    k_ln_bwd_params(dy, tdy, x, t, mean, rstd, rows, w, packed, scratch, s);
+  const bool want_params = dgain || dbias;
+  // per-LN buffers: the all-reduces and the gradient update stay on the
+  // comm stream (joined at the end of the layer backward)
+  float* packed =
+      want_params ? static_cast<float*>(wsget(c, tag + ".packed", 2 * w * 4)) : nullptr;
+  if (c.grid.q == 1 && k_ln_fused_supported(w)) {
+    // one-member row group: the [rows, 2] all-reduce moves nothing, so row
+    // statistics, dx and the dgain/dbias partials are one pass over dy, x
+    coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305 (metered)
+    float* scratch = static_cast<float*>(
+        wsget(c, "ln.fscratch", k_ln_fused_scratch_floats(rows, w) * 4));
+    k_ln_fused_bwd(dy, tdy, x, t, mean, rstd, gain, rows, w, resid, tr, dx, tdx, packed,
+                   scratch, s);
+  } else {
+    k_ln_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, s);
+    stream_dep(c, s, cs);
+    coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305
+    stream_dep(c, cs, s);
+    k_ln_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w, (double)rd.hidden_total,
+                   resid, tr, dx, tdx, s);
+    if (want_params) {
+      float* scratch =
+          static_cast<float*>(wsget(c, "ln.pscratch", k_ln_params_scratch_floats(rows, w) * 4));
+      k_ln_bwd_params(dy, tdy, x, t, mean, rstd, rows, w, packed, scratch, s);
+    }
+  }
+  if (want_params) {
     stream_dep(c, s, cs);
     coll_allreduce(c, COL, packed, 2 * w, cs);    // ref layers.cpp:331
     coll_allreduce(c, DEPTH, packed, 2 * w, cs);  // ref layers.cpp:332

@@ -396,3 +396,77 @@ def test_comm_noop_keeps_schedule_and_meter(tess, orc):
     finally:
         for cx in ctxs:
             cx.close()
+
+
+@pytest.mark.parametrize("q,d,allow", [(1, 1, False), (1, 2, True)])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layernorm_fused_single_pass(tess, orc, q, d, allow, dtype):
+    """hidden/q a multiple of 4096 with a one-member row group: the fused
+    single-pass LayerNorm kernels (stats + apply; stats + dx + dgain/dbias)
+    against the fp64 oracle."""
+    b, s, h, nh = 2, 8, 4096, 32
+    rnd = f32r if dtype == "f32" else bf16r
+    x, dy, P = _layer_inputs(orc, b, s, h, 17, rnd)
+    want = orc.layer_run("layernorm", x, dy, P, b, s, nh)
+    res = tess.layer_run("layernorm", x, dy, P, tess.LayerDims(b, s, h, nh),
+                         tess.GridSpec(q, d, allow), dtype=dtype)
+    if dtype == "f32":
+        _compare_layer(res, want, 1e-5, rel_diff)
+    else:
+        _compare_layer(res, want, 2e-2, frob)
+    sr, sk = orc.layer_stats("layernorm", q, d, b, s, h)
+    assert (res.stats.per_rank == sr).all() and (res.stats.per_kind == sk).all()
+
+
+@pytest.mark.parametrize("h", [8192, 12288])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layernorm_fused_vs_torch(tess, h, dtype):
+    """The fused LayerNorm at the wider hidden sizes (two and three 4096-column
+    passes per thread; 12288 is cfg4's) against torch fp32 LayerNorm fwd+bwd
+    (eps 1e-5, ref layers.hpp:48) on the same rounded inputs."""
+    import torch
+    torch.manual_seed(1)
+    dev = torch.device("cuda", 0)
+    rows = 64
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    x = torch.randn(rows, h, device=dev).to(tdt)
+    dy = torch.randn(rows, h, device=dev).to(tdt)
+    gain = (1 + 0.1 * torch.randn(h, device=dev)).float()
+    bias = (0.1 * torch.randn(h, device=dev)).float()
+    ctx = tess.init_local(tess.GridSpec(1, 1))[0]
+    try:
+        dummy = torch.zeros(8, device=dev, dtype=tdt)
+        shard = tess.BlockShardC(*[dummy.data_ptr()] * 4, gain.data_ptr(), bias.data_ptr(),
+                                 gain.data_ptr(), bias.data_ptr(), 1e-5)
+        G = [torch.zeros(8, device=dev) for _ in range(4)] + \
+            [torch.zeros(h, device=dev) for _ in range(4)]
+        grads = tess.BlockGradsC(*[t.data_ptr() for t in G])
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        dims = tess.LayerDims(1, rows, h, 32)
+        st = torch.cuda.current_stream().cuda_stream
+        ctx.layer_forward("layernorm", dtype, dims, shard, x.data_ptr(), y.data_ptr(), stream=st)
+        ctx.layer_backward("layernorm", dtype, dims, shard, dy.data_ptr(), dx.data_ptr(), grads,
+                           stream=st)
+        torch.cuda.synchronize()
+    finally:
+        ctx.close()
+    xr = x.float().requires_grad_(True)
+    g_, b_ = gain.clone().requires_grad_(True), bias.clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (h,), g_, b_, eps=1e-5)
+    yr.backward(dy.float())
+    tol = 1e-5 if dtype == "f32" else 1e-2
+
+    def rel(a, r):
+        return ((a.float() - r).norm() / r.norm()).item()
+    errs = {"y": rel(y, yr.detach()), "dx": rel(dx, xr.grad), "dgain": rel(G[4], g_.grad),
+            "dbias": rel(G[5], b_.grad)}
+    assert max(errs.values()) <= tol, errs
+
+
+def test_block_fused_layernorm_bf16(tess, orc):
+    b, s, h, nh = 1, 8, 4096, 32
+    x, dy, P = _layer_inputs(orc, b, s, h, 18, bf16r)
+    want = orc.layer_run("block", x, dy, P, b, s, nh)
+    res = tess.layer_run("block", x, dy, P, tess.LayerDims(b, s, h, nh), tess.GridSpec(1, 1),
+                         dtype="bf16")
+    _compare_layer(res, want, 2e-2, frob)
