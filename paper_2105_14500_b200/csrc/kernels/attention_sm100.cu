@@ -20,8 +20,9 @@
 //               while the other tile's softmax runs.
 //   warps 2-5   softmax of tile A (warp w owns TMEM lanes 32*(w%4)..+31:
 //               thread = query row), warps 6-9 tile B. Row max / exp2 /
-//               row sum in registers; P (bf16) written to shared memory in
-//               the UMMA K-major 128B-swizzled layout; lazy rescaling of O
+//               row sum in registers; P (bf16) written back over the consumed
+//               S columns of tensor memory, the P V MMA reading its A operand
+//               from TMEM (only V streams from shared memory); lazy rescaling of O
 //               (only when the running max grows by more than 2^8, exact
 //               because the final normalisation uses the same max).
 // TMEM: S_A [0,128), S_B [128,256), O_A [256,256+hd), O_B [384,384+hd).
@@ -58,6 +59,7 @@ constexpr int BKV = 128;  // keys per tile (UMMA N of S, K of P V)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
+
 struct FwdParams {
   CUtensorMap tm_qkv;  // 3-D view [cols, S, samples] of qkv, box {64, 128, 1}
   int S, H, n_pairs, n_kv;
@@ -72,35 +74,15 @@ template <int HD>
 struct FwdCfg {
   static constexpr int Q_BYTES = BQ * HD * 2;    // one 128-row tile of Q (or K, V)
   static constexpr int KV_BYTES = BKV * HD * 2;
-  static constexpr int P_BYTES = BQ * BKV * 2;
-  static constexpr int KV_STAGES = HD == 128 ? 3 : 6;
+  static constexpr int KV_STAGES = HD == 128 ? 5 : 10;
   static constexpr int OFF_QA = 0;
   static constexpr int OFF_QB = Q_BYTES;
-  static constexpr int OFF_PA = 2 * Q_BYTES;
-  static constexpr int OFF_PB = OFF_PA + P_BYTES;
-  static constexpr int OFF_KV = OFF_PB + P_BYTES;
+  static constexpr int OFF_KV = 2 * Q_BYTES;
   static constexpr int OFF_BAR = OFF_KV + KV_STAGES * KV_BYTES;
   static constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;  // + barriers + alignment slack
   static constexpr int TMEM_COLS = 512;
   static constexpr int TM_S0 = 0, TM_O0 = 256;
 };
-
-// P (bf16, row r of this thread, 128 keys) -> shared memory, UMMA K-major
-// SWIZZLE_128B layout: [key chunk kc (64 keys)][row][128 B], 16-byte unit u of
-// a row stored at unit u ^ (row % 8).
-__device__ __forceinline__ void store_p_row(uint32_t p_base, int r, const float (&p)[BKV]) {
-  const uint32_t row_base = p_base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
-#pragma unroll
-  for (int kc = 0; kc < 2; ++kc) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k0 = kc * 64 + u * 8;
-      st_shared_v4(row_base + kc * 16384u + (uint32_t)((u ^ (r & 7)) << 4),
-                   pack_bf16x2(p[k0 + 0], p[k0 + 1]), pack_bf16x2(p[k0 + 2], p[k0 + 3]),
-                   pack_bf16x2(p[k0 + 4], p[k0 + 5]), pack_bf16x2(p[k0 + 6], p[k0 + 7]));
-    }
-  }
-}
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ FwdParams p) {
@@ -185,7 +167,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       constexpr uint32_t idesc_s = idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16(BQ, HD, false, true);
       const uint32_t sq0 = smem_u32(smem + C::OFF_QA);  // Q_B, P_B follow at fixed offsets
-      const uint32_t sp0 = smem_u32(smem + C::OFF_PA);
       int stage = 0;
       uint32_t phase = 0;
       auto next_kv = [&]() {
@@ -207,14 +188,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         mma_commit(&s_full[t]);
       };
+      // O += P V with P (bf16 pairs) in tensor memory: the consumed S columns
+      // [0, 64) of the tile's S buffer, 8 columns per 16 keys
       auto issue_pv = [&](int t, uint32_t skv, bool acc) {
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint32_t aoff = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
-          mma_bf16(tmem + C::TM_O0 + t * 128, make_sdesc(sp0 + t * C::P_BYTES + aoff, 16, 1024),
-                   make_sdesc(skv + (uint32_t)kk * 2048u, 16384, 1024), idesc_pv,
-                   (acc || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16_ts(tmem + C::TM_O0 + t * 128, tmem + C::TM_S0 + t * BKV + kk * 8,
+                      make_sdesc(skv + (uint32_t)kk * 2048u, 16384, 1024), idesc_pv,
+                      (acc || kk > 0) ? 1u : 0u);
       };
       mbar_wait(q_full, 0);
       tc_fence_after();
@@ -255,7 +236,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t t_s = tmem + lane_off + C::TM_S0 + t * BKV;
     const uint32_t t_o = tmem + lane_off + C::TM_O0 + t * 128;
-    const uint32_t p_base = smem_u32(smem + (t == 0 ? C::OFF_PA : C::OFF_PB));
     const float cl2 = p.c;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < p.n_kv; ++j) {
@@ -311,6 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         m_used = m_new;
       }
+      // all exponentials on MUFU: moving a share to the FMA pipe (exp2_poly)
+      // measured slower (25 %: +6 %, 50 %: +22 %) -- the softmax is issue-bound
       float rs = 0.f;
 #pragma unroll
       for (int e = 0; e < BKV; ++e) {
@@ -318,8 +300,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         rs += s[e];
       }
       l += rs;
-      store_p_row(p_base, r, s);
-      fence_proxy_async_smem();
+      // P (bf16 pairs, lower key in the low half) over the consumed S columns
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) pk[e] = pack_bf16x2(s[h * 64 + 2 * e], s[h * 64 + 2 * e + 1]);
+        tmem_st32(t_s + h * 32, pk);
+      }
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);

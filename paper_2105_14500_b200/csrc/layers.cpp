@@ -380,13 +380,20 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   if (use_fused_attn(t, rd)) {
     void* o = wsget(c, tag + ".o", rows * hq * esz);
     float* lse = static_cast<float*>(wsget(c, tag + ".lse", (size_t)rd.samples_local * H * S * 4));
-    float* dout32 = static_cast<float*>(wsget(c, "attn.dout32", rows * hq * 4));
+    float* dout32 =
+        c.grid.q == 1 ? nullptr : static_cast<float*>(wsget(c, "attn.dout32", rows * hq * 4));
     void* dout = wsget(c, "attn.dout", rows * hq * esz);
     void* dqkv = wsget(c, "attn.dqkv", rows * ld * esz);
     float* delta = static_cast<float*>(wsget(c, "attn.delta", (size_t)rd.samples_local * H * S * 4));
     void* dst = wsget(c, "attn.dst", (size_t)rd.samples_local * H * S * S * esz);
-    nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
-    k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
+    if (c.grid.q == 1) {
+      // no row reduce: the GEMM epilogue rounds straight to bf16 (bitwise the
+      // same as fp32 + convert)
+      nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout, t), s, &wp.proj);
+    } else {
+      nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
+      k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
+    }
     weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
     for (int64_t smp = 0; smp < rd.samples_local; ++smp)
       k_attn_delta(static_cast<const char*>(dout) + (size_t)smp * S * hq * esz,
