@@ -774,14 +774,15 @@ struct TileQ {
 // consumers per tile: leader MMA thread + 8 epilogue warps per CTA + peer producer
 constexpr int kTQConsumers = 1 + 8 + 1 + 8;
 
-template <int ST, int NH>
+template <int ST, int NH, int BNP = 256>
 struct Cfg2 {
-  static constexpr int HALF = 128;  // rows of A / columns of B per CTA and half
+  static constexpr int HALF = 128;       // rows of A per CTA
+  static constexpr int BH = BNP / 2;     // columns of B per CTA and half (MMA N = BNP)
   static constexpr int A_BYTES = HALF * BK * 2;
-  static constexpr int B_BYTES = NH * HALF * BK * 2;
+  static constexpr int B_BYTES = NH * BH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = ST;
-  static constexpr int TMEM_COLS = 512;  // 2 x 256 fp32 columns
+  static constexpr int TMEM_COLS = 512;  // 2 accumulator slots of up to 256 fp32 columns
   // NH = 2: per-epilogue-warp TMA-store staging (2 x 2 KB per warp)
   static constexpr int EPI_BYTES = NH == 2 ? 8 * 4096 : 0;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
@@ -814,10 +815,10 @@ __device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int&
   }
 }
 
-template <bool A_MN, bool B_MN, int ST, int NH>
+template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
-  using C = Cfg2<ST, NH>;
+  using C = Cfg2<ST, NH, BNP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -910,13 +911,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
               // the pair's columns [n0 + 256h, +256): this CTA stages its 128
-              const int nr = n0 + h * 256 + (int)cta * C::HALF;
-              uint8_t* sbh = sb + h * (C::HALF * BK * 2);
+              const int nr = n0 + h * BNP + (int)cta * C::BH;
+              uint8_t* sbh = sb + h * (C::BH * BK * 2);
               if (!B_MN) {
                 tma_load_4d_2sm(sbh, mb, &full_bar[stage], k, nr, b0, b1, p.hint_b);
               } else {
 #pragma unroll
-                for (int c = 0; c < C::HALF / 64; ++c)
+                for (int c = 0; c < C::BH / 64; ++c)
                   tma_load_4d_2sm(sbh + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0, b1,
                                   p.hint_b);
               }
@@ -933,7 +934,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0 && cta == 0) {
       // ------------------------------------------ MMA issuer (leader CTA)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(256 >> 3) << 17) |
+                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BNP >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
@@ -954,8 +955,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               mbar_wait(&tempty_bar[slot], ((slot_phase >> slot) & 1) ^ 1);
               tc_fence_after();
             }
-            const uint32_t d_tmem = tmem_base + slot * 256;
-            const uint32_t sbh = sb + h * (C::HALF * BK * 2);
+            const uint32_t d_tmem = tmem_base + slot * BNP;
+            const uint32_t sbh = sb + h * (C::BH * BK * 2);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = A_MN ? make_sdesc(sa + k * 2048, 8192, 1024)
@@ -999,8 +1000,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int slot = NH == 1 ? acc : h;
         mbar_wait(&tfull_bar[slot], (slot_phase >> slot) & 1);
         tc_fence_after();
-        const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + slot * 256;
-        epilogue_tile(p, b0, b1, m, n0 + h * 256, 256, trow, (warp - 2) / 4,
+        const uint32_t trow = tmem_base + ((uint32_t)(quad * 32) << 16) + slot * BNP;
+        epilogue_tile(p, b0, b1, m, n0 + h * BNP, BNP, trow, (warp - 2) / 4,
                       tma_epi ? &st : nullptr, lane, mrow0);
         tc_fence_before();
         __syncwarp();
@@ -1167,38 +1168,42 @@ int* tile_counter_slot(cudaStream_t stream) {
   return slot;
 }
 
-template <bool A_MN, bool B_MN, int ST, int NH>
+template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
 cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
   Params p = p_in;
   static const bool static_order = std::getenv("TESS_GEMM_STATIC") != nullptr;
   p.tile_counter = static_order ? nullptr : tile_counter_slot(stream);
-  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH>;
+  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP>;
+  using C = Cfg2<ST, NH, BNP>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg2<ST, NH>::SMEM_BYTES);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   static const bool nonpersist = std::getenv("TESS_GEMM_NONPERSIST") != nullptr;
   const int pairs = std::max(1, num_sms() / 2);
   const int grid = 2 * (nonpersist ? p.num_tiles : std::min(p.num_tiles, pairs));
-  kern<<<grid, kThreads, Cfg2<ST, NH>::SMEM_BYTES, stream>>>(p);
+  kern<<<grid, kThreads, C::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <int ST, int NH>
+template <int ST, int NH, int BNP>
 cudaError_t launch_pair_st(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
-  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH>(p, s);
-  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH>(p, s);
-  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH>(p, s);
-  return launch_2cta<true, false, ST, NH>(p, s);
+  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH, BNP>(p, s);
+  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH, BNP>(p, s);
+  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH, BNP>(p, s);
+  return launch_2cta<true, false, ST, NH, BNP>(p, s);
 }
 
-cudaError_t launch_pair(const Params& p, int nh, bool a_mn, bool b_mn, cudaStream_t s) {
-  // smem ring depth: 7 x 32 KB stages for 256 x 256 tiles, 4 x 48 KB for 256 x 512
-  if (nh == 2) return launch_pair_st<4, 2>(p, a_mn, b_mn, s);
-  return launch_pair_st<7, 1>(p, a_mn, b_mn, s);
+// tile_n = 128: 256 x 128 pair tiles (N = hd products); 256: 256 x 256,
+// two TMEM accumulators; 512: 256 x 512 (NH = 2, see Cfg2).
+cudaError_t launch_pair(const Params& p, int tile_n, bool a_mn, bool b_mn, cudaStream_t s) {
+  // smem ring depth: 9 x 24 KB (128), 7 x 32 KB (256), 4 x 48 KB (512)
+  if (tile_n == 512) return launch_pair_st<4, 2, 256>(p, a_mn, b_mn, s);
+  if (tile_n == 128) return launch_pair_st<9, 1, 128>(p, a_mn, b_mn, s);
+  return launch_pair_st<7, 1, 256>(p, a_mn, b_mn, s);
 }
 
 // 256-column halves per pair tile (see Cfg2): 2 when the wider tile does not
@@ -1224,13 +1229,25 @@ int pair_halves(const GemmDesc& d) {
   return (2 * w2 * 100 <= slack * w1) ? 2 : 1;
 }
 
+// Pair-tile width: 128 for N <= 128 (the N = head_dim products), else 256 per
+// accumulator half (x pair_halves).
+int pair_tile_n(const GemmDesc& d) {
+  if (d.N <= 128) return 128;
+  return 256 * pair_halves(d);
+}
+
 bool use_pair_kernel(int64_t M, int64_t N) {
   static int mode = -1;  // TESS_GEMM_2CTA=0 forces the 1-CTA kernel (A/B testing)
   if (mode < 0) {
     const char* e = std::getenv("TESS_GEMM_2CTA");
     mode = (e && e[0] == '0') ? 0 : 1;
   }
-  return mode == 1 && M > 128 && N > 128;
+  // 256 x 128 pair tiles (N <= 128) are opt-in (TESS_GEMM_PAIR128=1): the one
+  // such product of the step (dQ = dS K, N = head_dim) is HBM-bound on reading
+  // dS^T, where they measured no better than the 1-CTA 128 x 128 kernel
+  static const bool pair128 = std::getenv("TESS_GEMM_PAIR128") &&
+                              std::getenv("TESS_GEMM_PAIR128")[0] == '1';
+  return mode == 1 && M > 128 && (N > 128 || (pair128 && N > 64));
 }
 
 template <int BN>
@@ -1262,7 +1279,7 @@ std::string gemm_kernel_name(const GemmDesc& d) {
            std::to_string((int)d.trans_b) + ">";
   if (sm100::use_pair_kernel(d.M, d.N))
     return "gemm_bf16_2cta_kernel<" + std::to_string(am) + "," + std::to_string(bm) + "," +
-           std::to_string(256 * sm100::pair_halves(d)) + ">";
+           std::to_string(sm100::pair_tile_n(d)) + ">";
   return "gemm_bf16_kernel<" + std::to_string(d.N > 128 ? 256 : 128) + "," + std::to_string(am) +
          "," + std::to_string(bm) + ">";
 }
@@ -1273,7 +1290,8 @@ int gemm_bf16_stat_tiles(const GemmDesc& d) {
 }
 
 int gemm_bf16_tile_n(const GemmDesc& d) {
-  return (sm100::use_pair_kernel(d.M, d.N) || d.N > 128) ? 256 : 128;
+  if (sm100::use_pair_kernel(d.M, d.N)) return sm100::pair_tile_n(d);
+  return d.N > 128 ? 256 : 128;
 }
 
 cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
@@ -1289,11 +1307,12 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   Params p;
   std::memset(&p, 0, sizeof(p));
   const bool pair = use_pair_kernel(d.M, d.N);
-  const int nh = pair ? pair_halves(d) : 1;
+  const int pair_tn = pair ? pair_tile_n(d) : 0;
+  const int nh = pair_tn == 512 ? 2 : 1;
   const int BN = d.N > 128 ? 256 : 128;
   // TMA box rows for K-major operands: 128 (A, and B in the pair kernel) or BN.
   const int a_box = BM;
-  const int b_box = pair ? 128 : BN;
+  const int b_box = pair ? (pair_tn == 128 ? 64 : 128) : BN;
   const bool a_mn = d.trans_a;   // A stored [K, M]: M contiguous
   const bool b_mn = !d.trans_b;  // B stored [K, N]: N contiguous
   int total_kb = 0;
@@ -1349,7 +1368,7 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.M = static_cast<int>(d.M);
   p.N = static_cast<int>(d.N);
   p.nb0 = static_cast<int>(d.nb0);
-  const int tile_m = pair ? 256 : BM, tile_n = pair ? 256 * nh : BN;
+  const int tile_m = pair ? 256 : BM, tile_n = pair ? pair_tn : BN;
   p.tiles_m = static_cast<int>((d.M + tile_m - 1) / tile_m);
   p.tiles_n = static_cast<int>((d.N + tile_n - 1) / tile_n);
   p.tiles_per_batch = p.tiles_m * p.tiles_n;
@@ -1418,7 +1437,7 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
                  encode_out(&p.tma_z, d.z, bf, d.N, d.M, d.ldz, d.nb0, d.zs0, d.nb1, d.zs1));
   }
   p.nst = static_cast<int>((d.N + tile_n - 1) / tile_n) * kEpiHalves;
-  cudaError_t e = pair        ? launch_pair(p, nh, a_mn, b_mn, stream)
+  cudaError_t e = pair        ? launch_pair(p, pair_tn, a_mn, b_mn, stream)
                   : BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
                               : launch_bn<128>(p, a_mn, b_mn, stream);
   if (e != cudaSuccess) g_gemm_err = std::string("gemm_bf16_sm100 launch: ") +
