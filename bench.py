@@ -34,6 +34,19 @@ HIDDEN, HEADS, SEQ, B_PER_GPU = 12288, 96, 2048, 4
 SAMPLE = dict(batch=4, seq=128, hidden=512, heads=8)
 
 
+def arm_config(gpus, grid_str=None):
+    """The `config` both arms report: BASELINE configs[3] at this GPU count."""
+    q, d, _ = GRIDS.get(gpus, (1, 1, True))
+    p = d * q * q
+    batch = B_PER_GPU * p
+    return {"workload": "cfg4: Tesseract Transformer block fwd+bwd (attention, no mask, + "
+                        "MLP + distributed LayerNorm), weak scaling b=4*p",
+            "grid": grid_str or f"[{q},{q},{d}]", "global_batch": batch, "seq_len": SEQ,
+            "hidden": HIDDEN, "heads": HEADS, "rows_per_rank": batch * SEQ // (d * q),
+            "parallelism": f"tesseract[{q},{q},{d}]",
+            "l2": "inputs larger than L2 (per-GPU weights+activations >> 126 MB)"}
+
+
 def layer_flops(batch, seq, hidden):
     """Algorithmic flops of one block fwd+bwd (2*m*n*k of GEMMs + attention
     contractions): 72*T*h^2 + 12*T*s*h, T = batch*seq."""
@@ -160,7 +173,9 @@ def run_reference_arm(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "reference CPU layer_run(Block) sample", **SAMPLE},
+            # same workload as the GPU arm; each step runs a bounded sample of it
+            # (flop-normalised, see cpu_baseline.sample)
+            "config": {**arm_config(args.gpus), "reference_sample": dict(SAMPLE)},
             "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": kind,
                              "sample": desc},
             "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -365,12 +380,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random inputs and random-init weights of the named shapes)",
-            "config": {
-                "workload": "cfg4: Tesseract Transformer block fwd+bwd (attention, no mask, + "
-                            "MLP + distributed LayerNorm), weak scaling b=4*p",
-                "grid": grid.to_string(), "global_batch": batch, "seq_len": s, "hidden": h,
-                "heads": nh, "rows_per_rank": rows, "parallelism": f"tesseract{grid}",
-                "l2": "inputs larger than L2 (per-GPU weights+activations >> 126 MB)"},
+            "config": arm_config(args.gpus, grid.to_string()),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "peak_source": f"{peak_src} bf16_tflops_sustained", "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,

@@ -291,8 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         m_used = m_new;
       }
-      // all exponentials on MUFU: moving a share to the FMA pipe (exp2_poly)
-      // measured slower (25 %: +6 %, 50 %: +22 %) -- the softmax is issue-bound
+      // all exponentials on MUFU: moving a share to the FMA pipe (a degree-5
+      // polynomial exp2) measured slower (25 %: +6 %, 50 %: +22 %) -- the
+      // softmax is issue-bound, not MUFU-bound
       float rs = 0.f;
 #pragma unroll
       for (int e = 0; e < BKV; ++e) {

@@ -283,23 +283,6 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-// 2^x on the FMA pipe (offloads the MUFU unit): Cody-Waite split by the
-// 1.5*2^23 magic-number rounding, 2^f for f in [-0.5, 0.5] by a degree-5
-// polynomial (rel. err < 4e-6), exponent added in the integer domain.
-// x <= ~126; x < -126 flushes to 0 (like ex2.approx.ftz).
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -127.0f);
-  const float t = x + 12582912.0f;  // round-to-nearest integer in the low mantissa bits
-  const float j = t - 12582912.0f;
-  const float f = x - j;
-  float p = fmaf(f, 1.3333558e-3f, 9.6181291e-3f);
-  p = fmaf(p, f, 5.5504109e-2f);
-  p = fmaf(p, f, 2.4022651e-1f);
-  p = fmaf(p, f, 6.9314718e-1f);
-  p = fmaf(p, f, 1.0f);
-  const int bits = __float_as_int(p) + (__float_as_int(t) << 23);
-  return x <= -126.0f ? 0.0f : __int_as_float(bits);
-}
 
 }  // namespace sm100
 }  // namespace tess
