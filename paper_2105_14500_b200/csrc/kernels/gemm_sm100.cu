@@ -1148,7 +1148,7 @@ cudaError_t launch(const Params& p, cudaStream_t stream) {
 // Per-device ring of tile counters for the pair kernel's dynamic schedule;
 // each launch takes the next slot and zeroes it on its stream.
 int* tile_counter_slot(cudaStream_t stream) {
-  constexpr int kSlots = 4096;
+  constexpr int kSlots = 65536;  // a slot is reused only 65536 launches later
   static std::mutex mu;
   static int* bufs[64] = {};
   static unsigned next[64] = {};
