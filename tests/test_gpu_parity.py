@@ -470,3 +470,45 @@ def test_block_fused_layernorm_bf16(tess, orc):
     res = tess.layer_run("block", x, dy, P, tess.LayerDims(b, s, h, nh), tess.GridSpec(1, 1),
                          dtype="bf16")
     _compare_layer(res, want, 2e-2, frob)
+
+
+@pytest.mark.parametrize("variant", ["nn", "nt", "tn"])
+@pytest.mark.parametrize("out", ["bf16", "f32", "f32_accumulate"])
+def test_gemm_ragged_wide_tiles(tess, variant, out):
+    """Ragged M, N, K (not multiples of the 256 x 512 pair tile or the 64-deep
+    k-block) on shapes the dispatcher routes to the 256 x 512 pair kernel with
+    the TMA-store / TMA-reduce-add epilogue and the dynamic tile schedule,
+    against a torch fp32 product of the same bf16 inputs."""
+    import torch
+    torch.manual_seed(7)
+    dev = torch.device("cuda", 0)
+    M, N, K = 2000, 2600, 1000
+    bf = torch.bfloat16
+    if variant == "nn":
+        a, b = torch.randn(M, K, device=dev, dtype=bf), torch.randn(K, N, device=dev, dtype=bf)
+        ref = a.float() @ b.float()
+        dims = (M, K, K, N)
+    elif variant == "nt":
+        a, b = torch.randn(M, K, device=dev, dtype=bf), torch.randn(N, K, device=dev, dtype=bf)
+        ref = a.float() @ b.float().t()
+        dims = (M, K, N, K)
+    else:
+        a, b = torch.randn(K, M, device=dev, dtype=bf), torch.randn(K, N, device=dev, dtype=bf)
+        ref = a.float().t() @ b.float()
+        dims = (K, M, K, N)
+    acc = out == "f32_accumulate"
+    ctype = "bf16" if out == "bf16" else "f32"
+    c = (torch.randn(M, N, device=dev) if acc else
+         torch.zeros(M, N, device=dev, dtype=bf if out == "bf16" else torch.float32))
+    c0 = c.clone()
+    ctx = tess.init_local(tess.GridSpec(1, 1))[0]
+    try:
+        ctx.matmul(variant, "bf16", a.data_ptr(), dims[0], dims[1], b.data_ptr(), dims[2],
+                   dims[3], c.data_ptr(), c_dtype=ctype, accumulate=acc,
+                   stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        ctx.close()
+    want = ref + c0 if acc else ref
+    err = ((c.float() - want).norm() / want.norm()).item()
+    assert err <= (5e-3 if out == "bf16" else 1e-5), err
