@@ -42,8 +42,9 @@ struct AttnDesc {
 bool attn_fused_supported(const AttnDesc& d);
 
 cudaError_t attn_fwd_sm100(const AttnDesc& d, cudaStream_t s);
-// Writes dK and dV (bf16) into dqkv and dS^T into dst; the caller finishes
-// dQ = dS K with one batched tcgen05 GEMM over dst (deterministic: no atomics).
+// Writes dK and dV (bf16) into dqkv and the UNSCALED dS^T = (P (dP - delta))^T
+// into dst; the caller finishes dQ = scale * dS K with one batched tcgen05
+// GEMM over dst (alpha = scale; deterministic: no atomics).
 cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s);
 
 const char* attn_last_error();

@@ -54,6 +54,7 @@ namespace sm100 {
 namespace attn {
 
 constexpr int kThreads = 320;
+constexpr int kBwdThreads = 576;  // backward: TMA + MMA warps + 16 softmax-gradient warps
 constexpr int BQ = 128;   // query rows per tile (UMMA M)
 constexpr int BKV = 128;  // keys per tile (UMMA N of S, K of P V)
 constexpr float kLog2e = 1.4426950408889634f;
@@ -352,31 +353,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 
 
 // --------------------------------------------------------------- backward
-// One CTA = one (sample, head, 128-key tile); it walks the 64-query tiles
+// One CTA = one (sample, head, 128-key tile); it walks the 128-query tiles
 // i of the sequence. 320 threads:
 //   warp 0      TMA producer: K, V of the key tile once; then Q_i, dO_i
-//               (64 x hd, boxes {64, 64}) through a RING-slot FIFO.
-//   warp 1      MMA issuer + TMEM owner. Per query tile:
-//                 S^T(i+1) = K Q_{i+1}^T, dP^T(i+1) = V dO_{i+1}^T  (M=128, N=64)
-//                 dV += P^T(i) dO_i, dK += dS^T(i) Q_i                (M=128, N=hd)
-//               with S^T / dP^T double buffered in TMEM, so the next
-//               tile's scores run under this tile's softmax.
-//   warps 2-9   thread = key row (TMEM lane), two warps per lane quadrant
-//               (32 query columns each): P^T = 2^(c*S^T - lse[q]),
-//               dS^T = P^T (dP^T - delta[q]) / sqrt(hd), both bf16 into
-//               shared memory (UMMA K-major SW128) for the dV/dK MMAs; dS^T
-//               also leaves by TMA store for dQ = dS K (one batched GEMM).
+//               (128 x hd, boxes {64, 128}) through a RING-slot FIFO.
+//   warp 1      MMA issuer + TMEM owner. Per query tile, all MMAs at
+//               M=128, N=128 (full tcgen05 rate; N=64 tiles run at ~70 %):
+//                 S^T(i) = K Q_i^T, dP^T(i) = V dO_i^T   (A = K / V, smem)
+//                 dV += P^T(i) dO_i   (A = P^T in TMEM, written by the softmax
+//                                      over the consumed S^T columns)
+//                 dK += dS^T(i) Q_i   (A = dS^T in shared memory)
+//               S^T / dP^T are single-buffered (TMEM holds S^T, dP^T, dV, dK);
+//               dP^T(i+1) is issued as soon as tile i's scores sit in
+//               registers, S^T(i+1) after dV(i) has read P^T(i).
+//   warps 2-17  four groups of 4 warps split each tile's 128 queries (group
+//               g: columns [32g, 32g+32)); thread = key row (TMEM lane):
+//               P^T = 2^(c*S^T - lse[q]) -> TMEM (bf16 pairs), dS^T = P^T
+//               (dP^T - delta[q]) -> shared memory (UMMA K-major SW128, chunk
+//               g/2) and, by TMA store, to HBM for dQ = dS K (one batched
+//               GEMM; the 1/sqrt(hd) goes to dK's epilogue and dQ's alpha).
 // Q_i and dO_i tiles are used twice with different majorness: K-major B of
 // the score MMAs ([N=q][K=hd]) and MN-major B of dV/dK ([K=q][N=hd]) -- the
 // same bytes under two descriptors.
-// TMEM: S^T bufs [0,64) [64,128), dP^T bufs [128,192) [192,256),
-//       dV [256, 256+hd), dK [384, 384+hd).
-constexpr int BQB = 64;  // queries per backward tile
+// TMEM: S^T / P^T [0,128), dP^T [128,256), dV [256, 256+hd), dK [384, 384+hd).
+constexpr int BQB = 128;  // queries per backward tile
 
 struct BwdParams {
   CUtensorMap tm_kv;   // qkv view, box {64, 128}: K, V of the key tile
-  CUtensorMap tm_q;    // qkv view, box {64, 64}: Q_i
-  CUtensorMap tm_do;   // dO view [hq cols, S, samples], box {64, 64}
+  CUtensorMap tm_q;    // qkv view, box {64, 128}: Q_i
+  CUtensorMap tm_do;   // dO view [hq cols, S, samples], box {64, 128}
   CUtensorMap tm_dst;  // dS^T view [S q, S k, samples*H], box {64, 128} (store)
   int S, H, n_kt, n_qt;
   float c;      // scale * log2(e)
@@ -388,8 +393,7 @@ struct BwdParams {
   long long* trace;  // debug (TESS_ATTN_TRACE): per-phase clock64 of CTA 0, [event][tile]
 };
 
-// trace events (CTA 0 only): MMA issue of S^T(i), MMA pds_full(i) seen,
-// softmax (quad-0 warp of the owning group) sdp_full(i) seen, math done, pds_full(i) arrive
+// trace events (CTA 0 only)
 enum {
   TR_MMA_S = 0, TR_MMA_P = 1, TR_SM_IN = 2, TR_SM_MATH = 3, TR_SM_OUT = 4,
   TR_SM_LOADED = 5, TR_MMA_FREE = 6, TR_MMA_GDONE = 7, TR_N = 8
@@ -400,18 +404,17 @@ __device__ __forceinline__ void trace_ev(const BwdParams& p, int ev, int tile) {
 
 template <int HD>
 struct BwdCfg {
-  static constexpr int KV_BYTES = 128 * HD * 2;   // K or V tile
+  static constexpr int KV_BYTES = 128 * HD * 2;    // K or V tile
   static constexpr int SLOT_BYTES = BQB * HD * 2;  // Q_i or dO_i
-  static constexpr int RING = HD == 128 ? 6 : 10;
-  static constexpr int PD_BYTES = 128 * BQB * 2;   // P^T or dS^T tile
+  static constexpr int RING = HD == 128 ? 4 : 8;
+  static constexpr int DS_BYTES = 128 * BQB * 2;   // dS^T tile (2 chunks of 64 queries)
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = KV_BYTES;
   static constexpr int OFF_RING = 2 * KV_BYTES;
-  static constexpr int OFF_P = OFF_RING + RING * SLOT_BYTES;  // 2 buffers
-  static constexpr int OFF_DS = OFF_P + 2 * PD_BYTES;         // 2 buffers
-  static constexpr int OFF_LD = OFF_DS + 2 * PD_BYTES;  // per group x 2 bufs: lse 64 | delta 64
-  static constexpr int OFF_BAR = OFF_LD + 2 * 2 * 128 * 4;
-  static constexpr int USED = OFF_BAR + 256;
+  static constexpr int OFF_DS = OFF_RING + RING * SLOT_BYTES;
+  static constexpr int OFF_LD = OFF_DS + DS_BYTES;  // 4 groups x 2 bufs: lse 32 | delta 32
+  static constexpr int OFF_BAR = OFF_LD + 4 * 2 * 64 * 4;
+  static constexpr int USED = OFF_BAR + 512;
   // the dynamic window is 1024-aligned in practice; the kernel checks and
   // traps if the slack we could afford does not cover its misalignment
   static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
@@ -433,7 +436,7 @@ __device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const 
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
+__global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -443,12 +446,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* kv_full = bars;                   // 1
   uint64_t* r_full = bars + 1;                // RING
   uint64_t* r_empty = r_full + C::RING;       // RING
-  uint64_t* sdp_full = r_empty + C::RING;     // 2
-  uint64_t* sdp_free = sdp_full + 2;          // 2
-  uint64_t* pds_full = sdp_free + 2;          // 2
-  uint64_t* pds_free = pds_full + 2;          // 2
-  uint64_t* ds_free = pds_free + 2;           // 2: TMA store of dS^T buffer done reading
-  uint64_t* fin = ds_free + 2;                // 1
+  uint64_t* sdp_full = r_empty + C::RING;     // 1: S^T(i) and dP^T(i) in TMEM
+  uint64_t* loaded = sdp_full + 1;            // 1: all 8 warps hold tile i's scores (count 8)
+  uint64_t* pds_full = loaded + 1;            // 1: P^T (TMEM) + dS^T (smem) written (count 8)
+  uint64_t* ds_free = pds_full + 1;           // 1: dK(i) done reading dS^T smem
+  uint64_t* st_free = ds_free + 1;            // 2: TMA store of dS^T chunk g done reading
+  uint64_t* fin = st_free + 2;                // 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
   const int warp = threadIdx.x / 32;
@@ -465,13 +468,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       mbar_init(&r_full[s], 1);
       mbar_init(&r_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sdp_full[b], 1);
-      mbar_init(&sdp_free[b], 4);  // the 4 warps of the group owning buffer b
-      mbar_init(&pds_full[b], 4);  // one arrive per warp of the owning group
-      mbar_init(&pds_free[b], 1);
-      mbar_init(&ds_free[b], 1);
-    }
+    mbar_init(sdp_full, 1);
+    mbar_init(loaded, 16);
+    mbar_init(pds_full, 16);
+    mbar_init(ds_free, 1);
+    mbar_init(&st_free[0], 1);
+    mbar_init(&st_free[1], 1);  // chunk c's storer: group 2c
     mbar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
@@ -510,9 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c) {
             if (which == 0)
-              tma_load_3d(dst + c * 8192, &p.tm_q, &r_full[stage], col_q + c * 64, i * BQB, smp);
+              tma_load_3d(dst + c * 16384, &p.tm_q, &r_full[stage], col_q + c * 64, i * BQB, smp);
             else
-              tma_load_3d(dst + c * 8192, &p.tm_do, &r_full[stage], head * HD + c * 64, i * BQB,
+              tma_load_3d(dst + c * 16384, &p.tm_do, &r_full[stage], head * HD + c * 64, i * BQB,
                           smp);
           }
           if (++stage == C::RING) {
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       constexpr uint32_t idesc_g = idesc_bf16(128, HD, false, true);
       const uint32_t sk = smem_u32(smem + C::OFF_K), sv = smem_u32(smem + C::OFF_V);
       const uint32_t ring = smem_u32(smem + C::OFF_RING);
+      const uint32_t sds = smem_u32(smem + C::OFF_DS);
       int stage = 0;
       uint32_t phase = 0;
       auto next_slot = [&]() {
@@ -541,24 +544,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
         return s;
       };
-      // A [128 x HD] K-major (chunk stride 16 KB) times B [64 x HD] K-major
-      // (chunk stride 8 KB) -> TMEM columns [d, d + 64).
+      // A [128 x HD] K-major (chunk stride 16 KB) times B [128 x HD] K-major
+      // (chunk stride 16 KB) -> TMEM columns [d, d + 128)
       auto issue_scores = [&](uint32_t d, uint32_t a, uint32_t b) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t ko = (uint32_t)(kk & 3) * 32u;
-          mma_bf16(d, make_sdesc(a + (uint32_t)(kk >> 2) * 16384u + ko, 16, 1024),
-                   make_sdesc(b + (uint32_t)(kk >> 2) * 8192u + ko, 16, 1024), idesc_s,
+          const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
+          mma_bf16(d, make_sdesc(a + off, 16, 1024), make_sdesc(b + off, 16, 1024), idesc_s,
                    kk > 0 ? 1u : 0u);
         }
-      };
-      // A [128 x 64] K-major (P^T or dS^T) times B [64 x HD] MN-major.
-      auto issue_grad = [&](uint32_t d, uint32_t a, uint32_t b, bool acc) {
-#pragma unroll
-        for (int kk = 0; kk < BQB / 16; ++kk)
-          mma_bf16(d, make_sdesc(a + (uint32_t)kk * 32u, 16, 1024),
-                   make_sdesc(b + (uint32_t)kk * 2048u, 8192, 1024), idesc_g,
-                   (acc || kk > 0) ? 1u : 0u);
       };
       mbar_wait(kv_full, 0);
       tc_fence_after();
@@ -567,32 +561,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       trace_ev(p, TR_MMA_S, 0);
       issue_scores(tmem + C::TM_ST, sk, ring + qs * C::SLOT_BYTES);
       issue_scores(tmem + C::TM_DPT, sv, ring + ds * C::SLOT_BYTES);
-      mma_commit(&sdp_full[0]);
+      mma_commit(sdp_full);
       for (int i = 0; i < p.n_qt; ++i) {
-        const int b = i & 1;
+        const bool more = i + 1 < p.n_qt;
         int qn = 0, dn = 0;
-        if (i + 1 < p.n_qt) {
-          mbar_wait(&sdp_free[b ^ 1], (((i + 1) >> 1) & 1) ^ 1);
-          tc_fence_after();
+        // tile i's scores are in registers: dP^T(i+1) into the dP^T columns
+        mbar_wait(loaded, i & 1);
+        tc_fence_after();
+        trace_ev(p, TR_MMA_FREE, i);
+        if (more) {
           qn = next_slot();
           dn = next_slot();
-          trace_ev(p, TR_MMA_S, i + 1);
-          issue_scores(tmem + C::TM_ST + (b ^ 1) * 64, sk, ring + qn * C::SLOT_BYTES);
-          issue_scores(tmem + C::TM_DPT + (b ^ 1) * 64, sv, ring + dn * C::SLOT_BYTES);
-          mma_commit(&sdp_full[b ^ 1]);
+          issue_scores(tmem + C::TM_DPT, sv, ring + dn * C::SLOT_BYTES);
         }
-        mbar_wait(&pds_full[b], (i >> 1) & 1);
+        // gradients of tile i once P^T (TMEM) and dS^T (smem) are written
+        mbar_wait(pds_full, i & 1);
         tc_fence_after();
         trace_ev(p, TR_MMA_P, i);
-        // (TR_MMA_FREE / TR_MMA_GDONE bracket this tile's gradient issue)
-        issue_grad(tmem + C::TM_DV, smem_u32(smem + C::OFF_P + b * C::PD_BYTES),
-                   ring + ds * C::SLOT_BYTES, i > 0);
+#pragma unroll
+        for (int kk = 0; kk < BQB / 16; ++kk)  // dV += P^T dO_i, P^T from TMEM
+          mma_bf16_ts(tmem + C::TM_DV, tmem + C::TM_ST + kk * 8,
+                      make_sdesc(ring + ds * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
+                      idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&r_empty[ds]);
-        issue_grad(tmem + C::TM_DK, smem_u32(smem + C::OFF_DS + b * C::PD_BYTES),
-                   ring + qs * C::SLOT_BYTES, i > 0);
+#pragma unroll
+        for (int kk = 0; kk < BQB / 16; ++kk)  // dK += dS^T Q_i
+          mma_bf16(tmem + C::TM_DK,
+                   make_sdesc(sds + (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u, 16,
+                              1024),
+                   make_sdesc(ring + qs * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
+                   idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&r_empty[qs]);
-        mma_commit(&pds_free[b]);
+        mma_commit(ds_free);
         trace_ev(p, TR_MMA_GDONE, i);
+        if (more) {
+          // S^T(i+1) over the P^T columns (after dV(i) in issue order)
+          trace_ev(p, TR_MMA_S, i + 1);
+          issue_scores(tmem + C::TM_ST, sk, ring + qn * C::SLOT_BYTES);
+          mma_commit(sdp_full);
+        }
         qs = qn;
         ds = dn;
       }
@@ -600,120 +607,114 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     }
   } else {
     // ------------------------------------------ softmax-gradient warps
-    // Two groups of 4 warps alternate query tiles (group g takes tiles
-    // i = g, g+2, ...), so one group's TMEM reads / math / smem writes overlap
-    // the other's; group g owns S^T/dP^T TMEM buffer g and P^T/dS^T smem
-    // buffer g. Warp (g, quad): key rows quad*32.., all 64 query columns of
-    // its tiles in two 32-column chunks.
     const int quad = warp & 3;
-    const int g = (warp - 2) >> 2;
-    const int half = g;                // dK/dV epilogue column half
-    const int r = quad * 32 + lane;    // key row within the tile
+    const int g = (warp - 2) >> 2;   // query columns [32g, 32g+32) of each tile
+    const int r = quad * 32 + lane;  // key row within the tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float cl2 = p.c, scale = p.scale;
-    const bool storer = quad == 0 && lane == 0;  // one TMA-store thread per group
+    // TMA store of dS^T chunk c (64 queries = groups 2c, 2c+1) by group 2c's thread
+    const bool storer = quad == 0 && lane == 0 && (g & 1) == 0;
+    const int chunk = g >> 1;
     const float* lse_h = p.lse + ((long long)smp * p.H + head) * p.S;
     const float* dlt_h = p.delta + ((long long)smp * p.H + head) * p.S;
-    // (lse, delta) of the group's tiles staged through shared memory, double
-    // buffered per group: the quad-0 warp loads tile i+2's 64 + 64 values
-    // while tile i is processed (L2 latency hidden), a 128-thread named
-    // barrier at the start of each tile orders them against the readers.
-    const uint32_t ldg_base = smem_u32(smem + C::OFF_LD) + (uint32_t)g * 1024u;  // [buf][lse|delta]
+    // (lse, delta) of the group's 32 query columns staged through shared
+    // memory, double buffered per group: the quad-0 warp loads tile i+1's
+    // values while tile i is processed, a 128-thread named barrier at the
+    // start of each tile orders them against the readers.
+    const uint32_t ldg_base = smem_u32(smem + C::OFF_LD) + (uint32_t)g * 512u;  // [buf][lse|delta]
     const bool ld_writer = quad == 0;
-    auto gload = [&](int i, float (&v)[4]) {
-      const int q0 = i * BQB + lane;
-      const bool ok0 = i < p.n_qt && q0 < p.S, ok1 = i < p.n_qt && q0 + 32 < p.S;
-      v[0] = ok0 ? __ldg(lse_h + q0) : INFINITY;  // 2^(x - inf) = 0: no contribution
-      v[1] = ok1 ? __ldg(lse_h + q0 + 32) : INFINITY;
-      v[2] = ok0 ? __ldg(dlt_h + q0) : 0.f;
-      v[3] = ok1 ? __ldg(dlt_h + q0 + 32) : 0.f;
+    auto gload = [&](int i, float (&v)[2]) {
+      const int q = i * BQB + g * 32 + lane;
+      const bool ok = i < p.n_qt && q < p.S;
+      v[0] = ok ? __ldg(lse_h + q) : INFINITY;  // 2^(x - inf) = 0: no contribution
+      v[1] = ok ? __ldg(dlt_h + q) : 0.f;
     };
-    auto sstore = [&](int i, const float (&v)[4]) {
-      const uint32_t a = ldg_base + (uint32_t)((i >> 1) & 1) * 512u + lane * 4;
+    auto sstore = [&](int i, const float (&v)[2]) {
+      const uint32_t a = ldg_base + (uint32_t)(i & 1) * 256u + lane * 4;
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[0]) : "memory");
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 128), "f"(v[1]) : "memory");
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 256), "f"(v[2]) : "memory");
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 384), "f"(v[3]) : "memory");
     };
     if (ld_writer) {
-      float v[4];
-      gload(g, v);
-      sstore(g, v);
+      float v[2];
+      gload(0, v);
+      sstore(0, v);
     }
-    const int b = g;
-    const uint32_t p_buf = smem_u32(smem + C::OFF_P + b * C::PD_BYTES);
-    const uint32_t ds_buf = smem_u32(smem + C::OFF_DS + b * C::PD_BYTES);
-    for (int i = g; i < p.n_qt; i += 2) {
-      const uint32_t k = (uint32_t)(i >> 1) & 1u;  // phase of this buffer's k-th use
-      const uint32_t ldw = ldg_base + k * 512u;    // this tile's (lse, delta)
-      named_bar_sync(1 + g, 128);  // tile i's staging written; tile i-2's readers done
-      float nv[4];
-      if (ld_writer) gload(i + 2, nv);
+    const uint32_t ds_chunk = smem_u32(smem + C::OFF_DS) + (uint32_t)chunk * 16384u;
+    for (int i = 0; i < p.n_qt; ++i) {
+      const uint32_t ph = (uint32_t)i & 1u;
+      const uint32_t ldw = ldg_base + ph * 256u;  // this tile's (lse, delta)
+      named_bar_sync(1 + g, 128);  // tile i's staging written; tile i-1's readers done
+      float nv[2];
+      if (ld_writer) gload(i + 1, nv);
       if (storer) {
-        // dS^T buffer b was last stored at tile i-2 by this thread: wait for
-        // that TMA store to finish reading, then release the buffer
+        // dS^T chunk was last stored at tile i-1 by this thread: wait for the
+        // TMA store to finish reading shared memory
         bulk_wait_read<0>();
-        mbar_arrive(&ds_free[b]);
+        mbar_arrive(&st_free[chunk]);
       }
-      mbar_wait(&sdp_full[b], k);
+      mbar_wait(sdp_full, ph);
       tc_fence_after();
-      if (quad == 0 && lane == 0) trace_ev(p, TR_SM_IN, i);
-      bool waited = false;
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32_nowait(tmem + lane_off + C::TM_ST + b * 64 + c * 32, sr);
-        tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + b * 64 + c * 32, dr);
-        tmem_wait_ld();
-        reg_fence32(sr);
-        reg_fence32(dr);
-        if (c == 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sdp_free[b]);
-          if (quad == 0 && lane == 0) trace_ev(p, TR_SM_LOADED, i);
-        }
-        float pv[32], gv[32];
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_IN, i);
+      // the group's 32 columns of S^T and dP^T into registers
+      uint32_t sr[32], dr[32];
+      tmem_ld32_nowait(tmem + lane_off + C::TM_ST + g * 32, sr);
+      tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + g * 32, dr);
+      tmem_wait_ld();
+      reg_fence32(sr);
+      reg_fence32(dr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(loaded);
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_LOADED, i);
+      // P^T into sr, unscaled dS^T = P^T (dP^T - delta) into dr (in place);
+      // the 1/sqrt(hd) is applied once to dK (epilogue) and dQ (GEMM alpha)
 #pragma unroll
-        for (int e4 = 0; e4 < 8; ++e4) {
-          float4 l4, d4;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w)
-                       : "r"(ldw + (uint32_t)(c * 32 + 4 * e4) * 4u));
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
-                       : "r"(ldw + 256u + (uint32_t)(c * 32 + 4 * e4) * 4u));
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+      for (int e4 = 0; e4 < 8; ++e4) {
+        float4 l4, d4;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w)
+                     : "r"(ldw + (uint32_t)(4 * e4) * 4u));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
+                     : "r"(ldw + 128u + (uint32_t)(4 * e4) * 4u));
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = 4 * e4 + u;
-            pv[e] = ex2_approx(fmaf(__uint_as_float(sr[e]), cl2, -lv[u]));
-            gv[e] = pv[e] * (__uint_as_float(dr[e]) - dv[u]) * scale;
-          }
+        for (int u = 0; u < 4; ++u) {
+          const int e = 4 * e4 + u;
+          const float pv = ex2_approx(fmaf(__uint_as_float(sr[e]), cl2, -lv[u]));
+          dr[e] = __float_as_uint(pv * (__uint_as_float(dr[e]) - dv[u]));
+          sr[e] = __float_as_uint(pv);
         }
-        if (!waited) {
-          if (quad == 0 && lane == 0) trace_ev(p, TR_SM_MATH, i);
-          // buffer b: dV/dK of tile i-2 done and its dS^T TMA store has read it
-          mbar_wait(&pds_free[b], k ^ 1u);
-          mbar_wait(&ds_free[b], k);
-          waited = true;
-        }
-        store_row32(p_buf, r, c * 4, pv);
-        store_row32(ds_buf, r, c * 4, gv);
       }
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_MATH, i);
+      // P^T over the S^T columns [16g, 16g+16) once all 16 warps read theirs
+      mbar_wait(loaded, ph);
+      {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack_bf16x2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
+        tmem_st16(tmem + lane_off + C::TM_ST + g * 16, pk);
+      }
+      // dS^T chunk: free once dK(i-1) read it and its TMA store read it
+      mbar_wait(ds_free, ph ^ 1u);
+      mbar_wait(&st_free[chunk], ph);
+      store_row32(ds_chunk, r, (g & 1) * 4, *reinterpret_cast<const float(*)[32]>(dr));
+      tmem_wait_st();
+      tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pds_full[b]);
-      if (quad == 0 && lane == 0) trace_ev(p, TR_SM_OUT, i);
+      if (lane == 0) mbar_arrive(pds_full);
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_OUT, i);
       if (storer) {
-        mbar_wait(&pds_full[b], k);  // the group's 4 warps wrote their rows
-        tma_store_3d(&p.tm_dst, smem + C::OFF_DS + b * C::PD_BYTES, i * BQB, k0,
+        mbar_wait(pds_full, ph);  // all rows of the chunk written
+        tma_store_3d(&p.tm_dst, smem + C::OFF_DS + chunk * 16384, i * BQB + chunk * 64, k0,
                      smp * p.H + head);
         bulk_commit();
       }
-      // tile i+2's (lse, delta) into the other staging buffer (last read at tile i-2)
-      if (ld_writer) sstore(i + 2, nv);
+      // tile i+1's (lse, delta) into the other staging buffer (last read at tile i-1)
+      if (ld_writer) sstore(i + 1, nv);
     }
     // ------------------------------------------------- dK, dV epilogue
     mbar_wait(fin, 0);
@@ -723,21 +724,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 #pragma unroll
     for (int which = 0; which < 2; ++which) {  // dK then dV
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        const int col = half * (HD / 2) + c * 32;
-        uint32_t v[32];
-        tmem_ld32_nowait(tmem + lane_off + (which == 0 ? C::TM_DK : C::TM_DV) + col, v);
+      for (int c = 0; c < HD / 64; ++c) {  // group g: columns [g*HD/4, (g+1)*HD/4)
+        const int col = g * (HD / 4) + c * 16;
+        uint32_t v[16];
+        tmem_ld16_nowait(tmem + lane_off + (which == 0 ? C::TM_DK : C::TM_DV) + col, v);
         tmem_wait_ld();
-        reg_fence32(v);
+        reg_fence16(v);
         if (krow < p.S) {
           __nv_bfloat16* dst = drow + which * HD + col;
+          const float f = which == 0 ? scale : 1.0f;  // dK carries the dS scale
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 2; ++u) {
             uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]), __uint_as_float(v[u * 8 + 1]));
-            w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]), __uint_as_float(v[u * 8 + 3]));
-            w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]), __uint_as_float(v[u * 8 + 5]));
-            w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]), __uint_as_float(v[u * 8 + 7]));
+            w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * f, __uint_as_float(v[u * 8 + 1]) * f);
+            w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * f, __uint_as_float(v[u * 8 + 3]) * f);
+            w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * f, __uint_as_float(v[u * 8 + 5]) * f);
+            w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * f, __uint_as_float(v[u * 8 + 7]) * f);
             *reinterpret_cast<uint4*>(dst + u * 8) = w;
           }
         }
@@ -817,7 +819,7 @@ cudaError_t launch_bwd(const BwdParams& p, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_bwd_kernel<HD><<<grid, kThreads, C::SMEM_BYTES, s>>>(p);
+  attn_bwd_kernel<HD><<<grid, kBwdThreads, C::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 

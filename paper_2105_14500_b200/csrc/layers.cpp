@@ -412,6 +412,7 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     gq.lda = S; gq.as0 = S * S; gq.as1 = H * S * S;
     gq.ldb = ld; gq.bs0 = 3 * hd; gq.bs1 = S * ld;
     gq.c = dqkv; gq.c_type = t; gq.ldc = ld; gq.cs0 = 3 * hd; gq.cs1 = S * ld;
+    gq.alpha = a.scale;  // the kernel stores dS without the 1/sqrt(hd)
     run_gemm(gq, s);
     nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s, &wp.qkv);
     weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
