@@ -267,6 +267,12 @@ def main():
         ctx.layer_backward("block", "bf16", dims, shard, dyp, dxp, grads, accumulate=False,
                            stream=sh)
 
+    def step_api(xp, yp, dyp, dxp):
+        # the user-facing call for a training step of the layer (rank-level
+        # layer_run: forward + backward with x and dy given together)
+        ctx.layer_step("block", "bf16", dims, shard, xp, dyp, yp, dxp, grads, accumulate=False,
+                       stream=sh)
+
     def barrier():
         torch.cuda.synchronize(dev)
         if dist:
@@ -354,11 +360,12 @@ def main():
         yh = torch.empty_like(xh).pin_memory()
         dxh = torch.empty_like(xh).pin_memory()
         for _ in range(max(1, args.warmup)):
-            step(xh.data_ptr(), yh.data_ptr(), dyh.data_ptr(), dxh.data_ptr())
+            step_api(xh.data_ptr(), yh.data_ptr(), dyh.data_ptr(), dxh.data_ptr())
+        ctx.stream_join(sh)
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            step(xh.data_ptr(), yh.data_ptr(), dyh.data_ptr(), dxh.data_ptr())
+            step_api(xh.data_ptr(), yh.data_ptr(), dyh.data_ptr(), dxh.data_ptr())
         ctx.stream_join(sh)  # the last step's host copies complete inside the timed region
         e1.record(stream)
         barrier()

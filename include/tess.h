@@ -225,6 +225,16 @@ tess_status tess_layer_backward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtyp
                                 const void* dy, void* dx, tess_block_grads* grads,
                                 int accumulate, float* dbias, void* stream);
 
+/* Forward + backward of one layer op in one call, both inputs given up front
+ * (the reference's layer_run(op, x, dy, ...) at rank level, layers.cpp:
+ * 604-692): identical results to tess_layer_forward + tess_layer_backward;
+ * a host dy is uploaded on a context side stream while the forward runs. */
+tess_status tess_layer_step(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
+                            const tess_layer_dims* dims, const tess_block_shard* shard,
+                            const void* bias_row0, const void* x, const void* dy, void* y,
+                            void* dx, tess_block_grads* grads, int accumulate, float* dbias,
+                            void* stream);
+
 /* Makes `stream` wait for everything the context still has in flight on its
  * side streams: pending host copies of layer outputs and deferred
  * collectives (the reference's calls return completed values; this is the

@@ -149,6 +149,8 @@ def _load() -> C.CDLL:
         "tess_set_trace": ([vp, i], i),
         "tess_set_comm_noop": ([vp, i], i),
         "tess_stream_join": ([vp, vp], i),
+        "tess_layer_step": ([vp, i, i, C.POINTER(_LayerDimsC), C.POINTER(BlockShardC), vp, vp, vp,
+                             vp, vp, C.POINTER(BlockGradsC), i, vp, vp], i),
         "tess_trace_text": ([vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], i),
         "tess_broadcast": ([vp, i, i, vp, C.c_size_t, C.c_size_t, vp], i),
         "tess_reduce": ([vp, i, i, vp, vp, C.c_size_t, vp], i),
@@ -549,6 +551,17 @@ class RankContext:
 
     def reset_stats(self):
         _check(lib.tess_reset_comm_stats(self.h))
+
+    def layer_step(self, op, dtype, dims: LayerDims, shard: BlockShardC, x, dy, y, dx,
+                   grads: Optional[BlockGradsC] = None, accumulate=False, bias_row0=None,
+                   dbias=None, stream=0):
+        """Forward + backward in one call (rank-level layer_run): a host dy is
+        uploaded while the forward runs."""
+        dc = dims.c()
+        _check(lib.tess_layer_step(self.h, LAYER_OPS[op], _dtype(dtype), C.byref(dc),
+                                   C.byref(shard), bias_row0, x, dy, y, dx,
+                                   C.byref(grads) if grads is not None else None,
+                                   int(accumulate), dbias, stream))
 
     def stream_join(self, stream=0):
         """Order `stream` after the context's in-flight host copies of layer

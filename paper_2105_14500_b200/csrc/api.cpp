@@ -431,4 +431,19 @@ tess_status tess_layer_backward(tess_ctx* c, tess_layer_op op, tess_dtype dt,
   });
 }
 
+tess_status tess_layer_step(tess_ctx* c, tess_layer_op op, tess_dtype dt,
+                            const tess_layer_dims* dims, const tess_block_shard* shard,
+                            const void* bias_row0, const void* x, const void* dy, void* y,
+                            void* dx, tess_block_grads* grads, int accumulate, float* dbias,
+                            void* stream) {
+  return guarded([&] {
+    Ctx& cx = need(c);
+    if (!dims || !shard || !x || !dy || !y || !dx) fail(TESS_ERR_INVALID, "null argument");
+    const DType t = to_dtype(dt);
+    if (t == DType::F64) fail(TESS_ERR_UNSUPPORTED, "fp64 compute: use TESS_F32 or TESS_BF16");
+    layer_step(cx, op, t, rank_dims(cx, *dims), *shard, static_cast<const float*>(bias_row0), x,
+               dy, y, dx, grads, accumulate != 0, dbias, S(stream));
+  });
+}
+
 }  // extern "C"

@@ -293,5 +293,9 @@ tess_ctx::~tess_ctx() {
     cudaStreamDestroy(copy_s);
   }
   for (auto& kv : copy_ev) cudaEventDestroy(kv.second);
+  if (up_s) {
+    cudaStreamSynchronize(up_s);
+    cudaStreamDestroy(up_s);
+  }
   for (auto e : ev_ring) cudaEventDestroy(e);
 }

@@ -39,6 +39,9 @@ struct tess_ctx {
   // is rewritten or by tess_stream_join.
   cudaStream_t copy_s = nullptr;
   std::map<std::string, cudaEvent_t> copy_ev;
+  std::map<std::string, std::pair<const char*, size_t>> copy_host;  // host range per copy
+  // Upload stream of tess_layer_step (dy goes up while the forward runs).
+  cudaStream_t up_s = nullptr;
   std::vector<cudaEvent_t> ev_ring;
   size_t ev_next = 0;
   ~tess_ctx();

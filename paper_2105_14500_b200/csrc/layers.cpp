@@ -492,6 +492,20 @@ void join_copy(Ctx& c, const std::string& name, cudaStream_t s) {
   TESS_CUDA(cudaStreamWaitEvent(s, it->second, 0));
   cudaEventDestroy(it->second);
   c.copy_ev.erase(it);
+  c.copy_host.erase(name);
+}
+
+// s waits for every pending host copy whose destination overlaps the host
+// range [p, p + bytes) about to be read (a host output fed back as an input).
+void join_host_overlap(Ctx& c, const void* p, size_t bytes, cudaStream_t s) {
+  const char* lo = static_cast<const char*>(p);
+  for (auto it = c.copy_host.begin(); it != c.copy_host.end();) {
+    const char* a = it->second.first;
+    const size_t n = it->second.second;
+    const std::string name = it->first;
+    ++it;
+    if (a < lo + bytes && lo < a + n) join_copy(c, name, s);
+  }
 }
 
 // Device staging buffer -> host on the context's copy stream, after the work
@@ -507,6 +521,7 @@ void async_d2h(Ctx& c, const std::string& name, void* host, const void* dev, siz
   TESS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   TESS_CUDA(cudaEventRecord(ev, cp));
   c.copy_ev[name] = ev;
+  c.copy_host[name] = {static_cast<const char*>(host), bytes};
 }
 
 std::string cache_tag(const Ctx& c, tess_layer_op op) {
@@ -535,6 +550,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   // Host buffers are staged through the context (x kept until backward).
   const void* x = x_in;
   if (!is_device_ptr(x_in)) {
+    join_host_overlap(c, x_in, act, s);  // x may be a pending host output of ours
     void* xs = wsget(c, tag + ".xstage", act);
     TESS_CUDA(cudaMemcpyAsync(xs, x_in, act, cudaMemcpyHostToDevice, s));
     x = xs;
@@ -606,6 +622,7 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   const void* x = it->second;
   const void* dy = dy_in;
   if (!is_device_ptr(dy_in)) {
+    join_host_overlap(c, dy_in, act, s);
     void* ds = wsget(c, "stage.dy", act);
     TESS_CUDA(cudaMemcpyAsync(ds, dy_in, act, cudaMemcpyHostToDevice, s));
     dy = ds;
@@ -680,6 +697,32 @@ void ctx_join(Ctx& c, cudaStream_t s) {
     cudaEventDestroy(kv.second);
   }
   c.copy_ev.clear();
+  c.copy_host.clear();
+}
+
+// Forward + backward in one call with both inputs known up front (the
+// reference's layer_run(op, x, dy, ...), layers.cpp:604-692, at rank level):
+// a host dy is uploaded on the context's upload stream while the forward
+// runs, instead of after it.
+void layer_step(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
+                const tess_block_shard& p, const float* bias_row0, const void* x, const void* dy,
+                void* y, void* dx, tess_block_grads* g, bool accumulate, float* dbias,
+                cudaStream_t s) {
+  const size_t act = (size_t)rd.rows * rd.hq * dtype_size(t);
+  const void* dyd = dy;
+  if (!is_device_ptr(dy)) {
+    if (!c.up_s) TESS_CUDA(cudaStreamCreateWithFlags(&c.up_s, cudaStreamNonBlocking));
+    void* ds = wsget(c, "stage.dy", act);
+    // the staging buffer's last reader (the previous backward) is on s before
+    // this point; the forward enqueued next is not waited for
+    stream_dep(c, s, c.up_s);
+    join_host_overlap(c, dy, act, c.up_s);
+    TESS_CUDA(cudaMemcpyAsync(ds, dy, act, cudaMemcpyHostToDevice, c.up_s));
+    dyd = ds;
+  }
+  layer_forward(c, op, t, rd, p, bias_row0, x, y, s);
+  if (dyd != dy) stream_dep(c, c.up_s, s);
+  layer_backward(c, op, t, rd, p, dyd, dx, g, accumulate, dbias, s);
 }
 
 }  // namespace tess

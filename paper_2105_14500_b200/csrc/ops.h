@@ -76,6 +76,10 @@ RankDims rank_dims(const Ctx& c, const tess_layer_dims& d);
 void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                    const tess_block_shard& p, const float* bias_row0, const void* x, void* y,
                    cudaStream_t s);
+void layer_step(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
+                const tess_block_shard& p, const float* bias_row0, const void* x, const void* dy,
+                void* y, void* dx, tess_block_grads* g, bool accumulate, float* dbias,
+                cudaStream_t s);
 void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                     const tess_block_shard& p, const void* dy, void* dx,
                     tess_block_grads* g, bool accumulate, float* dbias, cudaStream_t s);

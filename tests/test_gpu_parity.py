@@ -512,3 +512,57 @@ def test_gemm_ragged_wide_tiles(tess, variant, out):
     want = ref + c0 if acc else ref
     err = ((c.float() - want).norm() / want.norm()).item()
     assert err <= (5e-3 if out == "bf16" else 1e-5), err
+
+
+def test_layer_step_matches_forward_backward_host_buffers(tess, orc):
+    """tess_layer_step (x and dy together; a host dy uploads while the forward
+    runs) gives bitwise the results of tess_layer_forward +
+    tess_layer_backward, with pinned host inputs/outputs; a host output fed
+    back as the next input is ordered after its pending copy."""
+    import torch
+    b, s, h, nh = 2, 64, 256, 2
+    x, dy, P = _layer_inputs(orc, b, s, h, 19, bf16r)
+    dev = torch.device("cuda", 0)
+    bf = torch.bfloat16
+    names = ("w_qkv", "w_proj", "w_ff1", "w_ff2")
+    W = [torch.tensor(P[k], dtype=torch.float32, device=dev).to(bf).contiguous() for k in names]
+    LN = [torch.tensor(P[k], dtype=torch.float32, device=dev).contiguous()
+          for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")]
+    xh = torch.tensor(x, dtype=torch.float32).to(bf).pin_memory()
+    dyh = torch.tensor(dy, dtype=torch.float32).to(bf).pin_memory()
+    shard = tess.BlockShardC(*[t.data_ptr() for t in W + LN], 1e-5)
+    dims = tess.LayerDims(b, s, h, nh)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for mode in ("split", "step"):
+        ctx = tess.init_local(tess.GridSpec(1, 1))[0]
+        try:
+            yh, dxh = torch.empty_like(xh).pin_memory(), torch.empty_like(xh).pin_memory()
+            G = [torch.zeros(t.shape, device=dev) for t in W + LN]
+            grads = tess.BlockGradsC(*[t.data_ptr() for t in G])
+            for _ in range(2):
+                src = xh
+                if mode == "split":
+                    ctx.layer_forward("block", "bf16", dims, shard, src.data_ptr(), yh.data_ptr(),
+                                      stream=st)
+                    ctx.layer_backward("block", "bf16", dims, shard, dyh.data_ptr(),
+                                       dxh.data_ptr(), grads, stream=st)
+                else:
+                    ctx.layer_step("block", "bf16", dims, shard, src.data_ptr(), dyh.data_ptr(),
+                                   yh.data_ptr(), dxh.data_ptr(), grads, stream=st)
+            # chained: the host output y fed back as the next input
+            if mode == "split":
+                ctx.layer_forward("block", "bf16", dims, shard, yh.data_ptr(), dxh.data_ptr(),
+                                  stream=st)
+                ctx.layer_backward("block", "bf16", dims, shard, dyh.data_ptr(), yh.data_ptr(),
+                                   grads, stream=st)
+            else:
+                ctx.layer_step("block", "bf16", dims, shard, yh.data_ptr(), dyh.data_ptr(),
+                               dxh.data_ptr(), yh.data_ptr(), grads, stream=st)
+            ctx.stream_join(st)
+            torch.cuda.synchronize()
+            outs.append([yh.clone(), dxh.clone()] + [g.cpu() for g in G])
+        finally:
+            ctx.close()
+    for a, c in zip(*outs):
+        assert torch.equal(a, c)
