@@ -178,9 +178,20 @@ __global__ void colsum_finalize_kernel(const float* part, int64_t nchunk, int64_
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= cols * nq) return;
   const int64_t qi = c / cols, cc = c % cols;
-  float acc = 0.f;
-  for (int64_t k = 0; k < nchunk; ++k) acc += part[(k * nq + qi) * cols + cc];
-  out[c] = acc;
+  // four interleaved partial sums (fixed order: deterministic) keep several
+  // independent loads in flight per thread
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  const float* pc = part + qi * cols + cc;
+  const int64_t stride = nq * cols;
+  int64_t k = 0;
+  for (; k + 4 <= nchunk; k += 4) {
+    a0 += pc[(k + 0) * stride];
+    a1 += pc[(k + 1) * stride];
+    a2 += pc[(k + 2) * stride];
+    a3 += pc[(k + 3) * stride];
+  }
+  for (; k < nchunk; ++k) a0 += pc[k * stride];
+  out[c] = (a0 + a1) + (a2 + a3);
 }
 
 // ------------------------------------------------------------ LayerNorm
@@ -562,6 +573,44 @@ __global__ void attn_delta_kernel(const T* __restrict__ dO, const T* __restrict_
   if (lane == 0) delta[h * S + r] = acc;
 }
 
+// Vectorised delta for bf16 with hd % 8 == 0 and 32 % (hd / 8) == 0: a group
+// of hd/8 lanes per (row, head), one 16-byte load of dO and of O per lane,
+// all samples in one launch (rows = samples * S; delta[(smp*H + h)*S + r]).
+template <int LPG>
+__global__ void attn_delta_vec_kernel(const __nv_bfloat16* __restrict__ dO,
+                                      const __nv_bfloat16* __restrict__ O, int64_t ld, int64_t S,
+                                      int64_t H, int64_t rows, float* __restrict__ delta) {
+  constexpr int kGroups = 32 / LPG;
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32) * kGroups +
+                       lane / LPG;  // (row, head) pair
+  const int sub = lane % LPG;
+  float acc = 0.f;
+  const bool ok = item < rows * H;
+  int64_t ri = 0, h = 0;
+  if (ok) {
+    ri = item / H;
+    h = item % H;
+    const int64_t off = ri * ld + h * (LPG * 8) + sub * 8;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(dO + off));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(O + off));
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(b2[e]);
+      acc = fmaf(x.x, y.x, acc);
+      acc = fmaf(x.y, y.y, acc);
+    }
+  }
+#pragma unroll
+  for (int o = LPG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (ok && sub == 0) {
+    const int64_t smp = ri / S, r = ri % S;
+    delta[(smp * H + h) * S + r] = acc;
+  }
+}
+
 // --------------------------------------------------------- toy training
 constexpr int kMseBlocks = 1024;
 
@@ -799,13 +848,37 @@ void k_lse_combine(const float* stats, int64_t rows, int nst, float* lse, cudaSt
 }
 
 void k_attn_delta(const void* dO, const void* O, DType t, int64_t ld, int64_t S, int64_t H,
-                  int64_t hd, float* delta, cudaStream_t s) {
-  if (!S || !H) return;
+                  int64_t hd, float* delta, cudaStream_t s, int64_t samples) {
+  if (!S || !H || !samples) return;
   const int warps = 8;
+  const bool vec = t == DType::BF16 && (hd == 128 || hd == 64 || hd == 32) && ld % 8 == 0 &&
+                   reinterpret_cast<uintptr_t>(dO) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(O) % 16 == 0;
+  if (vec) {
+    const int64_t items = samples * S * H;
+    const int lpg = (int)(hd / 8), per_block = warps * (32 / lpg);
+    const unsigned g = (unsigned)((items + per_block - 1) / per_block);
+    const auto* a = static_cast<const __nv_bfloat16*>(dO);
+    const auto* b = static_cast<const __nv_bfloat16*>(O);
+    if (lpg == 16)
+      attn_delta_vec_kernel<16><<<g, 32 * warps, 0, s>>>(a, b, ld, S, H, samples * S, delta);
+    else if (lpg == 8)
+      attn_delta_vec_kernel<8><<<g, 32 * warps, 0, s>>>(a, b, ld, S, H, samples * S, delta);
+    else
+      attn_delta_vec_kernel<4><<<g, 32 * warps, 0, s>>>(a, b, ld, S, H, samples * S, delta);
+    count_launch();
+    TESS_CUDA(cudaGetLastError());
+    return;
+  }
   const unsigned g = (unsigned)((S * H + warps - 1) / warps);
-  TESS_DISPATCH(t, T, attn_delta_kernel<T><<<g, 32 * warps, 0, s>>>((const T*)dO, (const T*)O, ld,
-                                                                      S, H, hd, delta));
-  count_launch();
+  const size_t esz = dtype_size(t);
+  for (int64_t smp = 0; smp < samples; ++smp) {
+    const char* a = static_cast<const char*>(dO) + (size_t)smp * S * ld * esz;
+    const char* b = static_cast<const char*>(O) + (size_t)smp * S * ld * esz;
+    TESS_DISPATCH(t, T, attn_delta_kernel<T><<<g, 32 * warps, 0, s>>>(
+                            (const T*)a, (const T*)b, ld, S, H, hd, delta + (size_t)smp * H * S));
+    count_launch();
+  }
   TESS_CUDA(cudaGetLastError());
 }
 

@@ -85,10 +85,11 @@ void k_softmax_fwd(const float* S, void* P, DType t, int64_t rows, int64_t L, cu
 // lse[r] = log-sum-exp (log2 units) over the nst RowStats partials
 // (max, sum-exp2) of row r.
 void k_lse_combine(const float* stats, int64_t rows, int nst, float* lse, cudaStream_t s);
-// delta[h][r] = sum_d dO[r, h*hd + d] * O[r, h*hd + d]  (= rowsum(P * dP),
-// the softmax-backward row term; rows S, heads H, row stride ld).
+// delta[(smp*H + h)*S + r] = sum_d dO[smp*S + r, h*hd + d] * O[smp*S + r, h*hd + d]
+// (= rowsum(P * dP), the softmax-backward row term) for `samples` samples of
+// S rows, heads H, row stride ld (one launch on the bf16 path).
 void k_attn_delta(const void* dO, const void* O, DType t, int64_t ld, int64_t S, int64_t H,
-                  int64_t hd, float* delta, cudaStream_t s);
+                  int64_t hd, float* delta, cudaStream_t s, int64_t samples = 1);
 // dS = scale * P * (dP - sum_c P*dP); dP fp32.
 void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t rows, int64_t L,
                    float scale, cudaStream_t s);

@@ -395,10 +395,7 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
       k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
     }
     weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
-    for (int64_t smp = 0; smp < rd.samples_local; ++smp)
-      k_attn_delta(static_cast<const char*>(dout) + (size_t)smp * S * hq * esz,
-                   static_cast<const char*>(o) + (size_t)smp * S * hq * esz, t, hq, S, H, hd,
-                   delta + (size_t)smp * H * S, s);
+    k_attn_delta(dout, o, t, hq, S, H, hd, delta, s, rd.samples_local);
     AttnDesc a = attn_desc(rd, qkv, o, lse);
     a.dout = dout;
     a.delta = delta;
