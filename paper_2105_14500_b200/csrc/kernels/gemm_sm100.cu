@@ -6,18 +6,27 @@
 // (proj/src/algorithms.cpp:34-76) and by the per-head attention loops
 // (proj/src/layers.cpp:392-405, 430-448).
 //
-// CTA layout (192 threads, one CTA per SM, grid = min(tiles, #SMs)):
+// Two kernels, both persistent and warp-specialised (320 threads, one CTA per
+// SM):
 //   warp 0      TMA producer: one elected lane streams A/B k-blocks into a
 //               STAGES-deep shared-memory ring (128B-swizzled boxes).
-//   warp 1      MMA issuer + TMEM owner: one lane issues
-//               tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN, K=16) into a
-//               double-buffered fp32 accumulator in tensor memory and
-//               commits each stage back to the producer.
-//   warps 2..5  epilogue: tcgen05.ld the accumulator (warp w reads TMEM lanes
-//               32*(w%4)..+31), apply alpha / bias-free epilogue (store,
-//               accumulate, residual add, exact-erf GeLU) and write C.
-// The accumulator is double buffered (2*BN TMEM columns), so the epilogue of
-// tile i overlaps the MMAs of tile i+1.
+//   warp 1      MMA issuer + TMEM owner: one lane issues tcgen05.mma into
+//               fp32 accumulators in tensor memory and commits each stage
+//               back to the producer.
+//   warps 2..9  epilogue: two warps per TMEM lane quadrant (warp w reads
+//               lanes 32*(w%4)..+31) split the 32-column chunks; alpha and the
+//               fused epilogue (store, accumulate, residual add, exact-erf
+//               GeLU / GeLU', softmax forward / backward, row statistics).
+// * gemm_bf16_kernel<BN>: one CTA, M=128 x N=BN MMAs (cta_group::1), the
+//   accumulator double buffered (2*BN TMEM columns) so the epilogue of tile i
+//   overlaps the MMAs of tile i+1; used for N <= 128.
+// * gemm_bf16_2cta_kernel<.., NH, BNP>: a CTA pair on one TPC
+//   (cta_group::2, M=256 x N=BNP MMAs, each CTA stages half of A and half of
+//   B); pair tiles 256 x 256 (two TMEM accumulators) or 256 x 512 (NH = 2:
+//   both 256-column halves in TMEM, a quarter less L2->SM traffic per flop,
+//   TMA-store / TMA-reduce-add epilogue); tiles handed out in order from an
+//   atomic counter so concurrently running tiles share their A/B panels in
+//   L2 (see DESIGN.md section 3 for the measurements behind each choice).
 //
 // Operand majorness is a template parameter, so the three Tesseract
 // variants need no transposes in HBM:

@@ -1,17 +1,22 @@
 // Rank-level Transformer layers on the Tesseract grid (reference
 // proj/src/layers.cpp:242-517), B200 version:
-//  * LayerNorm: per-row partial statistics (sum, centred M2, w*mu^2 -- a
+//  * LayerNorm: with a one-member row group (q == 1) one fused single-pass
+//    kernel each way (stats + apply; stats + dx + dgain/dbias partials);
+//    otherwise per-row partial statistics (sum, centred M2, w*mu^2 -- a
 //    Chan-style combination that avoids E[x^2]-E[x]^2 cancellation in fp32)
-//    all-reduced over the row group, then normalise; the meter charges the
-//    reference's [rows, 2] payload (layers.cpp:258).
+//    all-reduced over the row group, then normalise. The meter charges the
+//    reference's [rows, 2] payload either way (layers.cpp:258).
 //  * FF: FF1 GEMM with the exact-erf GeLU fused into its epilogue (stores the
-//    pre-activation z and h = gelu(z)); FF2 GEMM with the residual add fused.
-//  * Attention: batched tcgen05 GEMMs per local sample over the local heads
-//    (per-head interleaved Q|K|V columns addressed by TMA strides, no copies),
-//    row softmax, P kept for the backward like the reference (layers.cpp:403).
-//    No causal mask (reference semantics).
+//    pre-activation z and h = gelu(z)); FF2 GEMM with the residual add fused;
+//    GeLU' fused into the FF2-dgrad epilogue when q == 1.
+//  * Attention (bf16): the fused tcgen05 kernels of kernels/attention_sm100.cu
+//    (S, P never in HBM; the row log-sum-exp is cached instead of the
+//    reference's probs) plus one batched dQ GEMM; the fp32 parity mode keeps
+//    batched GEMMs + row softmax with P cached like the reference
+//    (layers.cpp:403). Per-head interleaved Q|K|V columns are addressed by
+//    TMA coordinates, no copies. No causal mask (reference semantics).
 //  * Residual adds are fused into GEMM epilogues (forward) or into the
-//    LayerNorm-backward apply kernel (backward).
+//    LayerNorm-backward kernels (backward).
 // Forward caches live in the context workspace under per-op names until the
 // matching backward.
 #include <cmath>
