@@ -35,6 +35,17 @@ class Comm {
                       cudaStream_t s) = 0;
   // In-place fp32 sum delivered at every member.
   virtual void allreduce(Family f, float* buf, size_t n, cudaStream_t s) = 0;
+  // Pair exchange for reductions fused into a GEMM epilogue (groups of two):
+  // publishes `mine` (ready once s reaches this point) and returns the
+  // partner's buffer, readable from this rank's device, with s ordered after
+  // the partner's ready point; nullptr when the backend cannot map peer
+  // memory (the caller then uses reduce). pair_close marks the end of the
+  // reads on s and orders s after the partner's reads of `mine`.
+  virtual bool pair_capable(Family) { return false; }
+  virtual const float* pair_open(Family, const float* /*mine*/, size_t /*n*/, cudaStream_t) {
+    return nullptr;
+  }
+  virtual void pair_close(Family, cudaStream_t) {}
   virtual void barrier() = 0;
   virtual void* nccl_comm(Family) { return nullptr; }
 };

@@ -199,6 +199,39 @@ class LocalComm : public Comm {
     }
   }
 
+  // Phase A of a kind-3 call: exchange {pointer, ready event}; phase B in
+  // pair_close. Peer pointers are directly addressable (same device, or a
+  // peer device with peer access enabled by make_local_world).
+  bool pair_capable(Family f) override {
+    const Grid& g = w_->grid;
+    if (g.group_size(f) != 2) return false;
+    const int other_dev = w_->devices[g.rank_of(
+        g.member_at(f, g.group_index(c_, f), 1 - g.slot_in_group(c_, f)))];
+    int can = 1;
+    if (other_dev != device_) cudaDeviceCanAccessPeer(&can, device_, other_dev);
+    return can != 0;
+  }
+
+  const float* pair_open(Family f, const float* mine, size_t n, cudaStream_t s) override {
+    if (!pair_capable(f)) return nullptr;
+    Ctx x = enter(f, 3, 0, n * 4, mine, s);
+    pair_ = x;
+    pair_f_ = f;
+    const Post& o = x.rv->a[x.par][1 - x.slot];
+    TESS_CUDA(cudaStreamWaitEvent(s, o.ev, 0));
+    return static_cast<const float*>(o.ptr);
+  }
+
+  void pair_close(Family f, cudaStream_t s) override {
+    Ctx x = pair_;
+    if (!x.rv || f != pair_f_) fail(TESS_ERR_SPMD, "pair_close without pair_open");
+    pair_ = Ctx();
+    TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
+    x.rv->b[x.par][x.slot] = {nullptr, ev_b_[f][x.par], 3, 0, 0};
+    w_->wait(*x.rv, x.gsize);
+    TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][1 - x.slot].ev, 0));
+  }
+
   void barrier() override { w_->wait(w_->world, w_->grid.size()); }
 
  private:
@@ -250,6 +283,8 @@ class LocalComm : public Comm {
   uint64_t calls_[3] = {0, 0, 0};
   float* scratch_ = nullptr;
   size_t scratch_n_ = 0;
+  Ctx pair_;  // open pair exchange (pair_open .. pair_close)
+  Family pair_f_ = ROW;
 };
 
 }  // namespace

@@ -274,6 +274,11 @@ void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, siz
   if (!c.comm_noop) c.comm->reduce(f, root, send, recv, n, s);
 }
 
+void coll_reduce_note(Ctx& c, Family f, int root, size_t n) {
+  c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, n, false);
+  trace_event(c, 1, f, root, n);
+}
+
 void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s) {
   c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), 0, n, true);
   trace_event(c, 2, f, 0, n);

@@ -59,6 +59,9 @@ void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t el
 void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, size_t n,
                  cudaStream_t s);
 void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s);
+// Meters and traces a reduce whose data movement is fused into the owner's
+// GEMM epilogue (summa.cpp pair reduce): same CommStats / trace entry.
+void coll_reduce_note(Ctx& c, Family f, int root, size_t n);
 
 // Records a collective whose group has a single member (no data moves): the
 // reference still counts the call in its trace step sequence.

@@ -19,6 +19,7 @@
 //    the remaining backward compute.
 // The collective sequence (kind, family, root, payload elements) is the
 // reference's, so the host meter reproduces its CommStats.
+#include <cstdlib>
 #include <string>
 
 #include "kernels/kernels.h"
@@ -62,6 +63,52 @@ void finish(const float* res, int64_t rows, int64_t cols, const Out& out, cudaSt
   } else {
     fail(TESS_ERR_UNSUPPORTED, "epilogue not supported after a reduction");
   }
+}
+
+// Pair reduce fused into the owner's GEMM (q == 2 groups whose backend maps
+// the partner's memory; TESS_PAIR_REDUCE=0 turns it off). Every rank first
+// computes the partial it contributes to its partner's result, publishes it,
+// then computes its own partial with a Resid epilogue that reads the
+// partner's contribution tile by tile from peer memory and adds it: the
+// reduce's data movement runs inside the GEMM instead of a collective after
+// it. With two members the sum is order-free, so the result is bitwise the
+// slot-ascending reduce of the reference (runtime.cpp:310-312).
+bool use_pair_reduce(Ctx& c, Family f) {
+  static const bool env_off =
+      std::getenv("TESS_PAIR_REDUCE") && std::getenv("TESS_PAIR_REDUCE")[0] == '0';
+  return !env_off && c.grid.group_size(f) == 2 && c.comm->pair_capable(f);
+}
+
+// One partial GEMM of a pair reduce, or its value for an empty contraction:
+// `peer` null -> C = A.B (zeros when k == 0); else C = A.B + peer.
+void pair_gemm(GemmDesc g, int64_t k, float* dst, const float* peer, size_t n, cudaStream_t s) {
+  if (n == 0) return;
+  if (k == 0) {
+    if (peer)
+      TESS_CUDA(cudaMemcpyAsync(dst, peer, n * 4, cudaMemcpyDefault, s));
+    else
+      TESS_CUDA(cudaMemsetAsync(dst, 0, n * 4, s));
+    return;
+  }
+  g.c = dst;
+  g.c_type = DType::F32;
+  g.ldc = g.N;
+  g.epi = peer ? Epi::Resid : Epi::Store;
+  g.r = peer;
+  g.ldr = g.N;
+  g.alpha = 1.0f;
+  run_gemm(g, s);
+}
+
+// Exchange + owner GEMM of a pair reduce over family f.
+void pair_reduce_owner(Ctx& c, Family f, const GemmDesc& g, int64_t k, float* part,
+                       float* result, size_t n, cudaStream_t s) {
+  // comm_noop (exposed-comm timing): same GEMMs, the partner's buffer
+  // replaced by this rank's own contribution (no exchange).
+  const float* peer = c.comm_noop ? part : c.comm->pair_open(f, part, n, s);
+  if (!peer) fail(TESS_ERR_SPMD, "pair reduce: partner buffer unavailable");
+  pair_gemm(g, k, result, peer, n, s);
+  if (!c.comm_noop) c.comm->pair_close(f, s);
 }
 
 }  // namespace
@@ -132,6 +179,35 @@ void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
                          : (into_out ? static_cast<float*>(out.c)
                                      : static_cast<float*>(c.ws->get("nt.r", n * 4)));
   stream_dep(c, s, cs);
+  if (!direct && use_pair_reduce(c, ROW)) {
+    // collectives in the reference's order (algorithms.cpp:53-56): panels
+    // move now, the row reduces are fused into the owner GEMM below
+    void* bts[2];
+    for (int t = 0; t < 2; ++t) {
+      if (bp && bp->valid) {
+        bts[t] = bp->ptr[t];
+      } else {
+        bts[t] = c.coord.i == t ? const_cast<void*>(b)
+                                : c.ws->get("nt.b" + std::to_string(t), br * an * esz);
+        coll_bcast(c, COL, t, bts[t], br * an * esz, (uint64_t)(br * an), cs);
+      }
+      coll_reduce_note(c, ROW, t, n);
+    }
+    stream_dep(c, cs, s);
+    const int me = c.coord.j;
+    GemmDesc g = base_desc(in, ar, br, Out());
+    g.trans_b = true;
+    g.lda = an;
+    g.ldb = an;
+    float* part = static_cast<float*>(c.ws->get("nt.p0", n * 4));
+    g.seg[0] = {a, bts[1 - me], an};
+    pair_gemm(g, an, part, nullptr, n, s);  // contribution to the partner (slot 1-me)
+    g.seg[0] = {a, bts[me], an};
+    pair_reduce_owner(c, ROW, g, an, part, result, n, s);
+    if (!into_out) finish(result, ar, br, out, s);
+    stream_dep(c, s, cs);  // panel buffers free for the next broadcasts
+    return;
+  }
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:53: column broadcast of B(t, j)
     void* bt;
@@ -190,6 +266,34 @@ void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
                          : (into_out ? static_cast<float*>(out.c)
                                      : static_cast<float*>(c.ws->get(rname, n * 4)));
   stream_dep(c, s, cs);
+  if (!direct && use_pair_reduce(c, COL)) {
+    void* ats[2];
+    for (int t = 0; t < 2; ++t) {
+      // ref algorithms.cpp:67-70: row broadcast of A(h, t), column reduce to
+      // slot t (fused into the owner GEMM below)
+      ats[t] = c.coord.j == t ? const_cast<void*>(a)
+                              : c.ws->get("tn.a" + std::to_string(t), ar * an * esz);
+      coll_bcast(c, ROW, t, ats[t], ar * an * esz, (uint64_t)(ar * an), cs);
+      coll_reduce_note(c, COL, t, n);
+    }
+    stream_dep(c, cs, s);
+    const int me = c.coord.i;
+    GemmDesc g = base_desc(in, an, bn, Out());
+    g.trans_a = true;
+    g.lda = an;
+    g.ldb = bn;
+    float* part = static_cast<float*>(c.ws->get("tn.p0", n * 4));
+    g.seg[0] = {ats[1 - me], b, ar};
+    pair_gemm(g, ar, part, nullptr, n, s);
+    g.seg[0] = {ats[me], b, ar};
+    pair_reduce_owner(c, COL, g, ar, part, result, n, s);
+    stream_dep(c, s, cs);
+    // ref algorithms.cpp:72-74: depth all-reduce of the layer partial
+    if (depth) coll_allreduce(c, DEPTH, result, n, cs);
+    if (!into_out) finish(result, an, bn, out, cs);
+    if (!defer) stream_dep(c, cs, s);
+    return;
+  }
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:67: row broadcast of A(h, t)
     void* at = c.coord.j == t ? const_cast<void*>(a)
