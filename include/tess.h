@@ -333,6 +333,16 @@ tess_status tess_profile_json(char* buf, size_t cap, size_t* needed);
  * last trace into out (up to 512 values). No reference counterpart. */
 tess_status tess_debug_attn_trace(long long* out, int n);
 
+/* Test hook of the peer-window transport behind the fused pair reduce of the
+ * NCCL backend (CUDA IPC window + system-scope release/acquire sequence
+ * words): two processes (rank 0 and 1, same or different GPUs) swap IPC
+ * handles through files in `dir` and run `iters` acquire/fill/open/check/
+ * close rounds of n floats (2n after half-way: the window grows). *bad =
+ * elements that did not match the partner's pattern. Replaces nothing in the
+ * reference (its reduce is runtime.cpp:485-513). */
+tess_status tess_debug_peer_window(int rank, const char* dir, size_t n, int iters,
+                                   unsigned long long* bad);
+
 #ifdef __cplusplus
 }
 #endif

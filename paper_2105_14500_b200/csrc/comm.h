@@ -42,6 +42,10 @@ class Comm {
   // memory (the caller then uses reduce). pair_close marks the end of the
   // reads on s and orders s after the partner's reads of `mine`.
   virtual bool pair_capable(Family) { return false; }
+  // Buffer for this rank's contribution when the backend needs it in memory
+  // it exported to the partner (collective: both members, same n); nullptr
+  // = any device buffer will do.
+  virtual float* pair_buffer(Family, size_t /*n*/, cudaStream_t) { return nullptr; }
   virtual const float* pair_open(Family, const float* /*mine*/, size_t /*n*/, cudaStream_t) {
     return nullptr;
   }

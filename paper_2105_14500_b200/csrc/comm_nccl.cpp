@@ -26,6 +26,7 @@
 #include <mutex>
 
 #include "comm.h"
+#include "peer.h"
 
 namespace tess {
 
@@ -139,6 +140,14 @@ class NcclComm : public Comm {
   }
 
   ~NcclComm() override {
+    for (auto& w : win_) {
+      if (!w) continue;
+      try {
+        w->drain(0);
+      } catch (...) {
+      }
+      w.reset();
+    }
     for (int f = 0; f < 3; ++f)
       if (comm_[f]) nccl().CommDestroy(comm_[f]);
     if (world_) nccl().CommDestroy(world_);
@@ -179,12 +188,55 @@ class NcclComm : public Comm {
 
   void* nccl_comm(Family f) override { return comm_[f]; }
 
+  // Fused pair reduce over CUDA-IPC peer windows (peer.h): q = 2 groups.
+  bool pair_capable(Family f) override { return comm_[f] && g_.group_size(f) == 2; }
+
+  float* pair_buffer(Family f, size_t n, cudaStream_t s) override {
+    if (!pair_capable(f)) return nullptr;
+    if (!win_[f]) {
+      ncclComm_t cm = comm_[f];
+      const int me = g_.slot_in_group(c_, f);
+      // Blocking swap of the IPC handles: each slot broadcasts its own.
+      win_[f] = std::make_unique<PeerWindow>([cm, me](const void* mine, void* theirs,
+                                                      size_t bytes) {
+        // drain: no earlier operation of this communicator may still be in
+        // flight on another stream when the swap runs on the default stream
+        TESS_CUDA(cudaDeviceSynchronize());
+        void* d = nullptr;
+        TESS_CUDA(cudaMalloc(&d, 2 * bytes));
+        TESS_CUDA(cudaMemcpy(static_cast<char*>(d) + me * bytes, mine, bytes,
+                             cudaMemcpyHostToDevice));
+        for (int r = 0; r < 2; ++r) {
+          char* slot = static_cast<char*>(d) + r * bytes;
+          TESS_NCCL(nccl().Broadcast(slot, slot, bytes, ncclUint8, r, cm, 0));
+        }
+        TESS_CUDA(cudaStreamSynchronize(0));
+        TESS_CUDA(cudaMemcpy(theirs, static_cast<char*>(d) + (1 - me) * bytes, bytes,
+                             cudaMemcpyDeviceToHost));
+        TESS_CUDA(cudaFree(d));
+      });
+    }
+    return win_[f]->acquire(n, s);
+  }
+
+  const float* pair_open(Family f, const float* mine, size_t, cudaStream_t s) override {
+    if (!win_[f] || mine != win_[f]->local())
+      fail(TESS_ERR_SPMD, "pair_open: contribution not in the peer window");
+    return win_[f]->open(s);
+  }
+
+  void pair_close(Family f, cudaStream_t s) override {
+    if (!win_[f]) fail(TESS_ERR_SPMD, "pair_close without pair_open");
+    win_[f]->close(s);
+  }
+
  private:
   Grid g_;
   int rank_;
   Coord c_;
   ncclComm_t world_ = nullptr;
   ncclComm_t comm_[3] = {nullptr, nullptr, nullptr};
+  std::unique_ptr<PeerWindow> win_[3];
 };
 
 }  // namespace

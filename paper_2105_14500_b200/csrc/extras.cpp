@@ -139,3 +139,61 @@ tess_status tess_load_matrix(const char* path, int64_t* rows, int64_t* cols, dou
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Self-test of the peer window transport (peer.h) between two PROCESSES that
+// swap IPC handles through files in `dir` (no NCCL: it refuses two ranks on
+// one GPU, CUDA IPC does not). Each of `iters` rounds: acquire, fill our
+// window with a rank/round pattern, open, check the partner's, close; the
+// window grows half-way through. *bad = mismatching elements seen.
+#include <chrono>
+#include <cstdio>
+#include <thread>
+
+#include "peer.h"
+
+extern "C" tess_status tess_debug_peer_window(int rank, const char* dir, size_t n, int iters,
+                                              unsigned long long* bad) {
+  return guarded([&] {
+    if ((rank != 0 && rank != 1) || !dir || !bad || n == 0 || iters <= 0)
+      fail(TESS_ERR_INVALID, "tess_debug_peer_window: bad arguments");
+    int gen = 0;
+    const std::string d(dir);
+    PeerWindow w([&](const void* mine, void* theirs, size_t bytes) {
+      const std::string me = d + "/pw." + std::to_string(rank) + "." + std::to_string(gen);
+      const std::string other =
+          d + "/pw." + std::to_string(1 - rank) + "." + std::to_string(gen);
+      ++gen;
+      {
+        std::ofstream f(me + ".tmp", std::ios::binary);
+        f.write(static_cast<const char*>(mine), (std::streamsize)bytes);
+      }
+      std::rename((me + ".tmp").c_str(), me.c_str());
+      const auto t0 = std::chrono::steady_clock::now();
+      for (;;) {
+        std::ifstream f(other, std::ios::binary);
+        if (f && f.read(static_cast<char*>(theirs), (std::streamsize)bytes)) break;
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          fail(TESS_ERR_SPMD, "peer window self-test: partner did not publish " + other);
+        std::this_thread::sleep_for(std::chrono::milliseconds(5));
+      }
+    });
+    cudaStream_t s;
+    TESS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    unsigned long long* dbad = nullptr;
+    TESS_CUDA(cudaMalloc(&dbad, sizeof(*dbad)));
+    TESS_CUDA(cudaMemset(dbad, 0, sizeof(*dbad)));
+    for (int it = 0; it < iters; ++it) {
+      const size_t m = it >= iters / 2 ? 2 * n : n;
+      float* mine = w.acquire(m, s);
+      k_peer_fill(mine, m, (float)(rank * 100000 + it * 7), s);
+      const float* theirs = w.open(s);
+      k_peer_check(theirs, m, (float)((1 - rank) * 100000 + it * 7), dbad, s);
+      w.close(s);
+    }
+    w.drain(s);
+    TESS_CUDA(cudaMemcpy(bad, dbad, sizeof(*bad), cudaMemcpyDeviceToHost));
+    cudaFree(dbad);
+    cudaStreamDestroy(s);
+  });
+}

@@ -94,4 +94,14 @@ void k_attn_delta(const void* dO, const void* O, DType t, int64_t ld, int64_t S,
 void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t rows, int64_t L,
                    float scale, cudaStream_t s);
 
+// ---- peer windows (kernels/peer.cu) ----------------------------------------
+// System-scope release store of v into *flag (a partner's window header).
+void k_peer_signal(uint32_t* flag, uint32_t v, cudaStream_t s);
+// Spins with acquire loads until *flag >= v; traps after 60 s.
+void k_peer_wait(const uint32_t* flag, uint32_t v, cudaStream_t s);
+// Self-test pattern: dst[i] = base + (i % 4093); check counts mismatches.
+void k_peer_fill(float* dst, size_t n, float base, cudaStream_t s);
+void k_peer_check(const float* src, size_t n, float base, unsigned long long* bad,
+                  cudaStream_t s);
+
 }  // namespace tess

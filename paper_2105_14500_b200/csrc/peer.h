@@ -1,0 +1,62 @@
+// Peer window: a device buffer this rank exports to its partner in a
+// two-member group through CUDA IPC (one process per GPU over NVLink /
+// NVSwitch), so a GEMM epilogue on one GPU can read the other's partial
+// directly — the transport of the fused pair reduce (summa.cpp). Replaces the
+// data movement of RankCtx::reduce (reference runtime.cpp:485-513) for q = 2
+// groups; ordering is stream-level, with no host synchronisation per use:
+//
+//   acquire(n, s) -> local buffer; s waits until the partner has finished
+//                    reading this buffer's previous contents ("done" >= e)
+//   open(s)       -> partner's buffer; signals "ready" = e+1 to the partner
+//                    and makes s wait for the partner's "ready" >= e+1
+//   close(s)      -> signals "done" = e+1 (this rank stopped reading); e++
+//
+// The header of each window holds the two sequence words the PARTNER writes
+// (system-scope release stores, kernels/peer.cu). Growing the window is
+// collective (both members call acquire with the same n): streams are
+// drained, the partner's old mapping is closed and new IPC handles are
+// exchanged through the caller-supplied blocking `Exchange`.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+
+namespace tess {
+
+class PeerWindow {
+ public:
+  // exchange(mine, theirs, bytes): blocking swap of `bytes` with the partner.
+  using Exchange = std::function<void(const void* mine, void* theirs, size_t bytes)>;
+
+  explicit PeerWindow(Exchange ex) : ex_(std::move(ex)) {}
+  ~PeerWindow();
+  PeerWindow(const PeerWindow&) = delete;
+  PeerWindow& operator=(const PeerWindow&) = delete;
+
+  float* acquire(size_t n, cudaStream_t s);
+  const float* open(cudaStream_t s);
+  void close(cudaStream_t s);
+  // Blocks until the partner stopped reading our window (before teardown).
+  void drain(cudaStream_t s);
+  float* local() const { return data(base_); }
+
+ private:
+  static constexpr size_t kHeader = 256;  // [0] ready, [1] done (written by the partner)
+  static float* data(void* b) {
+    return b ? reinterpret_cast<float*>(static_cast<char*>(b) + kHeader) : nullptr;
+  }
+  static uint32_t* flags(void* b) { return static_cast<uint32_t*>(b); }
+  void grow(size_t n, cudaStream_t s);
+
+  Exchange ex_;
+  void* base_ = nullptr;  // own window (cudaMalloc, exported)
+  void* peer_ = nullptr;  // partner's window (cudaIpcOpenMemHandle)
+  size_t cap_ = 0;        // floats
+  uint32_t epoch_ = 0;
+  bool opened_ = false;
+};
+
+}  // namespace tess

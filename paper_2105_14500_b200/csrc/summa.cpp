@@ -100,6 +100,13 @@ void pair_gemm(GemmDesc g, int64_t k, float* dst, const float* peer, size_t n, c
   run_gemm(g, s);
 }
 
+// Where this rank's contribution goes: the backend's exported window (NCCL:
+// CUDA IPC) or, for the in-process backend, any workspace buffer.
+float* pair_part(Ctx& c, Family f, const std::string& tag, size_t n, cudaStream_t s) {
+  float* w = c.comm_noop ? nullptr : c.comm->pair_buffer(f, n, s);
+  return w ? w : static_cast<float*>(c.ws->get(tag, n * 4));
+}
+
 // Exchange + owner GEMM of a pair reduce over family f.
 void pair_reduce_owner(Ctx& c, Family f, const GemmDesc& g, int64_t k, float* part,
                        float* result, size_t n, cudaStream_t s) {
@@ -199,7 +206,7 @@ void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
     g.trans_b = true;
     g.lda = an;
     g.ldb = an;
-    float* part = static_cast<float*>(c.ws->get("nt.p0", n * 4));
+    float* part = pair_part(c, ROW, "nt.p0", n, s);
     g.seg[0] = {a, bts[1 - me], an};
     pair_gemm(g, an, part, nullptr, n, s);  // contribution to the partner (slot 1-me)
     g.seg[0] = {a, bts[me], an};
@@ -282,7 +289,7 @@ void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
     g.trans_a = true;
     g.lda = an;
     g.ldb = bn;
-    float* part = static_cast<float*>(c.ws->get("tn.p0", n * 4));
+    float* part = pair_part(c, COL, "tn.p0", n, s);
     g.seg[0] = {ats[1 - me], b, ar};
     pair_gemm(g, ar, part, nullptr, n, s);
     g.seg[0] = {ats[me], b, ar};
