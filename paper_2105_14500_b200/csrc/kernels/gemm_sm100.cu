@@ -71,6 +71,7 @@ struct Params {
   int tiles_m, tiles_n, tiles_per_batch, num_tiles;
   int group_m;
   int skip_store;               // experiment: epilogue computes but does not store
+  int mma_lead;                 // NH == 2: half-0 MMAs lead while half 1 drains
   int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch) or null
   int raster_n;                 // pair kernel: 1 = groups of group_m N-tiles, N fastest
   unsigned long long hint_a, hint_b;  // pair kernel: L2 cache policy of the A / B TMA loads
@@ -951,7 +952,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t slot_phase = 0;  // bit s = phase of slot s
       for (;;) {
         if (tq.pop(cta, false) < 0) break;
-        for (int kb = 0; kb < p.total_kb; ++kb) {
+        int kb0 = 0;
+        if (NH == 2 && p.mma_lead) {
+          // Lead phase: the epilogue drains half 0 first, so start this
+          // tile's half-0 MMAs on up to STAGES k-blocks while it is still
+          // draining half 1, then catch half 1 up on the same (still held)
+          // stages and release them. Hides the half-1 drain under MMAs.
+          const int lead = p.total_kb < C::STAGES ? p.total_kb : C::STAGES;
+          const int st0 = stage;
+          const uint32_t ph0 = phase;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(&tempty_bar[h], ((slot_phase >> h) & 1) ^ 1);
+            tc_fence_after();
+            int sg = st0;
+            uint32_t ph = ph0;
+#pragma unroll 1
+            for (int kb = 0; kb < lead; ++kb) {
+              if (h == 0) {
+                mbar_wait(&full_bar[sg], ph);
+                tc_fence_after();
+              }
+              const uint32_t sa = smem_u32(smem + sg * C::STAGE_BYTES);
+              const uint32_t sbh = sa + C::A_BYTES + h * (C::BH * BK * 2);
+              const uint32_t d_tmem = tmem_base + h * BNP;
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k) {
+                const uint64_t ad = A_MN ? make_sdesc(sa + k * 2048, 8192, 1024)
+                                         : make_sdesc(sa + k * 32, 16, 1024);
+                const uint64_t bd = B_MN ? make_sdesc(sbh + k * 2048, 8192, 1024)
+                                         : make_sdesc(sbh + k * 32, 16, 1024);
+                mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              }
+              if (h == 1) mma_commit_2sm(&empty_bar[sg]);
+              if (++sg == C::STAGES) {
+                sg = 0;
+                ph ^= 1;
+              }
+            }
+            if (h == 1) {
+              stage = sg;
+              phase = ph;
+            }
+          }
+          kb0 = lead;
+        }
+        for (int kb = kb0; kb < p.total_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -959,7 +1005,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int h = 0; h < NH; ++h) {
             const int slot = NH == 1 ? acc : h;
-            if (kb == 0) {
+            if (kb == 0 && kb0 == 0) {
               // the accumulator slot must have been drained by the epilogue
               mbar_wait(&tempty_bar[slot], ((slot_phase >> slot) & 1) ^ 1);
               tc_fence_after();
@@ -1315,6 +1361,9 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   }
   Params p;
   std::memset(&p, 0, sizeof(p));
+  static const int env_lead =
+      std::getenv("TESS_GEMM_LEAD") && std::getenv("TESS_GEMM_LEAD")[0] == '0' ? 0 : 1;
+  p.mma_lead = env_lead;
   const bool pair = use_pair_kernel(d.M, d.N);
   const int pair_tn = pair ? pair_tile_n(d) : 0;
   const int nh = pair_tn == 512 ? 2 : 1;
