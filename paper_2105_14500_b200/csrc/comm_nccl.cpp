@@ -189,11 +189,26 @@ class NcclComm : public Comm {
   void* nccl_comm(Family f) override { return comm_[f]; }
 
   // Fused pair reduce over CUDA-IPC peer windows (peer.h): q = 2 groups.
-  bool pair_capable(Family f) override { return comm_[f] && g_.group_size(f) == 2; }
+  // Collective on first use per family (both members reach it at the same
+  // program point): maps a small window and agrees on the outcome.
+  bool pair_capable(Family f) override {
+    if (!comm_[f] || g_.group_size(f) != 2) return false;
+    if (!probed_[f]) {
+      probed_[f] = true;
+      make_window(f);
+      pair_ok_[f] = win_[f]->probe(0);
+      if (!pair_ok_[f]) win_[f].reset();
+    }
+    return pair_ok_[f];
+  }
 
   float* pair_buffer(Family f, size_t n, cudaStream_t s) override {
     if (!pair_capable(f)) return nullptr;
-    if (!win_[f]) {
+    return win_[f]->acquire(n, s);
+  }
+
+  void make_window(Family f) {
+    {
       ncclComm_t cm = comm_[f];
       const int me = g_.slot_in_group(c_, f);
       // Blocking swap of the IPC handles: each slot broadcasts its own.
@@ -216,7 +231,6 @@ class NcclComm : public Comm {
         TESS_CUDA(cudaFree(d));
       });
     }
-    return win_[f]->acquire(n, s);
   }
 
   const float* pair_open(Family f, const float* mine, size_t, cudaStream_t s) override {
@@ -237,6 +251,8 @@ class NcclComm : public Comm {
   ncclComm_t world_ = nullptr;
   ncclComm_t comm_[3] = {nullptr, nullptr, nullptr};
   std::unique_ptr<PeerWindow> win_[3];
+  bool probed_[3] = {false, false, false};
+  bool pair_ok_[3] = {false, false, false};
 };
 
 }  // namespace

@@ -13,7 +13,7 @@ PeerWindow::~PeerWindow() {
   if (base_) cudaFree(base_);
 }
 
-void PeerWindow::grow(size_t n, cudaStream_t s) {
+bool PeerWindow::grow(size_t n, cudaStream_t s) {
   // Nothing of ours may still touch the old windows: our own reads of the
   // partner's window and the partner's reads of ours (done >= epoch).
   if (base_) k_peer_wait(&flags(base_)[1], epoch_, s);
@@ -34,12 +34,27 @@ void PeerWindow::grow(size_t n, cudaStream_t s) {
   base_ = nb;
   cap_ = n;
   epoch_ = 0;
-  TESS_CUDA(cudaIpcOpenMemHandle(&peer_, theirs, cudaIpcMemLazyEnablePeerAccess));
+  const cudaError_t e = cudaIpcOpenMemHandle(&peer_, theirs, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    peer_ = nullptr;
+  }
+  // both members must agree before anyone relies on the mapping
+  const unsigned char ok = peer_ != nullptr;
+  unsigned char ok_theirs = 0;
+  ex_(&ok, &ok_theirs, 1);
+  if (ok && ok_theirs) return true;
+  if (peer_) cudaIpcCloseMemHandle(peer_);
+  peer_ = nullptr;
+  return false;
 }
+
+bool PeerWindow::probe(cudaStream_t s) { return grow(1024, s); }
 
 float* PeerWindow::acquire(size_t n, cudaStream_t s) {
   if (opened_) fail(TESS_ERR_SPMD, "peer window: acquire while open");
-  if (!base_ || n > cap_) grow(n, s);
+  if ((!base_ || n > cap_) && !grow(n, s))
+    fail(TESS_ERR_CUDA, "peer window: cannot map the partner's window");
   // the partner finished reading what we published last time
   if (epoch_) k_peer_wait(&flags(base_)[1], epoch_, s);
   return data(base_);

@@ -36,6 +36,11 @@ class PeerWindow {
   PeerWindow(const PeerWindow&) = delete;
   PeerWindow& operator=(const PeerWindow&) = delete;
 
+  // Collective first mapping of a small window; false (on both members)
+  // when either side cannot map the other's memory (no peer access between
+  // the GPUs, devices hidden from the process): the caller then keeps the
+  // collective path.
+  bool probe(cudaStream_t s);
   float* acquire(size_t n, cudaStream_t s);
   const float* open(cudaStream_t s);
   void close(cudaStream_t s);
@@ -49,7 +54,7 @@ class PeerWindow {
     return b ? reinterpret_cast<float*>(static_cast<char*>(b) + kHeader) : nullptr;
   }
   static uint32_t* flags(void* b) { return static_cast<uint32_t*>(b); }
-  void grow(size_t n, cudaStream_t s);
+  bool grow(size_t n, cudaStream_t s);
 
   Exchange ex_;
   void* base_ = nullptr;  // own window (cudaMalloc, exported)
