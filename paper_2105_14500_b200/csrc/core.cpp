@@ -298,6 +298,7 @@ tess_ctx::~tess_ctx() {
     cudaStreamDestroy(copy_s);
   }
   for (auto& kv : copy_ev) cudaEventDestroy(kv.second);
+  for (auto& kv : stage_free) cudaEventDestroy(kv.second);
   if (up_s) {
     cudaStreamSynchronize(up_s);
     cudaStreamDestroy(up_s);

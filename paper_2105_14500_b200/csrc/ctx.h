@@ -40,8 +40,13 @@ struct tess_ctx {
   cudaStream_t copy_s = nullptr;
   std::map<std::string, cudaEvent_t> copy_ev;
   std::map<std::string, std::pair<const char*, size_t>> copy_host;  // host range per copy
-  // Upload stream of tess_layer_step (dy goes up while the forward runs).
+  // Upload stream of tess_layer_step: host x and dy go up into staging
+  // buffers double-buffered per call (stage_par), each copy waiting only for
+  // its buffer's previous reader (stage_free), so it overlaps the previous
+  // step's compute.
   cudaStream_t up_s = nullptr;
+  std::map<std::string, int> stage_par;
+  std::map<std::string, cudaEvent_t> stage_free;
   std::vector<cudaEvent_t> ev_ring;
   size_t ev_next = 0;
   ~tess_ctx();

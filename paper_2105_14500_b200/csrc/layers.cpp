@@ -702,29 +702,59 @@ void ctx_join(Ctx& c, cudaStream_t s) {
   c.copy_host.clear();
 }
 
+namespace {
+
+// Host input -> the next of two device staging buffers `name`0/1 on the
+// upload stream, once that buffer's previous reader (two calls ago) is done:
+// with the host enqueueing ahead of the GPU the copy overlaps the previous
+// step's compute instead of queueing behind it. `used` names the buffer for
+// stage_release.
+const void* stage_upload(Ctx& c, const std::string& name, const void* host, size_t bytes,
+                         std::string* used) {
+  if (!c.up_s) TESS_CUDA(cudaStreamCreateWithFlags(&c.up_s, cudaStreamNonBlocking));
+  int& par = c.stage_par[name];
+  *used = name + std::to_string(par);
+  par ^= 1;
+  void* d = wsget(c, *used, bytes);
+  const auto it = c.stage_free.find(*used);
+  if (it != c.stage_free.end()) TESS_CUDA(cudaStreamWaitEvent(c.up_s, it->second, 0));
+  join_host_overlap(c, host, bytes, c.up_s);  // the host range may be a pending output of ours
+  TESS_CUDA(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, c.up_s));
+  return d;
+}
+
+// The staging buffer's last reader has been enqueued on s.
+void stage_release(Ctx& c, const std::string& used, cudaStream_t s) {
+  if (used.empty()) return;
+  cudaEvent_t& e = c.stage_free[used];
+  if (!e) TESS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TESS_CUDA(cudaEventRecord(e, s));
+}
+
+}  // namespace
+
 // Forward + backward in one call with both inputs known up front (the
 // reference's layer_run(op, x, dy, ...), layers.cpp:604-692, at rank level):
-// a host dy is uploaded on the context's upload stream while the forward
-// runs, instead of after it.
+// host x and dy are uploaded on the context's upload stream into per-call
+// double-buffered staging, x gating the forward and dy only the backward.
 void layer_step(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                 const tess_block_shard& p, const float* bias_row0, const void* x, const void* dy,
                 void* y, void* dx, tess_block_grads* g, bool accumulate, float* dbias,
                 cudaStream_t s) {
   const size_t act = (size_t)rd.rows * rd.hq * dtype_size(t);
-  const void* dyd = dy;
-  if (!is_device_ptr(dy)) {
-    if (!c.up_s) TESS_CUDA(cudaStreamCreateWithFlags(&c.up_s, cudaStreamNonBlocking));
-    void* ds = wsget(c, "stage.dy", act);
-    // the staging buffer's last reader (the previous backward) is on s before
-    // this point; the forward enqueued next is not waited for
-    stream_dep(c, s, c.up_s);
-    join_host_overlap(c, dy, act, c.up_s);
-    TESS_CUDA(cudaMemcpyAsync(ds, dy, act, cudaMemcpyHostToDevice, c.up_s));
-    dyd = ds;
+  std::string xb, db;
+  const void* xd = x;
+  if (!is_device_ptr(x)) {
+    xd = stage_upload(c, cache_tag(c, op) + ".xin", x, act, &xb);
+    stream_dep(c, c.up_s, s);  // the forward waits for x only
   }
-  layer_forward(c, op, t, rd, p, bias_row0, x, y, s);
+  const void* dyd = dy;
+  if (!is_device_ptr(dy)) dyd = stage_upload(c, "stage.dyin", dy, act, &db);
+  layer_forward(c, op, t, rd, p, bias_row0, xd, y, s);
   if (dyd != dy) stream_dep(c, c.up_s, s);
   layer_backward(c, op, t, rd, p, dyd, dx, g, accumulate, dbias, s);
+  stage_release(c, xb, s);
+  stage_release(c, db, s);
 }
 
 }  // namespace tess

@@ -18,5 +18,5 @@ ev = [[buf[e * 64 + t] for t in range(64)] for e in range(8)]
 t0 = min(v for row in ev for v in row if v)
 names = ["MMA scores(i)", "MMA pds_full(i)", "SM sdp_full(i)", "SM chunk0 done", "SM pds_full", "SM tmem loaded", "MMA sdp_free(i)", "MMA grads(i) out"]
 print("tile " + " ".join(f"{n:>18s}" for n in names))
-for t in range(32):
+for t in range(int(os.environ.get("TILES", "16"))):
     print(f"{t:4d} " + " ".join(f"{(ev[e][t] - t0) if ev[e][t] else -1:18d}" for e in range(8)))
