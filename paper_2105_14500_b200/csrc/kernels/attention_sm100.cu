@@ -378,6 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 // same bytes under two descriptors.
 // TMEM: S^T / P^T [0,128), dP^T [128,256), dV [256, 256+hd), dK [384, 384+hd).
 constexpr int BQB = 128;  // queries per backward tile
+// which of every 4 exponentials of the backward use exp2_fma (bit u)
+#ifndef TESS_ATTN_BWD_POLY
+#define TESS_ATTN_BWD_POLY 8
+#endif
+constexpr int kBwdPolyMask = TESS_ATTN_BWD_POLY;
 
 struct BwdParams {
   CUtensorMap tm_kv;   // qkv view, box {64, 128}: K, V of the key tile
@@ -422,6 +427,22 @@ struct BwdCfg {
   static constexpr int TMEM_COLS = 512;
   static constexpr int TM_ST = 0, TM_DPT = 128, TM_DV = 256, TM_DK = 384;
 };
+
+// 2^x on the FMA/ALU pipes (round-to-nearest split, degree-3 polynomial on
+// [-0.5, 0.5], max rel. error 2.2e-4 -- far below the bf16 rounding of P):
+// the backward's exp2/dS math is MUFU-bound (16 K ex2 per tile at 16/clk),
+// so a share of the exponentials moves here. x is clamped at -125 so the
+// exponent add cannot underflow (2^-125 instead of 0 for masked columns,
+// whose dO / Q rows are zero).
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: rint(x) in the low mantissa bits
+  const float j = t - 12582912.0f;
+  const float f = x - j;
+  const float p =
+      fmaf(fmaf(fmaf(0.05286731571f, f, 0.2421521395f), f, 0.6935868263f), f, 0.9999627471f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 
 // 32 bf16 values of row r (columns [u0*8, u0*8+32) of a 64-column K-major
 // SW128 tile) -> shared memory.
@@ -683,7 +704,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int e = 4 * e4 + u;
-          const float pv = ex2_approx(fmaf(__uint_as_float(sr[e]), cl2, -lv[u]));
+          const float xv = fmaf(__uint_as_float(sr[e]), cl2, -lv[u]);
+          const float pv = (kBwdPolyMask >> u) & 1 ? exp2_fma(xv) : ex2_approx(xv);
           dr[e] = __float_as_uint(pv * (__uint_as_float(dr[e]) - dv[u]));
           sr[e] = __float_as_uint(pv);
         }
