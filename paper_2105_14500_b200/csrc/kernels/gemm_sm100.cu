@@ -72,6 +72,7 @@ struct Params {
   int group_m;
   int skip_store;               // experiment: epilogue computes but does not store
   int mma_lead;                 // NH == 2: half-0 MMAs lead while half 1 drains
+  int serp;                     // serpentine K order across waves (L2 reuse)
   int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch) or null
   int raster_n;                 // pair kernel: 1 = groups of group_m N-tiles, N fastest
   unsigned long long hint_a, hint_b;  // pair kernel: L2 cache policy of the A / B TMA loads
@@ -901,10 +902,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int b0, b1, m0, n0;
         decode_pair_tile(p, tile, b0, b1, m0, n0);
         const int mr = m0 + (int)cta * C::HALF;
-        for (int s = 0; s < p.nseg; ++s) {
+        // Serpentine K: odd waves walk K backwards, so a wave starts on the
+        // k-blocks the previous wave touched last -- still in L2 for the
+        // operand panels the two waves share.
+        const bool rev = p.serp && ((tile / nclusters) & 1);
+        for (int si = 0; si < p.nseg; ++si) {
+          const int s = rev ? p.nseg - 1 - si : si;
           const CUtensorMap* ma = &p.tma_a[s];
           const CUtensorMap* mb = &p.tma_b[s];
-          for (int kb = 0; kb < p.seg_kb[s]; ++kb) {
+          for (int ki = 0; ki < p.seg_kb[s]; ++ki) {
+            const int kb = rev ? p.seg_kb[s] - 1 - ki : ki;
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * C::STAGE_BYTES;
             uint8_t* sb = sa + C::A_BYTES;
@@ -1364,6 +1371,9 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   static const int env_lead =
       std::getenv("TESS_GEMM_LEAD") && std::getenv("TESS_GEMM_LEAD")[0] == '0' ? 0 : 1;
   p.mma_lead = env_lead;
+  static const int env_serp =
+      std::getenv("TESS_GEMM_SERP") && std::getenv("TESS_GEMM_SERP")[0] == '0' ? 0 : 1;
+  p.serp = env_serp;
   const bool pair = use_pair_kernel(d.M, d.N);
   const int pair_tn = pair ? pair_tile_n(d) : 0;
   const int nh = pair_tn == 512 ? 2 : 1;
