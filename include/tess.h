@@ -254,6 +254,16 @@ tess_status tess_set_cache_slot(tess_ctx* ctx, int slot);
  * Results computed while it is on are meaningless. */
 tess_status tess_set_comm_noop(tess_ctx* ctx, int enable);
 
+/* 1-D tensor-parallel (Megatron) layer scheme for this rank (BASELINE config
+ * 5's comparator; the reference ships only its two-linear kernel,
+ * algorithms.cpp:244-265). Needs a [1,1,p] line grid (q == 1): x, dy, y, dx
+ * are the full [batch*seq, hidden] activations on every rank; the shard
+ * holds W_qkv / W_ff1 column blocks k (heads [k n/p, (k+1) n/p)), W_proj /
+ * W_ff2 row blocks k, and the full LayerNorm vectors; the proj / FF2 outputs
+ * and the QKV / FF1 dgrads are all-reduced over the depth group, weight
+ * gradients stay per shard. Applies to the layer calls that follow. */
+tess_status tess_set_megatron(tess_ctx* ctx, int enable);
+
 /* ---------------------------------------------------------- global level
  * Whole-matrix operators with host fp64 buffers, mirroring the reference's
  * value-semantics API: partition -> per-rank SPMD (one host thread per rank,
@@ -304,6 +314,16 @@ tess_status tess_megatron_1d_linear(int p, tess_dtype compute, const double* x, 
                                     const double* w2, int64_t w2r, int64_t w2c, double* out,
                                     const int* devices, uint64_t* stats_rank,
                                     uint64_t* stats_kind);
+
+/* Global-level 1-D (Megatron) counterpart of tess_layer_run on p ranks (see
+ * tess_set_megatron): same argument meaning, outputs combined from the
+ * shards (column / row blocks of the weight gradients, the replicated y, dx
+ * and LayerNorm gradients from rank 0). bias_add is not supported. */
+tess_status tess_megatron_layer_run(tess_layer_op op, const tess_layer_dims* dims, int p,
+                                    tess_dtype compute, const double* x, const double* dy,
+                                    const double* const* params, double eps, double* y,
+                                    double* dx, double* const* grads, const int* devices,
+                                    uint64_t* stats_rank, uint64_t* stats_kind);
 
 /* ref: matrix.cpp:352-370 checksum (FNV-1a over rows, cols and the
  * little-endian doubles; printed by the reference as "fnv1a:%x"). */

@@ -148,6 +148,7 @@ def _load() -> C.CDLL:
         "tess_reset_comm_stats": ([vp], i),
         "tess_set_trace": ([vp, i], i),
         "tess_set_comm_noop": ([vp, i], i),
+        "tess_set_megatron": ([vp, i], i),
         "tess_stream_join": ([vp, vp], i),
         "tess_layer_step": ([vp, i, i, C.POINTER(_LayerDimsC), C.POINTER(BlockShardC), vp, vp, vp,
                              vp, vp, C.POINTER(BlockGradsC), i, vp, vp], i),
@@ -169,6 +170,8 @@ def _load() -> C.CDLL:
                                      u64p], i),
         "tess_layer_run": ([i, C.POINTER(_LayerDimsC), i, i, i, i, dp, dp, C.POINTER(dp),
                             C.c_double, dp, dp, C.POINTER(dp), dp, ip, u64p, u64p], i),
+        "tess_megatron_layer_run": ([i, C.POINTER(_LayerDimsC), i, i, dp, dp, C.POINTER(dp),
+                                     C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -457,6 +460,29 @@ def layer_run(op: str, x, dy, params: Dict[str, np.ndarray], dims: LayerDims, gr
     return LayerRunResult(y, dx, dict(zip(PARAM_NAMES, grads)), dbias, CommStats(sr, sk))
 
 
+def megatron_layer_run(op: str, x, dy, params: Dict[str, np.ndarray], dims: LayerDims, p: int,
+                       dtype="f32", eps: float = 1e-5,
+                       devices: Optional[Sequence[int]] = None) -> LayerRunResult:
+    """Forward + backward of one layer op in the 1-D (Megatron) scheme on p
+    ranks: heads / FF columns split, activations replicated, partial outputs
+    all-reduced (the config-5 comparator; tess_megatron_layer_run)."""
+    x, dy = _f64(x), _f64(dy)
+    h = dims.hidden
+    if x.shape != (dims.batch * dims.seq, h) or dy.shape != x.shape:
+        raise ShapeError("activation must be [batch*seq, hidden]")
+    prm = [_f64(params[n]) for n in PARAM_NAMES]
+    grads = [np.zeros(s) for s in _param_shapes(h)]
+    y, dx = np.zeros_like(x), np.zeros_like(x)
+    P = (C.POINTER(C.c_double) * 8)(*[_dptr(t) for t in prm])
+    G = (C.POINTER(C.c_double) * 8)(*[_dptr(t) for t in grads])
+    sr, sk = _stats_bufs(p)
+    dc = dims.c()
+    _check(lib.tess_megatron_layer_run(LAYER_OPS[op], C.byref(dc), p, _dtype(dtype), _dptr(x),
+                                       _dptr(dy), P, eps, _dptr(y), _dptr(dx), G,
+                                       _devices(devices, p), _u64(sr), _u64(sk)))
+    return LayerRunResult(y, dx, dict(zip(PARAM_NAMES, grads)), np.zeros(h), CommStats(sr, sk))
+
+
 def summa_matmul(a, b, q: int, dtype="f32", devices=None) -> AlgoResult:
     """SUMMA on a [q,q] mesh (algorithms.cpp:105-118) = the [q,q,1] Tesseract NN."""
     return tesseract_matmul(a, b, GridSpec(q, 1), "nn", dtype=dtype, devices=devices)
@@ -567,6 +593,11 @@ class RankContext:
         """Order `stream` after the context's in-flight host copies of layer
         outputs and deferred collectives (read host outputs after this)."""
         _check(lib.tess_stream_join(self.h, C.c_void_p(stream)))
+
+    def set_megatron(self, on=True):
+        """1-D (Megatron) layer scheme for the layer calls that follow
+        ([1,1,p] line grid; see tess_set_megatron)."""
+        _check(lib.tess_set_megatron(self.h, int(on)))
 
     def set_comm_noop(self, on=True):
         """Collectives metered but moving no data (timing the step without

@@ -269,6 +269,15 @@ tess_status tess_set_comm_noop(tess_ctx* c, int enable) {
   });
 }
 
+tess_status tess_set_megatron(tess_ctx* c, int enable) {
+  return guarded([&] {
+    if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
+    if (enable && c->grid.q != 1)
+      fail(TESS_ERR_GRID, "the 1-D scheme runs on a [1,1,p] line grid (q == 1)");
+    c->megatron = enable != 0;
+  });
+}
+
 tess_status tess_set_trace(tess_ctx* c, int enable) {
   return guarded([&] {
     if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");

@@ -22,6 +22,12 @@ struct tess_ctx {
   // Measurement only (tess_set_comm_noop): collectives are metered and traced
   // but move no data, to time the step without communication (exposed comm).
   bool comm_noop = false;
+  // 1-D tensor-parallel (Megatron) layer scheme on a [1,1,p] line grid
+  // (tess_set_megatron; BASELINE config 5's comparator): activations
+  // replicated, W_qkv / W_ff1 column-split, W_proj / W_ff2 row-split, the
+  // partial outputs of proj / FF2 (forward) and QKV / FF1 dgrads (backward)
+  // all-reduced over the depth group; weight shards are not depth-reduced.
+  bool megatron = false;
   uint64_t step = 0;  // collective sequence number (RankCtx::step_)
   std::vector<tess::TraceEvent> trace;
   std::unique_ptr<tess::Workspace> ws;

@@ -430,6 +430,125 @@ tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q,
   });
 }
 
+// The 1-D tensor-parallel (Megatron) counterpart of tess_layer_run, BASELINE
+// config 5's comparator built from megatron_1d_linear (ref algorithms.cpp:
+// 244-265: Column1D / Row1D weight split, depth all-reduce of the partials)
+// applied to the whole block: on a [1,1,p] line grid every rank holds x and
+// dy, heads [k n/p, (k+1) n/p) -- W_qkv / W_ff1 column shards, W_proj / W_ff2
+// row shards -- and the LayerNorm vectors; the proj / FF2 outputs and the
+// QKV / FF1 dgrads are all-reduced over the line. Same math as the reference
+// block (layers.cpp:460-487), so the oracle's ref::transformer_block checks it.
+tess_status tess_megatron_layer_run(tess_layer_op op, const tess_layer_dims* dims, int p,
+                                    tess_dtype compute, const double* x, const double* dy,
+                                    const double* const* params, double eps, double* y,
+                                    double* dx, double* const* grads, const int* devices,
+                                    uint64_t* sr, uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    if (!dims || !x || !dy || !params || !y || !dx) fail(TESS_ERR_INVALID, "null argument");
+    if (op == TESS_OP_BIAS_ADD) fail(TESS_ERR_UNSUPPORTED, "1-D scheme: no bias_add op");
+    if (p < 1) fail(TESS_ERR_GRID, "p must be >= 1");
+    const tess_layer_dims D = *dims;
+    const int64_t h = D.hidden, T = (int64_t)D.batch * D.seq;
+    if (D.heads <= 0 || D.heads % p != 0 || h % D.heads != 0)
+      fail(TESS_ERR_DIVISIBILITY, "1-D scheme: heads must divide hidden and be divisible by p");
+    const int64_t hp = h / p;
+    Runner R(1, p, true, devices);
+    DevMat dX, dDY, W[4], LN[4];
+    upload(dX, R.unique_devices(), x, (size_t)(T * h), t);
+    upload(dDY, R.unique_devices(), dy, (size_t)(T * h), t);
+    const int64_t wshape[4][2] = {{h, 3 * h}, {h, h}, {h, 4 * h}, {4 * h, h}};
+    const bool colsplit[4] = {true, false, true, false};
+    for (int i = 0; i < 4; ++i)
+      upload(W[i], R.unique_devices(), params[i], (size_t)(wshape[i][0] * wshape[i][1]), t);
+    for (int i = 0; i < 4; ++i)
+      upload(LN[i], R.unique_devices(), params[4 + i], (size_t)h, DType::F32);
+    std::vector<float> ys, dxs, gl[4];
+    std::vector<std::vector<float>> gw[4];
+    for (auto& v : gw) v.resize(p);
+    const size_t e = dtype_size(t);
+    R.run([&](Ctx& c, cudaStream_t s) {
+      c.megatron = true;
+      const int k = c.coord.k;  // line grid: rank index = depth slot
+      const void* wl[4];
+      int64_t lsh[4][2];
+      for (int i = 0; i < 4; ++i) {
+        const int64_t r = wshape[i][0], cols = wshape[i][1];
+        const char* src = static_cast<const char*>(W[i].on(c.device));
+        if (colsplit[i]) {  // Column1D: columns [k cols/p, (k+1) cols/p)
+          const int64_t cw = cols / p;
+          void* b = c.ws->get("mg.w" + std::to_string(i), (size_t)(r * cw) * e);
+          TESS_CUDA(cudaMemcpy2DAsync(b, cw * e, src + (size_t)(k * cw) * e, cols * e, cw * e, r,
+                                      cudaMemcpyDeviceToDevice, s));
+          wl[i] = b;
+          lsh[i][0] = r;
+          lsh[i][1] = cw;
+        } else {  // Row1D: rows [k r/p, (k+1) r/p)
+          const int64_t rh = r / p;
+          wl[i] = src + (size_t)(k * rh * cols) * e;
+          lsh[i][0] = rh;
+          lsh[i][1] = cols;
+        }
+      }
+      tess_block_shard sh;
+      sh.w_qkv = wl[0];
+      sh.w_proj = wl[1];
+      sh.w_ff1 = wl[2];
+      sh.w_ff2 = wl[3];
+      sh.ln1_gain = static_cast<const float*>(LN[0].on(c.device));
+      sh.ln1_bias = static_cast<const float*>(LN[1].on(c.device));
+      sh.ln2_gain = static_cast<const float*>(LN[2].on(c.device));
+      sh.ln2_bias = static_cast<const float*>(LN[3].on(c.device));
+      sh.eps = eps;
+      float* gp[8];
+      size_t gsz[8];
+      for (int i = 0; i < 8; ++i) {
+        gsz[i] = i < 4 ? (size_t)(lsh[i][0] * lsh[i][1]) : (size_t)h;
+        gp[i] = static_cast<float*>(c.ws->get("g.grad" + std::to_string(i), gsz[i] * 4));
+        TESS_CUDA(cudaMemsetAsync(gp[i], 0, gsz[i] * 4, s));
+      }
+      tess_block_grads gr{gp[0], gp[1], gp[2], gp[3], gp[4], gp[5], gp[6], gp[7]};
+      void* ly = c.ws->get("g.y", (size_t)(T * h) * e);
+      void* ldx = c.ws->get("g.dxo", (size_t)(T * h) * e);
+      const tess_dtype td = t == DType::F32 ? TESS_F32 : TESS_BF16;
+      call(tess_layer_forward(&c, op, td, &D, &sh, nullptr, dX.on(c.device), ly, s));
+      call(tess_layer_backward(&c, op, td, &D, &sh, dDY.on(c.device), ldx, &gr, 1, nullptr, s));
+      for (int i = 0; i < 4; ++i) gw[i][k] = fetch(gp[i], gsz[i], DType::F32, s);
+      if (k == 0) {
+        ys = fetch(ly, (size_t)(T * h), t, s);
+        dxs = fetch(ldx, (size_t)(T * h), t, s);
+        for (int i = 0; i < 4; ++i) gl[i] = fetch(gp[4 + i], (size_t)h, DType::F32, s);
+      }
+      c.megatron = false;
+    });
+    for (size_t i = 0; i < ys.size(); ++i) y[i] = ys[i];
+    for (size_t i = 0; i < dxs.size(); ++i) dx[i] = dxs[i];
+    if (grads) {
+      for (int i = 0; i < 4; ++i) {
+        if (!grads[i]) continue;
+        const int64_t r = wshape[i][0], cols = wshape[i][1];
+        for (int k = 0; k < p; ++k) {
+          const auto& v = gw[i][k];
+          if (colsplit[i]) {
+            const int64_t cw = cols / p;
+            for (int64_t rr = 0; rr < r; ++rr)
+              for (int64_t cc = 0; cc < cw; ++cc) grads[i][rr * cols + k * cw + cc] = v[rr * cw + cc];
+          } else {
+            const int64_t rh = r / p;
+            for (int64_t rr = 0; rr < rh; ++rr)
+              for (int64_t cc = 0; cc < cols; ++cc) grads[i][(k * rh + rr) * cols + cc] = v[rr * cols + cc];
+          }
+        }
+      }
+      for (int i = 0; i < 4; ++i)
+        if (grads[4 + i])
+          for (int64_t cc = 0; cc < h; ++cc) grads[4 + i][cc] = gl[i][cc];
+    }
+    (void)hp;
+    R.stats(sr, sk);
+  });
+}
+
 // ref layers.cpp:947-1036 (the sharded half of train_toy): `layers` blocks,
 // MSE loss with global_sum_rank (row, column, depth all-reduce of the local
 // sum, layers.cpp:519-526), backward through every block, plain SGD on every

@@ -35,6 +35,25 @@ RankDims rank_dims(const Ctx& c, const tess_layer_dims& d) {
   auto req = [](bool ok, const std::string& what) {
     if (!ok) fail(TESS_ERR_DIVISIBILITY, what);
   };
+  if (c.megatron) {
+    // 1-D scheme: every rank holds all rows and heads [k n/p, (k+1) n/p)
+    const int p = c.grid.size();
+    req(q == 1, "1-D scheme needs a [1,1,p] line grid");
+    req(d.heads > 0 && d.heads % p == 0, "heads (" + std::to_string(d.heads) +
+                                             ") not divisible by p (" + std::to_string(p) + ")");
+    req(d.hidden % d.heads == 0, "hidden (" + std::to_string(d.hidden) +
+                                     ") not divisible by heads (" + std::to_string(d.heads) + ")");
+    RankDims r;
+    r.seq = d.seq;
+    r.head_dim = d.hidden / d.heads;
+    r.heads_local = d.heads / p;
+    r.samples_local = d.batch;
+    r.hidden_total = d.hidden;
+    r.hq = d.hidden / p;
+    r.hin = d.hidden;
+    r.rows = (int64_t)d.batch * d.seq;
+    return r;
+  }
   req(d.batch % (dd * q) == 0, "batch (" + std::to_string(d.batch) + ") not divisible by d*q (" +
                                    std::to_string(dd * q) + ")");
   req(d.hidden % q == 0, "hidden (" + std::to_string(d.hidden) + ") not divisible by q (" +
@@ -50,6 +69,7 @@ RankDims rank_dims(const Ctx& c, const tess_layer_dims& d) {
   r.samples_local = d.batch / (dd * q);
   r.hidden_total = d.hidden;
   r.hq = d.hidden / q;
+  r.hin = r.hq;
   r.rows = r.samples_local * d.seq;
   return r;
 }
@@ -69,7 +89,7 @@ Out out_to(void* p, DType t, int64_t ld = 0) {
 // ----------------------------------------------------------- LayerNorm
 void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const void* x,
             const float* gain, const float* bias, double eps, void* y, cudaStream_t s) {
-  const int64_t rows = rd.rows, w = rd.hq;
+  const int64_t rows = rd.rows, w = rd.hin;
   float* stats = static_cast<float*>(wsget(c, "ln.stats", rows * 3 * 4));
   float* mean = static_cast<float*>(wsget(c, tag + ".mean", rows * 4));
   float* rstd = static_cast<float*>(wsget(c, tag + ".rstd", rows * 4));
@@ -100,7 +120,7 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
 void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const void* dy,
             DType tdy, const void* x, const float* gain, const void* resid, DType tr, void* dx,
             DType tdx, float* dgain, float* dbias, bool accumulate, cudaStream_t s) {
-  const int64_t rows = rd.rows, w = rd.hq;
+  const int64_t rows = rd.rows, w = rd.hin;
   const float* mean = static_cast<const float*>(wsget(c, tag + ".mean", rows * 4));
   const float* rstd = static_cast<const float*>(wsget(c, tag + ".rstd", rows * 4));
   float* stats = static_cast<float*>(wsget(c, "ln.bstats", rows * 2 * 4));
@@ -134,7 +154,8 @@ void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   if (want_params) {
     stream_dep(c, s, cs);
     coll_allreduce(c, COL, packed, 2 * w, cs);    // ref layers.cpp:331
-    coll_allreduce(c, DEPTH, packed, 2 * w, cs);  // ref layers.cpp:332
+    // (1-D scheme: every rank already holds the full, identical LN gradient)
+    if (!c.megatron) coll_allreduce(c, DEPTH, packed, 2 * w, cs);  // ref layers.cpp:332
     for (int k = 0; k < 2; ++k) {
       float* dst = k == 0 ? dgain : dbias;
       if (!dst) continue;
@@ -159,7 +180,9 @@ void weight_grad(Ctx& c, DType t, const void* a, int64_t ar, int64_t an, const v
   float* dst = g ? g : static_cast<float*>(wsget(c, "wgrad.discard", (size_t)an * bn * 4));
   // deferred: reduce + depth all-reduce + gradient write hide under the rest
   // of the backward (layer_backward joins the comm stream before returning)
-  tn_product(c, t, a, ar, an, b, bn, true, grad_out(dst, g && accumulate), s, /*defer=*/true);
+  // (1-D scheme: each rank owns a weight shard, nothing to sum over depth)
+  tn_product(c, t, a, ar, an, b, bn, !c.megatron, grad_out(dst, g && accumulate), s,
+             /*defer=*/true);
 }
 
 // Weight panels of a layer broadcast over the column group up front (they do
@@ -197,8 +220,8 @@ void ff_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   Out o1 = out_to(h, t);
   o1.epi = Epi::Gelu;
   o1.z = z;
-  nn_product(c, t, x, rows, hq, p.w_ff1, 4 * hq, o1, s, &wp.ff1);
-  nn_product(c, t, h, rows, 4 * hq, p.w_ff2, hq, yout, s, &wp.ff2);
+  nn_product(c, t, x, rows, rd.hin, p.w_ff1, 4 * hq, o1, s, &wp.ff1);
+  nn_product(c, t, h, rows, 4 * hq, p.w_ff2, rd.hin, yout, s, &wp.ff2);
 }
 
 // ref layers.cpp:362-379: NT, gelu', NT, TN, TN. dx written fp32.
@@ -215,15 +238,15 @@ void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     Out od = out_to(dz, t);
     od.epi = Epi::DGelu;
     od.r = z;
-    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, od, s, &wp.ff2);
+    nt_product(c, t, dy, rows, rd.hin, p.w_ff2, 4 * hq, od, s, &wp.ff2);
   } else {
     float* dh = static_cast<float*>(wsget(c, "ff.dh", rows * 4 * hq * 4));
-    nt_product(c, t, dy, rows, hq, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s, &wp.ff2);
+    nt_product(c, t, dy, rows, rd.hin, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s, &wp.ff2);
     k_gelu_bwd(dh, z, dz, t, (size_t)rows * 4 * hq, s);  // ref layers.cpp:365
   }
-  nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, hq, out_to(dx_f32, DType::F32), s, &wp.ff1);
-  weight_grad(c, t, h, rows, 4 * hq, dy, hq, g ? g->w_ff2 : nullptr, accumulate, s);
-  weight_grad(c, t, x, rows, hq, dz, 4 * hq, g ? g->w_ff1 : nullptr, accumulate, s);
+  nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, rd.hin, out_to(dx_f32, DType::F32), s, &wp.ff1);
+  weight_grad(c, t, h, rows, 4 * hq, dy, rd.hin, g ? g->w_ff2 : nullptr, accumulate, s);
+  weight_grad(c, t, x, rows, rd.hin, dz, 4 * hq, g ? g->w_ff1 : nullptr, accumulate, s);
 }
 
 // ----------------------------------------------------------- attention
@@ -284,16 +307,16 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   if (use_fused_attn(t, rd)) {
     void* o = wsget(c, tag + ".o", rows * hq * esz);
     float* lse = static_cast<float*>(wsget(c, tag + ".lse", (size_t)rd.samples_local * H * S * 4));
-    nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
+    nn_product(c, t, x, rows, rd.hin, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
     run_attn(true, attn_desc(rd, qkv, o, lse), s);
-    nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s, &wp.proj);
+    nn_product(c, t, o, rows, hq, p.w_proj, rd.hin, yout, s, &wp.proj);
     return;
   }
   void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
   void* o = wsget(c, tag + ".o", rows * hq * esz);
   const bool fused = t == DType::BF16;
   float* Sbuf = fused ? nullptr : static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
-  nn_product(c, t, x, rows, hq, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
+  nn_product(c, t, x, rows, rd.hin, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
   const float scale = (float)(1.0 / std::sqrt((double)hd));
   const char* base = static_cast<const char*>(qkv);
   for (int64_t smp = 0; smp < rd.samples_local; ++smp) {
@@ -371,7 +394,7 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g2.cs0 = hd;
     run_gemm(g2, s);
   }
-  nn_product(c, t, o, rows, hq, p.w_proj, hq, yout, s, &wp.proj);
+  nn_product(c, t, o, rows, hq, p.w_proj, rd.hin, yout, s, &wp.proj);
 }
 
 // ref layers.cpp:416-456: NT, TN, per-head local backward, NT, TN.
@@ -394,12 +417,12 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     if (c.grid.q == 1) {
       // no row reduce: the GEMM epilogue rounds straight to bf16 (bitwise the
       // same as fp32 + convert)
-      nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout, t), s, &wp.proj);
+      nt_product(c, t, dy, rows, rd.hin, p.w_proj, hq, out_to(dout, t), s, &wp.proj);
     } else {
-      nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
+      nt_product(c, t, dy, rows, rd.hin, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
       k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
     }
-    weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
+    weight_grad(c, t, o, rows, hq, dy, rd.hin, g ? g->w_proj : nullptr, accumulate, s);
     k_attn_delta(dout, o, t, hq, S, H, hd, delta, s, rd.samples_local);
     AttnDesc a = attn_desc(rd, qkv, o, lse);
     a.dout = dout;
@@ -416,8 +439,8 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     gq.c = dqkv; gq.c_type = t; gq.ldc = ld; gq.cs0 = 3 * hd; gq.cs1 = S * ld;
     gq.alpha = a.scale;  // the kernel stores dS without the 1/sqrt(hd)
     run_gemm(gq, s);
-    nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s, &wp.qkv);
-    weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
+    nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, rd.hin, out_to(dx_f32, DType::F32), s, &wp.qkv);
+    weight_grad(c, t, x, rows, rd.hin, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
     return;
   }
   const void* P = wsget(c, tag + ".P", (size_t)rd.samples_local * H * S * S * esz);
@@ -429,9 +452,9 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   float* dP = fused ? nullptr : static_cast<float*>(wsget(c, "attn.S", (size_t)H * S * S * 4));
   float* delta = fused ? static_cast<float*>(wsget(c, "attn.delta", (size_t)H * S * 4)) : nullptr;
   void* dS = wsget(c, "attn.dS", (size_t)H * S * S * esz);
-  nt_product(c, t, dy, rows, hq, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
+  nt_product(c, t, dy, rows, rd.hin, p.w_proj, hq, out_to(dout32, DType::F32), s, &wp.proj);
   if (t != DType::F32) k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
-  weight_grad(c, t, o, rows, hq, dy, hq, g ? g->w_proj : nullptr, accumulate, s);
+  weight_grad(c, t, o, rows, hq, dy, rd.hin, g ? g->w_proj : nullptr, accumulate, s);
   const float scale = (float)(1.0 / std::sqrt((double)hd));
   for (int64_t smp = 0; smp < rd.samples_local; ++smp) {
     const char* q0 = static_cast<const char*>(qkv) + (size_t)smp * S * ld * esz;
@@ -478,8 +501,8 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     g4.c = dq0 + hd * esz; g4.c_type = t; g4.ldc = ld; g4.cs0 = 3 * hd;
     run_gemm(g4, s);
   }
-  nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, hq, out_to(dx_f32, DType::F32), s, &wp.qkv);
-  weight_grad(c, t, x, rows, hq, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
+  nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, rd.hin, out_to(dx_f32, DType::F32), s, &wp.qkv);
+  weight_grad(c, t, x, rows, rd.hin, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
 }
 
 cudaStream_t copy_stream(Ctx& c) {
@@ -526,6 +549,16 @@ void async_d2h(Ctx& c, const std::string& name, void* host, const void* dev, siz
   c.copy_host[name] = {static_cast<const char*>(host), bytes};
 }
 
+// 1-D scheme: sum of the ranks' fp32 activation partials (proj / FF2 out,
+// QKV / FF1 dgrads) over the line's depth group; a no-op for Tesseract.
+void mg_allreduce(Ctx& c, float* buf, size_t n, cudaStream_t s) {
+  if (!c.megatron) return;
+  cudaStream_t cs = comm_stream(c, s);
+  stream_dep(c, s, cs);
+  coll_allreduce(c, DEPTH, buf, n, cs);
+  stream_dep(c, cs, s);
+}
+
 std::string cache_tag(const Ctx& c, tess_layer_op op) {
   return "s" + std::to_string(c.cache_slot) + ".op" + std::to_string((int)op);
 }
@@ -546,7 +579,7 @@ bool is_device_ptr(const void* p) {
 void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                    const tess_block_shard& p, const float* bias_row0, const void* x_in,
                    void* y_out, cudaStream_t s) {
-  const int64_t rows = rd.rows, hq = rd.hq;
+  const int64_t rows = rd.rows, hq = rd.hin;  // activation width
   const size_t act = (size_t)rows * hq * dtype_size(t);
   const std::string tag = cache_tag(c, op);
   // Host buffers are staged through the context (x kept until backward).
@@ -568,11 +601,23 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       ln_fwd(c, t, rd, tag + ".ln", x, p.ln1_gain, p.ln1_bias, p.eps, y, s);
       break;
     case TESS_OP_FEEDFORWARD:
-      ff_fwd(c, t, rd, tag + ".ff", p, x, out_to(y, t), s, wp);
+    case TESS_OP_ATTENTION: {
+      Out yo = out_to(y, t);
+      float* part = nullptr;
+      if (c.megatron) {  // rank partial, summed over the line
+        part = static_cast<float*>(wsget(c, "mg.part", (size_t)rows * hq * 4));
+        yo = out_to(part, DType::F32);
+      }
+      if (op == TESS_OP_FEEDFORWARD)
+        ff_fwd(c, t, rd, tag + ".ff", p, x, yo, s, wp);
+      else
+        attn_fwd(c, t, rd, tag + ".attn", p, x, yo, s, wp);
+      if (part) {
+        mg_allreduce(c, part, (size_t)rows * hq, s);
+        k_convert(part, DType::F32, y, t, (size_t)rows * hq, s);
+      }
       break;
-    case TESS_OP_ATTENTION:
-      attn_fwd(c, t, rd, tag + ".attn", p, x, out_to(y, t), s, wp);
-      break;
+    }
     case TESS_OP_BIAS_ADD: {
       // ref layers.cpp:491-503: bias lives at i == 0, column broadcast.
       float* b = static_cast<float*>(wsget(c, "bias.row", hq * 4));
@@ -593,6 +638,19 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       void* r1 = wsget(c, tag + ".r1", act);
       void* ln2 = wsget(c, tag + ".ln2out", act);
       ln_fwd(c, t, rd, tag + ".ln1", x, p.ln1_gain, p.ln1_bias, p.eps, ln1, s);
+      if (c.megatron) {
+        // 1-D scheme: the proj / FF2 outputs are rank partials; the residual
+        // adds follow their line all-reduces
+        float* part = static_cast<float*>(wsget(c, "mg.part", (size_t)rows * hq * 4));
+        attn_fwd(c, t, rd, tag + ".attn", p, ln1, out_to(part, DType::F32), s, wp);
+        mg_allreduce(c, part, (size_t)rows * hq, s);
+        k_add(x, t, part, DType::F32, r1, t, (size_t)rows * hq, s);
+        ln_fwd(c, t, rd, tag + ".ln2", r1, p.ln2_gain, p.ln2_bias, p.eps, ln2, s);
+        ff_fwd(c, t, rd, tag + ".ff", p, ln2, out_to(part, DType::F32), s, wp);
+        mg_allreduce(c, part, (size_t)rows * hq, s);
+        k_add(r1, t, part, DType::F32, y, t, (size_t)rows * hq, s);
+        break;
+      }
       Out ao = out_to(r1, t);
       ao.epi = Epi::Resid;
       ao.r = x;
@@ -615,7 +673,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
 void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                     const tess_block_shard& p, const void* dy_in, void* dx_out,
                     tess_block_grads* g, bool accumulate, float* dbias, cudaStream_t s) {
-  const int64_t rows = rd.rows, hq = rd.hq;
+  const int64_t rows = rd.rows, hq = rd.hin;  // activation width
   const size_t act = (size_t)rows * hq * dtype_size(t);
   const std::string tag = cache_tag(c, op);
   const auto it = c.fwd_x.find(c.cache_slot * 8 + (int)op);
@@ -642,12 +700,14 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     case TESS_OP_FEEDFORWARD: {
       float* dxf = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
       ff_bwd(c, t, rd, tag + ".ff", p, x, dy, dxf, g, accumulate, s, wp);
+      mg_allreduce(c, dxf, (size_t)rows * hq, s);
       k_convert(dxf, DType::F32, dx, t, (size_t)rows * hq, s);
       break;
     }
     case TESS_OP_ATTENTION: {
       float* dxf = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
       attn_bwd(c, t, rd, tag + ".attn", p, x, dy, dxf, g, accumulate, s, wp);
+      mg_allreduce(c, dxf, (size_t)rows * hq, s);
       k_convert(dxf, DType::F32, dx, t, (size_t)rows * hq, s);
       break;
     }
@@ -675,11 +735,13 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       const void* ln2 = wsget(c, tag + ".ln2out", act);
       float* dff = static_cast<float*>(wsget(c, "blk.dx32", (size_t)rows * hq * 4));
       ff_bwd(c, t, rd, tag + ".ff", p, ln2, dy, dff, g, accumulate, s, wp);
+      mg_allreduce(c, dff, (size_t)rows * hq, s);  // 1-D scheme: FF1 dgrad partials
       void* dr1 = wsget(c, "blk.dr1", act);
       ln_bwd(c, t, rd, tag + ".ln2", dff, DType::F32, r1, p.ln2_gain, dy, t, dr1, t,
              g ? g->ln2_gain : nullptr, g ? g->ln2_bias : nullptr, accumulate, s);
       float* dat = static_cast<float*>(wsget(c, "blk.dattn32", (size_t)rows * hq * 4));
       attn_bwd(c, t, rd, tag + ".attn", p, ln1, dr1, dat, g, accumulate, s, wp);
+      mg_allreduce(c, dat, (size_t)rows * hq, s);  // 1-D scheme: QKV dgrad partials
       ln_bwd(c, t, rd, tag + ".ln1", dat, DType::F32, x, p.ln1_gain, dr1, t, dx, t,
              g ? g->ln1_gain : nullptr, g ? g->ln1_bias : nullptr, accumulate, s);
       break;
@@ -741,7 +803,7 @@ void layer_step(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                 const tess_block_shard& p, const float* bias_row0, const void* x, const void* dy,
                 void* y, void* dx, tess_block_grads* g, bool accumulate, float* dbias,
                 cudaStream_t s) {
-  const size_t act = (size_t)rd.rows * rd.hq * dtype_size(t);
+  const size_t act = (size_t)rd.rows * rd.hin * dtype_size(t);
   std::string xb, db;
   const void* xd = x;
   if (!is_device_ptr(x)) {

@@ -64,7 +64,8 @@ void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
 // ------------------------------------------------------------------ layers
 struct RankDims {
   int64_t rows = 0;       // local activation rows = samples_local * seq
-  int64_t hq = 0;         // hidden / q
+  int64_t hq = 0;         // hidden / q (1-D scheme: hidden / p, the local head width)
+  int64_t hin = 0;        // activation width on this rank: hq (1-D scheme: hidden)
   int64_t seq = 0;
   int64_t head_dim = 0;
   int64_t heads_local = 0;
