@@ -216,7 +216,10 @@ tess_status tess_matmul(tess_ctx* ctx, tess_variant v, tess_dtype in, const void
  * valid on i == 0 ranks (ref: layers.cpp:507-517).
  * Host outputs (y, dx in host memory) leave on the context's copy stream so
  * they overlap the caller's next work; order a stream after them with
- * tess_stream_join before reading them (the global operators do). */
+ * tess_stream_join before reading them (the global operators do). Pinned
+ * host inputs are read asynchronously (cudaMemcpyAsync semantics): keep
+ * them unchanged until the call's work has completed (tess_stream_join +
+ * a stream synchronize); pageable ones are consumed before the call returns. */
 tess_status tess_layer_forward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
                                const tess_layer_dims* dims, const tess_block_shard* shard,
                                const void* bias_row0, const void* x, void* y, void* stream);
@@ -228,7 +231,10 @@ tess_status tess_layer_backward(tess_ctx* ctx, tess_layer_op op, tess_dtype dtyp
 /* Forward + backward of one layer op in one call, both inputs given up front
  * (the reference's layer_run(op, x, dy, ...) at rank level, layers.cpp:
  * 604-692): identical results to tess_layer_forward + tess_layer_backward;
- * a host dy is uploaded on a context side stream while the forward runs. */
+ * host x and dy go up on a context upload stream into staging buffers
+ * double-buffered per call, each copy waiting only for its buffer's reader
+ * two calls back: consecutive steps' copies overlap the previous step's
+ * compute; x gates the forward, dy only the backward. */
 tess_status tess_layer_step(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
                             const tess_layer_dims* dims, const tess_block_shard* shard,
                             const void* bias_row0, const void* x, const void* dy, void* y,
