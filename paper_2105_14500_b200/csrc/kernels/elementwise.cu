@@ -335,6 +335,23 @@ __device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
   reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
+// 8 values held as raw 16-byte vectors (bf16: one uint4, fp32: two) -> floats.
+__device__ __forceinline__ void unpack8(const uint4 (&u)[1], float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[0]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void unpack8(const uint4 (&u)[2], float (&v)[8]) {
+  v[0] = __uint_as_float(u[0].x); v[1] = __uint_as_float(u[0].y);
+  v[2] = __uint_as_float(u[0].z); v[3] = __uint_as_float(u[0].w);
+  v[4] = __uint_as_float(u[1].x); v[5] = __uint_as_float(u[1].y);
+  v[6] = __uint_as_float(u[1].z); v[7] = __uint_as_float(u[1].w);
+}
+
 // Deterministic block sums of two values (fixed-order combine of warp sums).
 __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -419,6 +436,16 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
     const float mu = mean[r], rs = rstd[r];
     float d[NV][8], xh[NV][8];
     float a = 0.f, b = 0.f;
+    // the residual is loaded with dy / x (raw 16-byte vectors), not after
+    // the block reduction: one HBM round trip per row instead of two
+    uint4 rr[NV][sizeof(TR) / 2];
+    if (resid) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int u = 0; u < (int)(sizeof(TR) / 2); ++u)
+          rr[k][u] = __ldg(reinterpret_cast<const uint4*>(resid + r * w + c0 + k * kLnSpan) + u);
+    }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       float g[8];
@@ -433,18 +460,18 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
         b += xh[k][e] * dxh;
         dg[k][e] += d[k][e] * xh[k][e];
         db[k][e] += d[k][e];
+        d[k][e] = dxh;  // only dy * gain is needed from here on
       }
     }
     const float2 t = block_sum2(a, b, red);
     const float md = t.x / (float)w, mxd = t.y / (float)w;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      float o[8], g[8];
-      ld8(gain + c0 + k * kLnSpan, g);
-      if (resid) ld8(resid + r * w + c0 + k * kLnSpan, o);
+      float o[8];
+      if (resid) unpack8(rr[k], o);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float v = rs * (d[k][e] * g[e] - md - xh[k][e] * mxd);
+        const float v = rs * (d[k][e] - md - xh[k][e] * mxd);
         o[e] = resid ? o[e] + v : v;
       }
       st8(dx + r * w + c0 + k * kLnSpan, o);
