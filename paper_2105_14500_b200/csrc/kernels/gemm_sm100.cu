@@ -74,6 +74,11 @@ struct Params {
   int mma_lead;                 // NH == 2: half-0 MMAs lead while half 1 drains
   int serp;                     // serpentine K order across waves (L2 reuse)
   int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch) or null
+  // Work units shared by concurrent launches (multicast clusters + a pair
+  // companion on the SMs the clusters cannot use): unit = `sub` vertically
+  // adjacent pair tiles; this launch's first wave takes units unit_base +
+  // cluster index, later ones unit_stride + atomicAdd(tile_counter).
+  int sub, unit_base, unit_stride;
   int raster_n;                 // pair kernel: 1 = groups of group_m N-tiles, N fastest
   unsigned long long hint_a, hint_b;  // pair kernel: L2 cache policy of the A / B TMA loads
   void* c;
@@ -678,17 +683,31 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, ui
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask = 0x3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
       "[%0], %1;" ::"r"(smem_u32(bar)),
-      "h"((uint16_t)0x3)
+      "h"(mask)
       : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+// 2-SM TMA load multicast to the CTAs in `mask` (same smem offset in each);
+// every destination's complete_tx goes to its pair leader's barrier.
+__device__ __forceinline__ void tma_load_4d_2sm_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                   int c0, int c1, int c2, int c3, uint16_t mask,
+                                                   unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7, %8;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3), "h"(mask), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar, uint32_t leader = 0) {
   uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(leader));
   // relaxed: the arrive only publishes "TMEM drained" (tcgen05.wait::ld has
   // completed the reads); a release would add a GPU-scope MEMBAR that waits
   // for every outstanding epilogue store of this thread.
@@ -755,7 +774,7 @@ struct TileQ {
   // Consumer: next tile id (-1 = done). A single thread (whole_warp false)
   // or all 32 lanes of a warp (whole_warp true: every lane reads, then lane 0
   // releases the slot) to the leader CTA's empty barrier.
-  __device__ __forceinline__ int pop(uint32_t cta, bool whole_warp) {
+  __device__ __forceinline__ int pop(uint32_t rank, bool whole_warp) {
     mbar_wait_cluster(&full[slot], ph);
     const int t = *reinterpret_cast<volatile int*>(&ids[slot]);
     bool arrive = true;
@@ -764,7 +783,7 @@ struct TileQ {
       arrive = (threadIdx.x % 32) == 0;
     }
     if (arrive) {
-      if (cta == 0)
+      if (rank == 0)
         mbar_arrive(&empty[slot]);
       else
         mbar_arrive_cluster(mapa_u32(smem_u32(&empty[slot]), 0));
@@ -772,18 +791,19 @@ struct TileQ {
     advance();
     return t;
   }
-  // Leader producer: publish t to both CTAs of the pair.
-  __device__ __forceinline__ void push(int t) {
+  // Cluster leader's producer: publish t to all `ncta` CTAs of the cluster.
+  __device__ __forceinline__ void push(int t, int ncta) {
     mbar_wait(&empty[slot], ph ^ 1);
     ids[slot] = t;
-    st_cluster_u32(mapa_u32(smem_u32(&ids[slot]), 1), t);
+    for (int r = 1; r < ncta; ++r) st_cluster_u32(mapa_u32(smem_u32(&ids[slot]), r), t);
     mbar_arrive(&full[slot]);
-    mbar_arrive_cluster(mapa_u32(smem_u32(&full[slot]), 1));
+    for (int r = 1; r < ncta; ++r) mbar_arrive_cluster(mapa_u32(smem_u32(&full[slot]), r));
     advance();
   }
 };
-// consumers per tile: leader MMA thread + 8 epilogue warps per CTA + peer producer
-constexpr int kTQConsumers = 1 + 8 + 1 + 8;
+// consumers per tile and cluster of MC pairs: each pair's MMA thread, 8
+// epilogue warps per CTA, every producer but the cluster leader's
+__host__ __device__ constexpr int tq_consumers(int mc) { return mc + 16 * mc + 2 * mc - 1; }
 
 template <int ST, int NH, int BNP = 256>
 struct Cfg2 {
@@ -826,8 +846,13 @@ __device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int&
   }
 }
 
-template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// MC = pairs per cluster. MC = 2: two pairs on vertically adjacent tiles
+// (rows m0, m0 + 256; same columns) share every B stage -- CTA (c, pair h)
+// loads half h of CTA c's B columns once and TMA-multicasts it to both pairs,
+// a third less L2 -> SM operand traffic; each stage is then released only
+// when both pairs' MMAs have read it (empty barriers count MC commits).
+template <bool A_MN, bool B_MN, int ST, int NH, int BNP, int MC = 1>
+__global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
   using C = Cfg2<ST, NH, BNP>;
   extern __shared__ uint8_t smem_raw[];
@@ -845,15 +870,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t cta = cluster_ctarank();
-  const int cluster = blockIdx.x >> 1;
-  const int nclusters = gridDim.x >> 1;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t cta = rank & 1;          // role in the CTA pair
+  const int pr = (int)(rank >> 1);        // pair index in the cluster
+  const uint32_t leader = rank & ~1u;     // this pair's MMA CTA
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pr));
+  const uint16_t all_mask = (uint16_t)((1u << (2 * MC)) - 1);
+  const int cluster = blockIdx.x / (2 * MC);
   TileQ tq{tq_ids, tq_full, tq_empty, 0, 0};
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], MC);  // one commit per pair (B stages are shared)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -861,7 +890,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int q = 0; q < kTQ; ++q) {
       mbar_init(&tq_full[q], 1);
-      mbar_init(&tq_empty[q], kTQConsumers);
+      mbar_init(&tq_empty[q], tq_consumers(MC));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < p.nseg; ++s) {
@@ -886,26 +915,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // -------------------------------------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      int next = cluster;  // first wave static
+      int next = p.unit_base + cluster;  // first wave static
+      int unit = -1, sub = 0;
       for (;;) {
-        int tile;
-        if (cta == 0) {
-          tile = next < p.num_tiles ? next : -1;
-          tq.push(tile);
+        int tile;  // unit * p.sub + sub-tile
+        if (rank == 0) {
+          if (sub == 0) {
+            unit = next < p.num_tiles ? next : -1;
+            // fetch the following unit now: the atomic's latency hides under this one's loads
+            if (unit >= 0)
+              next = p.tile_counter ? p.unit_stride + atomicAdd(p.tile_counter, 1)
+                                    : unit + p.unit_stride;
+          }
+          tile = unit < 0 ? -1 : unit * p.sub + sub;
+          if (++sub == p.sub) sub = 0;
+          tq.push(tile, 2 * MC);
           if (tile < 0) break;
-          // fetch the following tile now: the atomic's latency hides under this tile's loads
-          next = p.tile_counter ? nclusters + atomicAdd(p.tile_counter, 1) : tile + nclusters;
         } else {
-          tile = tq.pop(cta, false);
+          tile = tq.pop(rank, false);
           if (tile < 0) break;
         }
         int b0, b1, m0, n0;
-        decode_pair_tile(p, tile, b0, b1, m0, n0);
+        decode_pair_tile(p, tile / p.sub, b0, b1, m0, n0);
+        m0 = m0 * MC * p.sub + (pr + (tile % p.sub)) * 256;  // unit row -> this pair's rows
         const int mr = m0 + (int)cta * C::HALF;
         // Serpentine K: odd waves walk K backwards, so a wave starts on the
         // k-blocks the previous wave touched last -- still in L2 for the
         // operand panels the two waves share.
-        const bool rev = p.serp && ((tile / nclusters) & 1);
+        const bool rev = p.serp && (((tile / p.sub) / p.unit_stride) & 1);
         for (int si = 0; si < p.nseg; ++si) {
           const int s = rev ? p.nseg - 1 - si : si;
           const CUtensorMap* ma = &p.tma_a[s];
@@ -930,6 +967,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               // the pair's columns [n0 + 256h, +256): this CTA stages its 128
               const int nr = n0 + h * BNP + (int)cta * C::BH;
               uint8_t* sbh = sb + h * (C::BH * BK * 2);
+              if (MC > 1) {
+                // half h of role `cta`'s columns is loaded by pair h and
+                // multicast to the same role in every pair of the cluster
+                if (h != pr) continue;
+                const uint16_t mask = (uint16_t)(0x5u << cta);  // ranks cta, cta + 2
+                if (!B_MN) {
+                  tma_load_4d_2sm_mc(sbh, mb, &full_bar[stage], k, nr, b0, b1, mask, p.hint_b);
+                } else {
+#pragma unroll
+                  for (int c = 0; c < C::BH / 64; ++c)
+                    tma_load_4d_2sm_mc(sbh + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0,
+                                       b1, mask, p.hint_b);
+                }
+                continue;
+              }
               if (!B_MN) {
                 tma_load_4d_2sm(sbh, mb, &full_bar[stage], k, nr, b0, b1, p.hint_b);
               } else {
@@ -958,7 +1010,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;  // NH == 1: alternating slot; NH == 2: both slots every tile
       uint32_t slot_phase = 0;  // bit s = phase of slot s
       for (;;) {
-        if (tq.pop(cta, false) < 0) break;
+        if (tq.pop(rank, false) < 0) break;
         int kb0 = 0;
         if (NH == 2 && p.mma_lead) {
           // Lead phase: the epilogue drains half 0 first, so start this
@@ -991,7 +1043,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                          : make_sdesc(sbh + k * 32, 16, 1024);
                 mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
               }
-              if (h == 1) mma_commit_2sm(&empty_bar[sg]);
+              if (h == 1) mma_commit_2sm(&empty_bar[sg], all_mask);
               if (++sg == C::STAGES) {
                 sg = 0;
                 ph ^= 1;
@@ -1028,7 +1080,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }
           }
-          mma_commit_2sm(&empty_bar[stage]);
+          mma_commit_2sm(&empty_bar[stage], all_mask);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1037,7 +1089,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           const int slot = NH == 1 ? acc : h;
-          mma_commit_2sm(&tfull_bar[slot]);
+          mma_commit_2sm(&tfull_bar[slot], pair_mask);
           slot_phase ^= 1u << slot;
         }
         if (NH == 1) acc ^= 1;
@@ -1051,10 +1103,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     EpiStage st{smem_u32(epi_smem) + (uint32_t)(warp - 2) * 4096u, 0};
     const bool tma_epi = NH == 2 && p.tma_epi;
     for (;;) {
-      const int tile = tq.pop(cta, true);
+      const int tile = tq.pop(rank, true);
       if (tile < 0) break;
       int b0, b1, m0, n0;
-      decode_pair_tile(p, tile, b0, b1, m0, n0);
+      decode_pair_tile(p, tile / p.sub, b0, b1, m0, n0);
+      m0 = m0 * MC * p.sub + (pr + (tile % p.sub)) * 256;
       const int mrow0 = m0 + (int)cta * C::HALF + quad * 32;
       const int m = mrow0 + lane;
 #pragma unroll 1
@@ -1067,7 +1120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                       tma_epi ? &st : nullptr, lane, mrow0);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&tempty_bar[slot]);
+        if (lane == 0) mbar_arrive_leader(&tempty_bar[slot], leader);
         slot_phase ^= 1u << slot;
       }
       if (NH == 1) acc ^= 1;
@@ -1230,39 +1283,143 @@ int* tile_counter_slot(cudaStream_t stream) {
   return slot;
 }
 
+// Largest number of co-resident clusters of 2*MC CTAs (GPC fragmentation:
+// on 148 SMs only 33 four-CTA clusters fit).
+template <typename K>
+int max_active_clusters(K kern, int ncta, int smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncta * 64);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = ncta;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms() / ncta;
+  }
+  return n;
+}
+
 template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
+cudaError_t set_smem(int mc) {
+  using C = Cfg2<ST, NH, BNP>;
+  cudaError_t e = mc > 1 ? cudaFuncSetAttribute(gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 2>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                C::SMEM_BYTES)
+                         : cudaFuncSetAttribute(gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                C::SMEM_BYTES);
+  return e;
+}
+
+#define TESS_CUDA_RET(expr)               \
+  do {                                    \
+    const cudaError_t e_ = (expr);        \
+    if (e_ != cudaSuccess) return e_;     \
+  } while (0)
+
+// Companion stream (per device) for the pair launch that runs beside the
+// multicast clusters, and the events ordering it against the caller's stream.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+SideStream* side_stream() {
+  static SideStream ss[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& x = ss[dev & 63];
+  if (!x.s) {
+    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.ev[1], cudaEventDisableTiming);
+  }
+  return &x;
+}
+
+template <bool A_MN, bool B_MN, int ST, int NH, int BNP, int MC = 1>
 cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
   Params p = p_in;
   static const bool static_order = std::getenv("TESS_GEMM_STATIC") != nullptr;
   p.tile_counter = static_order ? nullptr : tile_counter_slot(stream);
-  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP>;
   using C = Cfg2<ST, NH, BNP>;
   static bool attr_set = false;
+  static int max_clusters = 0;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    cudaError_t e = set_smem<A_MN, B_MN, ST, NH, BNP>(1);
+    if (e == cudaSuccess && MC > 1) e = set_smem<A_MN, B_MN, ST, NH, BNP>(MC);
     if (e != cudaSuccess) return e;
+    if (MC > 1) {
+      max_clusters = max_active_clusters(gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, MC>,
+                                         2 * MC, C::SMEM_BYTES);
+      if (std::getenv("TESS_GEMM_MC_DEBUG"))
+        std::fprintf(stderr, "tess gemm: %d active clusters of %d CTAs (SMs %d)\n",
+                     max_clusters, 2 * MC, num_sms());
+    }
     attr_set = true;
   }
-  static const bool nonpersist = std::getenv("TESS_GEMM_NONPERSIST") != nullptr;
-  const int pairs = std::max(1, num_sms() / 2);
-  const int grid = 2 * (nonpersist ? p.num_tiles : std::min(p.num_tiles, pairs));
-  kern<<<grid, kThreads, C::SMEM_BYTES, stream>>>(p);
-  return cudaGetLastError();
+  if (MC == 1) {
+    static const bool nonpersist = std::getenv("TESS_GEMM_NONPERSIST") != nullptr;
+    const int pairs = std::max(1, num_sms() / 2);
+    const int n = nonpersist ? p.num_tiles : std::min(p.num_tiles, pairs);
+    p.sub = 1;
+    p.unit_base = 0;
+    p.unit_stride = n;
+    gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1><<<2 * n, kThreads, C::SMEM_BYTES, stream>>>(p);
+    return cudaGetLastError();
+  }
+  // units of MC vertically adjacent pair tiles: the clusters multicast B
+  // inside a unit; a pair companion on the SMs the clusters leave free takes
+  // whole units (two pair tiles each) from the same counter
+  const int nbatch = p.num_tiles / p.tiles_per_batch;
+  p.tiles_m /= MC;
+  p.tiles_per_batch = p.tiles_m * p.tiles_n;
+  p.num_tiles = p.tiles_per_batch * nbatch;
+  const int sms = num_sms();
+  const int na = std::max(1, std::min(std::min(max_clusters, sms / (2 * MC)), p.num_tiles));
+  const int nb = std::max(0, std::min((sms - 2 * MC * na) / 2, p.num_tiles - na));
+  p.unit_stride = na + nb;
+  SideStream* side = nb > 0 ? side_stream() : nullptr;
+  if (side) {
+    TESS_CUDA_RET(cudaEventRecord(side->ev[0], stream));  // counter zeroed, inputs ready
+    TESS_CUDA_RET(cudaStreamWaitEvent(side->s, side->ev[0], 0));
+  }
+  p.sub = 1;
+  p.unit_base = 0;
+  gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, MC>
+      <<<2 * MC * na, kThreads, C::SMEM_BYTES, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !side) return e;
+  p.sub = MC;
+  p.unit_base = na;
+  gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1><<<2 * nb, kThreads, C::SMEM_BYTES, side->s>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  TESS_CUDA_RET(cudaEventRecord(side->ev[1], side->s));
+  TESS_CUDA_RET(cudaStreamWaitEvent(stream, side->ev[1], 0));
+  return cudaSuccess;
 }
 
-template <int ST, int NH, int BNP>
+template <int ST, int NH, int BNP, int MC = 1>
 cudaError_t launch_pair_st(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
-  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH, BNP>(p, s);
-  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH, BNP>(p, s);
-  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH, BNP>(p, s);
-  return launch_2cta<true, false, ST, NH, BNP>(p, s);
+  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH, BNP, MC>(p, s);
+  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH, BNP, MC>(p, s);
+  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH, BNP, MC>(p, s);
+  return launch_2cta<true, false, ST, NH, BNP, MC>(p, s);
 }
 
 // tile_n = 128: 256 x 128 pair tiles (N = hd products); 256: 256 x 256,
 // two TMEM accumulators; 512: 256 x 512 (NH = 2, see Cfg2).
 cudaError_t launch_pair(const Params& p, int tile_n, bool a_mn, bool b_mn, cudaStream_t s) {
   // smem ring depth: 9 x 24 KB (128), 7 x 32 KB (256), 4 x 48 KB (512)
+  static const bool mc = std::getenv("TESS_GEMM_MC") && std::getenv("TESS_GEMM_MC")[0] == '1';
+  if (tile_n == 512 && mc && p.tiles_m % 2 == 0) return launch_pair_st<4, 2, 256, 2>(p, a_mn, b_mn, s);
   if (tile_n == 512) return launch_pair_st<4, 2, 256>(p, a_mn, b_mn, s);
   if (tile_n == 128) return launch_pair_st<9, 1, 128>(p, a_mn, b_mn, s);
   return launch_pair_st<7, 1, 256>(p, a_mn, b_mn, s);
