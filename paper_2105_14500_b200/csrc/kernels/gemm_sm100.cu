@@ -1382,9 +1382,17 @@ cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
   p.tiles_per_batch = p.tiles_m * p.tiles_n;
   p.num_tiles = p.tiles_per_batch * nbatch;
   const int sms = num_sms();
-  const int na = std::max(1, std::min(std::min(max_clusters, sms / (2 * MC)), p.num_tiles));
-  const int nb = std::max(0, std::min((sms - 2 * MC * na) / 2, p.num_tiles - na));
-  p.unit_stride = na + nb;
+  const int units = p.num_tiles;
+  const int na = std::max(1, std::min(std::min(max_clusters, sms / (2 * MC)), units));
+  int nb = std::max(0, std::min((sms - 2 * MC * na) / 2, units - na));
+  // Static split so both launches finish together: a cluster retires a unit
+  // per tile time, a companion pair one per MC tile times. The clusters take
+  // [0, units - uc) dynamically, the companion [units - uc, units) round-robin.
+  const int uc = nb > 0 ? (int)((long long)units * nb / (MC * na + nb)) : 0;
+  if (uc == 0) nb = 0;
+  nb = std::min(nb, std::max(uc, 0));
+  p.num_tiles = units - uc;
+  p.unit_stride = na;
   SideStream* side = nb > 0 ? side_stream() : nullptr;
   if (side) {
     TESS_CUDA_RET(cudaEventRecord(side->ev[0], stream));  // counter zeroed, inputs ready
@@ -1397,7 +1405,10 @@ cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !side) return e;
   p.sub = MC;
-  p.unit_base = na;
+  p.unit_base = units - uc;
+  p.num_tiles = units;
+  p.unit_stride = nb;
+  p.tile_counter = nullptr;  // static round-robin over its range
   gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1><<<2 * nb, kThreads, C::SMEM_BYTES, side->s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
