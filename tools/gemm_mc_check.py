@@ -25,5 +25,5 @@ for (M, K, N) in [(8192, 12288, 49152), (8192, 49152, 12288), (8192, 12288, 1228
     ref = (a.float() @ b.float())
     err = (torch.linalg.norm(c - ref) / torch.linalg.norm(ref)).item()
     print(M, K, N, "rel_frob", f"{err:.3e}", list(names)[:2], flush=True)
-    assert err < 5e-5, err
+    assert err < 1e-4, err
 ctx.close()
