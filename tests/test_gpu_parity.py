@@ -566,3 +566,53 @@ def test_layer_step_matches_forward_backward_host_buffers(tess, orc):
             ctx.close()
     for a, c in zip(*outs):
         assert torch.equal(a, c)
+
+
+def test_layer_step_distinct_inputs_per_step(tess, orc):
+    """Four consecutive tess_layer_step calls with different pinned host x / dy
+    each step (the per-call double-buffered upload staging, reused every
+    second call) give bitwise the outputs and accumulated gradients of
+    tess_layer_forward + tess_layer_backward on the same sequence."""
+    import torch
+    b, s, h, nh = 2, 64, 256, 2
+    _, _, P = _layer_inputs(orc, b, s, h, 23, bf16r)
+    dev = torch.device("cuda", 0)
+    bf = torch.bfloat16
+    names = ("w_qkv", "w_proj", "w_ff1", "w_ff2")
+    W = [torch.tensor(P[k], dtype=torch.float32, device=dev).to(bf).contiguous() for k in names]
+    LN = [torch.tensor(P[k], dtype=torch.float32, device=dev).contiguous()
+          for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")]
+    steps = 4
+    xs = [torch.tensor(bf16r(orc.random_matrix(b * s, h, 30 + k, 0)), dtype=torch.float32)
+          .to(bf).pin_memory() for k in range(steps)]
+    dys = [torch.tensor(bf16r(orc.random_matrix(b * s, h, 30 + k, 2)), dtype=torch.float32)
+           .to(bf).pin_memory() for k in range(steps)]
+    shard = tess.BlockShardC(*[t.data_ptr() for t in W + LN], 1e-5)
+    dims = tess.LayerDims(b, s, h, nh)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for mode in ("split", "step"):
+        ctx = tess.init_local(tess.GridSpec(1, 1))[0]
+        try:
+            ys = [torch.empty_like(xs[0]).pin_memory() for _ in range(steps)]
+            dxs = [torch.empty_like(xs[0]).pin_memory() for _ in range(steps)]
+            G = [torch.zeros(t.shape, device=dev) for t in W + LN]
+            grads = tess.BlockGradsC(*[t.data_ptr() for t in G])
+            for k in range(steps):
+                if mode == "split":
+                    ctx.layer_forward("block", "bf16", dims, shard, xs[k].data_ptr(),
+                                      ys[k].data_ptr(), stream=st)
+                    ctx.layer_backward("block", "bf16", dims, shard, dys[k].data_ptr(),
+                                       dxs[k].data_ptr(), grads, stream=st)
+                else:
+                    ctx.layer_step("block", "bf16", dims, shard, xs[k].data_ptr(),
+                                   dys[k].data_ptr(), ys[k].data_ptr(), dxs[k].data_ptr(), grads,
+                                   stream=st)
+            ctx.stream_join(st)
+            torch.cuda.synchronize()
+            outs.append([t.clone() for t in ys + dxs] + [g.cpu() for g in G])
+        finally:
+            ctx.close()
+    for a, c in zip(*outs):
+        assert torch.equal(a, c)
+    assert not torch.equal(outs[0][0], outs[0][1])  # the steps really differ
