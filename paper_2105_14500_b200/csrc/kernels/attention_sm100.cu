@@ -54,7 +54,28 @@ long long* attn_debug_trace() { return g_attn_trace; }
 namespace sm100 {
 namespace attn {
 
+// 2^x on the FMA/ALU pipes (round-to-nearest split, degree-3 polynomial on
+// [-0.5, 0.5], max rel. error 2.2e-4 -- far below the bf16 rounding of P):
+// the backward's exp2/dS math is MUFU-bound (16 K ex2 per tile at 16/clk),
+// so a share of the exponentials moves here. x is clamped at -125 so the
+// exponent add cannot underflow (2^-125 instead of 0 for masked columns,
+// whose dO / Q rows are zero).
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: rint(x) in the low mantissa bits
+  const float j = t - 12582912.0f;
+  const float f = x - j;
+  const float p =
+      fmaf(fmaf(fmaf(0.05286731571f, f, 0.2421521395f), f, 0.6935868263f), f, 0.9999627471f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 constexpr int kThreads = 320;
+// which of every 8 exponentials of the forward use exp2_fma (bit e & 7)
+#ifndef TESS_ATTN_FWD_POLY
+#define TESS_ATTN_FWD_POLY 0
+#endif
+constexpr int kFwdPolyMask = TESS_ATTN_FWD_POLY;
 constexpr int kBwdThreads = 576;  // backward: TMA + MMA warps + 16 softmax-gradient warps
 constexpr int BQ = 128;   // query rows per tile (UMMA M)
 constexpr int BKV = 128;  // keys per tile (UMMA N of S, K of P V)
@@ -269,9 +290,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         for (int e = 0; e < BKV; ++e)
           if (e >= nvalid) s[e] = -INFINITY;
       }
-      float mx = s[0];
+      // row max / row sum as 8 independent chains (a single 128-long
+      // dependent fmax / fadd chain is ~4 clk x 128 of latency per tile)
+      float mp[8];
 #pragma unroll
-      for (int e = 1; e < BKV; ++e) mx = fmaxf(mx, s[e]);
+      for (int k = 0; k < 8; ++k) mp[k] = s[k];
+#pragma unroll
+      for (int e = 8; e < BKV; ++e) mp[e & 7] = fmaxf(mp[e & 7], s[e]);
+      const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                             fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
       const float m_new = fmaxf(m_used, mx * cl2);
       const bool need = m_new > m_used + kRescaleThreshold;
       if (__any_sync(0xffffffffu, need)) {
@@ -296,13 +323,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       // all exponentials on MUFU: moving a share to the FMA pipe (a degree-5
       // polynomial exp2) measured slower (25 %: +6 %, 50 %: +22 %) -- the
       // softmax is issue-bound, not MUFU-bound
-      float rs = 0.f;
+      float rp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int e = 0; e < BKV; ++e) {
-        s[e] = ex2_approx(fmaf(s[e], cl2, -m_used));
-        rs += s[e];
+        const float xv = fmaf(s[e], cl2, -m_used);
+        s[e] = (kFwdPolyMask >> (e & 7)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
+        rp[e & 7] += s[e];
       }
-      l += rs;
+      l += ((rp[0] + rp[1]) + (rp[2] + rp[3])) + ((rp[4] + rp[5]) + (rp[6] + rp[7]));
       // P (bf16 pairs, lower key in the low half) over the consumed S columns
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -428,21 +456,6 @@ struct BwdCfg {
   static constexpr int TM_ST = 0, TM_DPT = 128, TM_DV = 256, TM_DK = 384;
 };
 
-// 2^x on the FMA/ALU pipes (round-to-nearest split, degree-3 polynomial on
-// [-0.5, 0.5], max rel. error 2.2e-4 -- far below the bf16 rounding of P):
-// the backward's exp2/dS math is MUFU-bound (16 K ex2 per tile at 16/clk),
-// so a share of the exponentials moves here. x is clamped at -125 so the
-// exponent add cannot underflow (2^-125 instead of 0 for masked columns,
-// whose dO / Q rows are zero).
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -125.0f);
-  const float t = x + 12582912.0f;  // 1.5 * 2^23: rint(x) in the low mantissa bits
-  const float j = t - 12582912.0f;
-  const float f = x - j;
-  const float p =
-      fmaf(fmaf(fmaf(0.05286731571f, f, 0.2421521395f), f, 0.6935868263f), f, 0.9999627471f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
 // 32 bf16 values of row r (columns [u0*8, u0*8+32) of a 64-column K-major
 // SW128 tile) -> shared memory.
