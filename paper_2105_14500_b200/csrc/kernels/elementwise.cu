@@ -382,23 +382,24 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_fwd_kernel(
   const int c0 = threadIdx.x * 8;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     float v[NV][8];
-    float s = 0.f;
+    // one block reduction per row: sums of x - x0 and (x - x0)^2, shifted by
+    // the row's first element so the variance does not cancel
+    const float x0 = ldf<T>(x + r * w, 0);
+    float s = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       ld8(x + r * w + c0 + k * kLnSpan, v[k]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += v[k][e];
-    }
-    const float mu = block_sum2(s, 0.f, red).x / (float)w;
-    float m2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < NV; ++k)
-#pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float d = v[k][e] - mu;
-        m2 += d * d;
+        const float d = v[k][e] - x0;
+        s += d;
+        s2 = fmaf(d, d, s2);
       }
-    const float var = block_sum2(m2, 0.f, red).x / (float)w;
+    }
+    const float2 t = block_sum2(s, s2, red);
+    const float dm = t.x / (float)w;
+    const float mu = x0 + dm;
+    const float var = fmaxf(t.y / (float)w - dm * dm, 0.f);
     const float rstd = 1.0f / sqrtf(var + eps);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
