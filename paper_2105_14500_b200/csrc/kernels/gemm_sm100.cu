@@ -26,7 +26,12 @@
 //   both 256-column halves in TMEM, a quarter less L2->SM traffic per flop,
 //   TMA-store / TMA-reduce-add epilogue); tiles handed out in order from an
 //   atomic counter so concurrently running tiles share their A/B panels in
-//   L2 (see DESIGN.md section 3 for the measurements behind each choice).
+//   L2, odd waves walking K backwards (serpentine) and, for 256 x 512 tiles,
+//   the next tile's half-0 MMAs leading while the epilogue drains half 1.
+//   Optional MC = 2 (TESS_GEMM_MC=1, off by default): two pairs per cluster
+//   share B stages by TMA multicast, plus a pair companion launch on the SMs
+//   the 4-CTA clusters cannot use (see DESIGN.md section 3 for the
+//   measurements behind each choice).
 //
 // Operand majorness is a template parameter, so the three Tesseract
 // variants need no transposes in HBM:
