@@ -15,7 +15,7 @@ import sys
 
 def our_name(ncu_name):
     # <A_MN, B_MN, stages, halves[, pair MMA N]> -> tile width = halves * N
-    m = re.search(r"gemm_bf16_2cta_kernel<(\w+), (\w+), (\d+), (\d+)(?:, (\d+))?>", ncu_name)
+    m = re.search(r"gemm_bf16_2cta_kernel<(\w+), (\w+), (\d+), (\d+)(?:, (\d+))?(?:, (\d+))?>", ncu_name)
     if m:
         b = lambda v: "1" if v in ("true", "1") else "0"  # noqa: E731
         bnp = int(m[5]) if m[5] else 256
