@@ -7,9 +7,13 @@ FF2 -> +res), forward + backward with weight/LN gradients, h=12288, 96 heads,
 seq 2048, batch 4 per GPU-equivalent (b = 4 * p), bf16 storage with fp32
 accumulation, on the [q,q,d] grid for N GPUs:
     N=1 [1,1,1]   N=2 [1,1,2]   N=4 [2,2,1]   N=8 [2,2,2]
-One process per GPU (torchrun for N>1), NCCL row/column/depth communicators
-inside libtess; torch.distributed (gloo) only for the unique-id exchange,
-barriers and the max-over-ranks timing reduction.
+One process per GPU (torchrun for N>1; started without torchrun and with
+--gpus N > 1, bench.py re-launches itself under torch.distributed.run), NCCL
+row/column/depth communicators inside libtess; torch.distributed (gloo) only
+for the unique-id exchange, barriers and the max-over-ranks timing
+reduction. Synthetic weights are seeded per TesseractB block (i, j), so the
+depth replicas of a weight block are identical; `--dry-run` stops after the
+rendezvous and prints every rank's (rank, device, coordinate).
 
 Prints ONE JSON line on rank 0 (see the contract in the task statement).
 `--impl reference` times the reference's own CPU implementation
@@ -27,8 +31,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2105_14500_b200.launch import GRIDS, grid_for, rank_env, seeds, spawn  # noqa: E402
+
 METRIC = "Transformer-layer fwd+bwd TFLOP/s at [2,2,2] on 8×B200; step ms; exposed comm %"
-GRIDS = {1: (1, 1, True), 2: (1, 2, True), 4: (2, 1, False), 8: (2, 2, False)}
 HIDDEN, HEADS, SEQ, B_PER_GPU = 12288, 96, 2048, 4
 # CPU sample for the reference / cpu_baseline legs (bounded CPU work)
 SAMPLE = dict(batch=4, seq=128, hidden=512, heads=8)
@@ -196,17 +201,40 @@ def main():
     ap.add_argument("--seq", type=int, default=SEQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="stop after the rendezvous; rank 0 prints each rank's placement")
     args = ap.parse_args()
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world if world > 1 else args.gpus
+    rank, local_rank, world = rank_env()
+    if world == 1 and args.gpus > 1 and args.impl == "tess":
+        # started without torchrun: one process per GPU, this one only launches
+        grid_for(args.gpus)
+        raise SystemExit(spawn(os.path.abspath(__file__), sys.argv[1:], args.gpus))
+    if world > 1:
+        args.gpus = world
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
+
+    if args.dry_run:
+        import paper_2105_14500_b200 as tess
+        q, d, allow = grid_for(args.gpus)
+        grid = tess.GridSpec(q, d, allow)
+        c = grid.coord_of(rank)
+        me = {"rank": rank, "local_rank": local_rank, "device": local_rank,
+              "coord": [c.i, c.j, c.k], "grid": grid.to_string(), "seeds": seeds(grid, rank)}
+        allr = [None] * world
+        if dist:
+            dist.all_gather_object(allr, me)
+        else:
+            allr = [me]
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "world": world, "ranks": allr}), flush=True)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -217,9 +245,7 @@ def main():
     import torch
     import paper_2105_14500_b200 as tess
 
-    if args.gpus not in GRIDS:
-        raise SystemExit(f"--gpus must be one of {sorted(GRIDS)}")
-    q, d, allow = GRIDS[args.gpus]
+    q, d, allow = grid_for(args.gpus)
     grid = tess.GridSpec(q, d, allow)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -238,20 +264,24 @@ def main():
     rows = batch * s // (d * q)
     hq = h // q
     bf = torch.bfloat16
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
+    sd = seeds(grid, rank)
+    gens = {}
+    for fam, seed in sd.items():
+        gens[fam] = torch.Generator(device=dev)
+        gens[fam].manual_seed(seed)
 
-    def rnd(shape, scale, dtype=bf):
-        return (torch.rand(shape, device=dev, generator=g) * 2 - 1).mul_(scale).to(dtype)
+    def rnd(shape, scale, fam, dtype=bf):
+        return (torch.rand(shape, device=dev, generator=gens[fam]) * 2 - 1).mul_(scale).to(dtype)
 
-    # synthetic inputs of the named shapes; random-init weights (TesseractB blocks)
+    # synthetic inputs of the named shapes; random-init weights: TesseractB
+    # blocks seeded by (i, j) (identical depth replicas), LN by j
     ws = 1.0 / (h ** 0.5)
-    W = {"w_qkv": rnd((hq, 3 * hq), ws), "w_proj": rnd((hq, hq), ws),
-         "w_ff1": rnd((hq, 4 * hq), ws), "w_ff2": rnd((4 * hq, hq), ws)}
-    LN = {"ln1_gain": 1 + rnd((hq,), 0.1, torch.float32), "ln1_bias": rnd((hq,), 0.1, torch.float32),
-          "ln2_gain": 1 + rnd((hq,), 0.1, torch.float32), "ln2_bias": rnd((hq,), 0.1, torch.float32)}
-    x = rnd((rows, hq), 1.0)
-    dy = rnd((rows, hq), 1.0)
+    W = {"w_qkv": rnd((hq, 3 * hq), ws, "weight"), "w_proj": rnd((hq, hq), ws, "weight"),
+         "w_ff1": rnd((hq, 4 * hq), ws, "weight"), "w_ff2": rnd((4 * hq, hq), ws, "weight")}
+    LN = {k: (1 if k.endswith("gain") else 0) + rnd((hq,), 0.1, "ln", torch.float32)
+          for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")}
+    x = rnd((rows, hq), 1.0, "activation")
+    dy = rnd((rows, hq), 1.0, "activation")
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
     G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in {**W, **LN}.items()}

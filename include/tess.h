@@ -347,7 +347,9 @@ uint64_t tess_kernel_launches(void);
 /* GEMM launch profiling: when enabled, every local GEMM launch is bracketed
  * by CUDA events on its own stream; tess_profile_read synchronises them and
  * returns the summed device time (ms), algorithmic flops (2*M*N*K per
- * launch) and launch count since the last tess_profile_enable. */
+ * launch) and launch count since the last tess_profile_enable.
+ * on: 0 off, 1 keyed per kernel instantiation, 2 keyed per instantiation
+ * plus shape and epilogue ("... M= N= K= b= epi=<Epi>"). */
 tess_status tess_profile_enable(int on);
 tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
 /* Per kernel instantiation since tess_profile_enable, as JSON text

@@ -684,9 +684,11 @@ def kernel_launches() -> int:
     return int(lib.tess_kernel_launches())
 
 
-def profile_enable(on: bool = True) -> None:
-    """Bracket every local GEMM launch with CUDA events on its stream."""
-    _check(lib.tess_profile_enable(int(on)))
+def profile_enable(on: bool = True, detail: bool = False) -> None:
+    """Bracket every local GEMM launch with CUDA events on its stream.
+    detail: key the profile by instantiation + shape + epilogue
+    ("<kernel> M=.. N=.. K=.. b=.. epi=<n>", n = Epi in kernels/gemm.h)."""
+    _check(lib.tess_profile_enable((2 if detail else 1) if on else 0))
 
 
 def profile_kernels() -> dict:

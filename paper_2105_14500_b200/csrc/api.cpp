@@ -72,7 +72,7 @@ const char* tess_version(void) { return "tess-b200 0.1 (sm_100a, tcgen05)"; }
 uint64_t tess_kernel_launches(void) { return g_launches.load(); }
 
 tess_status tess_profile_enable(int on) {
-  return guarded([&] { profile_enable(on != 0); });
+  return guarded([&] { profile_enable(on == 2 ? 2 : on != 0 ? 1 : 0); });
 }
 
 tess_status tess_debug_attn_trace(long long* out, int n) {

@@ -147,12 +147,14 @@ void prof_end(ProfToken& t, cudaStream_t s) {
   delete rec;
 }
 
+bool g_prof_detail = false;
+
 bool prof_detail() {
   static const bool detail = [] {
     const char* e = std::getenv("TESS_PROFILE_DETAIL");
     return e && e[0] == '1';
   }();
-  return detail;
+  return detail || g_prof_detail;
 }
 
 void run_gemm(const GemmDesc& g, cudaStream_t s) {
@@ -175,8 +177,10 @@ void run_gemm(const GemmDesc& g, cudaStream_t s) {
   prof_end(tok, s);
 }
 
-void profile_enable(bool on) {
+void profile_enable(int mode) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
+  const bool on = mode != 0;
+  g_prof_detail = mode == 2;
   for (auto& r : g_prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

@@ -48,7 +48,7 @@ struct ProfToken {
 ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s);
 void prof_end(ProfToken& t, cudaStream_t s);
 bool prof_detail();
-void profile_enable(bool on);
+void profile_enable(int mode);  // 0 off, 1 per instantiation, 2 + shape/epilogue
 void profile_read(double* ms, double* flops, uint64_t* launches);
 std::string profile_json();
 

@@ -372,6 +372,38 @@ __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
   return t;
 }
 
+// Deterministic block (mean, M2) of equal-count per-thread partials by
+// Chan's pairwise combination: a butterfly over the warp (symmetric, so every
+// lane holds the same pair), then the warps' pairs in fixed order. No
+// E[x^2] - E[x]^2 anywhere, so a row whose mean is large against its spread
+// (or whose first element is an outlier) does not cancel.
+__device__ __forceinline__ float2 block_meanvar(float m, float M2, float n, float2* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float mo = __shfl_xor_sync(0xffffffffu, m, o);
+    const float Mo = __shfl_xor_sync(0xffffffffu, M2, o);
+    const float dlt = mo - m;
+    M2 = M2 + Mo + dlt * dlt * (0.5f * n);
+    m = 0.5f * (m + mo);
+    n *= 2.f;
+  }
+  __syncthreads();  // red is reused row after row
+  if (lane == 0) red[warp] = make_float2(m, M2);
+  __syncthreads();
+  float2 t = red[0];
+  float nt = n;
+#pragma unroll
+  for (int w = 1; w < kLnThreads / 32; ++w) {
+    const float dlt = red[w].x - t.x;
+    const float tot = nt + n;
+    t.y = t.y + red[w].y + dlt * dlt * (nt * n / tot);
+    t.x = t.x + dlt * (n / tot);
+    nt = tot;
+  }
+  return t;
+}
+
 template <typename T, int NV>
 __global__ void __launch_bounds__(kLnThreads) ln_fused_fwd_kernel(
     const T* __restrict__ x, int64_t rows, const float* __restrict__ gain,
@@ -382,24 +414,29 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_fwd_kernel(
   const int c0 = threadIdx.x * 8;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     float v[NV][8];
-    // one block reduction per row: sums of x - x0 and (x - x0)^2, shifted by
-    // the row's first element so the variance does not cancel
-    const float x0 = ldf<T>(x + r * w, 0);
-    float s = 0.f, s2 = 0.f;
+    // one block reduction per row: each thread's (mean, sum of squared
+    // deviations) over its NV*8 register-resident values, combined by
+    // Chan's formula (block_meanvar)
+    float s = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       ld8(x + r * w + c0 + k * kLnSpan, v[k]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = v[k][e] - x0;
-        s += d;
-        s2 = fmaf(d, d, s2);
-      }
+      for (int e = 0; e < 8; ++e) s += v[k][e];
     }
-    const float2 t = block_sum2(s, s2, red);
-    const float dm = t.x / (float)w;
-    const float mu = x0 + dm;
-    const float var = fmaxf(t.y / (float)w - dm * dm, 0.f);
+    constexpr float kN = (float)(NV * 8);
+    const float lm = s / kN;
+    float m2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = v[k][e] - lm;
+        m2 = fmaf(d, d, m2);
+      }
+    const float2 t = block_meanvar(lm, m2, kN, red);
+    const float mu = t.x;
+    const float var = fmaxf(t.y / (float)w, 0.f);
     const float rstd = 1.0f / sqrtf(var + eps);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {

@@ -28,10 +28,7 @@
 //   atomic counter so concurrently running tiles share their A/B panels in
 //   L2, odd waves walking K backwards (serpentine) and, for 256 x 512 tiles,
 //   the next tile's half-0 MMAs leading while the epilogue drains half 1.
-//   Optional MC = 2 (TESS_GEMM_MC=1, off by default): two pairs per cluster
-//   share B stages by TMA multicast, plus a pair companion launch on the SMs
-//   the 4-CTA clusters cannot use (see DESIGN.md section 3 for the
-//   measurements behind each choice).
+//   (DESIGN.md section 3 has the measurements behind each choice.)
 //
 // Operand majorness is a template parameter, so the three Tesseract
 // variants need no transposes in HBM:
@@ -75,17 +72,11 @@ struct Params {
   int nb0;
   int tiles_m, tiles_n, tiles_per_batch, num_tiles;
   int group_m;
-  int skip_store;               // experiment: epilogue computes but does not store
   int mma_lead;                 // NH == 2: half-0 MMAs lead while half 1 drains
-  int serp;                     // serpentine K order across waves (L2 reuse)
-  int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch) or null
-  // Work units shared by concurrent launches (multicast clusters + a pair
-  // companion on the SMs the clusters cannot use): unit = `sub` vertically
-  // adjacent pair tiles; this launch's first wave takes units unit_base +
-  // cluster index, later ones unit_stride + atomicAdd(tile_counter).
-  int sub, unit_base, unit_stride;
-  int raster_n;                 // pair kernel: 1 = groups of group_m N-tiles, N fastest
-  unsigned long long hint_a, hint_b;  // pair kernel: L2 cache policy of the A / B TMA loads
+  int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch)
+  // Pair kernel: the first wave takes tiles = pair index, later ones
+  // wave + atomicAdd(tile_counter); odd waves walk K backwards (serpentine).
+  int wave;
   void* c;
   int c_bf16;
   long long ldc, cs0, cs1;
@@ -465,12 +456,12 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, i
     tmem_ld32(trow + c * 32, r);  // warp-collective: executed by every lane
     if (st) {
       // warp-uniform: every lane stages its row, the store clips rows >= M
-      if (n < p.N && !p.skip_store) {
+      if (n < p.N) {
         float v[32];
         epilogue_values(p, b0, b1, m, r, aux, v);
         epilogue_chunk_tma(p, *st, lane, b0, b1, n, mrow0, v);
       }
-    } else if (nvalid > 0 && !p.skip_store) {
+    } else if (nvalid > 0) {
       if (stats)
         row_stats_chunk(r, p.alpha, nvalid, rmax, rsum);
       else
@@ -668,9 +659,11 @@ __device__ __forceinline__ void cluster_sync() {
                    : "memory");
 }
 
+constexpr unsigned long long kEvictNormal = 0x1000000000000000ull;  // L2 policy of operand loads
+
 __device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
                                                 int c0, int c1, int c2, int c3,
-                                                unsigned long long policy) {
+                                                unsigned long long policy = kEvictNormal) {
   asm volatile(
       "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
@@ -693,20 +686,6 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask = 0x
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
       "[%0], %1;" ::"r"(smem_u32(bar)),
       "h"(mask)
-      : "memory");
-}
-
-// 2-SM TMA load multicast to the CTAs in `mask` (same smem offset in each);
-// every destination's complete_tx goes to its pair leader's barrier.
-__device__ __forceinline__ void tma_load_4d_2sm_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                                   int c0, int c1, int c2, int c3, uint16_t mask,
-                                                   unsigned long long policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4, %5, %6}], [%2], %7, %8;" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1),
-      "r"(c2), "r"(c3), "h"(mask), "l"(policy)
       : "memory");
 }
 
@@ -806,9 +785,9 @@ struct TileQ {
     advance();
   }
 };
-// consumers per tile and cluster of MC pairs: each pair's MMA thread, 8
-// epilogue warps per CTA, every producer but the cluster leader's
-__host__ __device__ constexpr int tq_consumers(int mc) { return mc + 16 * mc + 2 * mc - 1; }
+// consumers per tile: the MMA thread, 8 epilogue warps per CTA, the
+// non-leader CTA's producer
+constexpr int kTQConsumers = 1 + 16 + 1;
 
 template <int ST, int NH, int BNP = 256>
 struct Cfg2 {
@@ -832,32 +811,17 @@ __device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int&
   const int r = tile - b * p.tiles_per_batch;
   b0 = b % p.nb0;
   b1 = b / p.nb0;
-  if (!p.raster_n) {
-    const int width = p.group_m * p.tiles_n;
-    const int g = r / width;
-    const int first_m = g * p.group_m;
-    const int gm = min(p.tiles_m - first_m, p.group_m);
-    const int in = r - g * width;
-    m0 = (first_m + in % gm) * 256;
-    n0 = (in / gm) * p.tile_n;
-  } else {
-    const int width = p.group_m * p.tiles_m;
-    const int g = r / width;
-    const int first_n = g * p.group_m;
-    const int gn = min(p.tiles_n - first_n, p.group_m);
-    const int in = r - g * width;
-    n0 = (first_n + in % gn) * p.tile_n;
-    m0 = (in / gn) * 256;
-  }
+  const int width = p.group_m * p.tiles_n;
+  const int g = r / width;
+  const int first_m = g * p.group_m;
+  const int gm = min(p.tiles_m - first_m, p.group_m);
+  const int in = r - g * width;
+  m0 = (first_m + in % gm) * 256;
+  n0 = (in / gm) * p.tile_n;
 }
 
-// MC = pairs per cluster. MC = 2: two pairs on vertically adjacent tiles
-// (rows m0, m0 + 256; same columns) share every B stage -- CTA (c, pair h)
-// loads half h of CTA c's B columns once and TMA-multicasts it to both pairs,
-// a third less L2 -> SM operand traffic; each stage is then released only
-// when both pairs' MMAs have read it (empty barriers count MC commits).
-template <bool A_MN, bool B_MN, int ST, int NH, int BNP, int MC = 1>
-__global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
+template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
   using C = Cfg2<ST, NH, BNP>;
   extern __shared__ uint8_t smem_raw[];
@@ -876,18 +840,14 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
-  const uint32_t cta = rank & 1;          // role in the CTA pair
-  const int pr = (int)(rank >> 1);        // pair index in the cluster
-  const uint32_t leader = rank & ~1u;     // this pair's MMA CTA
-  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pr));
-  const uint16_t all_mask = (uint16_t)((1u << (2 * MC)) - 1);
-  const int cluster = blockIdx.x / (2 * MC);
+  const uint32_t cta = rank;              // role in the CTA pair (0 = MMA leader)
+  const int cluster = blockIdx.x / 2;
   TileQ tq{tq_ids, tq_full, tq_empty, 0, 0};
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], MC);  // one commit per pair (B stages are shared)
+      mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -895,7 +855,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int q = 0; q < kTQ; ++q) {
       mbar_init(&tq_full[q], 1);
-      mbar_init(&tq_empty[q], tq_consumers(MC));
+      mbar_init(&tq_empty[q], kTQConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < p.nseg; ++s) {
@@ -920,34 +880,26 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
       // -------------------------------------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      int next = p.unit_base + cluster;  // first wave static
-      int unit = -1, sub = 0;
+      int next = cluster;  // first wave static
       for (;;) {
-        int tile;  // unit * p.sub + sub-tile
+        int tile;
         if (rank == 0) {
-          if (sub == 0) {
-            unit = next < p.num_tiles ? next : -1;
-            // fetch the following unit now: the atomic's latency hides under this one's loads
-            if (unit >= 0)
-              next = p.tile_counter ? p.unit_stride + atomicAdd(p.tile_counter, 1)
-                                    : unit + p.unit_stride;
-          }
-          tile = unit < 0 ? -1 : unit * p.sub + sub;
-          if (++sub == p.sub) sub = 0;
-          tq.push(tile, 2 * MC);
+          tile = next < p.num_tiles ? next : -1;
+          // fetch the following tile now: the atomic's latency hides under this one's loads
+          if (tile >= 0) next = p.wave + atomicAdd(p.tile_counter, 1);
+          tq.push(tile, 2);
           if (tile < 0) break;
         } else {
           tile = tq.pop(rank, false);
           if (tile < 0) break;
         }
         int b0, b1, m0, n0;
-        decode_pair_tile(p, tile / p.sub, b0, b1, m0, n0);
-        m0 = m0 * MC * p.sub + (pr + (tile % p.sub)) * 256;  // unit row -> this pair's rows
+        decode_pair_tile(p, tile, b0, b1, m0, n0);
         const int mr = m0 + (int)cta * C::HALF;
         // Serpentine K: odd waves walk K backwards, so a wave starts on the
         // k-blocks the previous wave touched last -- still in L2 for the
         // operand panels the two waves share.
-        const bool rev = p.serp && (((tile / p.sub) / p.unit_stride) & 1);
+        const bool rev = (tile / p.wave) & 1;
         for (int si = 0; si < p.nseg; ++si) {
           const int s = rev ? p.nseg - 1 - si : si;
           const CUtensorMap* ma = &p.tma_a[s];
@@ -960,40 +912,23 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
             if (cta == 0) mbar_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
             const int k = kb * BK;
             if (!A_MN) {
-              tma_load_4d_2sm(sa, ma, &full_bar[stage], k, mr, b0, b1, p.hint_a);
+              tma_load_4d_2sm(sa, ma, &full_bar[stage], k, mr, b0, b1);
             } else {
 #pragma unroll
               for (int c = 0; c < C::HALF / 64; ++c)
-                tma_load_4d_2sm(sa + c * 8192, ma, &full_bar[stage], mr + c * 64, k, b0, b1,
-                                p.hint_a);
+                tma_load_4d_2sm(sa + c * 8192, ma, &full_bar[stage], mr + c * 64, k, b0, b1);
             }
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
               // the pair's columns [n0 + 256h, +256): this CTA stages its 128
               const int nr = n0 + h * BNP + (int)cta * C::BH;
               uint8_t* sbh = sb + h * (C::BH * BK * 2);
-              if (MC > 1) {
-                // half h of role `cta`'s columns is loaded by pair h and
-                // multicast to the same role in every pair of the cluster
-                if (h != pr) continue;
-                const uint16_t mask = (uint16_t)(0x5u << cta);  // ranks cta, cta + 2
-                if (!B_MN) {
-                  tma_load_4d_2sm_mc(sbh, mb, &full_bar[stage], k, nr, b0, b1, mask, p.hint_b);
-                } else {
-#pragma unroll
-                  for (int c = 0; c < C::BH / 64; ++c)
-                    tma_load_4d_2sm_mc(sbh + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0,
-                                       b1, mask, p.hint_b);
-                }
-                continue;
-              }
               if (!B_MN) {
-                tma_load_4d_2sm(sbh, mb, &full_bar[stage], k, nr, b0, b1, p.hint_b);
+                tma_load_4d_2sm(sbh, mb, &full_bar[stage], k, nr, b0, b1);
               } else {
 #pragma unroll
                 for (int c = 0; c < C::BH / 64; ++c)
-                  tma_load_4d_2sm(sbh + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0, b1,
-                                  p.hint_b);
+                  tma_load_4d_2sm(sbh + c * 8192, mb, &full_bar[stage], nr + c * 64, k, b0, b1);
               }
             }
             if (++stage == C::STAGES) {
@@ -1048,7 +983,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
                                          : make_sdesc(sbh + k * 32, 16, 1024);
                 mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
               }
-              if (h == 1) mma_commit_2sm(&empty_bar[sg], all_mask);
+              if (h == 1) mma_commit_2sm(&empty_bar[sg]);
               if (++sg == C::STAGES) {
                 sg = 0;
                 ph ^= 1;
@@ -1085,7 +1020,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
               mma_bf16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }
           }
-          mma_commit_2sm(&empty_bar[stage], all_mask);
+          mma_commit_2sm(&empty_bar[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1094,7 +1029,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
           const int slot = NH == 1 ? acc : h;
-          mma_commit_2sm(&tfull_bar[slot], pair_mask);
+          mma_commit_2sm(&tfull_bar[slot]);
           slot_phase ^= 1u << slot;
         }
         if (NH == 1) acc ^= 1;
@@ -1111,8 +1046,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
       const int tile = tq.pop(rank, true);
       if (tile < 0) break;
       int b0, b1, m0, n0;
-      decode_pair_tile(p, tile / p.sub, b0, b1, m0, n0);
-      m0 = m0 * MC * p.sub + (pr + (tile % p.sub)) * 256;
+      decode_pair_tile(p, tile, b0, b1, m0, n0);
       const int mrow0 = m0 + (int)cta * C::HALF + quad * 32;
       const int m = mrow0 + lane;
 #pragma unroll 1
@@ -1125,7 +1059,7 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(kThreads, 1)
                       tma_epi ? &st : nullptr, lane, mrow0);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&tempty_bar[slot], leader);
+        if (lane == 0) mbar_arrive_leader(&tempty_bar[slot]);
         slot_phase ^= 1u << slot;
       }
       if (NH == 1) acc ^= 1;
@@ -1158,17 +1092,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-CUtensorMapL2promotion l2_promotion() {
-  static const CUtensorMapL2promotion v = [] {
-    const char* e = std::getenv("TESS_GEMM_PROMO");  // 0 none, 1 64B, 2 128B, 3 256B
-    const int k = e ? std::atoi(e) : 3;
-    return k == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-           : k == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-           : k == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  }();
-  return v;
-}
 
 // Output view for the TMA-store epilogue: [N, M, nb0, nb1] of bf16 / f32
 // with a {32 | 16, 32, 1, 1} box (64-byte rows) and SWIZZLE_64B.
@@ -1223,7 +1146,7 @@ bool encode_view(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer
   }
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr),
                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
@@ -1234,32 +1157,50 @@ bool encode_view(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer
 
 std::atomic<int> g_sm_reserve{0};
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (dev >= 0 && dev < kMaxDevices) ? dev : 0;
+}
+
 // SMs the persistent GEMMs may occupy: all of them, minus the ones left for
 // NCCL kernels when this process has peers (gemm_set_sm_reserve), so that
 // collectives on the comm stream run concurrently with the GEMMs.
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static int count[kMaxDevices] = {};
+  static std::once_flag once[kMaxDevices];
+  const int dev = current_device();
+  std::call_once(once[dev], [dev] {
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
+    count[dev] = n > 0 ? n : 148;
+  });
+  const int n = count[dev];
   const int r = g_sm_reserve.load(std::memory_order_relaxed);
   return (r > 0 && r < n - 2) ? ((n - r) & ~1) : n;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (thread-safe: the in-process backend launches from one thread per rank).
+template <auto Kern>
+cudaError_t ensure_smem(int bytes) {
+  static cudaError_t status[kMaxDevices];
+  static std::once_flag once[kMaxDevices];
+  const int dev = current_device();
+  std::call_once(once[dev], [&] {
+    status[dev] = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  });
+  return status[dev];
 }
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const Params& p, cudaStream_t stream) {
   using C = Cfg<BN>;
   auto kern = gemm_bf16_kernel<BN, A_MN, B_MN>;
-  static bool attr_set = false;  // per instantiation; benign race
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  const cudaError_t e = ensure_smem<gemm_bf16_kernel<BN, A_MN, B_MN>>(C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
   const int grid = std::min(p.num_tiles, num_sms());
   kern<<<grid, kThreads, C::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
@@ -1270,11 +1211,9 @@ cudaError_t launch(const Params& p, cudaStream_t stream) {
 int* tile_counter_slot(cudaStream_t stream) {
   constexpr int kSlots = 65536;  // a slot is reused only 65536 launches later
   static std::mutex mu;
-  static int* bufs[64] = {};
-  static unsigned next[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
+  static int* bufs[kMaxDevices] = {};
+  static unsigned next[kMaxDevices] = {};
+  const int dev = current_device();
   int* slot;
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -1288,202 +1227,63 @@ int* tile_counter_slot(cudaStream_t stream) {
   return slot;
 }
 
-// Largest number of co-resident clusters of 2*MC CTAs (GPC fragmentation:
-// on 148 SMs only 33 four-CTA clusters fit).
-template <typename K>
-int max_active_clusters(K kern, int ncta, int smem) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ncta * 64);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute at;
-  at.id = cudaLaunchAttributeClusterDimension;
-  at.val.clusterDim.x = ncta;
-  at.val.clusterDim.y = 1;
-  at.val.clusterDim.z = 1;
-  cfg.attrs = &at;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
-    cudaGetLastError();
-    n = num_sms() / ncta;
-  }
-  return n;
-}
-
 template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
-cudaError_t set_smem(int mc) {
-  using C = Cfg2<ST, NH, BNP>;
-  cudaError_t e = mc > 1 ? cudaFuncSetAttribute(gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 2>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                C::SMEM_BYTES)
-                         : cudaFuncSetAttribute(gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                C::SMEM_BYTES);
-  return e;
-}
-
-#define TESS_CUDA_RET(expr)               \
-  do {                                    \
-    const cudaError_t e_ = (expr);        \
-    if (e_ != cudaSuccess) return e_;     \
-  } while (0)
-
-// Companion stream (per device) for the pair launch that runs beside the
-// multicast clusters, and the events ordering it against the caller's stream.
-struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-};
-SideStream* side_stream() {
-  static SideStream ss[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  SideStream& x = ss[dev & 63];
-  if (!x.s) {
-    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&x.ev[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&x.ev[1], cudaEventDisableTiming);
-  }
-  return &x;
-}
-
-template <bool A_MN, bool B_MN, int ST, int NH, int BNP, int MC = 1>
 cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
-  Params p = p_in;
-  static const bool static_order = std::getenv("TESS_GEMM_STATIC") != nullptr;
-  p.tile_counter = static_order ? nullptr : tile_counter_slot(stream);
   using C = Cfg2<ST, NH, BNP>;
-  static bool attr_set = false;
-  static int max_clusters = 0;
-  if (!attr_set) {
-    cudaError_t e = set_smem<A_MN, B_MN, ST, NH, BNP>(1);
-    if (e == cudaSuccess && MC > 1) e = set_smem<A_MN, B_MN, ST, NH, BNP>(MC);
-    if (e != cudaSuccess) return e;
-    if (MC > 1) {
-      max_clusters = max_active_clusters(gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, MC>,
-                                         2 * MC, C::SMEM_BYTES);
-      if (std::getenv("TESS_GEMM_MC_DEBUG"))
-        std::fprintf(stderr, "tess gemm: %d active clusters of %d CTAs (SMs %d)\n",
-                     max_clusters, 2 * MC, num_sms());
-    }
-    attr_set = true;
-  }
-  if (MC == 1) {
-    static const bool nonpersist = std::getenv("TESS_GEMM_NONPERSIST") != nullptr;
-    const int pairs = std::max(1, num_sms() / 2);
-    const int n = nonpersist ? p.num_tiles : std::min(p.num_tiles, pairs);
-    p.sub = 1;
-    p.unit_base = 0;
-    p.unit_stride = n;
-    gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1><<<2 * n, kThreads, C::SMEM_BYTES, stream>>>(p);
-    return cudaGetLastError();
-  }
-  // units of MC vertically adjacent pair tiles: the clusters multicast B
-  // inside a unit; a pair companion on the SMs the clusters leave free takes
-  // whole units (two pair tiles each) from the same counter
-  const int nbatch = p.num_tiles / p.tiles_per_batch;
-  p.tiles_m /= MC;
-  p.tiles_per_batch = p.tiles_m * p.tiles_n;
-  p.num_tiles = p.tiles_per_batch * nbatch;
-  const int sms = num_sms();
-  const int units = p.num_tiles;
-  const int na = std::max(1, std::min(std::min(max_clusters, sms / (2 * MC)), units));
-  int nb = std::max(0, std::min((sms - 2 * MC * na) / 2, units - na));
-  // Static split so both launches finish together: a cluster retires a unit
-  // per tile time, a companion pair one per MC tile times. The clusters take
-  // [0, units - uc) dynamically, the companion [units - uc, units) round-robin.
-  const int uc = nb > 0 ? (int)((long long)units * nb / (MC * na + nb)) : 0;
-  if (uc == 0) nb = 0;
-  nb = std::min(nb, std::max(uc, 0));
-  p.num_tiles = units - uc;
-  p.unit_stride = na;
-  SideStream* side = nb > 0 ? side_stream() : nullptr;
-  if (side) {
-    TESS_CUDA_RET(cudaEventRecord(side->ev[0], stream));  // counter zeroed, inputs ready
-    TESS_CUDA_RET(cudaStreamWaitEvent(side->s, side->ev[0], 0));
-  }
-  p.sub = 1;
-  p.unit_base = 0;
-  gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, MC>
-      <<<2 * MC * na, kThreads, C::SMEM_BYTES, stream>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || !side) return e;
-  p.sub = MC;
-  p.unit_base = units - uc;
-  p.num_tiles = units;
-  p.unit_stride = nb;
-  p.tile_counter = nullptr;  // static round-robin over its range
-  gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP, 1><<<2 * nb, kThreads, C::SMEM_BYTES, side->s>>>(p);
-  e = cudaGetLastError();
+  auto kern = gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP>;
+  const cudaError_t e = ensure_smem<gemm_bf16_2cta_kernel<A_MN, B_MN, ST, NH, BNP>>(C::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  TESS_CUDA_RET(cudaEventRecord(side->ev[1], side->s));
-  TESS_CUDA_RET(cudaStreamWaitEvent(stream, side->ev[1], 0));
-  return cudaSuccess;
+  Params p = p_in;
+  p.tile_counter = tile_counter_slot(stream);
+  if (!p.tile_counter) return cudaErrorMemoryAllocation;
+  const int n = std::min(p.num_tiles, std::max(1, num_sms() / 2));  // persistent: one pair per TPC
+  p.wave = n;
+  kern<<<2 * n, kThreads, C::SMEM_BYTES, stream>>>(p);
+  return cudaGetLastError();
 }
 
-template <int ST, int NH, int BNP, int MC = 1>
+template <int ST, int NH, int BNP>
 cudaError_t launch_pair_st(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
-  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH, BNP, MC>(p, s);
-  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH, BNP, MC>(p, s);
-  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH, BNP, MC>(p, s);
-  return launch_2cta<true, false, ST, NH, BNP, MC>(p, s);
+  if (!a_mn && b_mn) return launch_2cta<false, true, ST, NH, BNP>(p, s);
+  if (!a_mn && !b_mn) return launch_2cta<false, false, ST, NH, BNP>(p, s);
+  if (a_mn && b_mn) return launch_2cta<true, true, ST, NH, BNP>(p, s);
+  return launch_2cta<true, false, ST, NH, BNP>(p, s);
 }
 
-// tile_n = 128: 256 x 128 pair tiles (N = hd products); 256: 256 x 256,
-// two TMEM accumulators; 512: 256 x 512 (NH = 2, see Cfg2).
+// tile_n = 256: 256 x 256 pair tiles, two TMEM accumulators; 512: 256 x 512
+// (NH = 2, see Cfg2). Shared-memory ring: 7 x 32 KB (256), 4 x 48 KB (512).
 cudaError_t launch_pair(const Params& p, int tile_n, bool a_mn, bool b_mn, cudaStream_t s) {
-  // smem ring depth: 9 x 24 KB (128), 7 x 32 KB (256), 4 x 48 KB (512)
-  static const bool mc = std::getenv("TESS_GEMM_MC") && std::getenv("TESS_GEMM_MC")[0] == '1';
-  if (tile_n == 512 && mc && p.tiles_m % 2 == 0) return launch_pair_st<4, 2, 256, 2>(p, a_mn, b_mn, s);
   if (tile_n == 512) return launch_pair_st<4, 2, 256>(p, a_mn, b_mn, s);
-  if (tile_n == 128) return launch_pair_st<9, 1, 128>(p, a_mn, b_mn, s);
   return launch_pair_st<7, 1, 256>(p, a_mn, b_mn, s);
 }
 
-// 256-column halves per pair tile (see Cfg2): 2 when the wider tile does not
-// cost a partial extra wave over the 148 SMs (74 pairs) and the epilogue has
-// no per-256-column-tile layout (RowStats partials, attention epilogues).
+// 256-column halves per pair tile (see Cfg2): 2 when the wider tile costs at
+// most 10 % of extra wave time over the 148 SMs (74 pairs) -- measured +3.5 %
+// step throughput under the power cap even at a partial extra wave -- and the
+// epilogue has no per-256-column-tile layout (RowStats partials, attention
+// epilogues). TESS_GEMM_NH=1|2 forces the choice (tests pin both tiles).
 int pair_halves(const GemmDesc& d) {
   static const int env = [] {
-    const char* e = std::getenv("TESS_GEMM_NH");  // 1 forces 256 x 256 tiles
+    const char* e = std::getenv("TESS_GEMM_NH");
     return e ? std::atoi(e) : 0;
   }();
   if (env == 1) return 1;
   if (d.epi == Epi::RowStats || d.epi == Epi::SoftmaxFwd || d.epi == Epi::SoftmaxBwd) return 1;
   if (d.N <= 256) return 1;
+  if (env == 2) return 2;
   const long long pairs = std::max(1, num_sms() / 2);
   const long long tm = (d.M + 255) / 256, b = d.nb0 * d.nb1;
   const long long t1 = tm * ((d.N + 255) / 256) * b, t2 = tm * ((d.N + 511) / 512) * b;
   const long long w1 = (t1 + pairs - 1) / pairs, w2 = (t2 + pairs - 1) / pairs;
-  if (env == 2) return 2;
-  static const int slack = [] {  // % of extra wave time the wider tile may cost
-    const char* e = std::getenv("TESS_GEMM_NH_SLACK");
-    return e ? std::atoi(e) : 110;
-  }();
-  return (2 * w2 * 100 <= slack * w1) ? 2 : 1;
+  return (2 * w2 * 100 <= 110 * w1) ? 2 : 1;
 }
 
-// Pair-tile width: 128 for N <= 128 (the N = head_dim products), else 256 per
-// accumulator half (x pair_halves).
-int pair_tile_n(const GemmDesc& d) {
-  if (d.N <= 128) return 128;
-  return 256 * pair_halves(d);
-}
+int pair_tile_n(const GemmDesc& d) { return 256 * pair_halves(d); }
 
-bool use_pair_kernel(int64_t M, int64_t N) {
-  static int mode = -1;  // TESS_GEMM_2CTA=0 forces the 1-CTA kernel (A/B testing)
-  if (mode < 0) {
-    const char* e = std::getenv("TESS_GEMM_2CTA");
-    mode = (e && e[0] == '0') ? 0 : 1;
-  }
-  // 256 x 128 pair tiles (N <= 128) are opt-in (TESS_GEMM_PAIR128=1): the one
-  // such product of the step (dQ = dS K, N = head_dim) is HBM-bound on reading
-  // dS^T, where they measured no better than the 1-CTA 128 x 128 kernel
-  static const bool pair128 = std::getenv("TESS_GEMM_PAIR128") &&
-                              std::getenv("TESS_GEMM_PAIR128")[0] == '1';
-  return mode == 1 && M > 128 && (N > 128 || (pair128 && N > 64));
-}
+// The pair kernel for M > 128 and N > 128. N <= 128 (the dQ = dS K product,
+// N = head_dim) stays on the 1-CTA 128 x 128 kernel: that product is
+// HBM-bound on reading dS^T, where 256 x 128 pair tiles measured no better.
+bool use_pair_kernel(int64_t M, int64_t N) { return M > 128 && N > 128; }
 
 template <int BN>
 cudaError_t launch_bn(const Params& p, bool a_mn, bool b_mn, cudaStream_t s) {
@@ -1541,19 +1341,14 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   }
   Params p;
   std::memset(&p, 0, sizeof(p));
-  static const int env_lead =
-      std::getenv("TESS_GEMM_LEAD") && std::getenv("TESS_GEMM_LEAD")[0] == '0' ? 0 : 1;
-  p.mma_lead = env_lead;
-  static const int env_serp =
-      std::getenv("TESS_GEMM_SERP") && std::getenv("TESS_GEMM_SERP")[0] == '0' ? 0 : 1;
-  p.serp = env_serp;
+  p.mma_lead = 1;
   const bool pair = use_pair_kernel(d.M, d.N);
   const int pair_tn = pair ? pair_tile_n(d) : 0;
   const int nh = pair_tn == 512 ? 2 : 1;
   const int BN = d.N > 128 ? 256 : 128;
   // TMA box rows for K-major operands: 128 (A, and B in the pair kernel) or BN.
   const int a_box = BM;
-  const int b_box = pair ? (pair_tn == 128 ? 64 : 128) : BN;
+  const int b_box = pair ? 128 : BN;
   const bool a_mn = d.trans_a;   // A stored [K, M]: M contiguous
   const bool b_mn = !d.trans_b;  // B stored [K, N]: N contiguous
   int total_kb = 0;
@@ -1620,32 +1415,6 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   }
   p.num_tiles = static_cast<int>(nt);
   p.group_m = pair ? 8 : 16;
-  if (pair) {
-    // experiment knobs (TESS_GEMM_GROUP / _RASTER / _HINT_A / _HINT_B)
-    static const int env_group = [] {
-      const char* e = std::getenv("TESS_GEMM_GROUP");
-      return e ? std::atoi(e) : 0;
-    }();
-    static const int env_raster = [] {
-      const char* e = std::getenv("TESS_GEMM_RASTER");
-      return e ? std::atoi(e) : 0;
-    }();
-    auto hint = [](const char* name) -> unsigned long long {
-      const char* e = std::getenv(name);
-      const int v = e ? std::atoi(e) : 0;
-      return v == 1 ? 0x12F0000000000000ull    // EVICT_FIRST
-             : v == 2 ? 0x14F0000000000000ull  // EVICT_LAST
-                      : 0x1000000000000000ull; // EVICT_NORMAL
-    };
-    static const unsigned long long env_ha = hint("TESS_GEMM_HINT_A");
-    static const unsigned long long env_hb = hint("TESS_GEMM_HINT_B");
-    if (env_group > 0) p.group_m = env_group;
-    static const int env_skip = std::getenv("TESS_GEMM_SKIP_STORE") ? 1 : 0;
-    p.skip_store = env_skip;
-    p.raster_n = env_raster;
-    p.hint_a = env_ha;
-    p.hint_b = env_hb;
-  }
   p.c = d.c;
   p.c_bf16 = d.c_type == DType::BF16;
   p.ldc = d.ldc;
@@ -1669,11 +1438,8 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
   p.ss1 = d.ss1;
   p.tile_n = tile_n;
   if (pair && nh == 2 && d.epi != Epi::RowStats) {
-    static const bool env_off = std::getenv("TESS_GEMM_TMA_EPI") &&
-                                std::getenv("TESS_GEMM_TMA_EPI")[0] == '0';
     const bool bf = d.c_type == DType::BF16;
-    p.tma_epi = !env_off &&
-                encode_out(&p.tma_c, d.c, bf, d.N, d.M, d.ldc, d.nb0, d.cs0, d.nb1, d.cs1) &&
+    p.tma_epi = encode_out(&p.tma_c, d.c, bf, d.N, d.M, d.ldc, d.nb0, d.cs0, d.nb1, d.cs1) &&
                 (d.epi != Epi::Gelu ||
                  encode_out(&p.tma_z, d.z, bf, d.N, d.M, d.ldz, d.nb0, d.zs0, d.nb1, d.zs1));
   }

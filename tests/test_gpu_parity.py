@@ -616,3 +616,40 @@ def test_layer_step_distinct_inputs_per_step(tess, orc):
     for a, c in zip(*outs):
         assert torch.equal(a, c)
     assert not torch.equal(outs[0][0], outs[0][1])  # the steps really differ
+
+
+@pytest.mark.parametrize("offset,outlier", [(0.0, 0.0), (1000.0, 0.0), (0.0, 3000.0),
+                                            (-250.0, 4000.0)])
+def test_layernorm_fused_offset_rows_fp32(tess, offset, outlier):
+    """The fused single-pass LayerNorm (per-thread mean / M2 combined by Chan's
+    formula) on rows whose mean is far from zero or whose first element is
+    an outlier, against the fp64 LayerNorm of the same fp32 inputs
+    (reference layers.cpp:242-281 with hidden_total = h): no cancellation."""
+    import torch
+    h, rows = 12288, 32
+    g = torch.Generator().manual_seed(3)
+    x = (offset + torch.randn(rows, h, generator=g, dtype=torch.float64)).float()
+    x[:, 0] += outlier
+    gain = torch.ones(h)
+    bias = torch.zeros(h)
+    dev = torch.device("cuda", 0)
+    xd = x.to(dev)
+    gd, bd = gain.to(dev), bias.to(dev)
+    ctx = tess.init_local(tess.GridSpec(1, 1))[0]
+    try:
+        dummy = torch.zeros(8, device=dev)
+        shard = tess.BlockShardC(*[dummy.data_ptr()] * 4, gd.data_ptr(), bd.data_ptr(),
+                                 gd.data_ptr(), bd.data_ptr(), 1e-5)
+        y = torch.empty_like(xd)
+        ctx.layer_forward("layernorm", "f32", tess.LayerDims(1, rows, h, 32), shard,
+                          xd.data_ptr(), y.data_ptr(),
+                          stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        ctx.close()
+    xf = x.double()
+    mu = xf.mean(1, keepdim=True)
+    var = ((xf - mu) ** 2).mean(1, keepdim=True)
+    want = (xf - mu) / torch.sqrt(var + 1e-5)
+    err = ((y.cpu().double() - want).norm() / want.norm()).item()
+    assert err <= 1e-4, err

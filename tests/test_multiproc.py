@@ -4,21 +4,12 @@ NCCL unique-id exchange, max-over-ranks timing) and the communicator split
 plan libtess hands to ncclCommSplit (color = group_index, key = slot; ref
 grid.cpp:79-95), checked against the reference geometry."""
 import os
-import socket
 
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-GRIDS = {2: (1, 2, True), 8: (2, 2, False)}
-
-
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
+from paper_2105_14500_b200.launch import GRIDS, free_port as _free_port
 
 
 def _worker(rank, world, port, q, d, allow, out):
