@@ -107,7 +107,9 @@ def test_nh2_block_vs_oracle(tess, orc, q, d, allow):
     rows = b * s // (d * q)
     if rows > 128:  # the pair kernel needs M > 128 (rows per rank)
         ran = wide_tile_epilogues(kernels)
-        need = {EPI["store"], EPI["gelu"], EPI["resid"], EPI["dgelu"]}
+        need = {EPI["store"], EPI["gelu"], EPI["resid"]}
+        if q == 1:  # q > 1: dh is row-reduced first, GeLU' is applied after the reduce
+            need.add(EPI["dgelu"])
         assert need <= ran, (sorted(ran), sorted(kernels))
 
 
