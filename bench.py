@@ -324,6 +324,11 @@ def main():
     barrier()
     launches0 = tess.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # The timed region: K steps; every tensor-core launch (GEMMs, fused
+    # attention) and every memory-bound launch (LayerNorm, attention delta,
+    # ...) bracketed by CUDA events on its own stream, so the roofline's
+    # per-kernel times come from this very region.
+    tess.profile_enable(True)
     barrier()
     clocks.mark("t0")
     e0.record(stream)
@@ -334,9 +339,21 @@ def main():
     clocks.mark("t1")
     clk = clocks.stop()
     launches = tess.kernel_launches() - launches0
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local)
     flops = layer_flops(batch, s, h)
     value = flops / (ms * 1e-3) / 1e12
+    gemm_ms, gemm_flops, gemm_n = tess.profile_read()
+    per_kernel = tess.profile_kernels()
+    tess.profile_enable(False)
+    # the same K steps without the per-launch events (their cost, reported)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
+    e1.record(stream)
+    barrier()
+    ms_unprof = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
     # exposed communication: the same step with every collective
     # metered but moving no data; exposed = (t - t_noop) / t, max over ranks.
@@ -357,18 +374,25 @@ def main():
         ms_noop = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         exposed = max(0.0, (ms - ms_noop) / ms) if ms else None
 
-    # dominant kernel: the tcgen05 GEMM, timed per launch with events on its stream
-    tess.profile_enable(True)
-    step(x.data_ptr(), y.data_ptr(), dy.data_ptr(), dx.data_ptr())
-    torch.cuda.synchronize(dev)
-    gemm_ms, gemm_flops, gemm_n = tess.profile_read()
-    per_kernel = tess.profile_kernels()
-    tess.profile_enable(False)
-    peak, peak_src, _ = read_peaks()
-    # dominant kernel = the GEMM instantiation with the most device time;
-    # achieved = its algorithmic flops per launch / its mean launch duration
-    top, (top_ms, top_flops, top_n) = max(per_kernel.items(), key=lambda kv: kv[1][0])
+    # per-launch averages over the K timed steps (rank 0's own kernels)
+    ms_prof = ms_local
+    K = float(args.steps)
+    peak, peak_src, hbm_peak = read_peaks()
+    tensor = {k: v for k, v in per_kernel.items() if v[1] > 0}
+    memory = {k: v for k, v in per_kernel.items() if v[1] == 0}
+    # dominant kernel = the tensor-core instantiation with the most device
+    # time; achieved = its algorithmic flops per launch / its mean launch time
+    top, (top_ms, top_flops, top_n, _) = max(tensor.items(), key=lambda kv: kv[1][0])
     achieved = top_flops / (top_ms * 1e-3) / 1e12 if top_ms > 0 else None
+    # the same figure from the committed ncu launch list of one step (its
+    # SHARE of the step, cold-cache and serialised) x this run's step time
+    share = None
+    sp = os.path.join(ROOT, "profiles", "ncu_launch_share.json")
+    if os.path.exists(sp):
+        with open(sp) as f:
+            share = json.load(f).get(top)
+    achieved_ncu = (top_flops / top_n) / (share * ms / (top_n / K) * 1e-3) / 1e12 \
+        if share else None
     # DRAM bytes per launch of that kernel from the committed `ncu --set full`
     # capture of one step (tools/ncu_step.py -> tools/ncu_digest.py)
     traffic = None
@@ -381,6 +405,14 @@ def main():
     if os.path.exists(pk):
         with open(pk) as f:
             burst = json.load(f).get("bf16_tflops")
+    # step accounting: device time of every profiled launch vs the step
+    prof_sum = sum(v[0] for v in per_kernel.values()) / K
+    hbm = {k: {"ms_per_launch": v[0] / v[2], "launches_per_step": v[2] / K,
+               "bytes_per_launch": v[3] / v[2],
+               "gbs": v[3] / (v[0] * 1e-3) / 1e9 if v[0] > 0 else None,
+               "frac_of_hbm_peak": (v[3] / (v[0] * 1e-3) / 1e9) / hbm_peak
+               if v[0] > 0 and hbm_peak else None}
+           for k, v in sorted(memory.items())}
 
     # end to end through the C-ABI with host (pinned) buffers, copies inside
     e2e = None
@@ -421,17 +453,27 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "peak_source": f"{peak_src} bf16_tflops_sustained", "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": top, "kernel_launches_per_step": int(top_n),
+                         "kernel": top, "kernel_launches_per_step": top_n / K,
                          "kernel_flops_per_launch": top_flops / top_n,
                          "kernel_ms_per_launch": top_ms / top_n,
-                         "kernel_share_of_step": top_ms / ms if ms else None,
+                         "kernel_share_of_step": top_ms / K / ms_prof,
+                         "timing": "CUDA events around each launch inside the timed region",
+                         "ms_per_step_without_launch_events": ms_unprof,
+                         "ncu_share_of_step": share,
+                         "achieved_from_ncu_share": achieved_ncu,
+                         "frac_from_ncu_share": achieved_ncu / peak if achieved_ncu else None,
                          "frac_of_burst_peak": (achieved / burst) if achieved and burst else None,
                          # every tensor-core launch of the step (GEMMs + fused attention)
                          "tensor_kernels_tflops": gemm_flops / (gemm_ms * 1e-3) / 1e12,
-                         "tensor_kernels_ms_per_step": gemm_ms,
-                         "tensor_kernels_launches_per_step": gemm_n,
-                         "tensor_kernels_share_of_step": gemm_ms / ms if ms else None,
-                         "per_kernel_ms_flops_launches": per_kernel},
+                         "tensor_kernels_ms_per_step": gemm_ms / K,
+                         "tensor_kernels_launches_per_step": gemm_n / K,
+                         "tensor_kernels_share_of_step": gemm_ms / K / ms_prof,
+                         "profiled_kernels_ms_per_step": prof_sum,
+                         "unprofiled_ms_per_step": ms_prof - prof_sum,
+                         "per_kernel_ms_flops_launches_bytes":
+                             {k: [v[0] / K, v[1] / K, v[2] / K, v[3] / K]
+                              for k, v in per_kernel.items()},
+                         "hbm_kernels": hbm, "hbm_peak_gbs": hbm_peak},
             "exposed_comm_pct": 100.0 * exposed if exposed is not None else None,
             "ms_per_step_without_comm": ms_noop,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -692,7 +692,9 @@ def profile_enable(on: bool = True, detail: bool = False) -> None:
 
 
 def profile_kernels() -> dict:
-    """{kernel: (device_ms, flops, launches)} per GEMM kernel instantiation."""
+    """{kernel: (device_ms, flops, launches, bytes)} per profiled instantiation:
+    tensor-core launches carry algorithmic flops (2*m*n*k), memory-bound ones
+    (LayerNorm, attention delta, ...) their compulsory HBM bytes."""
     import json
     need = C.c_size_t()
     _check(lib.tess_profile_json(None, 0, C.byref(need)))

@@ -116,7 +116,8 @@ size_t Workspace::bytes_held() const {
 namespace {
 struct ProfRec {
   cudaEvent_t a, b;
-  double flops;
+  double flops;  // algorithmic 2*m*n*k (tensor-core launches)
+  double bytes;  // compulsory HBM bytes (memory-bound launches)
   int device;
   std::string kernel;
 };
@@ -125,10 +126,10 @@ bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
 }  // namespace
 
-ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s) {
+ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s, double bytes) {
   ProfToken t;
   if (!g_prof_on) return t;
-  auto* rec = new ProfRec{nullptr, nullptr, flops, 0, kernel};
+  auto* rec = new ProfRec{nullptr, nullptr, flops, bytes, 0, kernel};
   cudaGetDevice(&rec->device);
   TESS_CUDA(cudaEventCreate(&rec->a));
   TESS_CUDA(cudaEventCreate(&rec->b));
@@ -192,7 +193,10 @@ void profile_enable(int mode) {
 void profile_read(double* ms, double* flops, uint64_t* launches) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   double t = 0, f = 0;
+  uint64_t n = 0;
   for (auto& r : g_prof) {
+    if (r.flops <= 0) continue;  // tensor-core launches only
+    ++n;
     cudaSetDevice(r.device);
     TESS_CUDA(cudaEventSynchronize(r.b));
     float m = 0;
@@ -202,13 +206,13 @@ void profile_read(double* ms, double* flops, uint64_t* launches) {
   }
   if (ms) *ms = t;
   if (flops) *flops = f;
-  if (launches) *launches = g_prof.size();
+  if (launches) *launches = n;
 }
 
-// Per kernel instantiation: {"name": [ms, flops, launches], ...}
+// Per kernel instantiation: {"name": [ms, flops, launches, bytes], ...}
 std::string profile_json() {
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  std::map<std::string, std::array<double, 3>> agg;
+  std::map<std::string, std::array<double, 4>> agg;
   for (auto& r : g_prof) {
     cudaSetDevice(r.device);
     TESS_CUDA(cudaEventSynchronize(r.b));
@@ -218,13 +222,14 @@ std::string profile_json() {
     a[0] += m;
     a[1] += r.flops;
     a[2] += 1;
+    a[3] += r.bytes;
   }
   std::string s = "{";
   for (auto& kv : agg) {
     if (s.size() > 1) s += ", ";
     char buf[256];
-    std::snprintf(buf, sizeof(buf), "\"%s\": [%.6f, %.6e, %.0f]", kv.first.c_str(), kv.second[0],
-                  kv.second[1], kv.second[2]);
+    std::snprintf(buf, sizeof(buf), "\"%s\": [%.6f, %.6e, %.0f, %.6e]", kv.first.c_str(),
+                  kv.second[0], kv.second[1], kv.second[2], kv.second[3]);
     s += buf;
   }
   return s + "}";

@@ -45,8 +45,22 @@ enum Family { ROW = 0, COL = 1, DEPTH = 2 };
 struct ProfToken {
   void* rec = nullptr;
 };
-ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s);
+ProfToken prof_begin(const std::string& kernel, double flops, cudaStream_t s, double bytes = 0);
 void prof_end(ProfToken& t, cudaStream_t s);
+// Profiles one memory-bound launch (its compulsory HBM bytes) for the scope.
+struct ProfMem {
+  ProfToken tok;
+  cudaStream_t s;
+  ProfMem(const char* kernel, double bytes, cudaStream_t st) : s(st) {
+    tok = prof_begin(kernel, 0, st, bytes);
+  }
+  ~ProfMem() {
+    try {
+      prof_end(tok, s);
+    } catch (...) {
+    }
+  }
+};
 bool prof_detail();
 void profile_enable(int mode);  // 0 off, 1 per instantiation, 2 + shape/epilogue
 void profile_read(double* ms, double* flops, uint64_t* launches);

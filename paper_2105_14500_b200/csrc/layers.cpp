@@ -99,10 +99,14 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
     c.meter.reduce(1, 0, 0, (uint64_t)rows * 2, true);
     if (c.trace_on) c.trace.push_back({c.rank, c.step, 2, ROW, 0, (uint64_t)rows * 2 * 8});
     c.step++;
+    ProfMem pm("ln_fused_fwd_kernel", (double)rows * (w * 2.0 * dtype_size(t) + 8), s);
     k_ln_fused_fwd(x, t, rows, w, gain, bias, eps, y, mean, rstd, s);
     return;
   }
-  k_ln_stats(x, t, rows, w, stats, s);
+  {
+    ProfMem pm("ln_stats_kernel", (double)rows * (w * dtype_size(t) + 12), s);
+    k_ln_stats(x, t, rows, w, stats, s);
+  }
   // ref layers.cpp:258: row all-reduce of the [rows, 2] sums (metered as such)
   c.meter.reduce(c.grid.group_size(ROW), c.grid.slot_in_group(c.coord, ROW), 0,
                  (uint64_t)rows * 2, true);
@@ -112,6 +116,7 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   stream_dep(c, s, cs);
   if (!c.comm_noop) c.comm->allreduce(ROW, stats, rows * 3, cs);
   stream_dep(c, cs, s);
+  ProfMem pm("ln_apply_kernel", (double)rows * (w * 2.0 * dtype_size(t) + 20), s);
   k_ln_apply(x, t, stats, rows, w, (double)rd.hidden_total, gain, bias, eps, y, mean, rstd, s);
 }
 
@@ -136,18 +141,32 @@ void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
     coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305 (metered)
     float* scratch = static_cast<float*>(
         wsget(c, "ln.fscratch", k_ln_fused_scratch_floats(rows, w) * 4));
+    ProfMem pm("ln_fused_bwd_kernel",
+               (double)rows * (w * (double)(dtype_size(tdy) + dtype_size(t) + dtype_size(tdx) +
+                                            (resid ? dtype_size(tr) : 0)) + 8), s);
     k_ln_fused_bwd(dy, tdy, x, t, mean, rstd, gain, rows, w, resid, tr, dx, tdx, packed,
                    scratch, s);
   } else {
-    k_ln_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, s);
+    {
+      ProfMem pm("ln_bwd_stats_kernel",
+                 (double)rows * (w * (double)(dtype_size(tdy) + dtype_size(t)) + 16), s);
+      k_ln_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, s);
+    }
     stream_dep(c, s, cs);
     coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305
     stream_dep(c, cs, s);
-    k_ln_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w, (double)rd.hidden_total,
-                   resid, tr, dx, tdx, s);
+    {
+      ProfMem pm("ln_bwd_apply_kernel",
+                 (double)rows * (w * (double)(dtype_size(tdy) + dtype_size(t) + dtype_size(tdx) +
+                                              (resid ? dtype_size(tr) : 0)) + 16), s);
+      k_ln_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w, (double)rd.hidden_total,
+                     resid, tr, dx, tdx, s);
+    }
     if (want_params) {
       float* scratch =
           static_cast<float*>(wsget(c, "ln.pscratch", k_ln_params_scratch_floats(rows, w) * 4));
+      ProfMem pm("ln_bwd_params_kernel",
+                 (double)rows * (w * (double)(dtype_size(tdy) + dtype_size(t)) + 8), s);
       k_ln_bwd_params(dy, tdy, x, t, mean, rstd, rows, w, packed, scratch, s);
     }
   }
@@ -242,6 +261,7 @@ void ff_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
   } else {
     float* dh = static_cast<float*>(wsget(c, "ff.dh", rows * 4 * hq * 4));
     nt_product(c, t, dy, rows, rd.hin, p.w_ff2, 4 * hq, out_to(dh, DType::F32), s, &wp.ff2);
+    ProfMem pm("gelu_bwd_kernel", (double)rows * 4 * hq * (4.0 + 2 * dtype_size(t)), s);
     k_gelu_bwd(dh, z, dz, t, (size_t)rows * 4 * hq, s);  // ref layers.cpp:365
   }
   nt_product(c, t, dz, rows, 4 * hq, p.w_ff1, rd.hin, out_to(dx_f32, DType::F32), s, &wp.ff1);
@@ -423,7 +443,11 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
       k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
     }
     weight_grad(c, t, o, rows, hq, dy, rd.hin, g ? g->w_proj : nullptr, accumulate, s);
-    k_attn_delta(dout, o, t, hq, S, H, hd, delta, s, rd.samples_local);
+    {
+      ProfMem pm("attn_delta_vec_kernel",
+                 (double)rows * hq * 2.0 * dtype_size(t) + (double)rd.samples_local * H * S * 4, s);
+      k_attn_delta(dout, o, t, hq, S, H, hd, delta, s, rd.samples_local);
+    }
     AttnDesc a = attn_desc(rd, qkv, o, lse);
     a.dout = dout;
     a.delta = delta;
@@ -716,6 +740,7 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
       float* csum = static_cast<float*>(wsget(c, "bias.colsum", hq * 4));
       float* scratch =
           static_cast<float*>(wsget(c, "bias.scratch", k_colsum_scratch_floats(rows, hq) * 4));
+      ProfMem pm("colsum_kernel", (double)rows * hq * dtype_size(t) + hq * 4.0, s);
       k_colsum(dy, t, rows, hq, csum, scratch, s);
       float* red = static_cast<float*>(wsget(c, "bias.red", hq * 4));
       cudaStream_t cs = comm_stream(c, s);

@@ -103,6 +103,7 @@ def test_nh2_block_vs_oracle(tess, orc, q, d, allow):
     errs = {"y": frob(res.y, want["y"]), "dx": frob(res.dx, want["dx"])}
     for k, v in want["grads"].items():
         errs[k] = frob(res.grads[k], v)
+    print(f"nh2 block [{q},{q},{d}] errs {errs}")
     assert max(errs.values()) <= 2e-2, errs
     rows = b * s // (d * q)
     if rows > 128:  # the pair kernel needs M > 128 (rows per rank)
@@ -254,6 +255,7 @@ def test_cfg4_block_vs_torch(tess):
     errs = {"y": rel(y, ry), "dx": rel(dx, rdx)}
     for k, g in zip(names, G):
         errs[k] = rel(g.reshape(rg[k].shape), rg[k])
+    print(f"cfg4 block errs {errs}")
     assert max(errs.values()) <= 2e-2, errs
 
 
@@ -295,4 +297,5 @@ def test_cfg2_linear_vs_torch(tess, variant):
         ctx.close()
     assert EPI["store"] in wide_tile_epilogues(kernels), sorted(kernels)
     err = ((c.float() - ref).norm() / ref.norm()).item()
+    print(f"cfg2 {variant} err {err:.3e}")
     assert err <= (5e-3 if out[0] == "bf16" else 1e-4), err

@@ -27,7 +27,8 @@ def our_name(ncu_name):
     m = re.search(r"(attn_(fwd|bwd)_kernel<\d+>)", ncu_name)
     if m:
         return m[1]
-    return ncu_name.split("(")[0].replace("void ", "")
+    m = re.search(r"(\w+_kernel)\b", ncu_name)  # memory-bound kernels: base name
+    return m[1] if m else ncu_name.split("(")[0].replace("void ", "")
 
 
 KEEP = {

@@ -50,6 +50,7 @@ k = tess.profile_kernels()
 tess.profile_enable(False)
 tot = sum(v[0] for v in k.values())
 print(json.dumps({"step_ms": step_ms, "gemm_ms": tot}))
-for name, (ms, fl, n) in sorted(k.items(), key=lambda kv: -kv[1][0]):
-    print(f"{ms:8.3f} ms {100 * ms / step_ms:5.1f}%  {fl / ms / 1e9:7.1f} TF/s  x{int(n):3d}  {name}")
+for name, (ms, fl, n, by) in sorted(k.items(), key=lambda kv: -kv[1][0]):
+    rate = f"{fl / ms / 1e9:7.1f} TF/s" if fl else f"{by / ms / 1e6:7.1f} GB/s"
+    print(f"{ms:8.3f} ms {100 * ms / step_ms:5.1f}%  {rate}  x{int(n):3d}  {name}")
 ctx.close()
