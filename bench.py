@@ -166,6 +166,22 @@ def cpu_sample_run(reps_min_s=10.0, reps_max_s=30.0, max_reps=None):
     return fl / per / 1e12, per, kind, cores, desc, np
 
 
+def cpu_legs():
+    """config 1 tesseract_matmul / tesseract_backward_dense
+    at full size and the Block sample, best of 3, each with OMP_NUM_THREADS =
+    nproc and = 1 (each its own process: OpenMP reads it once)."""
+    out = {}
+    for omp in (os.cpu_count() or 1, 1):
+        env = dict(os.environ, OMP_NUM_THREADS=str(omp))
+        try:
+            r = subprocess.run([sys.executable, "-m", "oracle.cpu_legs"], cwd=ROOT, env=env,
+                               capture_output=True, text=True, timeout=240)
+            out[f"omp{omp}"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except (subprocess.SubprocessError, ValueError, IndexError) as e:
+            out[f"omp{omp}"] = {"error": str(e)[:200]}
+    return out
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -441,7 +457,10 @@ def main():
     if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
         tf, per, kind, cores, desc, _ = cpu_sample_run()
         cpu = {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": kind, "sample": desc,
-               "seconds_per_call": per}
+               "seconds_per_call": per, "omp_num_threads": cores,
+               "sample_scale": "cfg4 tokens x1/16 (T=512 vs 8192), hidden x1/24 (512 vs "
+                               "12288), heads 8 vs 96; flop-normalised",
+               "legs": cpu_legs()}
 
     if rank == 0:
         line = {
