@@ -290,6 +290,23 @@ tess_status tess_tesseract_backward(int q, int d, int allow_d_gt_q, tess_dtype c
                                     double* db, const int* devices, uint64_t* stats_rank,
                                     uint64_t* stats_kind);
 /* ref: algorithms.hpp:78-80 tesseract_backward_dense */
+
+/* The last global call made by the calling host thread (tesseract_matmul,
+ * tesseract_backward, layer_run, megatron_layer_run, train_toy): per-rank,
+ * per-kind send counters sent_by_kind [p][5][2] (messages, elements per
+ * CollectiveKind Broadcast, Reduce, AllReduce, Shift, PointToPoint) and
+ * per-rank receive counters recv [p][2]; *ranks = p. These rebuild the
+ * reference's CommStats exactly: add_send(r, kind, m, e) per (r, kind) and
+ * add_recv(r, any kind, m, e) per r (runtime.hpp:56-59; receives carry no
+ * kind, runtime.cpp:59-64). cap_ranks: rank capacity of the buffers. */
+tess_status tess_global_last_stats(int* ranks, uint64_t* sent_by_kind, uint64_t* recv,
+                                   size_t cap_ranks);
+/* Record collective traces in the global calls of this host thread (the
+ * reference's TesseractOptions::record_trace, algorithms.hpp:24-30), and read
+ * the last call's trace: write_trace() text, ranks in order (runtime.cpp:90-96,
+ * 149-156). */
+tess_status tess_set_global_trace(int enable);
+tess_status tess_global_last_trace(char* buf, size_t cap, size_t* needed);
 tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q, int d,
                            int allow_d_gt_q, tess_dtype compute, const double* x,
                            const double* dy, const double* const* params, double eps,

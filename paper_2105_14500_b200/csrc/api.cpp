@@ -288,12 +288,7 @@ tess_status tess_set_trace(tess_ctx* c, int enable) {
 tess_status tess_trace_text(const tess_ctx* c, char* buf, size_t cap, size_t* needed) {
   return guarded([&] {
     if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
-    static const char* kinds[5] = {"broadcast", "reduce", "all_reduce", "shift", "p2p"};
-    static const char* groups[3] = {"row", "col", "depth"};
-    std::string s;  // ref: runtime.cpp:90-96
-    for (const auto& e : c->trace)
-      s += std::to_string(e.rank) + ":" + std::to_string(e.step) + " " + kinds[e.kind] + " " +
-           groups[e.group] + " " + std::to_string(e.root) + " " + std::to_string(e.bytes) + "\n";
+    const std::string s = trace_text(c->trace);
     if (needed) *needed = s.size() + 1;
     if (buf && cap) {
       const size_t n = std::min(cap - 1, s.size());

@@ -112,6 +112,16 @@ size_t Workspace::bytes_held() const {
   return t;
 }
 
+std::string trace_text(const std::vector<TraceEvent>& trace) {
+  static const char* kinds[5] = {"broadcast", "reduce", "all_reduce", "shift", "p2p"};
+  static const char* groups[3] = {"row", "col", "depth"};
+  std::string s;
+  for (const auto& e : trace)
+    s += std::to_string(e.rank) + ":" + std::to_string(e.step) + " " + kinds[e.kind] + " " +
+         groups[e.group] + " " + std::to_string(e.root) + " " + std::to_string(e.bytes) + "\n";
+  return s;
+}
+
 // ------------------------------------------------------------ local GEMM
 namespace {
 struct ProfRec {

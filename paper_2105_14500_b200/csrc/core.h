@@ -149,6 +149,10 @@ struct TraceEvent {
   uint64_t bytes;
 };
 
+// write_trace() text of a trace ("<rank>:<step> <kind> <group> <root>
+// <bytes>" per line, runtime.cpp:90-96).
+std::string trace_text(const std::vector<TraceEvent>& trace);
+
 // Device workspace: named, grow-only buffers owned by a context.
 class Workspace {
  public:

@@ -23,6 +23,20 @@ extern thread_local std::string g_last_error;
 
 namespace {
 
+// What the last global call on this host thread metered and traced: the
+// per-rank, per-kind send counters and per-rank receive counters from which
+// the reference's CommStats can be rebuilt exactly with add_send / add_recv
+// (runtime.hpp:56-59), and the concatenated per-rank trace (the order of
+// SpmdRunner::take_trace, runtime.cpp:149-156).
+struct LastRun {
+  int p = 0;
+  std::vector<uint64_t> sent;  // [p][5][2] messages, elements per CollectiveKind
+  std::vector<uint64_t> recv;  // [p][2]
+  std::string trace;
+};
+thread_local LastRun g_last_run;
+thread_local bool g_global_trace = false;
+
 struct Runner {
   Grid g;
   std::vector<int> devs;
@@ -36,6 +50,8 @@ struct Runner {
     ctx.resize(g.size(), nullptr);
     if (tess_init_local(q, d, allow, devs.data(), ctx.data()) != TESS_OK)
       fail(TESS_ERR_CUDA, std::string("init_local: ") + g_last_error);
+    for (auto* c : ctx) c->trace_on = g_global_trace;
+    g_last_run = LastRun{};
   }
   ~Runner() {
     for (auto* c : ctx)
@@ -97,6 +113,22 @@ struct Runner {
   }
 
   void stats(uint64_t* sr, uint64_t* sk) const {
+    LastRun& L = g_last_run;
+    L.p = g.size();
+    L.sent.assign((size_t)L.p * 10, 0);
+    L.recv.assign((size_t)L.p * 2, 0);
+    std::vector<TraceEvent> all;
+    for (int r = 0; r < g.size(); ++r) {
+      const Meter& m = ctx[r]->meter;
+      for (int k = 0; k < 5; ++k) {
+        L.sent[10 * r + 2 * k] = m.kind[k][0];
+        L.sent[10 * r + 2 * k + 1] = m.kind[k][1];
+      }
+      L.recv[2 * r] = m.recv_msgs;
+      L.recv[2 * r + 1] = m.recv_elems;
+      all.insert(all.end(), ctx[r]->trace.begin(), ctx[r]->trace.end());
+    }
+    L.trace = trace_text(all);
     if (sr)
       for (int r = 0; r < g.size(); ++r) {
         const Meter& m = ctx[r]->meter;
@@ -729,6 +761,39 @@ tess_status tess_megatron_1d_linear(int p, tess_dtype compute, const double* x, 
     });
     for (size_t i = 0; i < res.size(); ++i) out[i] = res[i];
     R.stats(sr, sk);
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+tess_status tess_set_global_trace(int enable) {
+  g_global_trace = enable != 0;
+  return TESS_OK;
+}
+
+tess_status tess_global_last_stats(int* ranks, uint64_t* sent_by_kind, uint64_t* recv,
+                                   size_t cap_ranks) {
+  return guarded([&] {
+    const LastRun& L = g_last_run;
+    if (ranks) *ranks = L.p;
+    if ((sent_by_kind || recv) && cap_ranks < (size_t)L.p)
+      fail(TESS_ERR_INVALID, "tess_global_last_stats: buffers hold fewer ranks than the run");
+    if (sent_by_kind) std::copy(L.sent.begin(), L.sent.end(), sent_by_kind);
+    if (recv) std::copy(L.recv.begin(), L.recv.end(), recv);
+  });
+}
+
+tess_status tess_global_last_trace(char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    const std::string& s = g_last_run.trace;
+    if (needed) *needed = s.size() + 1;
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
   });
 }
 
