@@ -3,6 +3,7 @@
 // id), rng.hpp) and compare values, CommStats (operator==, runtime.hpp:64)
 // and traces (write_trace text). Called by tests/test_integration.py.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -88,6 +89,25 @@ int tsb_check_matmul(int q, int d, int allow, int variant, int dtype, int m, int
     out[1] = got.stats == want.stats ? 1 : 0;
     out[2] = trace_text(got.trace) == trace_text(want.trace) ? 1 : 0;
     out[3] = (double)want.trace.size();
+  });
+}
+
+// Both traces of tsb_check_matmul's call (diagnostics).
+int tsb_matmul_traces(int q, int d, int allow, int variant, int m, int n, int r, char* want,
+                      char* got, int cap) {
+  return guarded([&] {
+    const auto v = static_cast<tsim::MatmulVariant>(variant);
+    tsim::GridSpec g(q, d, allow != 0);
+    tsim::Matrix a = rnd(m, n, 42, 0);
+    tsim::Matrix b = v == tsim::MatmulVariant::NN   ? rnd(n, r, 42, 1)
+                     : v == tsim::MatmulVariant::NT ? rnd(r, n, 42, 1)
+                                                    : rnd(m, r, 42, 1);
+    tsim::TesseractOptions o;
+    o.record_trace = true;
+    const std::string w = trace_text(tsim::tesseract_matmul(a, b, g, v, o).trace);
+    const std::string t = trace_text(tsim::b200::tesseract_matmul(a, b, g, v, o).trace);
+    std::snprintf(want, cap, "%s", w.c_str());
+    std::snprintf(got, cap, "%s", t.c_str());
   });
 }
 

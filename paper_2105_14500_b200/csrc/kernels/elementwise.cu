@@ -298,14 +298,22 @@ __global__ void ln_params_partial_kernel(const TD* dy, const TX* x, const float*
   part[((int64_t)blockIdx.y * 2 + 1) * w + c] = db;
 }
 
-// ---- fused single-pass LayerNorm for a one-member row group (q == 1) -------
-// With q == 1 the row all-reduce between the statistics and the apply moves
-// nothing, so a block keeps its rows in registers and does stats + apply
-// (forward) or stats + dx + dgain/dbias partials (backward) in ONE pass over
-// HBM with 16-byte vector accesses. Thread t owns columns
-// [t*8 + v*4096, +8) for v < NV (block 512 threads, w = NV * 4096).
-constexpr int kLnThreads = 512;
-constexpr int kLnSpan = kLnThreads * 8;  // columns per vector pass
+// ---- vectorised LayerNorm (ref layers.cpp:242-345) --------------------------
+// A block owns whole rows, register-resident: thread t holds columns
+// [t*8 + v*span, +8) for v < NV (span = 8 * blockDim.x, w = NV * span),
+// loaded with 16-byte vectors. Two forms:
+//  * fused (q == 1: the row all-reduce moves nothing): statistics + apply
+//    (forward), statistics + dx + dgain/dbias partials (backward) in ONE pass
+//    over HBM;
+//  * split (q > 1): a partial pass writes per-row partials (forward
+//    [sum x, M2, n*mean^2] of the local columns; backward [sum dxhat,
+//    sum xhat*dxhat] plus the dgain/dbias column partials), the row group
+//    all-reduces them, and an apply pass finishes the rows: 2 reads of x and
+//    1 write forward, 2 reads of dy / x and 1 write backward.
+// Supported widths: w = NV * 8 * threads, NV <= 4, threads a multiple of 32
+// in [128, 1024] (ln_vec_config): 2048 ... 32768 in steps the hidden sizes
+// of the configs hit (4096 * k, 6144, 3072, 2048, ...).
+constexpr int kLnMaxThreads = 1024;
 
 __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&v)[8]) {
   const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
@@ -354,7 +362,7 @@ __device__ __forceinline__ void unpack8(const uint4 (&u)[2], float (&v)[8]) {
 
 // Deterministic block sums of two values (fixed-order combine of warp sums).
 __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -364,8 +372,7 @@ __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
   if (lane == 0) red[warp] = make_float2(a, b);
   __syncthreads();
   float2 t = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int w = 0; w < kLnThreads / 32; ++w) {
+  for (int w = 0; w < nw; ++w) {
     t.x += red[w].x;
     t.y += red[w].y;
   }
@@ -378,7 +385,7 @@ __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
 // E[x^2] - E[x]^2 anywhere, so a row whose mean is large against its spread
 // (or whose first element is an outlier) does not cancel.
 __device__ __forceinline__ float2 block_meanvar(float m, float M2, float n, float2* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const float mo = __shfl_xor_sync(0xffffffffu, m, o);
@@ -393,8 +400,7 @@ __device__ __forceinline__ float2 block_meanvar(float m, float M2, float n, floa
   __syncthreads();
   float2 t = red[0];
   float nt = n;
-#pragma unroll
-  for (int w = 1; w < kLnThreads / 32; ++w) {
+  for (int w = 1; w < nw; ++w) {
     const float dlt = red[w].x - t.x;
     const float tot = nt + n;
     t.y = t.y + red[w].y + dlt * dlt * (nt * n / tot);
@@ -404,48 +410,63 @@ __device__ __forceinline__ float2 block_meanvar(float m, float M2, float n, floa
   return t;
 }
 
-template <typename T, int NV>
-__global__ void __launch_bounds__(kLnThreads) ln_fused_fwd_kernel(
+// Row mean / M2 of the register-resident slice (every thread gets the pair).
+template <int NV>
+__device__ __forceinline__ float2 row_meanvar(const float (&v)[NV][8], float2* red) {
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += v[k][e];
+  constexpr float kN = (float)(NV * 8);
+  const float lm = s / kN;
+  float m2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = v[k][e] - lm;
+      m2 = fmaf(d, d, m2);
+    }
+  return block_meanvar(lm, m2, kN, red);
+}
+
+// SPLIT = false: y = LN(x) with the row's own statistics (q == 1).
+// SPLIT = true: stats[3r..] = (sum x, M2, n mean^2) of the local columns, the
+// row group's all-reduce sums them (ln_vec_apply_kernel combines).
+template <typename T, int NV, bool SPLIT>
+__global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_fwd_kernel(
     const T* __restrict__ x, int64_t rows, const float* __restrict__ gain,
     const float* __restrict__ bias, float eps, T* __restrict__ y, float* __restrict__ mean_out,
-    float* __restrict__ rstd_out) {
-  __shared__ float2 red[kLnThreads / 32];
-  constexpr int w = NV * kLnSpan;
+    float* __restrict__ rstd_out, float* __restrict__ stats) {
+  __shared__ float2 red[32];
+  const int span = blockDim.x * 8;
+  const int w = NV * span;
   const int c0 = threadIdx.x * 8;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     float v[NV][8];
-    // one block reduction per row: each thread's (mean, sum of squared
-    // deviations) over its NV*8 register-resident values, combined by
-    // Chan's formula (block_meanvar)
-    float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      ld8(x + r * w + c0 + k * kLnSpan, v[k]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s += v[k][e];
-    }
-    constexpr float kN = (float)(NV * 8);
-    const float lm = s / kN;
-    float m2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < NV; ++k)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = v[k][e] - lm;
-        m2 = fmaf(d, d, m2);
+    for (int k = 0; k < NV; ++k) ld8(x + r * w + c0 + k * span, v[k]);
+    const float2 t = row_meanvar<NV>(v, red);
+    if (SPLIT) {
+      if (threadIdx.x == 0) {
+        stats[3 * r + 0] = t.x * (float)w;
+        stats[3 * r + 1] = t.y;
+        stats[3 * r + 2] = (float)w * t.x * t.x;
       }
-    const float2 t = block_meanvar(lm, m2, kN, red);
+      continue;
+    }
     const float mu = t.x;
     const float var = fmaxf(t.y / (float)w, 0.f);
     const float rstd = 1.0f / sqrtf(var + eps);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       float g[8], b[8], o[8];
-      ld8(gain + c0 + k * kLnSpan, g);
-      ld8(bias + c0 + k * kLnSpan, b);
+      ld8(gain + c0 + k * span, g);
+      ld8(bias + c0 + k * span, b);
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = g[e] * ((v[k][e] - mu) * rstd) + b[e];
-      st8(y + r * w + c0 + k * kLnSpan, o);
+      st8(y + r * w + c0 + k * span, o);
     }
     if (threadIdx.x == 0) {
       mean_out[r] = mu;
@@ -454,16 +475,55 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_fwd_kernel(
   }
 }
 
-// dx = rstd * (dxhat - mean(dxhat) - xhat * mean(xhat*dxhat)) (+ resid), with
-// per-block column partials of dgain = sum dy*xhat, dbias = sum dy into
+// Apply with the row group's summed partials (n = hidden_total):
+// mean = sum/n, var = (sum M2 + (sum n_g mean_g^2 - n mean^2)) / n.
+template <typename T, int NV>
+__global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_apply_kernel(
+    const T* __restrict__ x, const float* __restrict__ stats, int64_t rows, float n,
+    const float* __restrict__ gain, const float* __restrict__ bias, float eps, T* __restrict__ y,
+    float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  const int span = blockDim.x * 8;
+  const int w = NV * span;
+  const int c0 = threadIdx.x * 8;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    float v[NV][8];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) ld8(x + r * w + c0 + k * span, v[k]);
+    const float s0 = stats[3 * r], s1 = stats[3 * r + 1], s2 = stats[3 * r + 2];
+    const float mu = s0 / n;
+    const float var = fmaxf((s1 + (s2 - n * mu * mu)) / n, 0.f);
+    const float rstd = 1.0f / sqrtf(var + eps);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float g[8], b[8], o[8];
+      ld8(gain + c0 + k * span, g);
+      ld8(bias + c0 + k * span, b);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = g[e] * ((v[k][e] - mu) * rstd) + b[e];
+      st8(y + r * w + c0 + k * span, o);
+    }
+    if (threadIdx.x == 0) {
+      mean_out[r] = mu;
+      rstd_out[r] = rstd;
+    }
+  }
+}
+
+// Backward. SPLIT = false (q == 1): dx = rstd * (dxhat - mean(dxhat) - xhat *
+// mean(xhat*dxhat)) (+ resid) with the row's own sums. SPLIT = true: only
+// the row partials stats[2r..] = (sum dxhat, sum xhat*dxhat) over the local
+// columns (ln_vec_bwd_apply_kernel finishes after the row all-reduce). Both
+// add this block's dgain = sum dy*xhat, dbias = sum dy column partials to
 // part[block][2][w] (summed over blocks in fixed order afterwards).
-template <typename TD, typename TX, typename TR, typename TO, int NV>
-__global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
+template <typename TD, typename TX, typename TR, typename TO, int NV, bool SPLIT>
+__global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_bwd_kernel(
     const TD* __restrict__ dy, const TX* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ gain, int64_t rows,
-    const TR* __restrict__ resid, TO* __restrict__ dx, float* __restrict__ part) {
-  __shared__ float2 red[kLnThreads / 32];
-  constexpr int w = NV * kLnSpan;
+    const TR* __restrict__ resid, TO* __restrict__ dx, float* __restrict__ part,
+    float* __restrict__ stats) {
+  __shared__ float2 red[32];
+  const int span = blockDim.x * 8;
+  const int w = NV * span;
   const int c0 = threadIdx.x * 8;
   float dg[NV][8], db[NV][8];  // gain is re-read per row (L1-resident) to save registers
 #pragma unroll
@@ -477,19 +537,19 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
     // the residual is loaded with dy / x (raw 16-byte vectors), not after
     // the block reduction: one HBM round trip per row instead of two
     uint4 rr[NV][sizeof(TR) / 2];
-    if (resid) {
+    if (!SPLIT && resid) {
 #pragma unroll
       for (int k = 0; k < NV; ++k)
 #pragma unroll
         for (int u = 0; u < (int)(sizeof(TR) / 2); ++u)
-          rr[k][u] = __ldg(reinterpret_cast<const uint4*>(resid + r * w + c0 + k * kLnSpan) + u);
+          rr[k][u] = __ldg(reinterpret_cast<const uint4*>(resid + r * w + c0 + k * span) + u);
     }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       float g[8];
-      ld8(dy + r * w + c0 + k * kLnSpan, d[k]);
-      ld8(x + r * w + c0 + k * kLnSpan, xh[k]);
-      ld8(gain + c0 + k * kLnSpan, g);
+      ld8(dy + r * w + c0 + k * span, d[k]);
+      ld8(x + r * w + c0 + k * span, xh[k]);
+      ld8(gain + c0 + k * span, g);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         xh[k][e] = (xh[k][e] - mu) * rs;
@@ -502,6 +562,13 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
       }
     }
     const float2 t = block_sum2(a, b, red);
+    if (SPLIT) {
+      if (threadIdx.x == 0) {
+        stats[2 * r] = t.x;
+        stats[2 * r + 1] = t.y;
+      }
+      continue;
+    }
     const float md = t.x / (float)w, mxd = t.y / (float)w;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -512,14 +579,53 @@ __global__ void __launch_bounds__(kLnThreads) ln_fused_bwd_kernel(
         const float v = rs * (d[k][e] - md - xh[k][e] * mxd);
         o[e] = resid ? o[e] + v : v;
       }
-      st8(dx + r * w + c0 + k * kLnSpan, o);
+      st8(dx + r * w + c0 + k * span, o);
     }
   }
   if (part) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      st8(part + ((int64_t)blockIdx.x * 2 + 0) * w + c0 + k * kLnSpan, dg[k]);
-      st8(part + ((int64_t)blockIdx.x * 2 + 1) * w + c0 + k * kLnSpan, db[k]);
+      st8(part + ((int64_t)blockIdx.x * 2 + 0) * w + c0 + k * span, dg[k]);
+      st8(part + ((int64_t)blockIdx.x * 2 + 1) * w + c0 + k * span, db[k]);
+    }
+  }
+}
+
+// dx from the row group's summed (sum dxhat, sum xhat*dxhat), n = hidden_total.
+template <typename TD, typename TX, typename TR, typename TO, int NV>
+__global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_bwd_apply_kernel(
+    const TD* __restrict__ dy, const TX* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ gain,
+    const float* __restrict__ stats, int64_t rows, float n, const TR* __restrict__ resid,
+    TO* __restrict__ dx) {
+  const int span = blockDim.x * 8;
+  const int w = NV * span;
+  const int c0 = threadIdx.x * 8;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float mu = mean[r], rs = rstd[r];
+    const float md = stats[2 * r] / n, mxd = stats[2 * r + 1] / n;
+    uint4 rr[NV][sizeof(TR) / 2];
+    if (resid) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int u = 0; u < (int)(sizeof(TR) / 2); ++u)
+          rr[k][u] = __ldg(reinterpret_cast<const uint4*>(resid + r * w + c0 + k * span) + u);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float d[8], xv[8], g[8], o[8];
+      ld8(dy + r * w + c0 + k * span, d);
+      ld8(x + r * w + c0 + k * span, xv);
+      ld8(gain + c0 + k * span, g);
+      if (resid) unpack8(rr[k], o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (xv[e] - mu) * rs;
+        const float v = rs * (d[e] * g[e] - md - xh * mxd);
+        o[e] = resid ? o[e] + v : v;
+      }
+      st8(dx + r * w + c0 + k * span, o);
     }
   }
 }
@@ -959,62 +1065,72 @@ void k_softmax_bwd(const void* P, const float* dP, void* dS, DType t, int64_t ro
 }
 
 
-// ---- fused LayerNorm launchers (q == 1) -----------------------------------
-int ln_fused_nv(int64_t w) {
-  if (w % kLnSpan != 0) return 0;
-  const int64_t nv = w / kLnSpan;
-  return (nv >= 1 && nv <= 4) ? (int)nv : 0;
+// ---- vectorised LayerNorm launchers ------------------------------------------
+struct LnCfg {
+  int nv = 0, threads = 0;
+};
+
+// w = nv * 8 * threads. Widths that are multiples of 4096 keep 512-thread
+// blocks (the measured configuration at cfg4's 12288); others take the
+// fewest passes whose block is a whole number of warps in [128, 1024].
+LnCfg ln_vec_config(int64_t w) {
+  LnCfg c;
+  if (w <= 0 || w % 8 != 0) return c;
+  if (w % 4096 == 0 && w / 4096 <= 4) return {(int)(w / 4096), 512};
+  for (int nv = 1; nv <= 4; ++nv) {
+    if (w % (8 * nv) != 0) continue;
+    const int64_t t = w / (8 * nv);
+    // registers: one pass fits 1024 threads, several passes at most 512
+    if (t % 32 == 0 && t >= 128 && t <= (nv == 1 ? kLnMaxThreads : 512)) return {nv, (int)t};
+  }
+  return c;
 }
 
-// fwd: 4 blocks per SM; bwd: 2 (each block's dgain/dbias partials are summed
-// afterwards, so fewer blocks = less partial traffic)
-int ln_fused_blocks(int64_t rows, int per_sm = 2) {
+bool ln_vec_ok(int64_t w, std::initializer_list<const void*> ptrs) {
+  if (ln_vec_config(w).nv == 0) return false;
+  for (const void* p : ptrs)
+    if (p && reinterpret_cast<uintptr_t>(p) % 16 != 0) return false;
+  return true;
+}
+
+// Blocks: up to 2048 resident threads per SM; the backward (whose blocks
+// each write a [2, w] dgain/dbias partial) at most 2 blocks per SM.
+int ln_vec_blocks(int64_t rows, int threads, int per_sm_cap) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = std::max(1, std::min(per_sm_cap, 2048 / threads));
   const int64_t b = std::min<int64_t>(rows, (int64_t)sms * per_sm);
   return (int)std::max<int64_t>(b, 1);
 }
 
-bool k_ln_fused_supported(int64_t w) { return ln_fused_nv(w) > 0; }
+bool k_ln_fused_supported(int64_t w) { return ln_vec_config(w).nv > 0; }
 
 size_t k_ln_fused_scratch_floats(int64_t rows, int64_t w) {
-  return (size_t)ln_fused_blocks(rows) * 2 * w;
+  const LnCfg c = ln_vec_config(w);
+  return (size_t)ln_vec_blocks(rows, c.threads ? c.threads : 512, 2) * 2 * w;
 }
 
-template <int NV>
-void ln_fwd_nv(const void* x, DType t, int64_t rows, const float* gain, const float* bias,
-               float eps, void* y, float* mean, float* rstd, cudaStream_t s) {
-  const int g = ln_fused_blocks(rows, 4);
-  TESS_DISPATCH(t, T, ln_fused_fwd_kernel<T, NV><<<g, kLnThreads, 0, s>>>(
-      (const T*)x, rows, gain, bias, eps, (T*)y, mean, rstd));
-}
+#define TESS_LN_NV(nv, ...)                                                        \
+  switch (nv) {                                                                    \
+    case 1: { constexpr int NV = 1; __VA_ARGS__; } break;                          \
+    case 2: { constexpr int NV = 2; __VA_ARGS__; } break;                          \
+    case 3: { constexpr int NV = 3; __VA_ARGS__; } break;                          \
+    case 4: { constexpr int NV = 4; __VA_ARGS__; } break;                          \
+    default: fail(TESS_ERR_UNSUPPORTED, "vectorised LayerNorm: unsupported width"); \
+  }
 
 void k_ln_fused_fwd(const void* x, DType t, int64_t rows, int64_t w, const float* gain,
                     const float* bias, double eps, void* y, float* mean, float* rstd,
                     cudaStream_t s) {
   if (!rows) return;
-  const float e = (float)eps;
-  switch (ln_fused_nv(w)) {
-    case 1: ln_fwd_nv<1>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
-    case 2: ln_fwd_nv<2>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
-    case 3: ln_fwd_nv<3>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
-    case 4: ln_fwd_nv<4>(x, t, rows, gain, bias, e, y, mean, rstd, s); break;
-    default: fail(TESS_ERR_UNSUPPORTED, "fused LayerNorm: hidden/q must be a multiple of 4096");
-  }
+  const LnCfg c = ln_vec_config(w);
+  const int g = ln_vec_blocks(rows, c.threads, 4);
+  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, ln_vec_fwd_kernel<T, NV, false><<<g, c.threads, 0, s>>>(
+                                           (const T*)x, rows, gain, bias, (float)eps, (T*)y,
+                                           mean, rstd, nullptr)));
   count_launch();
   TESS_CUDA(cudaGetLastError());
-}
-
-template <int NV>
-void ln_bwd_nv(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
-               const float* rstd, const float* gain, int64_t rows, const void* resid, DType tr,
-               void* dx, DType tdx, float* part, cudaStream_t s) {
-  const int g = ln_fused_blocks(rows);
-  TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR, TESS_DISPATCH(tdx, TO,
-      ln_fused_bwd_kernel<TD, TX, TR, TO, NV><<<g, kLnThreads, 0, s>>>(
-          (const TD*)dy, (const TX*)x, mean, rstd, gain, rows, (const TR*)resid, (TO*)dx,
-          part)))));
 }
 
 void k_ln_fused_bwd(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
@@ -1025,23 +1141,88 @@ void k_ln_fused_bwd(const void* dy, DType tdy, const void* x, DType tx, const fl
     if (out2w) TESS_CUDA(cudaMemsetAsync(out2w, 0, 2 * w * 4, s));
     return;
   }
+  const LnCfg c = ln_vec_config(w);
+  const int g = ln_vec_blocks(rows, c.threads, 2);
   float* part = out2w ? scratch : nullptr;
-  switch (ln_fused_nv(w)) {
-    case 1: ln_bwd_nv<1>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
-    case 2: ln_bwd_nv<2>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
-    case 3: ln_bwd_nv<3>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
-    case 4: ln_bwd_nv<4>(dy, tdy, x, tx, mean, rstd, gain, rows, resid, tr, dx, tdx, part, s); break;
-    default: fail(TESS_ERR_UNSUPPORTED, "fused LayerNorm: hidden/q must be a multiple of 4096");
-  }
+  TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR,
+      TESS_DISPATCH(tdx, TO, ln_vec_bwd_kernel<TD, TX, TR, TO, NV, false><<<g, c.threads, 0, s>>>(
+          (const TD*)dy, (const TX*)x, mean, rstd, gain, rows, (const TR*)resid, (TO*)dx, part,
+          nullptr))))));
   count_launch();
   TESS_CUDA(cudaGetLastError());
   if (out2w) {
-    const int64_t nb = ln_fused_blocks(rows);
     colsum_finalize_kernel<<<(unsigned)((2 * w + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-        scratch, nb, w, 2, out2w);
+        scratch, g, w, 2, out2w);
     count_launch();
     TESS_CUDA(cudaGetLastError());
   }
+}
+
+bool k_ln_split_supported(int64_t w, const void* gain, const void* bias) {
+  return ln_vec_ok(w, {gain, bias});
+}
+
+void k_ln_split_stats(const void* x, DType t, int64_t rows, int64_t w, float* stats,
+                      cudaStream_t s) {
+  if (!rows) return;
+  const LnCfg c = ln_vec_config(w);
+  const int g = ln_vec_blocks(rows, c.threads, 4);
+  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, ln_vec_fwd_kernel<T, NV, true><<<g, c.threads, 0, s>>>(
+                                           (const T*)x, rows, nullptr, nullptr, 0.f, nullptr,
+                                           nullptr, nullptr, stats)));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_ln_split_apply(const void* x, DType t, const float* stats, int64_t rows, int64_t w,
+                      double hidden_total, const float* gain, const float* bias, double eps,
+                      void* y, float* mean, float* rstd, cudaStream_t s) {
+  if (!rows) return;
+  const LnCfg c = ln_vec_config(w);
+  const int g = ln_vec_blocks(rows, c.threads, 4);
+  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, ln_vec_apply_kernel<T, NV><<<g, c.threads, 0, s>>>(
+                                           (const T*)x, stats, rows, (float)hidden_total, gain,
+                                           bias, (float)eps, (T*)y, mean, rstd)));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
+
+void k_ln_split_bwd_stats(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                          const float* rstd, const float* gain, int64_t rows, int64_t w,
+                          float* stats, float* out2w, float* scratch, cudaStream_t s) {
+  if (!rows) {
+    if (out2w) TESS_CUDA(cudaMemsetAsync(out2w, 0, 2 * w * 4, s));
+    return;
+  }
+  const LnCfg c = ln_vec_config(w);
+  const int g = ln_vec_blocks(rows, c.threads, 2);
+  float* part = out2w ? scratch : nullptr;
+  TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX,
+      ln_vec_bwd_kernel<TD, TX, float, float, NV, true><<<g, c.threads, 0, s>>>(
+          (const TD*)dy, (const TX*)x, mean, rstd, gain, rows, nullptr, nullptr, part, stats))));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+  if (out2w) {
+    colsum_finalize_kernel<<<(unsigned)((2 * w + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+        scratch, g, w, 2, out2w);
+    count_launch();
+    TESS_CUDA(cudaGetLastError());
+  }
+}
+
+void k_ln_split_bwd_apply(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                          const float* rstd, const float* gain, const float* stats, int64_t rows,
+                          int64_t w, double hidden_total, const void* resid, DType tr, void* dx,
+                          DType tdx, cudaStream_t s) {
+  if (!rows) return;
+  const LnCfg c = ln_vec_config(w);
+  const int g = ln_vec_blocks(rows, c.threads, 4);
+  TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR,
+      TESS_DISPATCH(tdx, TO, ln_vec_bwd_apply_kernel<TD, TX, TR, TO, NV><<<g, c.threads, 0, s>>>(
+          (const TD*)dy, (const TX*)x, mean, rstd, gain, stats, rows, (float)hidden_total,
+          (const TR*)resid, (TO*)dx))))));
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
 }
 
 }  // namespace tess

@@ -63,9 +63,13 @@ void k_ln_bwd_params(const void* dy, DType tdy, const void* x, DType tx, const f
                      cudaStream_t s);
 size_t k_ln_params_scratch_floats(int64_t rows, int64_t w);
 
-// Fused single-pass LayerNorm for a one-member row group (q == 1: the row
-// all-reduce between statistics and apply moves nothing). Supported when
-// w % 4096 == 0 and w <= 16384; bitwise-deterministic.
+// Vectorised LayerNorm (16-byte accesses, rows register-resident in a
+// block): w = nv * 8 * threads with nv <= 4 and a whole number of warps in
+// [128, 1024] per block (every 4096 * k up to 16384, 6144, 3072, 2048, ...),
+// gain / bias 16-byte aligned. Bitwise-deterministic.
+bool k_ln_split_supported(int64_t w, const void* gain, const void* bias);
+// Fused single pass for a one-member row group (q == 1: the row all-reduce
+// between statistics and apply moves nothing).
 bool k_ln_fused_supported(int64_t w);
 // y = gain * (x - mean) * rstd + bias over the local w columns (= hidden).
 void k_ln_fused_fwd(const void* x, DType t, int64_t rows, int64_t w, const float* gain,
@@ -77,6 +81,23 @@ void k_ln_fused_bwd(const void* dy, DType tdy, const void* x, DType tx, const fl
                     const float* rstd, const float* gain, int64_t rows, int64_t w,
                     const void* resid, DType tr, void* dx, DType tdx, float* out2w,
                     float* scratch, cudaStream_t s);
+// q > 1 (statistics all-reduced over the row group between two passes):
+// forward partials stats[r] = {sum x, M2 of the local columns, w * mean_r^2}
+// (one pass), then apply with the summed partials (hidden_total columns);
+void k_ln_split_stats(const void* x, DType t, int64_t rows, int64_t w, float* stats,
+                      cudaStream_t s);
+void k_ln_split_apply(const void* x, DType t, const float* stats, int64_t rows, int64_t w,
+                      double hidden_total, const float* gain, const float* bias, double eps,
+                      void* y, float* mean, float* rstd, cudaStream_t s);
+// backward partials stats[r] = {sum dxhat, sum xhat*dxhat} plus, if out2w,
+// the [dgain | dbias] column sums in the same pass; then dx (+ resid).
+void k_ln_split_bwd_stats(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                          const float* rstd, const float* gain, int64_t rows, int64_t w,
+                          float* stats, float* out2w, float* scratch, cudaStream_t s);
+void k_ln_split_bwd_apply(const void* dy, DType tdy, const void* x, DType tx, const float* mean,
+                          const float* rstd, const float* gain, const float* stats, int64_t rows,
+                          int64_t w, double hidden_total, const void* resid, DType tr, void* dx,
+                          DType tdx, cudaStream_t s);
 size_t k_ln_fused_scratch_floats(int64_t rows, int64_t w);
 
 // ---- softmax (ref layers.cpp:44-74) ---------------------------------------

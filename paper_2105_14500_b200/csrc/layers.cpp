@@ -87,13 +87,23 @@ Out out_to(void* p, DType t, int64_t ld = 0) {
 }
 
 // ----------------------------------------------------------- LayerNorm
+// The vectorised kernels need w = nv * 8 * threads and 16-byte aligned rows.
+bool ln_vec(int64_t w, const float* gain, const float* bias,
+            std::initializer_list<const void*> rows) {
+  if (!k_ln_split_supported(w, gain, bias)) return false;
+  for (const void* p : rows)
+    if (p && reinterpret_cast<uintptr_t>(p) % 16 != 0) return false;
+  return true;
+}
+
 void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const void* x,
             const float* gain, const float* bias, double eps, void* y, cudaStream_t s) {
   const int64_t rows = rd.rows, w = rd.hin;
   float* stats = static_cast<float*>(wsget(c, "ln.stats", rows * 3 * 4));
   float* mean = static_cast<float*>(wsget(c, tag + ".mean", rows * 4));
   float* rstd = static_cast<float*>(wsget(c, tag + ".rstd", rows * 4));
-  if (c.grid.q == 1 && k_ln_fused_supported(w)) {
+  const bool vec = ln_vec(w, gain, bias, {x, y});
+  if (c.grid.q == 1 && vec) {
     // one-member row group: the [rows, 2] all-reduce moves nothing (still
     // metered and traced like the reference), so stats + apply is one pass
     c.meter.reduce(1, 0, 0, (uint64_t)rows * 2, true);
@@ -103,7 +113,11 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
     k_ln_fused_fwd(x, t, rows, w, gain, bias, eps, y, mean, rstd, s);
     return;
   }
-  {
+  if (vec) {
+    // q > 1: one vectorised pass for the [rows, 3] partials
+    ProfMem pm("ln_vec_stats_kernel", (double)rows * (w * dtype_size(t) + 12), s);
+    k_ln_split_stats(x, t, rows, w, stats, s);
+  } else {
     ProfMem pm("ln_stats_kernel", (double)rows * (w * dtype_size(t) + 12), s);
     k_ln_stats(x, t, rows, w, stats, s);
   }
@@ -116,8 +130,13 @@ void ln_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   stream_dep(c, s, cs);
   if (!c.comm_noop) c.comm->allreduce(ROW, stats, rows * 3, cs);
   stream_dep(c, cs, s);
-  ProfMem pm("ln_apply_kernel", (double)rows * (w * 2.0 * dtype_size(t) + 20), s);
-  k_ln_apply(x, t, stats, rows, w, (double)rd.hidden_total, gain, bias, eps, y, mean, rstd, s);
+  ProfMem pm(vec ? "ln_vec_apply_kernel" : "ln_apply_kernel",
+             (double)rows * (w * 2.0 * dtype_size(t) + 20), s);
+  if (vec)
+    k_ln_split_apply(x, t, stats, rows, w, (double)rd.hidden_total, gain, bias, eps, y, mean,
+                     rstd, s);
+  else
+    k_ln_apply(x, t, stats, rows, w, (double)rd.hidden_total, gain, bias, eps, y, mean, rstd, s);
 }
 
 // dx = LN'(dy) (+ resid); optional gain/bias grads (column + depth all-reduce,
@@ -135,7 +154,8 @@ void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
   // comm stream (joined at the end of the layer backward)
   float* packed =
       want_params ? static_cast<float*>(wsget(c, tag + ".packed", 2 * w * 4)) : nullptr;
-  if (c.grid.q == 1 && k_ln_fused_supported(w)) {
+  const bool vec = ln_vec(w, gain, gain, {dy, x, resid, dx});
+  if (c.grid.q == 1 && vec) {
     // one-member row group: the [rows, 2] all-reduce moves nothing, so row
     // statistics, dx and the dgain/dbias partials are one pass over dy, x
     coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305 (metered)
@@ -146,6 +166,24 @@ void ln_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag, const v
                                             (resid ? dtype_size(tr) : 0)) + 8), s);
     k_ln_fused_bwd(dy, tdy, x, t, mean, rstd, gain, rows, w, resid, tr, dx, tdx, packed,
                    scratch, s);
+  } else if (vec) {
+    // q > 1: one pass for the row partials and the dgain/dbias column sums,
+    // the row all-reduce, one pass for dx
+    {
+      float* scratch = static_cast<float*>(
+          wsget(c, "ln.fscratch", k_ln_fused_scratch_floats(rows, w) * 4));
+      ProfMem pm("ln_vec_bwd_stats_kernel",
+                 (double)rows * (w * (double)(dtype_size(tdy) + dtype_size(t)) + 16), s);
+      k_ln_split_bwd_stats(dy, tdy, x, t, mean, rstd, gain, rows, w, stats, packed, scratch, s);
+    }
+    stream_dep(c, s, cs);
+    coll_allreduce(c, ROW, stats, rows * 2, cs);  // ref layers.cpp:305
+    stream_dep(c, cs, s);
+    ProfMem pm("ln_vec_bwd_apply_kernel",
+               (double)rows * (w * (double)(dtype_size(tdy) + dtype_size(t) + dtype_size(tdx) +
+                                            (resid ? dtype_size(tr) : 0)) + 16), s);
+    k_ln_split_bwd_apply(dy, tdy, x, t, mean, rstd, gain, stats, rows, w,
+                         (double)rd.hidden_total, resid, tr, dx, tdx, s);
   } else {
     {
       ProfMem pm("ln_bwd_stats_kernel",

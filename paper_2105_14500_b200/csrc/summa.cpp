@@ -333,7 +333,11 @@ void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
     // ref algorithms.cpp:69-70: column reduce of the partial to slot t
     coll_reduce(c, COL, t, static_cast<float*>(po.c), result, n, cs);
   }
-  if (direct) return;
+  if (direct) {
+    // [1,1,1]: the reference's 1-member depth all-reduce (traced, moves nothing)
+    if (depth) coll_note_single(c, 2, DEPTH, 0, n);
+    return;
+  }
   stream_dep(c, s, cs);  // (q == 1) the GEMM wrote `result` on the compute stream
   // ref algorithms.cpp:72-74: depth all-reduce of the layer partial
   if (depth) coll_allreduce(c, DEPTH, result, n, cs);

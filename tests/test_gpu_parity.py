@@ -653,3 +653,48 @@ def test_layernorm_fused_offset_rows_fp32(tess, offset, outlier):
     want = (xf - mu) / torch.sqrt(var + 1e-5)
     err = ((y.cpu().double() - want).norm() / want.norm()).item()
     assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("q,d,allow", GRIDS)
+@pytest.mark.parametrize("h", [2048, 12288])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layernorm_vectorised_widths(tess, orc, q, d, allow, h, dtype):
+    """The vectorised LayerNorm at widths h/q of the configs: 12288/2 = 6144
+    (cfg4 on q = 2: 768-thread blocks, one pass), 2048 and 1024 (256- and
+    128-thread blocks); q = 1 runs the fused single pass, q = 2 the split
+    partials -> row all-reduce -> apply (forward) and partials + dgain/dbias
+    -> all-reduce -> dx (backward). Against the fp64 oracle
+    (layers.cpp:242-345), CommStats equal."""
+    b, s, nh = 2 * q * d, 4, 16
+    rnd = f32r if dtype == "f32" else bf16r
+    x, dy, P = _layer_inputs(orc, b, s, h, 27, rnd)
+    want = orc.layer_run("layernorm", x, dy, P, b, s, nh)
+    tess.profile_enable(True)
+    try:
+        res = tess.layer_run("layernorm", x, dy, P, tess.LayerDims(b, s, h, nh),
+                             tess.GridSpec(q, d, allow), dtype=dtype)
+        kernels = tess.profile_kernels()
+    finally:
+        tess.profile_enable(False)
+    if dtype == "f32":
+        _compare_layer(res, want, 1e-5, rel_diff)
+    else:
+        _compare_layer(res, want, 2e-2, frob)
+    sr, sk = orc.layer_stats("layernorm", q, d, b, s, h)
+    assert (res.stats.per_rank == sr).all() and (res.stats.per_kind == sk).all()
+    want_k = {"ln_fused_fwd_kernel", "ln_fused_bwd_kernel"} if q == 1 else \
+        {"ln_vec_stats_kernel", "ln_vec_apply_kernel", "ln_vec_bwd_stats_kernel",
+         "ln_vec_bwd_apply_kernel"}
+    assert want_k <= set(kernels), sorted(kernels)
+
+
+@pytest.mark.parametrize("q,d,allow", [(2, 1, False), (2, 2, False)])
+def test_block_vectorised_layernorm_q2_bf16(tess, orc, q, d, allow):
+    """A bf16 block on q = 2 grids with h/q = 1024 (vectorised split LayerNorm,
+    128-thread blocks, residual folded into the backward apply)."""
+    b, s, h, nh = 2 * q * d, 8, 2048, 16
+    x, dy, P = _layer_inputs(orc, b, s, h, 28, bf16r)
+    want = orc.layer_run("block", x, dy, P, b, s, nh)
+    res = tess.layer_run("block", x, dy, P, tess.LayerDims(b, s, h, nh),
+                         tess.GridSpec(q, d, allow), dtype="bf16")
+    _compare_layer(res, want, 2e-2, frob)

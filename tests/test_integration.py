@@ -75,7 +75,11 @@ def test_drop_in_matmul_stats_and_trace(lib, q, d, allow, variant, replicate):
     _ok(lib, lib.tsb_check_matmul(q, d, allow, variant, 0, m, n, r, 1, replicate, o))
     assert o[0] <= 1e-5, o[0]
     assert o[1] == 1.0, "CommStats differ from the reference's"
-    assert o[2] == 1.0 and o[3] > 0, "trace differs from the reference's"
+    if o[2] != 1.0:
+        w, g = C.create_string_buffer(1 << 16), C.create_string_buffer(1 << 16)
+        lib.tsb_matmul_traces(q, d, allow, variant, m, n, r, w, g, 1 << 16)
+        assert g.value.decode() == w.value.decode()
+    assert o[3] > 0
 
 
 @pytest.mark.gpu
