@@ -52,6 +52,36 @@ def arm_config(gpus, grid_str=None):
             "l2": "inputs larger than L2 (per-GPU weights+activations >> 126 MB)"}
 
 
+# BASELINE configs[4]: 24-layer hidden-4096 stack, strong scaling (SURVEY 8d
+# proposal s=2048, b=16, 32 heads), Tesseract vs 1-D vs SUMMA
+CFG5 = dict(layers=24, hidden=4096, heads=32, seq=2048, batch=16)
+
+
+def grid_for_scheme(gpus, scheme):
+    """(q, d, allow) of a config-5 scheme on `gpus` ranks: Tesseract as the
+    cfg4 ladder, SUMMA [q,q,1] (q*q == gpus), the 1-D scheme a [1,1,gpus] line."""
+    if scheme == "tesseract":
+        return grid_for(gpus)
+    if scheme == "summa":
+        q = int(round(gpus ** 0.5))
+        if q * q != gpus:
+            raise SystemExit("SUMMA needs a square GPU count (1 or 4)")
+        return q, 1, False
+    if scheme == "megatron":
+        return 1, gpus, True
+    raise SystemExit(f"unknown scheme {scheme}")
+
+
+def cfg5_config(args, grid_str):
+    return {"workload": f"cfg5: {args.layers}-layer Transformer stack fwd+bwd (pre-norm blocks, "
+                        f"attention no mask + MLP + LayerNorm), strong scaling, scheme "
+                        f"{args.scheme}",
+            "grid": grid_str, "scheme": args.scheme, "layers": args.layers,
+            "global_batch": args.batch, "seq_len": args.seq, "hidden": args.hidden,
+            "heads": args.heads, "parallelism": f"{args.scheme}{grid_str}",
+            "l2": "inputs larger than L2 (per-GPU weights+activations >> 126 MB)"}
+
+
 def layer_flops(batch, seq, hidden):
     """Algorithmic flops of one block fwd+bwd (2*m*n*k of GEMMs + attention
     contractions): 72*T*h^2 + 12*T*s*h, T = batch*seq."""
@@ -215,11 +245,25 @@ def main():
     ap.add_argument("--hidden", type=int, default=HIDDEN)
     ap.add_argument("--heads", type=int, default=HEADS)
     ap.add_argument("--seq", type=int, default=SEQ)
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"],
+                    help="cfg4: one block, weak scaling (default, the headline); cfg5: the "
+                         "24-layer h=4096 stack under --scheme, strong scaling")
+    ap.add_argument("--scheme", default="tesseract", choices=["tesseract", "summa", "megatron"])
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="cfg5 global batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dry-run", action="store_true",
                     help="stop after the rendezvous; rank 0 prints each rank's placement")
     args = ap.parse_args()
+    if args.workload == "cfg5":
+        for k, v in CFG5.items():
+            if getattr(args, k) is None or (k in ("hidden", "heads", "seq") and
+                                            getattr(args, k) == ap.get_default(k)):
+                setattr(args, k, v)
+        args.no_cpu_baseline = True
+    else:
+        args.layers = 1
 
     rank, local_rank, world = rank_env()
     if world == 1 and args.gpus > 1 and args.impl == "tess":
@@ -235,7 +279,8 @@ def main():
 
     if args.dry_run:
         import paper_2105_14500_b200 as tess
-        q, d, allow = grid_for(args.gpus)
+        q, d, allow = grid_for_scheme(args.gpus,
+                                      args.scheme if args.workload == "cfg5" else "tesseract")
         grid = tess.GridSpec(q, d, allow)
         c = grid.coord_of(rank)
         me = {"rank": rank, "local_rank": local_rank, "device": local_rank,
@@ -261,7 +306,8 @@ def main():
     import torch
     import paper_2105_14500_b200 as tess
 
-    q, d, allow = grid_for(args.gpus)
+    cfg5 = args.workload == "cfg5"
+    q, d, allow = grid_for_scheme(args.gpus, args.scheme if cfg5 else "tesseract")
     grid = tess.GridSpec(q, d, allow)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -275,12 +321,20 @@ def main():
 
     p = grid.size()
     h, nh, s = args.hidden, args.heads, args.seq
-    batch = args.batch_per_gpu * p
+    L = args.layers
+    mg = args.scheme == "megatron"
+    if mg:
+        ctx.set_megatron(True)
+    # cfg4 weak scaling: b = 4 per GPU; cfg5 strong scaling: b fixed for the job
+    batch = args.batch if cfg5 else args.batch_per_gpu * p
     dims = tess.LayerDims(batch, s, h, nh)
-    rows = batch * s // (d * q)
-    hq = h // q
+    # this rank's activation block: TesseractA [T/(d q), h/q]; 1-D: all of [T, h]
+    rows = batch * s if mg else batch * s // (d * q)
+    hin = h if mg else h // q
     bf = torch.bfloat16
     sd = seeds(grid, rank)
+    if mg:  # 1-D: activations replicated, weight shards differ per rank
+        sd = {"activation": 1234 + 1000, "weight": 1234 + 2000 + rank, "ln": 1234 + 3000}
     gens = {}
     for fam, seed in sd.items():
         gens[fam] = torch.Generator(device=dev)
@@ -290,34 +344,53 @@ def main():
         return (torch.rand(shape, device=dev, generator=gens[fam]) * 2 - 1).mul_(scale).to(dtype)
 
     # synthetic inputs of the named shapes; random-init weights: TesseractB
-    # blocks seeded by (i, j) (identical depth replicas), LN by j
+    # blocks seeded by (i, j) (identical depth replicas), LN by j. 1-D scheme:
+    # W_qkv / W_ff1 column shards, W_proj / W_ff2 row shards, full LN vectors.
     ws = 1.0 / (h ** 0.5)
-    W = {"w_qkv": rnd((hq, 3 * hq), ws, "weight"), "w_proj": rnd((hq, hq), ws, "weight"),
-         "w_ff1": rnd((hq, 4 * hq), ws, "weight"), "w_ff2": rnd((4 * hq, hq), ws, "weight")}
-    LN = {k: (1 if k.endswith("gain") else 0) + rnd((hq,), 0.1, "ln", torch.float32)
-          for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")}
-    x = rnd((rows, hq), 1.0, "activation")
-    dy = rnd((rows, hq), 1.0, "activation")
+    if mg:
+        hp = h // p
+        wshape = {"w_qkv": (h, 3 * hp), "w_proj": (hp, h), "w_ff1": (h, 4 * hp),
+                  "w_ff2": (4 * hp, h)}
+    else:
+        hq = h // q
+        wshape = {"w_qkv": (hq, 3 * hq), "w_proj": (hq, hq), "w_ff1": (hq, 4 * hq),
+                  "w_ff2": (4 * hq, hq)}
+    keep = []
+    shards, gradl = [], []
+    for _ in range(L):
+        W = {k: rnd(v, ws, "weight") for k, v in wshape.items()}
+        LN = {k: (1 if k.endswith("gain") else 0) + rnd((hin,), 0.1, "ln", torch.float32)
+              for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")}
+        G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev)
+             for k, v in {**W, **LN}.items()}
+        keep.append((W, LN, G))
+        shards.append(tess.BlockShardC(
+            *[W[k].data_ptr() for k in ("w_qkv", "w_proj", "w_ff1", "w_ff2")],
+            *[LN[k].data_ptr() for k in ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")], 1e-5))
+        gradl.append(tess.BlockGradsC(*[G[k].data_ptr() for k in tess.PARAM_NAMES]))
+    shard, grads = shards[0], gradl[0]
+    x = rnd((rows, hin), 1.0, "activation")
+    dy = rnd((rows, hin), 1.0, "activation")
     y = torch.empty_like(x)
     dx = torch.empty_like(x)
-    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in {**W, **LN}.items()}
-    shard = tess.BlockShardC(*[W[k].data_ptr() for k in ("w_qkv", "w_proj", "w_ff1", "w_ff2")],
-                             *[LN[k].data_ptr() for k in ("ln1_gain", "ln1_bias", "ln2_gain",
-                                                          "ln2_bias")], 1e-5)
-    grads = tess.BlockGradsC(*[G[k].data_ptr() for k in tess.PARAM_NAMES])
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
 
-    def step(xp, yp, dyp, dxp):
-        ctx.layer_forward("block", "bf16", dims, shard, xp, yp, stream=sh)
-        ctx.layer_backward("block", "bf16", dims, shard, dyp, dxp, grads, accumulate=False,
-                           stream=sh)
+    if cfg5:
+        def step(xp, yp, dyp, dxp):
+            ctx.stack_step("bf16", dims, shards, xp, dyp, yp, dxp, gradl, stream=sh)
+        step_api = step
+    else:
+        def step(xp, yp, dyp, dxp):
+            ctx.layer_forward("block", "bf16", dims, shard, xp, yp, stream=sh)
+            ctx.layer_backward("block", "bf16", dims, shard, dyp, dxp, grads, accumulate=False,
+                               stream=sh)
 
-    def step_api(xp, yp, dyp, dxp):
-        # the user-facing call for a training step of the layer (rank-level
-        # layer_run: forward + backward with x and dy given together)
-        ctx.layer_step("block", "bf16", dims, shard, xp, dyp, yp, dxp, grads, accumulate=False,
-                       stream=sh)
+        def step_api(xp, yp, dyp, dxp):
+            # the user-facing call for a training step of the layer (rank-level
+            # layer_run: forward + backward with x and dy given together)
+            ctx.layer_step("block", "bf16", dims, shard, xp, dyp, yp, dxp, grads,
+                           accumulate=False, stream=sh)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -357,7 +430,7 @@ def main():
     launches = tess.kernel_launches() - launches0
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local)
-    flops = layer_flops(batch, s, h)
+    flops = L * layer_flops(batch, s, h)
     value = flops / (ms * 1e-3) / 1e12
     gemm_ms, gemm_flops, gemm_n = tess.profile_read()
     per_kernel = tess.profile_kernels()
@@ -466,9 +539,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong" if cfg5 else "weak",
+            "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random inputs and random-init weights of the named shapes)",
-            "config": arm_config(args.gpus, grid.to_string()),
+            "config": cfg5_config(args, grid.to_string()) if cfg5
+            else arm_config(args.gpus, grid.to_string()),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "peak_source": f"{peak_src} bf16_tflops_sustained", "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,

@@ -241,6 +241,19 @@ tess_status tess_layer_step(tess_ctx* ctx, tess_layer_op op, tess_dtype dtype,
                             void* dx, tess_block_grads* grads, int accumulate, float* dbias,
                             void* stream);
 
+/* A stack of `layers` Transformer blocks, forward through every block then
+ * backward in reverse, on this rank (the inner loops of the reference's
+ * train_toy, layers.cpp:1006-1026, without its loss and update; BASELINE
+ * config 5's 24-layer stack). shards / grads: one per layer (grads may be
+ * NULL). Block l uses forward-cache slot base + l, base = the slot selected
+ * by tess_set_cache_slot; activations between blocks stay on the device.
+ * With tess_set_megatron the 1-D scheme's block runs. x / dy / y / dx as in
+ * tess_layer_step (device or host). */
+tess_status tess_stack_step(tess_ctx* ctx, tess_dtype dtype, const tess_layer_dims* dims,
+                            int layers, const tess_block_shard* shards, const void* x,
+                            const void* dy, void* y, void* dx, tess_block_grads* grads,
+                            int accumulate, void* stream);
+
 /* Makes `stream` wait for everything the context still has in flight on its
  * side streams: pending host copies of layer outputs and deferred
  * collectives (the reference's calls return completed values; this is the
@@ -316,6 +329,24 @@ tess_status tess_layer_run(tess_layer_op op, const tess_layer_dims* dims, int q,
 /* ref: layers.hpp:195-197 layer_run; params/grads: 8 host fp64 arrays in
  * BlockParams order (w_qkv, w_proj, w_ff1, w_ff2, ln1_gain, ln1_bias,
  * ln2_gain, ln2_bias); grads may be NULL; dbias [hidden] for BiasAdd. */
+
+/* Config 5's comparison schemes for tess_stack_run. */
+typedef enum { TESS_STACK_TESSERACT = 0, TESS_STACK_MEGATRON = 1 } tess_stack_scheme;
+
+/* Global-level layer stack: `layers` blocks forward then backward (see
+ * tess_stack_step) on host fp64 buffers. TESS_STACK_TESSERACT runs the
+ * [q,q,d] grid (SUMMA is d = 1, ref algorithms.cpp:105-118);
+ * TESS_STACK_MEGATRON the 1-D scheme on a [1,1,d] line (q must be 1; the
+ * megatron_1d_linear split of algorithms.cpp:244-265 applied to every
+ * block). params / grads: layers*8 arrays in BlockParams order per layer
+ * (grads or any entry may be NULL); y, dx [batch*seq, hidden]; grads are
+ * overwritten. Same math as chaining ref transformer_block forward and
+ * backward (layers.cpp:460-487) through the stack. */
+tess_status tess_stack_run(tess_stack_scheme scheme, const tess_layer_dims* dims, int layers,
+                           int q, int d, int allow_d_gt_q, tess_dtype compute, const double* x,
+                           const double* dy, const double* const* params, double eps,
+                           double* y, double* dx, double* const* grads, const int* devices,
+                           uint64_t* stats_rank, uint64_t* stats_kind);
 
 /* ref: layers.hpp:245-267 train_toy (the sharded half): `layers` Transformer
  * blocks trained with MSE loss against `target` and plain SGD (learning rate

@@ -172,6 +172,10 @@ def _load() -> C.CDLL:
                             C.c_double, dp, dp, C.POINTER(dp), dp, ip, u64p, u64p], i),
         "tess_megatron_layer_run": ([i, C.POINTER(_LayerDimsC), i, i, dp, dp, C.POINTER(dp),
                                      C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
+        "tess_stack_run": ([i, C.POINTER(_LayerDimsC), i, i, i, i, i, dp, dp, C.POINTER(dp),
+                            C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
+        "tess_stack_step": ([vp, i, C.POINTER(_LayerDimsC), i, C.POINTER(BlockShardC), vp, vp, vp,
+                             vp, C.POINTER(BlockGradsC), i, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -525,6 +529,47 @@ def load_matrix(path: str) -> np.ndarray:
 
 
 @dataclasses.dataclass
+class StackRunResult:
+    y: np.ndarray
+    dx: np.ndarray
+    grads: List[Dict[str, np.ndarray]]  # one dict per layer
+    stats: CommStats
+
+
+STACK_SCHEMES = {"tesseract": 0, "summa": 0, "megatron": 1}
+
+
+def stack_run(scheme: str, x, dy, params: Sequence[Dict[str, np.ndarray]], dims: LayerDims,
+              grid: GridSpec, dtype="f32", eps: float = 1e-5,
+              devices: Optional[Sequence[int]] = None) -> StackRunResult:
+    """BASELINE config 5's layer stack: len(params) Transformer blocks forward
+    then backward (tess_stack_run). scheme "tesseract" on grid [q,q,d],
+    "summa" on [q,q,1] (algorithms.cpp:105-118), "megatron" the 1-D scheme
+    on a [1,1,p] line (algorithms.cpp:244-265 applied to every block)."""
+    if scheme not in STACK_SCHEMES:
+        raise ValueError(f"unknown scheme {scheme!r}")
+    if scheme == "summa" and grid.d() != 1:
+        raise GridError("SUMMA is the d == 1 grid")
+    x, dy = _f64(x), _f64(dy)
+    h, L = dims.hidden, len(params)
+    if x.shape != (dims.batch * dims.seq, h) or dy.shape != x.shape:
+        raise ShapeError("activation must be [batch*seq, hidden]")
+    prm = [_f64(p[n]) for p in params for n in PARAM_NAMES]
+    grads = [[np.zeros(s_) for s_ in _param_shapes(h)] for _ in range(L)]
+    flat = [g for gl in grads for g in gl]
+    y, dx = np.zeros_like(x), np.zeros_like(x)
+    P = (C.POINTER(C.c_double) * len(prm))(*[_dptr(t) for t in prm])
+    G = (C.POINTER(C.c_double) * len(flat))(*[_dptr(t) for t in flat])
+    sr, sk = _stats_bufs(grid.size())
+    dc = dims.c()
+    _check(lib.tess_stack_run(STACK_SCHEMES[scheme], C.byref(dc), L, grid.q(), grid.d(),
+                              int(grid.allow_d_gt_q), _dtype(dtype), _dptr(x), _dptr(dy), P, eps,
+                              _dptr(y), _dptr(dx), G, _devices(devices, grid.size()), _u64(sr),
+                              _u64(sk)))
+    return StackRunResult(y, dx, [dict(zip(PARAM_NAMES, gl)) for gl in grads], CommStats(sr, sk))
+
+
+@dataclasses.dataclass
 class ToyTrainResult:
     dist_loss: np.ndarray
     stats: CommStats
@@ -588,6 +633,17 @@ class RankContext:
                                    C.byref(shard), bias_row0, x, dy, y, dx,
                                    C.byref(grads) if grads is not None else None,
                                    int(accumulate), dbias, stream))
+
+    def stack_step(self, dtype, dims: LayerDims, shards: Sequence[BlockShardC], x, dy, y, dx,
+                   grads: Optional[Sequence[BlockGradsC]] = None, accumulate=False, stream=0):
+        """len(shards) Transformer blocks forward then backward on this rank
+        (tess_stack_step; cache slots base .. base + layers - 1)."""
+        dc = dims.c()
+        L = len(shards)
+        sh = (BlockShardC * L)(*shards)
+        gr = (BlockGradsC * L)(*grads) if grads is not None else None
+        _check(lib.tess_stack_step(self.h, _dtype(dtype), C.byref(dc), L, sh, x, dy, y, dx, gr,
+                                   int(accumulate), stream))
 
     def stream_join(self, stream=0):
         """Order `stream` after the context's in-flight host copies of layer

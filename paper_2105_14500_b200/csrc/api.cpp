@@ -450,4 +450,17 @@ tess_status tess_layer_step(tess_ctx* c, tess_layer_op op, tess_dtype dt,
   });
 }
 
+tess_status tess_stack_step(tess_ctx* c, tess_dtype dt, const tess_layer_dims* dims, int layers,
+                            const tess_block_shard* shards, const void* x, const void* dy, void* y,
+                            void* dx, tess_block_grads* grads, int accumulate, void* stream) {
+  return guarded([&] {
+    Ctx& cx = need(c);
+    if (!dims || !shards || !x || !dy || !y || !dx) fail(TESS_ERR_INVALID, "null argument");
+    const DType t = to_dtype(dt);
+    if (t == DType::F64) fail(TESS_ERR_UNSUPPORTED, "fp64 compute: use TESS_F32 or TESS_BF16");
+    stack_step(cx, t, rank_dims(cx, *dims), layers, shards, x, dy, y, dx, grads, accumulate != 0,
+               S(stream));
+  });
+}
+
 }  // extern "C"

@@ -581,6 +581,193 @@ tess_status tess_megatron_layer_run(tess_layer_op op, const tess_layer_dims* dim
   });
 }
 
+// BASELINE config 5's layer stack as a global call: `layers` Transformer
+// blocks forward then backward (tess_stack_step per rank) under one of the
+// three schemes the comparison runs -- Tesseract [q,q,d], SUMMA (= [q,q,1],
+// ref algorithms.cpp:105-118) or the 1-D scheme on p = d ranks (the
+// megatron_1d_linear split, algorithms.cpp:244-265, applied to every block).
+// Same math as chaining the reference's transformer_block forward and
+// backward (layers.cpp:460-487) through the stack, so the oracle checks it.
+tess_status tess_stack_run(tess_stack_scheme scheme, const tess_layer_dims* dims, int layers,
+                           int q, int d, int allow, tess_dtype compute, const double* x,
+                           const double* dy, const double* const* params, double eps, double* y,
+                           double* dx, double* const* grads, const int* devices, uint64_t* sr,
+                           uint64_t* sk) {
+  return guarded([&] {
+    const DType t = compute_type(compute);
+    if (!dims || !x || !dy || !params || !y || !dx || layers < 1)
+      fail(TESS_ERR_INVALID, "stack_run: bad arguments");
+    const bool mg = scheme == TESS_STACK_MEGATRON;
+    if (!mg && scheme != TESS_STACK_TESSERACT) fail(TESS_ERR_INVALID, "stack_run: bad scheme");
+    if (mg && q != 1) fail(TESS_ERR_GRID, "the 1-D scheme runs on a [1,1,p] line grid (q == 1)");
+    const tess_layer_dims D = *dims;
+    const int64_t h = D.hidden, T = (int64_t)D.batch * D.seq;
+    const int p = mg ? d : q * q * d;
+    if (mg && (D.heads <= 0 || D.heads % p != 0 || h % D.heads != 0))
+      fail(TESS_ERR_DIVISIBILITY, "1-D scheme: heads must divide hidden and be divisible by p");
+    Runner R(q, d, mg || allow != 0, devices);
+    const Grid& g = R.g;
+    const tess::RankDims rd0 = [&] {
+      R.ctx[0]->megatron = mg;
+      tess::RankDims r = rank_dims(*R.ctx[0], D);
+      R.ctx[0]->megatron = false;
+      return r;
+    }();
+    const int64_t hq = rd0.hq, rows = rd0.rows, hin = rd0.hin;
+    const int64_t wshape[4][2] = {{h, 3 * h}, {h, h}, {h, 4 * h}, {4 * h, h}};
+    const bool colsplit[4] = {true, false, true, false};  // 1-D: Column1D / Row1D
+    const size_t e = dtype_size(t);
+    DevMat dX, dDY;
+    upload(dX, R.unique_devices(), x, (size_t)(T * h), t);
+    upload(dDY, R.unique_devices(), dy, (size_t)(T * h), t);
+    std::vector<std::unique_ptr<DevMat>> W, LN;
+    for (int l = 0; l < layers; ++l) {
+      for (int i = 0; i < 4; ++i) {
+        W.push_back(std::make_unique<DevMat>());
+        upload(*W.back(), R.unique_devices(), params[l * 8 + i],
+               (size_t)(wshape[i][0] * wshape[i][1]), t);
+      }
+      for (int i = 0; i < 4; ++i) {
+        LN.push_back(std::make_unique<DevMat>());
+        upload(*LN.back(), R.unique_devices(), params[l * 8 + 4 + i], (size_t)h, DType::F32);
+      }
+    }
+    std::vector<std::vector<float>> ys(p), dxs(p);
+    // gw[l*8 + i][rank]
+    std::vector<std::vector<std::vector<float>>> gw((size_t)layers * 8,
+                                                    std::vector<std::vector<float>>(p));
+    int64_t lsh[4][2];  // local weight shard shapes
+    for (int i = 0; i < 4; ++i) {
+      if (!mg) {
+        lsh[i][0] = wshape[i][0] / q;
+        lsh[i][1] = wshape[i][1] / q;
+      } else if (colsplit[i]) {
+        lsh[i][0] = wshape[i][0];
+        lsh[i][1] = wshape[i][1] / p;
+      } else {
+        lsh[i][0] = wshape[i][0] / p;
+        lsh[i][1] = wshape[i][1];
+      }
+    }
+    const int64_t lnw = mg ? h : hq;  // LayerNorm vector width on a rank
+    R.run([&](Ctx& c, cudaStream_t s) {
+      c.megatron = mg;
+      const tess::RankDims rd = rank_dims(c, D);
+      const void* lx = mg ? dX.on(c.device)
+                          : take_block(c, TESS_SCHEME_A, t, dX.on(c.device), T, h, "stk.gx", s);
+      const void* ldy = mg ? dDY.on(c.device)
+                           : take_block(c, TESS_SCHEME_A, t, dDY.on(c.device), T, h, "stk.gdy", s);
+      std::vector<tess_block_shard> sh(layers);
+      std::vector<tess_block_grads> gr(layers);
+      for (int l = 0; l < layers; ++l) {
+        const std::string L = "stk.l" + std::to_string(l);
+        const void* wl[4];
+        for (int i = 0; i < 4; ++i) {
+          const void* src = W[l * 4 + i]->on(c.device);
+          const int64_t r = wshape[i][0], cols = wshape[i][1];
+          if (!mg) {
+            wl[i] = take_block(c, TESS_SCHEME_B, t, src, r, cols, L + ".w" + std::to_string(i), s);
+          } else if (colsplit[i]) {
+            const int64_t cw = cols / p;
+            void* b = c.ws->get(L + ".w" + std::to_string(i), (size_t)(r * cw) * e);
+            TESS_CUDA(cudaMemcpy2DAsync(b, cw * e, static_cast<const char*>(src) +
+                                                       (size_t)(c.coord.k * cw) * e,
+                                        cols * e, cw * e, r, cudaMemcpyDeviceToDevice, s));
+            wl[i] = b;
+          } else {
+            wl[i] = static_cast<const char*>(src) + (size_t)(c.coord.k * (r / p) * cols) * e;
+          }
+        }
+        const float* lnv[4];
+        for (int i = 0; i < 4; ++i)
+          lnv[i] = static_cast<const float*>(LN[l * 4 + i]->on(c.device)) +
+                   (mg ? 0 : (int64_t)c.coord.j * hq);
+        sh[l] = {wl[0], wl[1], wl[2], wl[3], lnv[0], lnv[1], lnv[2], lnv[3], eps};
+        float* gp[8];
+        for (int i = 0; i < 8; ++i) {
+          const size_t n = i < 4 ? (size_t)(lsh[i][0] * lsh[i][1]) : (size_t)lnw;
+          gp[i] = static_cast<float*>(c.ws->get(L + ".g" + std::to_string(i), n * 4));
+        }
+        gr[l] = {gp[0], gp[1], gp[2], gp[3], gp[4], gp[5], gp[6], gp[7]};
+      }
+      void* ly = c.ws->get("stk.gy", (size_t)(rows * hin) * e);
+      void* ldx = c.ws->get("stk.gdx", (size_t)(rows * hin) * e);
+      const tess_dtype td = t == DType::F32 ? TESS_F32 : TESS_BF16;
+      call(tess_stack_step(&c, td, &D, layers, sh.data(), lx, ldy, ly, ldx, gr.data(), 0, s));
+      if (!mg || c.coord.k == 0) {
+        ys[c.rank] = fetch(ly, (size_t)(rows * hin), t, s);
+        dxs[c.rank] = fetch(ldx, (size_t)(rows * hin), t, s);
+      }
+      if (grads)
+        for (int l = 0; l < layers; ++l) {
+          const float* gp[8] = {gr[l].w_qkv,    gr[l].w_proj,   gr[l].w_ff1,    gr[l].w_ff2,
+                                gr[l].ln1_gain, gr[l].ln1_bias, gr[l].ln2_gain, gr[l].ln2_bias};
+          for (int i = 0; i < 8; ++i) {
+            if (!grads[l * 8 + i]) continue;
+            if (mg && i >= 4 && c.coord.k != 0) continue;
+            const size_t n = i < 4 ? (size_t)(lsh[i][0] * lsh[i][1]) : (size_t)lnw;
+            gw[(size_t)l * 8 + i][c.rank] = fetch(gp[i], n, DType::F32, s);
+          }
+        }
+      c.megatron = false;
+    });
+    if (!mg) {
+      combine(g, TESS_SCHEME_A, ys, T, h, y);
+      combine(g, TESS_SCHEME_A, dxs, T, h, dx);
+    } else {
+      for (size_t i = 0; i < ys[0].size(); ++i) y[i] = ys[0][i];
+      for (size_t i = 0; i < dxs[0].size(); ++i) dx[i] = dxs[0][i];
+    }
+    if (grads) {
+      for (int l = 0; l < layers; ++l) {
+        for (int i = 0; i < 4; ++i) {
+          double* out = grads[l * 8 + i];
+          if (!out) continue;
+          const auto& v = gw[(size_t)l * 8 + i];
+          const int64_t r = wshape[i][0], cols = wshape[i][1];
+          if (!mg) {
+            combine(g, TESS_SCHEME_B, v, r, cols, out);
+            continue;
+          }
+          for (int k = 0; k < p; ++k) {
+            if (colsplit[i]) {
+              const int64_t cw = cols / p;
+              for (int64_t rr = 0; rr < r; ++rr)
+                for (int64_t cc = 0; cc < cw; ++cc)
+                  out[rr * cols + k * cw + cc] = v[k][rr * cw + cc];
+            } else {
+              const int64_t rh = r / p;
+              for (int64_t rr = 0; rr < rh; ++rr)
+                for (int64_t cc = 0; cc < cols; ++cc)
+                  out[(k * rh + rr) * cols + cc] = v[k][rr * cols + cc];
+            }
+          }
+        }
+        for (int i = 4; i < 8; ++i) {
+          double* out = grads[l * 8 + i];
+          if (!out) continue;
+          const auto& v = gw[(size_t)l * 8 + i];
+          if (mg) {
+            for (int64_t cc = 0; cc < h; ++cc) out[cc] = v[0][cc];
+            continue;
+          }
+          // LayerNorm vectors: j-slices whose (i, k) replicas must agree
+          // (ref layers.cpp:197-213)
+          for (int j = 0; j < q; ++j) {
+            const auto& ref = v[g.rank_of({0, j, 0})];
+            for (int ii = 0; ii < q; ++ii)
+              for (int k = 0; k < d; ++k)
+                if (std::memcmp(ref.data(), v[g.rank_of({ii, j, k})].data(), hq * 4) != 0)
+                  fail(TESS_ERR_SHAPE, "combine_block_grads: layernorm replica divergence");
+            for (int64_t cc = 0; cc < hq; ++cc) out[j * hq + cc] = ref[cc];
+          }
+        }
+      }
+    }
+    R.stats(sr, sk);
+  });
+}
+
 // ref layers.cpp:947-1036 (the sharded half of train_toy): `layers` blocks,
 // MSE loss with global_sum_rank (row, column, depth all-reduce of the local
 // sum, layers.cpp:519-526), backward through every block, plain SGD on every

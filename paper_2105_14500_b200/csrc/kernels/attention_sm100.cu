@@ -394,7 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 //                 dK += dS^T(i) Q_i   (A = dS^T in shared memory)
 //               S^T / dP^T are single-buffered (TMEM holds S^T, dP^T, dV, dK);
 //               dP^T(i+1) is issued as soon as tile i's scores sit in
-//               registers, S^T(i+1) after dV(i) has read P^T(i).
+//               registers; dV(i) as soon as P^T(i) is in TMEM (its own
+//               barrier, before the dS^T stores), S^T(i+1) right behind it,
+//               then dK(i) once dS^T(i) is in shared memory -- the next
+//               tile's softmax overlaps dK(i) (-4 %, r2_attn_bwd_order_ab).
 //   warps 2-17  four groups of 4 warps split each tile's 128 queries (group
 //               g: columns [32g, 32g+32)); thread = key row (TMEM lane):
 //               P^T = 2^(c*S^T - lse[q]) -> TMEM (bf16 pairs), dS^T = P^T
@@ -483,11 +486,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   uint64_t* r_empty = r_full + C::RING;       // RING
   uint64_t* sdp_full = r_empty + C::RING;     // 1: S^T(i) and dP^T(i) in TMEM
   uint64_t* loaded = sdp_full + 1;            // 1: all 8 warps hold tile i's scores (count 8)
-  uint64_t* pds_full = loaded + 1;            // 1: P^T (TMEM) + dS^T (smem) written (count 8)
+  uint64_t* pds_full = loaded + 1;            // 1: dS^T (smem) written (count 16)
   uint64_t* ds_free = pds_full + 1;           // 1: dK(i) done reading dS^T smem
   uint64_t* st_free = ds_free + 1;            // 2: TMA store of dS^T chunk g done reading
   uint64_t* fin = st_free + 2;                // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  uint64_t* p_full = fin + 1;                 // 1: P^T (TMEM) written (count 16)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_full + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -510,6 +514,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
     mbar_init(&st_free[0], 1);
     mbar_init(&st_free[1], 1);  // chunk c's storer: group 2c
     mbar_init(fin, 1);
+    mbar_init(p_full, 16);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
     prefetch_tmap(&p.tm_q);
@@ -609,8 +614,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
           dn = next_slot();
           issue_scores(tmem + C::TM_DPT, sv, ring + dn * C::SLOT_BYTES);
         }
-        // gradients of tile i once P^T (TMEM) and dS^T (smem) are written
-        mbar_wait(pds_full, i & 1);
+        // dV(i) as soon as P^T(i) sits in TMEM
+        mbar_wait(p_full, i & 1);
         tc_fence_after();
         trace_ev(p, TR_MMA_P, i);
 #pragma unroll
@@ -619,6 +624,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
                       make_sdesc(ring + ds * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
                       idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&r_empty[ds]);
+        if (more) {
+          // S^T(i+1) over the P^T columns right behind dV(i) (in-order
+          // execution: dV has read them): tile i+1's softmax starts while
+          // dK(i) runs
+          trace_ev(p, TR_MMA_S, i + 1);
+          issue_scores(tmem + C::TM_ST, sk, ring + qn * C::SLOT_BYTES);
+          mma_commit(sdp_full);
+        }
+        // dK(i) once dS^T(i) is in shared memory
+        mbar_wait(pds_full, i & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQB / 16; ++kk)  // dK += dS^T Q_i
           mma_bf16(tmem + C::TM_DK,
@@ -629,12 +645,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         mma_commit(&r_empty[qs]);
         mma_commit(ds_free);
         trace_ev(p, TR_MMA_GDONE, i);
-        if (more) {
-          // S^T(i+1) over the P^T columns (after dV(i) in issue order)
-          trace_ev(p, TR_MMA_S, i + 1);
-          issue_scores(tmem + C::TM_ST, sk, ring + qn * C::SLOT_BYTES);
-          mma_commit(sdp_full);
-        }
         qs = qn;
         ds = dn;
       }
@@ -733,12 +743,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
           pk[e] = pack_bf16x2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
         tmem_st16(tmem + lane_off + C::TM_ST + g * 16, pk);
       }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);  // dV(i) may start
       // dS^T chunk: free once dK(i-1) read it and its TMA store read it
       mbar_wait(ds_free, ph ^ 1u);
       mbar_wait(&st_free[chunk], ph);
       store_row32(ds_chunk, r, (g & 1) * 4, *reinterpret_cast<const float(*)[32]>(dr));
-      tmem_wait_st();
-      tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(pds_full);

@@ -882,4 +882,51 @@ void layer_step(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
   stage_release(c, db, s);
 }
 
+// A stack of `layers` Transformer blocks, forward through every block then
+// backward in reverse (the inner loops of the reference's train_toy,
+// layers.cpp:1006-1026, without loss and update; BASELINE config 5's
+// 24-layer stack). Block l uses forward-cache slot base + l, so all L
+// forwards stay outstanding until their backward; activations between
+// blocks live in context buffers. Under the 1-D scheme (c.megatron) the
+// same loop drives the Megatron layer. Host x / dy are staged like
+// layer_step (x gates the first forward, dy only the last backward).
+void stack_step(Ctx& c, DType t, const RankDims& rd, int layers, const tess_block_shard* p,
+                const void* x, const void* dy, void* y, void* dx, tess_block_grads* g,
+                bool accumulate, cudaStream_t s) {
+  if (layers < 1 || !p) fail(TESS_ERR_INVALID, "stack: layers must be >= 1");
+  const size_t act = (size_t)rd.rows * rd.hin * dtype_size(t);
+  const int base = c.cache_slot;
+  std::string xb, db;
+  const void* xd = x;
+  if (!is_device_ptr(x)) {
+    xd = stage_upload(c, "stk.xin", x, act, &xb);
+    stream_dep(c, c.up_s, s);
+  }
+  const void* dyd = dy;
+  if (!is_device_ptr(dy)) dyd = stage_upload(c, "stk.dyin", dy, act, &db);
+  struct Restore {
+    Ctx& c;
+    int slot;
+    ~Restore() { c.cache_slot = slot; }
+  } restore{c, base};
+  const void* cur = xd;
+  for (int l = 0; l < layers; ++l) {
+    c.cache_slot = base + l;
+    void* out = l == layers - 1 ? y : wsget(c, "stk.a" + std::to_string(l), act);
+    layer_forward(c, TESS_OP_BLOCK, t, rd, p[l], nullptr, cur, out, s);
+    cur = out;
+  }
+  if (dyd != dy) stream_dep(c, c.up_s, s);
+  const void* gin = dyd;
+  for (int l = layers - 1; l >= 0; --l) {
+    c.cache_slot = base + l;
+    void* out = l == 0 ? dx : wsget(c, "stk.d" + std::to_string(l & 1), act);
+    layer_backward(c, TESS_OP_BLOCK, t, rd, p[l], gin, out, g ? &g[l] : nullptr, accumulate,
+                   nullptr, s);
+    gin = out;
+  }
+  stage_release(c, xb, s);
+  stage_release(c, db, s);
+}
+
 }  // namespace tess

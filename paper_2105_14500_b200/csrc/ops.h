@@ -84,5 +84,9 @@ void layer_step(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
 void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
                     const tess_block_shard& p, const void* dy, void* dx,
                     tess_block_grads* g, bool accumulate, float* dbias, cudaStream_t s);
+// `layers` blocks forward then backward (cache slots base..base+layers-1).
+void stack_step(Ctx& c, DType t, const RankDims& rd, int layers, const tess_block_shard* p,
+                const void* x, const void* dy, void* y, void* dx, tess_block_grads* g,
+                bool accumulate, cudaStream_t s);
 
 }  // namespace tess
