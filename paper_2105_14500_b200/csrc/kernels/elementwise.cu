@@ -7,6 +7,8 @@
 
 #include "../core.h"
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "kernels.h"
 
@@ -360,9 +362,14 @@ __device__ __forceinline__ void unpack8(const uint4 (&u)[2], float (&v)[8]) {
   v[6] = __uint_as_float(u[1].z); v[7] = __uint_as_float(u[1].w);
 }
 
-// Deterministic block sums of two values (fixed-order combine of warp sums).
+// Deterministic block sums of two values: warp butterflies, then the warps'
+// partials summed by one more butterfly over lanes [0, nw). Every thread
+// gets the same (bitwise) result: a butterfly combines v_l + v_(l^o), which
+// commutes. TH: compile-time block size (0 = blockDim.x).
+template <int TH>
 __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (TH ? TH : (int)blockDim.x) >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -371,21 +378,26 @@ __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
   __syncthreads();  // red is reused row after row
   if (lane == 0) red[warp] = make_float2(a, b);
   __syncthreads();
-  float2 t = make_float2(0.f, 0.f);
-  for (int w = 0; w < nw; ++w) {
-    t.x += red[w].x;
-    t.y += red[w].y;
+  float2 t = lane < nw ? red[lane] : make_float2(0.f, 0.f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+    t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
   }
   return t;
 }
 
-// Deterministic block (mean, M2) of equal-count per-thread partials by
-// Chan's pairwise combination: a butterfly over the warp (symmetric, so every
-// lane holds the same pair), then the warps' pairs in fixed order. No
-// E[x^2] - E[x]^2 anywhere, so a row whose mean is large against its spread
-// (or whose first element is an outlier) does not cancel.
+// Deterministic block (mean, M2) of equal-count (n) per-thread partials:
+// Chan's pairwise combination in a warp butterfly (symmetric, so every lane
+// holds the same pair), then across the nw warps the exact two-level form
+// mean = avg(m_w), M2 = sum M2_w + n_w sum (m_w - mean)^2, each sum a lane
+// butterfly -- no E[x^2] - E[x]^2 anywhere, so a row whose mean is large
+// against its spread (or an outlier element) does not cancel, and no
+// division sits in the per-row dependency chain.
+template <int TH>
 __device__ __forceinline__ float2 block_meanvar(float m, float M2, float n, float2* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (TH ? TH : (int)blockDim.x) >> 5;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const float mo = __shfl_xor_sync(0xffffffffu, m, o);
@@ -398,20 +410,20 @@ __device__ __forceinline__ float2 block_meanvar(float m, float M2, float n, floa
   __syncthreads();  // red is reused row after row
   if (lane == 0) red[warp] = make_float2(m, M2);
   __syncthreads();
-  float2 t = red[0];
-  float nt = n;
-  for (int w = 1; w < nw; ++w) {
-    const float dlt = red[w].x - t.x;
-    const float tot = nt + n;
-    t.y = t.y + red[w].y + dlt * dlt * (nt * n / tot);
-    t.x = t.x + dlt * (n / tot);
-    nt = tot;
-  }
-  return t;
+  const float2 w = lane < nw ? red[lane] : make_float2(0.f, 0.f);
+  float sm = w.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  const float mean = sm * (TH ? 1.0f / (float)(TH >> 5) : __frcp_rn((float)nw));
+  const float dl = lane < nw ? w.x - mean : 0.f;
+  float m2 = lane < nw ? fmaf(n * dl, dl, w.y) : 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+  return make_float2(mean, m2);
 }
 
 // Row mean / M2 of the register-resident slice (every thread gets the pair).
-template <int NV>
+template <int NV, int TH>
 __device__ __forceinline__ float2 row_meanvar(const float (&v)[NV][8], float2* red) {
   float s = 0.f;
 #pragma unroll
@@ -428,26 +440,28 @@ __device__ __forceinline__ float2 row_meanvar(const float (&v)[NV][8], float2* r
       const float d = v[k][e] - lm;
       m2 = fmaf(d, d, m2);
     }
-  return block_meanvar(lm, m2, kN, red);
+  return block_meanvar<TH>(lm, m2, kN, red);
 }
 
 // SPLIT = false: y = LN(x) with the row's own statistics (q == 1).
 // SPLIT = true: stats[3r..] = (sum x, M2, n mean^2) of the local columns, the
 // row group's all-reduce sums them (ln_vec_apply_kernel combines).
-template <typename T, int NV, bool SPLIT>
+// TH: compile-time block size (0 = blockDim.x; the launchers use 512 for
+// widths that are multiples of 4096, cfg4's 12288 among them).
+template <typename T, int NV, bool SPLIT, int TH>
 __global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_fwd_kernel(
     const T* __restrict__ x, int64_t rows, const float* __restrict__ gain,
     const float* __restrict__ bias, float eps, T* __restrict__ y, float* __restrict__ mean_out,
     float* __restrict__ rstd_out, float* __restrict__ stats) {
   __shared__ float2 red[32];
-  const int span = blockDim.x * 8;
+  const int span = (TH ? TH : (int)blockDim.x) * 8;
   const int w = NV * span;
   const int c0 = threadIdx.x * 8;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     float v[NV][8];
 #pragma unroll
     for (int k = 0; k < NV; ++k) ld8(x + r * w + c0 + k * span, v[k]);
-    const float2 t = row_meanvar<NV>(v, red);
+    const float2 t = row_meanvar<NV, TH>(v, red);
     if (SPLIT) {
       if (threadIdx.x == 0) {
         stats[3 * r + 0] = t.x * (float)w;
@@ -515,14 +529,14 @@ __global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_apply_ke
 // columns (ln_vec_bwd_apply_kernel finishes after the row all-reduce). Both
 // add this block's dgain = sum dy*xhat, dbias = sum dy column partials to
 // part[block][2][w] (summed over blocks in fixed order afterwards).
-template <typename TD, typename TX, typename TR, typename TO, int NV, bool SPLIT>
+template <typename TD, typename TX, typename TR, typename TO, int NV, bool SPLIT, int TH>
 __global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_bwd_kernel(
     const TD* __restrict__ dy, const TX* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ gain, int64_t rows,
     const TR* __restrict__ resid, TO* __restrict__ dx, float* __restrict__ part,
     float* __restrict__ stats) {
   __shared__ float2 red[32];
-  const int span = blockDim.x * 8;
+  const int span = (TH ? TH : (int)blockDim.x) * 8;
   const int w = NV * span;
   const int c0 = threadIdx.x * 8;
   float dg[NV][8], db[NV][8];  // gain is re-read per row (L1-resident) to save registers
@@ -561,7 +575,7 @@ __global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_bwd_kern
         d[k][e] = dxh;  // only dy * gain is needed from here on
       }
     }
-    const float2 t = block_sum2(a, b, red);
+    const float2 t = block_sum2<TH>(a, b, red);
     if (SPLIT) {
       if (threadIdx.x == 0) {
         stats[2 * r] = t.x;
@@ -1094,7 +1108,8 @@ bool ln_vec_ok(int64_t w, std::initializer_list<const void*> ptrs) {
 }
 
 // Blocks: up to 2048 resident threads per SM; the backward (whose blocks
-// each write a [2, w] dgain/dbias partial) at most 2 blocks per SM.
+// each write a [2, w] dgain/dbias partial) at most 2 blocks per SM. Upper
+// bound for the partial scratch; the launch grid is the resident count.
 int ln_vec_blocks(int64_t rows, int threads, int per_sm_cap) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1103,6 +1118,39 @@ int ln_vec_blocks(int64_t rows, int threads, int per_sm_cap) {
   const int64_t b = std::min<int64_t>(rows, (int64_t)sms * per_sm);
   return (int)std::max<int64_t>(b, 1);
 }
+
+// Grid of a row-looping LayerNorm kernel: the blocks that are resident at
+// once (registers bound the 512-thread blocks to 1-2 per SM), capped by
+// per_sm_cap and rows -- a second partial wave of blocks would run its rows
+// after the first wave instead of beside it.
+int ln_grid(const void* fn, int threads, int64_t rows, int per_sm_cap) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> occ;
+  int per = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ.find({fn, threads});
+    if (it == occ.end()) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0) != cudaSuccess) {
+        cudaGetLastError();
+        per = 1;
+      }
+      occ[{fn, threads}] = per;
+    } else {
+      per = it->second;
+    }
+  }
+  return ln_vec_blocks(rows, threads, std::max(1, std::min(per, per_sm_cap)));
+}
+
+#define TESS_LN_TH(threads, ...)                                                   \
+  if ((threads) == 512) {                                                          \
+    constexpr int TH = 512;                                                        \
+    __VA_ARGS__;                                                                   \
+  } else {                                                                         \
+    constexpr int TH = 0;                                                          \
+    __VA_ARGS__;                                                                   \
+  }
 
 bool k_ln_fused_supported(int64_t w) { return ln_vec_config(w).nv > 0; }
 
@@ -1125,10 +1173,12 @@ void k_ln_fused_fwd(const void* x, DType t, int64_t rows, int64_t w, const float
                     cudaStream_t s) {
   if (!rows) return;
   const LnCfg c = ln_vec_config(w);
-  const int g = ln_vec_blocks(rows, c.threads, 4);
-  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, ln_vec_fwd_kernel<T, NV, false><<<g, c.threads, 0, s>>>(
-                                           (const T*)x, rows, gain, bias, (float)eps, (T*)y,
-                                           mean, rstd, nullptr)));
+  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, TESS_LN_TH(c.threads, {
+    auto* k = ln_vec_fwd_kernel<T, NV, false, TH>;
+    const int g = ln_grid((const void*)k, c.threads, rows, 4);
+    k<<<g, c.threads, 0, s>>>((const T*)x, rows, gain, bias, (float)eps, (T*)y, mean, rstd,
+                              nullptr);
+  })));
   count_launch();
   TESS_CUDA(cudaGetLastError());
 }
@@ -1142,12 +1192,15 @@ void k_ln_fused_bwd(const void* dy, DType tdy, const void* x, DType tx, const fl
     return;
   }
   const LnCfg c = ln_vec_config(w);
-  const int g = ln_vec_blocks(rows, c.threads, 2);
+  int g = 1;
   float* part = out2w ? scratch : nullptr;
   TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR,
-      TESS_DISPATCH(tdx, TO, ln_vec_bwd_kernel<TD, TX, TR, TO, NV, false><<<g, c.threads, 0, s>>>(
-          (const TD*)dy, (const TX*)x, mean, rstd, gain, rows, (const TR*)resid, (TO*)dx, part,
-          nullptr))))));
+      TESS_DISPATCH(tdx, TO, TESS_LN_TH(c.threads, {
+        auto* k = ln_vec_bwd_kernel<TD, TX, TR, TO, NV, false, TH>;
+        g = ln_grid((const void*)k, c.threads, rows, 2);
+        k<<<g, c.threads, 0, s>>>((const TD*)dy, (const TX*)x, mean, rstd, gain, rows,
+                                  (const TR*)resid, (TO*)dx, part, nullptr);
+      }))))));
   count_launch();
   TESS_CUDA(cudaGetLastError());
   if (out2w) {
@@ -1166,10 +1219,12 @@ void k_ln_split_stats(const void* x, DType t, int64_t rows, int64_t w, float* st
                       cudaStream_t s) {
   if (!rows) return;
   const LnCfg c = ln_vec_config(w);
-  const int g = ln_vec_blocks(rows, c.threads, 4);
-  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, ln_vec_fwd_kernel<T, NV, true><<<g, c.threads, 0, s>>>(
-                                           (const T*)x, rows, nullptr, nullptr, 0.f, nullptr,
-                                           nullptr, nullptr, stats)));
+  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, {
+    auto* k = ln_vec_fwd_kernel<T, NV, true, 0>;
+    const int g = ln_grid((const void*)k, c.threads, rows, 4);
+    k<<<g, c.threads, 0, s>>>((const T*)x, rows, nullptr, nullptr, 0.f, nullptr, nullptr,
+                              nullptr, stats);
+  }));
   count_launch();
   TESS_CUDA(cudaGetLastError());
 }
@@ -1179,10 +1234,12 @@ void k_ln_split_apply(const void* x, DType t, const float* stats, int64_t rows, 
                       void* y, float* mean, float* rstd, cudaStream_t s) {
   if (!rows) return;
   const LnCfg c = ln_vec_config(w);
-  const int g = ln_vec_blocks(rows, c.threads, 4);
-  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, ln_vec_apply_kernel<T, NV><<<g, c.threads, 0, s>>>(
-                                           (const T*)x, stats, rows, (float)hidden_total, gain,
-                                           bias, (float)eps, (T*)y, mean, rstd)));
+  TESS_LN_NV(c.nv, TESS_DISPATCH(t, T, {
+    auto* k = ln_vec_apply_kernel<T, NV>;
+    const int g = ln_grid((const void*)k, c.threads, rows, 4);
+    k<<<g, c.threads, 0, s>>>((const T*)x, stats, rows, (float)hidden_total, gain, bias,
+                              (float)eps, (T*)y, mean, rstd);
+  }));
   count_launch();
   TESS_CUDA(cudaGetLastError());
 }
@@ -1195,11 +1252,14 @@ void k_ln_split_bwd_stats(const void* dy, DType tdy, const void* x, DType tx, co
     return;
   }
   const LnCfg c = ln_vec_config(w);
-  const int g = ln_vec_blocks(rows, c.threads, 2);
+  int g = 1;
   float* part = out2w ? scratch : nullptr;
-  TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX,
-      ln_vec_bwd_kernel<TD, TX, float, float, NV, true><<<g, c.threads, 0, s>>>(
-          (const TD*)dy, (const TX*)x, mean, rstd, gain, rows, nullptr, nullptr, part, stats))));
+  TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, {
+    auto* k = ln_vec_bwd_kernel<TD, TX, float, float, NV, true, 0>;
+    g = ln_grid((const void*)k, c.threads, rows, 2);
+    k<<<g, c.threads, 0, s>>>((const TD*)dy, (const TX*)x, mean, rstd, gain, rows, nullptr,
+                              nullptr, part, stats);
+  })));
   count_launch();
   TESS_CUDA(cudaGetLastError());
   if (out2w) {
@@ -1216,11 +1276,13 @@ void k_ln_split_bwd_apply(const void* dy, DType tdy, const void* x, DType tx, co
                           DType tdx, cudaStream_t s) {
   if (!rows) return;
   const LnCfg c = ln_vec_config(w);
-  const int g = ln_vec_blocks(rows, c.threads, 4);
   TESS_LN_NV(c.nv, TESS_DISPATCH(tdy, TD, TESS_DISPATCH(tx, TX, TESS_DISPATCH(tr, TR,
-      TESS_DISPATCH(tdx, TO, ln_vec_bwd_apply_kernel<TD, TX, TR, TO, NV><<<g, c.threads, 0, s>>>(
-          (const TD*)dy, (const TX*)x, mean, rstd, gain, stats, rows, (float)hidden_total,
-          (const TR*)resid, (TO*)dx))))));
+      TESS_DISPATCH(tdx, TO, {
+        auto* k = ln_vec_bwd_apply_kernel<TD, TX, TR, TO, NV>;
+        const int g = ln_grid((const void*)k, c.threads, rows, 4);
+        k<<<g, c.threads, 0, s>>>((const TD*)dy, (const TX*)x, mean, rstd, gain, stats, rows,
+                                  (float)hidden_total, (const TR*)resid, (TO*)dx);
+      })))));
   count_launch();
   TESS_CUDA(cudaGetLastError());
 }
