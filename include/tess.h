@@ -203,6 +203,37 @@ tess_status tess_matmul(tess_ctx* ctx, tess_variant v, tess_dtype in, const void
                         int64_t b_cols, void* c, tess_dtype c_type, uint32_t flags,
                         void* stream);
 
+/* Fused epilogue of a local product (north_star: bias / GeLU / dropout-scale
+ * in the tcgen05 GEMM epilogue; the reference's blocks have no linear biases
+ * and no dropout, layers.hpp:42-49, so this extends the path rather than
+ * replacing a reference call). Order per output element:
+ *   v = AB (+ bias[col]) ; GeLU: pre_activation = v, v = gelu(v) ;
+ *   dropout: v = keep ? v / (1 - p) : 0 ; v += residual ; store (or += with
+ *   TESS_ACCUMULATE).
+ * keep = a counter hash of (seed, row0 + local row, col0 + local col) -- the
+ * GLOBAL coordinate of the element, so every Tesseract block drops exactly
+ * what the unsharded product drops (host reference: tess_dropout_keep).
+ * bias: fp32 [local columns]; residual / pre_activation: the output's type
+ * and shape. bf16 inputs only. NN products on any grid (the epilogue runs on
+ * the one GEMM that owns the block); NT / TN only where no reduction follows
+ * (q == 1, and no depth sum). */
+typedef struct {
+  const float* bias;
+  int gelu;
+  void* pre_activation;
+  float dropout_p;
+  uint64_t dropout_seed;
+  int64_t row0, col0;
+  const void* residual;
+} tess_epilogue;
+
+tess_status tess_matmul_ex(tess_ctx* ctx, tess_variant v, tess_dtype in, const void* a,
+                           int64_t a_rows, int64_t a_cols, const void* b, int64_t b_rows,
+                           int64_t b_cols, void* c, tess_dtype c_type, uint32_t flags,
+                           const tess_epilogue* epilogue, void* stream);
+/* The dropout mask of tess_epilogue: 1 = element (row, col) kept. */
+int tess_dropout_keep(uint64_t seed, int64_t row, int64_t col, float p);
+
 /* ----------------------------------------------------------------- layers
  * ref: layers.hpp:123-161 (rank-level fwd/bwd) and layers.cpp:604-692
  * (layer_run). x, dy, y, dx are the rank's TesseractA activation blocks
@@ -265,6 +296,29 @@ tess_status tess_stream_join(tess_ctx* ctx, void* stream);
  * one outstanding forward each (the reference keeps caller-owned
  * BlockCacheRank objects, layers.hpp:114-119). Default 0. */
 tess_status tess_set_cache_slot(tess_ctx* ctx, int slot);
+
+/* Fault injection (the reference's verify inject_fault, verify.cpp:84-86,
+ * carried into the runtime so its failure semantics can be tested):
+ *   TESS_FAULT_PERTURB          global tesseract_matmul only: the combined
+ *                               result's element (0,0) += 1e-3 (exactly the
+ *                               reference's injected fault)
+ *   TESS_FAULT_RANK_FAIL        the rank raises at its collective number `at`
+ *                               (every partner aborts; the call fails with
+ *                               TESS_ERR_SPMD naming the coordinate)
+ *   TESS_FAULT_SKIP_COLLECTIVE  the rank silently skips collective `at`
+ *                               (its partners block; the in-process backend
+ *                               reports the deadlock naming every divergent
+ *                               rank and what it waits on, runtime.cpp:433-471)
+ * One-shot. tess_set_global_fault arms the next global call of this host
+ * thread (rank `rank` of its grid; ignored by PERTURB). */
+typedef enum {
+  TESS_FAULT_NONE = 0,
+  TESS_FAULT_PERTURB = 1,
+  TESS_FAULT_RANK_FAIL = 2,
+  TESS_FAULT_SKIP_COLLECTIVE = 3
+} tess_fault;
+tess_status tess_inject_fault(tess_ctx* ctx, tess_fault kind, int64_t at_collective);
+tess_status tess_set_global_fault(tess_fault kind, int rank, int64_t at_collective);
 
 /* Measurement switch (no reference counterpart): with enable != 0 every
  * collective of this context is metered and traced as usual but moves no
@@ -418,6 +472,24 @@ tess_status tess_debug_attn_trace(long long* out, int n);
  * reference (its reduce is runtime.cpp:485-513). */
 tess_status tess_debug_peer_window(int rank, const char* dir, size_t n, int iters,
                                    unsigned long long* bad);
+
+/* Test hooks of the SM-free SUMMA panel transport (csrc/summa.cpp,
+ * csrc/peer.h PanelLink): the GEMM may be launched before a panel lands and
+ * waits on the device per row chunk for a flag written with a stream memory
+ * operation after the chunk's copy-engine transfer.
+ * tess_debug_gemm_ready: one process; a two-segment NN GEMM [M,2K]x[2K,N]
+ * is launched, then (delay_ms later) its second A panel arrives from pinned
+ * host memory in `chunks` chunks; *bad = outputs differing (bitwise) from
+ * the same GEMM over resident panels; *ms_wait = device time of the flagged
+ * GEMM. tess_debug_panel_link: two processes (rank 0 root, rank 1 receiver,
+ * handles swapped through files in `dir`), `iters` pushes of a [M,K] panel
+ * (2M after half-way), each consumed by a GEMM the receiver launched before
+ * the root started the push; *bad as above. Replace nothing in the
+ * reference (its broadcasts are runtime.cpp:485-513). */
+tess_status tess_debug_gemm_ready(int64_t M, int64_t K, int64_t N, int chunks, int delay_ms,
+                                  unsigned long long* bad, float* ms_wait);
+tess_status tess_debug_panel_link(int rank, const char* dir, int64_t M, int64_t K, int64_t N,
+                                  int iters, int chunks, int delay_ms, unsigned long long* bad);
 
 #ifdef __cplusplus
 }

@@ -172,6 +172,8 @@ def _load() -> C.CDLL:
                             C.c_double, dp, dp, C.POINTER(dp), dp, ip, u64p, u64p], i),
         "tess_megatron_layer_run": ([i, C.POINTER(_LayerDimsC), i, i, dp, dp, C.POINTER(dp),
                                      C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
+        "tess_inject_fault": ([vp, i, i64], i),
+        "tess_set_global_fault": ([i, i, i64], i),
         "tess_stack_run": ([i, C.POINTER(_LayerDimsC), i, i, i, i, i, dp, dp, C.POINTER(dp),
                             C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
         "tess_stack_step": ([vp, i, C.POINTER(_LayerDimsC), i, C.POINTER(BlockShardC), vp, vp, vp,
@@ -504,6 +506,20 @@ def megatron_1d_linear(x, w1, w2, p: int, dtype="f32",
     return AlgoResult(out, CommStats(sr, sk))
 
 
+FAULTS = {"none": 0, "perturb": 1, "rank_fail": 2, "skip_collective": 3}
+
+
+def set_global_fault(kind: str, rank: int = 0, at_collective: int = 0) -> None:
+    """Arm a one-shot fault for the next global call of this thread
+    (tess_set_global_fault): "perturb" adds 1e-3 to element (0,0) of the
+    next tesseract_matmul result (the reference's verify inject_fault,
+    verify.cpp:84-86); "rank_fail" makes `rank` raise at its collective
+    number `at_collective`; "skip_collective" makes it skip that collective
+    (its partners block: the deadlock is reported naming every divergent
+    rank)."""
+    _check(lib.tess_set_global_fault(FAULTS[kind], rank, at_collective))
+
+
 def checksum(m) -> str:
     """FNV-1a fingerprint in the reference's format (matrix.cpp:352-370)."""
     m = _f64(m)
@@ -659,6 +675,11 @@ class RankContext:
         """Collectives metered but moving no data (timing the step without
         communication: exposed comm = (t - t_noop) / t)."""
         _check(lib.tess_set_comm_noop(self.h, int(on)))
+
+    def inject_fault(self, kind: str, at_collective: int = 0):
+        """One-shot fault at this rank's collective number `at_collective`
+        ("rank_fail" or "skip_collective"; see set_global_fault)."""
+        _check(lib.tess_inject_fault(self.h, FAULTS[kind], at_collective))
 
     def set_trace(self, on=True):
         _check(lib.tess_set_trace(self.h, int(on)))

@@ -5,6 +5,9 @@
 
 #include "kernels/kernels.h"
 #include "kernels/attention.h"
+#include <algorithm>
+#include <cmath>
+
 #include "ops.h"
 
 using namespace tess;
@@ -205,6 +208,7 @@ tess_status tess_init_local(int q, int d, int allow, const int* devices, tess_ct
 tess_status tess_destroy(tess_ctx* c) {
   return guarded([&] {
     if (!c) return;
+    if (c->world) local_world_rank_finished(c->world.get(), c->rank);
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     delete c;
@@ -259,6 +263,16 @@ tess_status tess_stream_join(tess_ctx* c, void* stream) {
     if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
     TESS_CUDA(cudaSetDevice(c->device));
     ctx_join(*c, static_cast<cudaStream_t>(stream));
+  });
+}
+
+tess_status tess_inject_fault(tess_ctx* c, tess_fault kind, int64_t at) {
+  return guarded([&] {
+    if (!c) fail(TESS_ERR_INVALID, "null tess_ctx");
+    if (kind < TESS_FAULT_NONE || kind > TESS_FAULT_SKIP_COLLECTIVE)
+      fail(TESS_ERR_INVALID, "unknown fault kind");
+    c->fault_kind = kind == TESS_FAULT_PERTURB ? 0 : (int)kind;
+    c->fault_at = at;
   });
 }
 
@@ -373,6 +387,19 @@ tess_status tess_unpartition(tess_ctx* c, tess_scheme scheme, tess_dtype dt, con
 tess_status tess_matmul(tess_ctx* c, tess_variant v, tess_dtype in, const void* a, int64_t ar,
                         int64_t ac, const void* b, int64_t br, int64_t bc, void* out,
                         tess_dtype ct, uint32_t flags, void* stream) {
+  return tess_matmul_ex(c, v, in, a, ar, ac, b, br, bc, out, ct, flags, nullptr, stream);
+}
+
+int tess_dropout_keep(uint64_t seed, int64_t row, int64_t col, float p) {
+  if (!(p > 0.f)) return 1;
+  const uint32_t th = (uint32_t)std::min(16777216.0, std::ceil((double)p * 16777216.0));
+  return dropout_keep(seed, (uint64_t)row, (uint64_t)col, th) ? 1 : 0;
+}
+
+tess_status tess_matmul_ex(tess_ctx* c, tess_variant v, tess_dtype in, const void* a, int64_t ar,
+                           int64_t ac, const void* b, int64_t br, int64_t bc, void* out,
+                           tess_dtype ct, uint32_t flags, const tess_epilogue* ep,
+                           void* stream) {
   return guarded([&] {
     Ctx& x = need(c);
     const DType ti = to_dtype(in), tc = to_dtype(ct);
@@ -383,6 +410,31 @@ tess_status tess_matmul(tess_ctx* c, tess_variant v, tess_dtype in, const void* 
     o.epi = (flags & TESS_ACCUMULATE) ? Epi::Accum : Epi::Store;
     if (o.epi == Epi::Accum && tc != DType::F32)
       fail(TESS_ERR_UNSUPPORTED, "TESS_ACCUMULATE needs an fp32 output");
+    if (ep && (ep->bias || ep->gelu || ep->dropout_p != 0.f || ep->residual)) {
+      if (ti != DType::BF16) fail(TESS_ERR_UNSUPPORTED, "fused epilogues need bf16 inputs");
+      if (!(ep->dropout_p >= 0.f && ep->dropout_p < 1.f))
+        fail(TESS_ERR_INVALID, "dropout_p must be in [0, 1)");
+      const bool reduced = x.grid.q > 1 || (v == TESS_TN && (flags & TESS_SUM_OVER_DEPTH) &&
+                                            x.grid.d > 1);
+      if (v != TESS_NN && reduced)
+        fail(TESS_ERR_UNSUPPORTED, "fused epilogues on NT / TN need q == 1 (no reduction)");
+      const int n_epi = (ep->gelu ? 1 : 0) + (ep->residual ? 1 : 0) + (o.epi == Epi::Accum);
+      if (n_epi > 1)
+        fail(TESS_ERR_UNSUPPORTED, "at most one of gelu, residual, TESS_ACCUMULATE");
+      if (ep->gelu) {
+        if (!ep->pre_activation) fail(TESS_ERR_INVALID, "gelu needs pre_activation");
+        o.epi = Epi::Gelu;
+        o.z = ep->pre_activation;
+      } else if (ep->residual) {
+        o.epi = Epi::Resid;
+        o.r = ep->residual;
+      }
+      o.bias = ep->bias;
+      o.drop_p = ep->dropout_p;
+      o.drop_seed = ep->dropout_seed;
+      o.drop_row0 = ep->row0;
+      o.drop_col0 = ep->col0;
+    }
     switch (v) {
       case TESS_NN:  // ref algorithms.cpp:34-45; check_inner :23-31
         if (ac != br)

@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "core.h"
@@ -50,6 +51,31 @@ class Comm {
     return nullptr;
   }
   virtual void pair_close(Family, cudaStream_t) {}
+  // SM-free panel broadcast (summa.cpp): the receiver's GEMM may be launched
+  // before the panel lands and waits per chunk on device flags (GemmReady).
+  // panel_async(f): the backend can deliver f's panels without any SM
+  // (copy engines + stream memory operations) and the group is a pair on
+  // distinct GPUs, so a spinning GEMM cannot starve the transfer.
+  virtual bool panel_async(Family) { return false; }
+  struct PanelRecv {
+    const void* buf = nullptr;       // where the panel is (root: src)
+    const uint32_t* flags = nullptr; // receiver: ready[c] per chunk
+    uint32_t epoch = 0;              // the value ready[c] reaches
+  };
+  // Collective over f (both members, same program order): root slot
+  // `root` sends `src` (bytes, in chunks of chunk_bytes); the receiver's
+  // copy lands in `dst` or a backend buffer (returned). Stream order on s
+  // after the root's producer; the receiver's flags are written on the
+  // transfer's own stream order. `tag` names the link (one per panel role).
+  virtual PanelRecv panel_bcast(Family, int /*root*/, const std::string& /*tag*/,
+                                const void* /*src*/, void* /*dst*/, size_t /*bytes*/,
+                                size_t /*chunk_bytes*/, cudaStream_t) {
+    fail(TESS_ERR_UNSUPPORTED, "panel_bcast: backend has no SM-free transport");
+  }
+  // Receiver: its reads of the link's last panel are done (stream order s).
+  virtual void panel_done(Family, const std::string& /*tag*/, cudaStream_t) {}
+  // The backend lands received panels in buffers of its own (dst unused).
+  virtual bool panel_owns_buffers() { return false; }
   virtual void barrier() = 0;
   virtual void* nccl_comm(Family) { return nullptr; }
 };
@@ -60,6 +86,9 @@ struct LocalWorld;
 std::shared_ptr<LocalWorld> make_local_world(const Grid& g, const std::vector<int>& devices);
 std::unique_ptr<Comm> make_local_comm(std::shared_ptr<LocalWorld> w, int rank);
 void local_world_fail(LocalWorld* w, const std::string& why);
+// The rank will make no further collective calls (its SPMD function
+// returned, or its context is destroyed): deadlock detection counts it.
+void local_world_rank_finished(LocalWorld* w, int rank);
 
 // ----------------------------------------------------------------- nccl
 void nccl_unique_id(void* out128);

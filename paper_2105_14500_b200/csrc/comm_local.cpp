@@ -19,7 +19,11 @@
 #include <condition_variable>
 #include <mutex>
 
+#include <cstdlib>
+#include <map>
+
 #include "comm.h"
+#include "peer.h"
 
 namespace tess {
 
@@ -43,6 +47,13 @@ struct Rendezvous {
 
 }  // namespace
 
+// What a blocked rank is waiting for (deadlock diagnosis).
+struct WaitInfo {
+  bool active = false;
+  const Rendezvous* rv = nullptr;
+  std::string what;
+};
+
 struct LocalWorld {
   Grid grid;
   std::vector<int> devices;
@@ -51,29 +62,79 @@ struct LocalWorld {
   std::atomic<bool> failed{false};
   std::mutex fail_mu;
   std::string failure;
+  // Deadlock detection (the reference's deadlock_check_locked,
+  // runtime.cpp:433-471): every live rank blocked in a rendezvous that can
+  // no longer complete means mismatched participation; the failure names
+  // each waiting rank and what it waits on.
+  std::mutex state_mu;
+  std::vector<WaitInfo> waiting;
+  std::vector<bool> done;
+  int finished = 0;
 
   void mark_failed(const std::string& why) {
     std::lock_guard<std::mutex> lk(fail_mu);
     if (!failed.exchange(true)) failure = why;
   }
 
-  void wait(Rendezvous& r, int gsize) {
+  // Every live rank blocked (caller holds state_mu): the last one to block
+  // declares the deadlock. A round that completes clears its waiters first.
+  void deadlock_check_locked() {
+    int blocked = 0;
+    for (const WaitInfo& w : waiting) blocked += w.active;
+    if (blocked == 0 || blocked + finished < grid.size()) return;
+    std::string msg = "deadlock: mismatched participation; divergent ranks:";
+    for (int r = 0; r < grid.size(); ++r) {
+      const WaitInfo& w = waiting[r];
+      if (!w.active) continue;
+      const Coord c = grid.coord_of(r);
+      msg += " (" + std::to_string(c.i) + "," + std::to_string(c.j) + "," + std::to_string(c.k) +
+             ") waits on " + w.what + ";";
+    }
+    if (finished > 0) msg += " " + std::to_string(finished) + " rank(s) already finished";
+    mark_failed(msg);
+  }
+
+  void rank_finished(int rank) {
+    std::lock_guard<std::mutex> lk(state_mu);
+    if (rank < 0 || rank >= (int)done.size() || done[rank]) return;
+    done[rank] = true;
+    ++finished;
+    if (!failed.load()) deadlock_check_locked();
+  }
+
+  void wait(Rendezvous& r, int gsize, int rank = -1, const std::string& what = std::string()) {
     std::unique_lock<std::mutex> lk(r.mu);
     const uint64_t g = r.gen;
     if (++r.arrived == gsize) {
       r.arrived = 0;
       ++r.gen;
+      {
+        std::lock_guard<std::mutex> sl(state_mu);
+        for (WaitInfo& w : waiting)
+          if (w.active && w.rv == &r) w.active = false;
+      }
       r.cv.notify_all();
       return;
+    }
+    if (rank >= 0) {
+      std::lock_guard<std::mutex> sl(state_mu);
+      waiting[rank] = {true, &r, what};
+      if (!failed.load()) deadlock_check_locked();
     }
     const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(600);
     while (r.gen == g) {
       r.cv.wait_for(lk, std::chrono::milliseconds(20));
       if (r.gen != g) break;
-      if (failed.load()) fail(TESS_ERR_SPMD, "aborted: another rank failed (" + failure + ")");
+      if (failed.load()) {
+        if (rank >= 0) {
+          std::lock_guard<std::mutex> sl(state_mu);
+          waiting[rank].active = false;
+        }
+        fail(TESS_ERR_SPMD, "aborted: " + failure);
+      }
       if (std::chrono::steady_clock::now() > deadline) {
-        mark_failed("collective rendezvous timed out (deadlock?)");
-        fail(TESS_ERR_SPMD, "collective rendezvous timed out (deadlock?)");
+        mark_failed("collective rendezvous timed out after 600 s waiting on " + what);
+        fail(TESS_ERR_SPMD, "collective rendezvous timed out after 600 s waiting on " + what);
       }
     }
   }
@@ -83,6 +144,8 @@ std::shared_ptr<LocalWorld> make_local_world(const Grid& g, const std::vector<in
   auto w = std::make_shared<LocalWorld>();
   w->grid = g;
   w->devices = devices;
+  w->waiting.resize(g.size());
+  w->done.assign(g.size(), false);
   for (int f = 0; f < 3; ++f) {
     const int n = g.group_count(Family(f));
     const int gs = g.group_size(Family(f));
@@ -139,6 +202,8 @@ class LocalComm : public Comm {
         cudaEventDestroy(ev_b_[f][p]);
       }
     if (scratch_) cudaFree(scratch_);
+    for (auto& m : flags_)
+      for (auto& kv : m) cudaFree(kv.second);
   }
 
   void bcast(Family f, int root, void* buf, size_t bytes, cudaStream_t s) override {
@@ -150,7 +215,7 @@ class LocalComm : public Comm {
     }
     TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
     x.rv->b[x.par][x.slot] = {buf, ev_b_[f][x.par], 0, root, bytes};
-    w_->wait(*x.rv, x.gsize);
+    w_->wait(*x.rv, x.gsize, rank_, x.what + " (completion)");
     if (x.slot == root)
       for (int o = 0; o < x.gsize; ++o)
         if (o != root) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][o].ev, 0));
@@ -173,7 +238,7 @@ class LocalComm : public Comm {
     }
     TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
     x.rv->b[x.par][x.slot] = {recv, ev_b_[f][x.par], 1, root, n * 4};
-    w_->wait(*x.rv, x.gsize);
+    w_->wait(*x.rv, x.gsize, rank_, x.what + " (completion)");
     if (x.slot != root) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][root].ev, 0));
   }
 
@@ -191,7 +256,7 @@ class LocalComm : public Comm {
     }
     TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
     x.rv->b[x.par][x.slot] = {buf, ev_b_[f][x.par], 2, 0, n * 4};
-    w_->wait(*x.rv, x.gsize);
+    w_->wait(*x.rv, x.gsize, rank_, x.what + " (completion)");
     if (n) {
       for (int o = 0; o < x.gsize; ++o)
         if (o != x.slot) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][o].ev, 0));
@@ -228,16 +293,72 @@ class LocalComm : public Comm {
     pair_ = Ctx();
     TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
     x.rv->b[x.par][x.slot] = {nullptr, ev_b_[f][x.par], 3, 0, 0};
-    w_->wait(*x.rv, x.gsize);
+    w_->wait(*x.rv, x.gsize, rank_, x.what + " (completion)");
     TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][1 - x.slot].ev, 0));
   }
 
-  void barrier() override { w_->wait(w_->world, w_->grid.size()); }
+  // SM-free panel broadcast between two distinct GPUs of this process: the
+  // receiver pulls the root's panel with peer copies (copy engines over
+  // NVLink) chunk by chunk, each chunk followed by a stream memory write of
+  // its ready flag. Ranks sharing one GPU keep the event-ordered bcast: a
+  // GEMM spinning on a flag could otherwise hold the SMs the partner's
+  // producer kernels need.
+  bool panel_async(Family f) override {
+    static const bool off = std::getenv("TESS_PANEL_ASYNC") &&
+                            std::getenv("TESS_PANEL_ASYNC")[0] == '0';
+    const Grid& g = w_->grid;
+    if (off || g.group_size(f) != 2 || !memops_available()) return false;
+    const int other_dev = w_->devices[g.rank_of(
+        g.member_at(f, g.group_index(c_, f), 1 - g.slot_in_group(c_, f)))];
+    if (other_dev == device_) return false;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, device_, other_dev);
+    return can != 0;
+  }
+
+  PanelRecv panel_bcast(Family f, int root, const std::string& tag, const void* src, void* dst,
+                        size_t bytes, size_t chunk_bytes, cudaStream_t s) override {
+    Ctx x = enter(f, 4, root, bytes, x_slot(f) == root ? src : dst, s);
+    PanelRecv r;
+    r.buf = x.slot == root ? src : dst;
+    if (!x.rv) return r;
+    if (x.slot != root && bytes) {
+      uint32_t*& fl = flags_[f][tag];
+      if (!fl) {
+        TESS_CUDA(cudaMalloc(&fl, PanelLink::kMaxChunks * 4));
+        TESS_CUDA(cudaMemset(fl, 0, PanelLink::kMaxChunks * 4));
+      }
+      const uint32_t e = ++epoch_[f][tag];
+      if (!chunk_bytes || chunk_bytes > bytes) chunk_bytes = bytes;
+      const size_t n = (bytes + chunk_bytes - 1) / chunk_bytes;
+      if (n > (size_t)PanelLink::kMaxChunks) fail(TESS_ERR_INVALID, "panel_bcast: too many chunks");
+      TESS_CUDA(cudaStreamWaitEvent(s, x.rv->a[x.par][root].ev, 0));
+      const char* from = static_cast<const char*>(x.rv->a[x.par][root].ptr);
+      for (size_t c = 0; c < n; ++c) {
+        const size_t off = c * chunk_bytes, len = std::min(chunk_bytes, bytes - off);
+        TESS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, from + off, len,
+                                  cudaMemcpyDefault, s));
+        stream_write_u32(s, fl + c, e);
+      }
+      r.flags = fl;
+      r.epoch = e;
+    }
+    TESS_CUDA(cudaEventRecord(ev_b_[f][x.par], s));
+    x.rv->b[x.par][x.slot] = {r.buf, ev_b_[f][x.par], 4, root, bytes};
+    w_->wait(*x.rv, x.gsize, rank_, x.what + " (completion)");
+    if (x.slot == root)
+      for (int o = 0; o < x.gsize; ++o)
+        if (o != root) TESS_CUDA(cudaStreamWaitEvent(s, x.rv->b[x.par][o].ev, 0));
+    return r;
+  }
+
+  void barrier() override { w_->wait(w_->world, w_->grid.size(), rank_, "barrier"); }
 
  private:
   struct Ctx {
     Rendezvous* rv = nullptr;
     int slot = 0, gsize = 1, par = 0;
+    std::string what;
   };
 
   Ctx enter(Family f, int kind, int root, size_t bytes, const void* ptr, cudaStream_t s) {
@@ -251,10 +372,18 @@ class LocalComm : public Comm {
     if (x.gsize > 8) fail(TESS_ERR_UNSUPPORTED, "local backend supports groups of <= 8");
     TESS_CUDA(cudaSetDevice(device_));
     x.rv = w_->rv[f][g.group_index(c_, f)].get();
-    x.par = static_cast<int>(calls_[f]++ & 1);
+    const uint64_t call = calls_[f]++;
+    x.par = static_cast<int>(call & 1);
     TESS_CUDA(cudaEventRecord(ev_a_[f][x.par], s));
     x.rv->a[x.par][x.slot] = {ptr, ev_a_[f][x.par], kind, root, bytes};
-    w_->wait(*x.rv, x.gsize);
+    static const char* kinds[] = {"broadcast", "reduce", "all_reduce", "pair exchange",
+                                  "panel broadcast"};
+    x.what = std::string(kinds[kind]) + " (root slot " + std::to_string(root) + ", " +
+             std::to_string(bytes) + " bytes) in " +
+             (f == ROW ? "row" : f == COL ? "column" : "depth") + " group " +
+             std::to_string(g.group_index(c_, f)) + ", its collective #" + std::to_string(call) +
+             " there";
+    w_->wait(*x.rv, x.gsize, rank_, x.what);
     const Post& p0 = x.rv->a[x.par][0];
     const Post& me = x.rv->a[x.par][x.slot];
     if (p0.kind != me.kind || p0.root != me.root || p0.bytes != me.bytes) {
@@ -285,6 +414,10 @@ class LocalComm : public Comm {
   size_t scratch_n_ = 0;
   Ctx pair_;  // open pair exchange (pair_open .. pair_close)
   Family pair_f_ = ROW;
+  std::map<std::string, uint32_t*> flags_[3];  // panel_bcast ready flags per link
+  std::map<std::string, uint32_t> epoch_[3];
+
+  int x_slot(Family f) const { return w_->grid.slot_in_group(c_, f); }
 };
 
 }  // namespace
@@ -294,5 +427,7 @@ std::unique_ptr<Comm> make_local_comm(std::shared_ptr<LocalWorld> w, int rank) {
 }
 
 void local_world_fail(LocalWorld* w, const std::string& why) { w->mark_failed(why); }
+
+void local_world_rank_finished(LocalWorld* w, int rank) { w->rank_finished(rank); }
 
 }  // namespace tess

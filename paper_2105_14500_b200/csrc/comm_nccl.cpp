@@ -21,8 +21,16 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <thread>
+
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <mutex>
 
 #include "comm.h"
@@ -46,6 +54,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t);
   const char* (*GetErrorString)(ncclResult_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
+  ncclResult_t (*CommAbort)(ncclComm_t);
 };
 
 const NcclApi& nccl() {
@@ -78,6 +88,9 @@ const NcclApi& nccl() {
     api.Reduce = reinterpret_cast<decltype(api.Reduce)>(sym("ncclReduce"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.CommGetAsyncError =
+        reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+    api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
   });
   if (!err.empty()) fail(TESS_ERR_SPMD, err);
   return api;
@@ -108,12 +121,15 @@ class NcclComm : public Comm {
     ncclUniqueId id;
     std::memcpy(&id, uid128, sizeof(id));
     TESS_NCCL(nccl().CommInitRank(&world_, g.size(), id, rank));
-    // The row/column/depth communicators run their kernels on at most
-    // `budget` CTAs, and the persistent GEMMs leave that many SMs free, so the
-    // comm stream's broadcasts / reductions overlap the GEMMs instead of
-    // queueing behind them (TESS_NCCL_SMS, default 8; 0 = NCCL defaults).
+    // No SMs are set aside for communication by default: the SUMMA panel
+    // broadcasts of the q = 2 groups move on copy engines (PanelLink), the
+    // NT/TN reduces inside the owner GEMMs (PeerWindow), so no GEMM ever
+    // waits on an NCCL kernel; the remaining NCCL calls (LayerNorm row
+    // statistics, depth all-reduces of weight gradients) run between GEMMs.
+    // TESS_NCCL_SMS=n caps the communicators at n CTAs and makes the
+    // persistent GEMMs leave n SMs free (the round-1 scheme).
     const char* env = std::getenv("TESS_NCCL_SMS");
-    const int budget = env ? std::atoi(env) : 8;
+    const int budget = env ? std::atoi(env) : 0;
     ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
     if (budget > 0) {
       cfg.minCTAs = 1;
@@ -137,9 +153,91 @@ class NcclComm : public Comm {
       if (nr != g.group_size(fam) || me != g.slot_in_group(c_, fam))
         fail(TESS_ERR_SPMD, "ncclCommSplit produced an unexpected group layout");
     }
+    const char* to = std::getenv("TESS_NCCL_TIMEOUT_S");
+    timeout_s_ = to ? std::atof(to) : 600.0;
+    TESS_CUDA(cudaGetDevice(&device_));
+    watchdog_ = std::thread([this] { watch(); });
+  }
+
+  // Failure semantics (the reference aborts an SPMD run whose rank failed or
+  // deadlocked, runtime.cpp:422-471): a watchdog polls every communicator's
+  // asynchronous error and the age of the oldest incomplete collective; on
+  // an NCCL error or a collective older than TESS_NCCL_TIMEOUT_S (default
+  // 600 s: a dead or divergent peer) it aborts all communicators
+  // (ncclCommAbort unblocks the kernels waiting on the peer) and every later
+  // call of this rank fails with TESS_ERR_SPMD carrying the reason.
+  void watch() {
+    cudaSetDevice(device_);
+    std::unique_lock<std::mutex> lk(wmu_);
+    while (!stop_) {
+      wcv_.wait_for(lk, std::chrono::milliseconds(50));
+      if (stop_ || failed_) continue;
+      std::string why;
+      for (ncclComm_t cm : {world_, comm_[0], comm_[1], comm_[2]}) {
+        if (!cm) continue;
+        ncclResult_t st = ncclSuccess;
+        if (nccl().CommGetAsyncError(cm, &st) == ncclSuccess && st != ncclSuccess &&
+            st != ncclInProgress) {
+          why = std::string("NCCL asynchronous error: ") + nccl().GetErrorString(st);
+          break;
+        }
+      }
+      while (why.empty() && !pending_.empty()) {
+        const cudaError_t q = cudaEventQuery(pending_.front().ev);
+        if (q == cudaErrorNotReady) {
+          const double age = std::chrono::duration<double>(std::chrono::steady_clock::now() -
+                                                           pending_.front().t0)
+                                 .count();
+          if (age > timeout_s_)
+            why = "collective " + pending_.front().what + " did not complete within " +
+                  std::to_string((int)timeout_s_) + " s (dead or divergent peer)";
+          break;
+        }
+        cudaGetLastError();
+        cudaEventDestroy(pending_.front().ev);
+        pending_.pop_front();
+      }
+      if (!why.empty()) {
+        failure_ = "rank (" + std::to_string(c_.i) + "," + std::to_string(c_.j) + "," +
+                   std::to_string(c_.k) + "): " + why;
+        failed_ = true;
+        for (ncclComm_t cm : {comm_[0], comm_[1], comm_[2], world_})
+          if (cm) nccl().CommAbort(cm);
+        aborted_ = true;
+      }
+    }
+  }
+
+  void check_alive() {
+    if (failed_) fail(TESS_ERR_SPMD, "aborted: " + failure_);
+  }
+
+  // Tracks the completion of the collective just enqueued on s.
+  void track(const char* kind, Family f, cudaStream_t s) {
+    cudaEvent_t ev;
+    TESS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TESS_CUDA(cudaEventRecord(ev, s));
+    std::lock_guard<std::mutex> lk(wmu_);
+    pending_.push_back({ev, std::chrono::steady_clock::now(),
+                        std::string(kind) + " #" + std::to_string(++ncoll_) + " in the " +
+                            (f == ROW ? "row" : f == COL ? "column" : "depth") + " group"});
   }
 
   ~NcclComm() override {
+    {
+      std::lock_guard<std::mutex> lk(wmu_);
+      stop_ = true;
+    }
+    wcv_.notify_all();
+    if (watchdog_.joinable()) watchdog_.join();
+    for (auto& p : pending_) cudaEventDestroy(p.ev);
+    pending_.clear();
+    if (aborted_) {  // communicators are gone; do not touch them again
+      for (int f = 0; f < 3; ++f) comm_[f] = nullptr;
+      world_ = nullptr;
+    }
+    cudaDeviceSynchronize();
+    for (auto& m : links_) m.clear();
     for (auto& w : win_) {
       if (!w) continue;
       try {
@@ -155,7 +253,9 @@ class NcclComm : public Comm {
 
   void bcast(Family f, int root, void* buf, size_t bytes, cudaStream_t s) override {
     if (!comm_[f] || !bytes) return;
+    check_alive();
     TESS_NCCL(nccl().Broadcast(buf, buf, bytes, ncclUint8, root, comm_[f], s));
+    track("broadcast", f, s);
   }
 
   void reduce(Family f, int root, const float* send, float* recv, size_t n,
@@ -165,18 +265,23 @@ class NcclComm : public Comm {
       return;
     }
     if (!n) return;
+    check_alive();
     // Non-root recv buffers are ignored by NCCL; pass send to keep it valid.
     const bool is_root = g_.slot_in_group(c_, f) == root;
     TESS_NCCL(nccl().Reduce(send, is_root ? recv : const_cast<float*>(send), n, ncclFloat32,
                          ncclSum, root, comm_[f], s));
+    track("reduce", f, s);
   }
 
   void allreduce(Family f, float* buf, size_t n, cudaStream_t s) override {
     if (!comm_[f] || !n) return;
+    check_alive();
     TESS_NCCL(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, comm_[f], s));
+    track("all_reduce", f, s);
   }
 
   void barrier() override {
+    check_alive();
     // A tiny all-reduce on the world communicator, then wait for it.
     float* tmp = nullptr;
     TESS_CUDA(cudaMalloc(&tmp, 4));
@@ -207,13 +312,15 @@ class NcclComm : public Comm {
     return win_[f]->acquire(n, s);
   }
 
-  void make_window(Family f) {
+  void make_window(Family f) { win_[f] = std::make_unique<PeerWindow>(exchange(f)); }
+
+  // Blocking swap of `bytes` with the pair partner over f's communicator
+  // (each slot broadcasts its own), for IPC handle exchanges.
+  std::function<void(const void*, void*, size_t)> exchange(Family f) {
     {
       ncclComm_t cm = comm_[f];
       const int me = g_.slot_in_group(c_, f);
-      // Blocking swap of the IPC handles: each slot broadcasts its own.
-      win_[f] = std::make_unique<PeerWindow>([cm, me](const void* mine, void* theirs,
-                                                      size_t bytes) {
+      return [cm, me](const void* mine, void* theirs, size_t bytes) {
         // drain: no earlier operation of this communicator may still be in
         // flight on another stream when the swap runs on the default stream
         TESS_CUDA(cudaDeviceSynchronize());
@@ -229,8 +336,41 @@ class NcclComm : public Comm {
         TESS_CUDA(cudaMemcpy(theirs, static_cast<char*>(d) + (1 - me) * bytes, bytes,
                              cudaMemcpyDeviceToHost));
         TESS_CUDA(cudaFree(d));
-      });
+      };
     }
+  }
+
+  // SM-free panel broadcast (PanelLink): copy-engine pushes into the
+  // receiver's IPC window + stream memory operations; no NCCL kernel.
+  bool panel_async(Family f) override {
+    static const bool off = std::getenv("TESS_PANEL_ASYNC") &&
+                            std::getenv("TESS_PANEL_ASYNC")[0] == '0';
+    return !off && memops_available() && pair_capable(f);
+  }
+
+  PanelRecv panel_bcast(Family f, int root, const std::string& tag, const void* src, void*,
+                        size_t bytes, size_t chunk_bytes, cudaStream_t s) override {
+    check_alive();
+    const bool receiver = g_.slot_in_group(c_, f) != root;
+    auto& link = links_[f][tag + "/" + std::to_string(root)];
+    if (!link) link = std::make_unique<PanelLink>(exchange(f), receiver);
+    PanelRecv r;
+    r.epoch = link->push(receiver ? nullptr : src, bytes, chunk_bytes, s);
+    if (receiver) {
+      r.buf = link->data();
+      r.flags = link->ready_flags();
+      last_link_[f][tag] = link.get();
+    } else {
+      r.buf = src;
+    }
+    return r;
+  }
+
+  bool panel_owns_buffers() override { return true; }
+
+  void panel_done(Family f, const std::string& tag, cudaStream_t s) override {
+    auto it = last_link_[f].find(tag);
+    if (it != last_link_[f].end()) it->second->done(s);
   }
 
   const float* pair_open(Family f, const float* mine, size_t, cudaStream_t s) override {
@@ -251,6 +391,25 @@ class NcclComm : public Comm {
   ncclComm_t world_ = nullptr;
   ncclComm_t comm_[3] = {nullptr, nullptr, nullptr};
   std::unique_ptr<PeerWindow> win_[3];
+  std::map<std::string, std::unique_ptr<PanelLink>> links_[3];
+  std::map<std::string, PanelLink*> last_link_[3];
+  // watchdog
+  struct Pending {
+    cudaEvent_t ev;
+    std::chrono::steady_clock::time_point t0;
+    std::string what;
+  };
+  int device_ = 0;
+  double timeout_s_ = 600.0;
+  std::thread watchdog_;
+  std::mutex wmu_;
+  std::condition_variable wcv_;
+  std::deque<Pending> pending_;
+  uint64_t ncoll_ = 0;
+  bool stop_ = false;
+  std::atomic<bool> failed_{false};
+  bool aborted_ = false;
+  std::string failure_;
   bool probed_[3] = {false, false, false};
   bool pair_ok_[3] = {false, false, false};
 };

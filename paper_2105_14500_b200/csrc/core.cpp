@@ -279,26 +279,66 @@ void coll_note_single(Ctx& c, int kind, Family f, int root, uint64_t elements) {
   trace_event(c, kind, f, root, elements);
 }
 
+// Fault injection (tess_inject_fault; the reference's verify inject_fault,
+// verify.cpp:84-86, carried into the runtime): at this rank's collective
+// number fault_at it fails (the SPMD error path) or silently skips the
+// collective (its partners then block: deadlock detection names them).
+static bool fault_skip(Ctx& c) {
+  if (!c.fault_kind || (int64_t)c.step != c.fault_at) return false;
+  const int k = c.fault_kind;
+  c.fault_kind = 0;
+  if (k == TESS_FAULT_RANK_FAIL)
+    fail(TESS_ERR_SPMD, "injected failure at collective #" + std::to_string(c.step));
+  if (k == TESS_FAULT_SKIP_COLLECTIVE) {
+    ++c.step;
+    return true;
+  }
+  return false;
+}
+
 void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t elements,
                 cudaStream_t s) {
+  if (fault_skip(c)) return;
   c.meter.bcast(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, elements);
   trace_event(c, 0, f, root, elements);
   if (!c.comm_noop) c.comm->bcast(f, root, buf, bytes, s);
 }
 
+Comm::PanelRecv coll_bcast_panel(Ctx& c, Family f, int root, const std::string& tag,
+                                 const void* src, void* dst, size_t bytes, uint64_t elements,
+                                 size_t chunk_bytes, cudaStream_t s) {
+  if (fault_skip(c)) {
+    Comm::PanelRecv r;
+    r.buf = c.grid.slot_in_group(c.coord, f) == root ? src : dst;
+    return r;
+  }
+  c.meter.bcast(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, elements);
+  trace_event(c, 0, f, root, elements);
+  const bool is_root = c.grid.slot_in_group(c.coord, f) == root;
+  if (c.comm_noop || c.grid.group_size(f) == 1) {
+    Comm::PanelRecv r;
+    r.buf = is_root ? src : dst;
+    return r;
+  }
+  return c.comm->panel_bcast(f, root, tag, src, dst, bytes, chunk_bytes, s);
+}
+
 void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, size_t n,
                  cudaStream_t s) {
+  if (fault_skip(c)) return;
   c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, n, false);
   trace_event(c, 1, f, root, n);
   if (!c.comm_noop) c.comm->reduce(f, root, send, recv, n, s);
 }
 
 void coll_reduce_note(Ctx& c, Family f, int root, size_t n) {
+  if (fault_skip(c)) return;
   c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), root, n, false);
   trace_event(c, 1, f, root, n);
 }
 
 void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s) {
+  if (fault_skip(c)) return;
   c.meter.reduce(c.grid.group_size(f), c.grid.slot_in_group(c.coord, f), 0, n, true);
   trace_event(c, 2, f, 0, n);
   if (!c.comm_noop) c.comm->allreduce(f, buf, n, s);

@@ -29,6 +29,10 @@ struct tess_ctx {
   // all-reduced over the depth group; weight shards are not depth-reduced.
   bool megatron = false;
   uint64_t step = 0;  // collective sequence number (RankCtx::step_)
+  // Fault injection (tess_inject_fault): at collective number fault_at this
+  // rank fails (2) or skips the collective (3); one-shot.
+  int fault_kind = 0;
+  int64_t fault_at = -1;
   std::vector<tess::TraceEvent> trace;
   std::unique_ptr<tess::Workspace> ws;
   // Forward caches are named by (cache slot, layer op); the slot lets several
@@ -67,6 +71,12 @@ using Ctx = tess_ctx;
 // `elements` is the reference's payload element count (for the meter).
 void coll_bcast(Ctx& c, Family f, int root, void* buf, size_t bytes, uint64_t elements,
                 cudaStream_t s);
+// The SM-free form of coll_bcast (Comm::panel_bcast), same meter and trace:
+// the receiver's panel may still be landing when this returns on the
+// device; its GEMM waits on the returned flags (GemmReady).
+Comm::PanelRecv coll_bcast_panel(Ctx& c, Family f, int root, const std::string& tag,
+                                 const void* src, void* dst, size_t bytes, uint64_t elements,
+                                 size_t chunk_bytes, cudaStream_t s);
 void coll_reduce(Ctx& c, Family f, int root, const float* send, float* recv, size_t n,
                  cudaStream_t s);
 void coll_allreduce(Ctx& c, Family f, float* buf, size_t n, cudaStream_t s);

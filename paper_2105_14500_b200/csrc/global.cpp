@@ -36,6 +36,10 @@ struct LastRun {
 };
 thread_local LastRun g_last_run;
 thread_local bool g_global_trace = false;
+// tess_set_global_fault: armed for the next global call of this thread
+thread_local int g_fault_kind = 0, g_fault_rank = 0;
+thread_local int64_t g_fault_at = -1;
+thread_local bool g_perturb_next = false;
 
 struct Runner {
   Grid g;
@@ -52,6 +56,13 @@ struct Runner {
       fail(TESS_ERR_CUDA, std::string("init_local: ") + g_last_error);
     for (auto* c : ctx) c->trace_on = g_global_trace;
     g_last_run = LastRun{};
+    if (g_fault_kind == TESS_FAULT_RANK_FAIL || g_fault_kind == TESS_FAULT_SKIP_COLLECTIVE) {
+      if (g_fault_rank >= 0 && g_fault_rank < g.size()) {
+        ctx[g_fault_rank]->fault_kind = g_fault_kind;
+        ctx[g_fault_rank]->fault_at = g_fault_at;
+      }
+      g_fault_kind = 0;
+    }
   }
   ~Runner() {
     for (auto* c : ctx)
@@ -85,6 +96,7 @@ struct Runner {
           fn(c, s);
           ctx_join(c, s);  // host copies of layer outputs + deferred collectives
           TESS_CUDA(cudaStreamSynchronize(s));
+          local_world_rank_finished(c.world.get(), c.rank);
         } catch (const tess::Error& e) {
           local_world_fail(c.world.get(), e.what());
           std::lock_guard<std::mutex> lk(mu);
@@ -325,6 +337,8 @@ tess_status tess_tesseract_matmul(int q, int d, int allow, tess_variant v, tess_
       blocks[x.rank] = fetch(lc, (size_t)lcr * lcc, DType::F32, s);
     });
     combine(g, csch, blocks, cr, cc, c);
+    if (g_perturb_next && cr > 0 && cc > 0) c[0] += 1e-3;  // ref verify.cpp:84-86
+    g_perturb_next = false;
     R.stats(sr, sk);
   });
 }
@@ -954,6 +968,17 @@ tess_status tess_megatron_1d_linear(int p, tess_dtype compute, const double* x, 
 }  // extern "C"
 
 extern "C" {
+
+tess_status tess_set_global_fault(tess_fault kind, int rank, int64_t at) {
+  return guarded([&] {
+    if (kind < TESS_FAULT_NONE || kind > TESS_FAULT_SKIP_COLLECTIVE)
+      fail(TESS_ERR_INVALID, "unknown fault kind");
+    g_perturb_next = kind == TESS_FAULT_PERTURB;
+    g_fault_kind = kind == TESS_FAULT_PERTURB ? 0 : (int)kind;
+    g_fault_rank = rank;
+    g_fault_at = at;
+  });
+}
 
 tess_status tess_set_global_trace(int enable) {
   g_global_trace = enable != 0;

@@ -48,6 +48,30 @@ struct GemmSeg {
   int64_t k = 0;            // K extent of the panel
 };
 
+// Segment readiness: SUMMA panels that are still landing when the GEMM is
+// launched (summa.cpp, Comm::panel_async). A producer waits, before its
+// first TMA load of segment s touching chunk c, until
+//   a_flags[s][c] >= a_epoch[s]  (a_flags[s] != nullptr; chunked, see below)
+//   b_flags[s][0] >= b_epoch[s]  (b_flags[s] != nullptr; whole panel)
+// (wrap-safe). c = row of the stored A panel / chunk_rows: the tile's M rows
+// when A is stored [M, K], its k-block when A is stored [K, M] (TN). The
+// panel transport writes the flags in stream order after the bytes landed
+// (cuStreamWriteValue32: no SM is involved, so a waiting persistent GEMM
+// cannot starve the transfer).
+struct GemmReady {
+  const uint32_t* a_flags[kMaxSegments] = {};
+  const uint32_t* b_flags[kMaxSegments] = {};
+  uint32_t a_epoch[kMaxSegments] = {};
+  uint32_t b_epoch[kMaxSegments] = {};
+  int chunks = 1;
+  int64_t chunk_rows = 0;  // 0: one chunk per panel
+  bool any() const {
+    for (int s = 0; s < kMaxSegments; ++s)
+      if (a_flags[s] || b_flags[s]) return true;
+    return false;
+  }
+};
+
 struct GemmDesc {
   int64_t M = 0, N = 0;
   int64_t nb0 = 1, nb1 = 1;  // batch extents (attention: heads, samples)
@@ -74,7 +98,34 @@ struct GemmDesc {
   // nst = gemm_bf16_stat_tiles(d) tiles per row.
   float* stats = nullptr;
   int64_t ss0 = 0, ss1 = 0;
+  GemmReady ready;
+  // Fused bias / dropout (tcgen05 kernels, Store / Accum / Resid / Gelu;
+  // unbatched): v = alpha*acc + bias[n]; Gelu: Z = v, v = gelu(v); dropout:
+  // v = keep(drop_seed, drop_row0 + m, drop_col0 + n) ? v / (1 - drop_p) : 0
+  // (dropout_keep(), a counter hash of the GLOBAL element coordinate, so a
+  // sharded product drops exactly the elements the unsharded one drops);
+  // Resid: v += R after the dropout. Not part of the reference (its blocks
+  // have neither linear biases nor dropout, layers.hpp:42-49).
+  const float* bias = nullptr;
+  float drop_p = 0.f;
+  uint64_t drop_seed = 0;
+  int64_t drop_row0 = 0, drop_col0 = 0;
 };
+
+// Dropout mask of element (row, col) under `seed` (host and device): keep
+// iff the top 24 bits of a splitmix64-style hash are >= p * 2^24.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline bool dropout_keep(uint64_t seed, uint64_t row, uint64_t col, uint32_t thresh24) {
+  uint64_t x = seed ^ (row * 0x9E3779B97F4A7C15ull) ^ (col * 0xC2B2AE3D27D4EB4Full);
+  x ^= x >> 31;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 29;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 32;
+  return (uint32_t)(x >> 40) >= thresh24;
+}
 
 // Name of the kernel instantiation gemm() launches for d (profiling).
 std::string gemm_kernel_name(const GemmDesc& d);

@@ -131,6 +131,7 @@ thread_local std::string g_simt_err;
 cudaError_t gemm_f32_simt(const GemmDesc& d, cudaStream_t stream) {
   using namespace simt;
   if (d.in != DType::F32 || d.c_type != DType::F32) return cudaErrorInvalidValue;
+  if (d.bias || d.drop_p > 0.f) return cudaErrorInvalidValue;  // tcgen05 epilogue only
   if (d.nseg < 1 || d.nseg > kMaxSegments) return cudaErrorInvalidValue;
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
   Params p;

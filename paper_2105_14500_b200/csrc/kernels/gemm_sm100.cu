@@ -41,6 +41,8 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -91,7 +93,60 @@ struct Params {
   float* stats;
   long long ss0, ss1;
   int nst, tile_n;
+  // fused bias / dropout (GemmDesc)
+  const float* bias;
+  int drop;
+  uint32_t drop_thresh;
+  float drop_scale;
+  unsigned long long drop_seed;
+  long long drop_row0, drop_col0;
+  // segment readiness (GemmReady)
+  int rdy;
+  const uint32_t* rdy_a[kMaxSegments];
+  const uint32_t* rdy_b[kMaxSegments];
+  uint32_t rdy_ea[kMaxSegments], rdy_eb[kMaxSegments];
+  int rdy_chunks, rdy_chunk_rows;
 };
+
+// Producer-side wait for a panel chunk delivered while the GEMM runs
+// (GemmReady). `seen` caches satisfied (segment, chunk) pairs of this
+// producer: one system-scope acquire load per pair, then nothing. The proxy
+// fence orders the acquire before the async-proxy (TMA) reads of the panel.
+// A panel that never lands traps after 120 s instead of hanging the GPU.
+__device__ __noinline__ void wait_flag(const uint32_t* f, uint32_t epoch) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 120ull * 1000000000ull) __trap();
+    __nanosleep(128);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void wait_seg_a(const Params& p, int s, int row, uint64_t& seen) {
+  const uint32_t* f = p.rdy_a[s];
+  if (!f) return;
+  int c = p.rdy_chunk_rows ? row / p.rdy_chunk_rows : 0;
+  if (c >= p.rdy_chunks) c = p.rdy_chunks - 1;
+  const int bit = s * p.rdy_chunks + c;  // < 32 (host checks chunks * nseg)
+  if ((seen >> bit) & 1ull) return;
+  wait_flag(f + c, p.rdy_ea[s]);
+  seen |= 1ull << bit;
+}
+
+__device__ __forceinline__ void wait_seg_b(const Params& p, int s, uint64_t& seen) {
+  const uint32_t* f = p.rdy_b[s];
+  if (!f) return;
+  const int bit = 32 + s;  // B panels cached in the high word
+  if ((seen >> bit) & 1ull) return;
+  wait_flag(f, p.rdy_eb[s]);
+  seen |= 1ull << bit;
+}
 
 // Exact-erf GeLU for the tcgen05 epilogues (ref layers.cpp:25-42), whose
 // outputs are stored in bf16: Phi(x) = 0.5 (1 + erf(x / sqrt 2)) by
@@ -288,6 +343,24 @@ __device__ __forceinline__ void epilogue_load_aux(const Params& p, int b0, int b
   }
 }
 
+// Bias of columns [n, n + 32) (clamped to N: columns past it are clipped).
+__device__ __forceinline__ void add_bias32(const Params& p, int n, float (&v)[32]) {
+  if (!p.bias) return;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] += __ldg(p.bias + min(n + j, p.N - 1));
+}
+
+__device__ __forceinline__ void dropout32(const Params& p, int m, int n, float (&v)[32]) {
+  if (!p.drop) return;
+  const unsigned long long row = (unsigned long long)(p.drop_row0 + m);
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    v[j] = dropout_keep(p.drop_seed, row, (unsigned long long)(p.drop_col0 + n + j),
+                        p.drop_thresh)
+               ? v[j] * p.drop_scale
+               : 0.f;
+}
+
 // Writes 32 consecutive columns [n, n + nvalid) of one output row.
 __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int b1, int m, int n,
                                                    int nvalid, const uint32_t (&acc)[32],
@@ -295,8 +368,10 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int 
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * p.alpha;
+  add_bias32(p, n, v);
   const int epi = p.epi;
   if (epi == (int)Epi::Resid || epi == (int)Epi::Accum) {
+    dropout32(p, m, n, v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] += aux[j];
   } else if (epi == (int)Epi::DGelu) {
@@ -319,6 +394,9 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int 
                   v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    dropout32(p, m, n, v);
+  } else if (epi == (int)Epi::Store) {
+    dropout32(p, m, n, v);
   }
   if (p.c_bf16)
     store32_bf16(batch_ptr<__nv_bfloat16>(p.c, p.cs0, p.cs1, b0, b1) + (long long)m * p.ldc + n,
@@ -331,14 +409,18 @@ __device__ __forceinline__ void epilogue_row_chunk(const Params& p, int b0, int 
 // storing (TMA-store path); for Gelu v is the pre-activation (the GeLU is
 // applied after Z is staged). Rows past M (partial tiles) compute garbage
 // that the TMA store clips.
-__device__ __forceinline__ void epilogue_values(const Params& p, int b0, int b1, int m,
+__device__ __forceinline__ void epilogue_values(const Params& p, int b0, int b1, int m, int n,
                                                 const uint32_t (&acc)[32], const float (&aux)[32],
                                                 float (&v)[32]) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * p.alpha;
+  add_bias32(p, n, v);
   const int epi = p.epi;
   const bool in_m = m < p.M;
-  if (epi == (int)Epi::Resid) {
+  if (epi == (int)Epi::Store || epi == (int)Epi::Accum) {
+    dropout32(p, m, n, v);
+  } else if (epi == (int)Epi::Resid) {
+    dropout32(p, m, n, v);
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] += aux[j];
   } else if (epi == (int)Epi::DGelu) {
@@ -402,7 +484,7 @@ __device__ __forceinline__ void stage_store(const CUtensorMap* map, EpiStage& st
 // One 32-column chunk through the TMA path: bf16 = one 32-column box, f32 =
 // two 16-column boxes; Gelu stores Z first; Accum is a TMA reduce-add into C.
 __device__ __forceinline__ void epilogue_chunk_tma(const Params& p, EpiStage& st, int lane,
-                                                   int b0, int b1, int n, int mrow0,
+                                                   int b0, int b1, int n, int mrow0, int m,
                                                    float (&v)[32]) {
   const bool bf16 = p.c_bf16;
   const bool reduce = p.epi == (int)Epi::Accum;
@@ -415,6 +497,7 @@ __device__ __forceinline__ void epilogue_chunk_tma(const Params& p, EpiStage& st
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    dropout32(p, m, n, v);
   }
   if (bf16) {
     stage_store(&p.tma_c, st, lane, v, true, reduce, n, mrow0, b0, b1);
@@ -458,8 +541,8 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, int b0, int b1, i
       // warp-uniform: every lane stages its row, the store clips rows >= M
       if (n < p.N) {
         float v[32];
-        epilogue_values(p, b0, b1, m, r, aux, v);
-        epilogue_chunk_tma(p, *st, lane, b0, b1, n, mrow0, v);
+        epilogue_values(p, b0, b1, m, n, r, aux, v);
+        epilogue_chunk_tma(p, *st, lane, b0, b1, n, mrow0, m, v);
       }
     } else if (nvalid > 0) {
       if (stats)
@@ -529,6 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      uint64_t seen = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         int b0, b1, m0, tn;
         decode_tile(p, tile, b0, b1, m0, tn);
@@ -536,7 +620,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < p.nseg; ++s) {
           const CUtensorMap* ma = &p.tma_a[s];
           const CUtensorMap* mb = &p.tma_b[s];
+          if (p.rdy) {
+            wait_seg_b(p, s, seen);
+            if (!A_MN) wait_seg_a(p, s, m0, seen);
+          }
           for (int kb = 0; kb < p.seg_kb[s]; ++kb) {
+            if (A_MN && p.rdy) wait_seg_a(p, s, kb * BK, seen);
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * C::STAGE_BYTES;
             uint8_t* sb = sa + C::A_BYTES;
@@ -880,6 +969,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // -------------------------------------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
+      uint64_t seen = 0;
       int next = cluster;  // first wave static
       for (;;) {
         int tile;
@@ -904,8 +994,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int s = rev ? p.nseg - 1 - si : si;
           const CUtensorMap* ma = &p.tma_a[s];
           const CUtensorMap* mb = &p.tma_b[s];
+          if (p.rdy) {
+            // this CTA loads B columns of the pair tile and its own A rows
+            wait_seg_b(p, s, seen);
+            if (!A_MN) wait_seg_a(p, s, mr, seen);
+          }
           for (int ki = 0; ki < p.seg_kb[s]; ++ki) {
             const int kb = rev ? p.seg_kb[s] - 1 - ki : ki;
+            if (A_MN && p.rdy) wait_seg_a(p, s, kb * BK, seen);
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * C::STAGE_BYTES;
             uint8_t* sb = sa + C::A_BYTES;
@@ -1444,6 +1540,41 @@ cudaError_t gemm_bf16_sm100(const GemmDesc& d, cudaStream_t stream) {
                  encode_out(&p.tma_z, d.z, bf, d.N, d.M, d.ldz, d.nb0, d.zs0, d.nb1, d.zs1));
   }
   p.nst = static_cast<int>((d.N + tile_n - 1) / tile_n) * kEpiHalves;
+  if (d.bias || d.drop_p > 0.f) {
+    const bool ok_epi = d.epi == Epi::Store || d.epi == Epi::Accum || d.epi == Epi::Resid ||
+                        d.epi == Epi::Gelu;
+    if (!ok_epi || d.nb0 != 1 || d.nb1 != 1 || !(d.drop_p >= 0.f && d.drop_p < 1.f)) {
+      g_gemm_err = "gemm_bf16_sm100: bias / dropout need an unbatched Store, Accum, Resid or "
+                   "Gelu epilogue and 0 <= p < 1";
+      return cudaErrorInvalidValue;
+    }
+    p.bias = d.bias;
+    if (d.drop_p > 0.f) {
+      p.drop = 1;
+      p.drop_thresh = (uint32_t)std::min(16777216.0, std::ceil((double)d.drop_p * 16777216.0));
+      p.drop_scale = 1.0f / (1.0f - d.drop_p);
+      p.drop_seed = d.drop_seed;
+      p.drop_row0 = d.drop_row0;
+      p.drop_col0 = d.drop_col0;
+    }
+  }
+  if (d.ready.any()) {
+    const GemmReady& r = d.ready;
+    if (r.chunks < 1 || r.chunks * d.nseg > 32 || r.chunk_rows < 0 || r.chunk_rows > (1 << 30) ||
+        (r.chunks > 1 && r.chunk_rows == 0)) {
+      g_gemm_err = "gemm_bf16_sm100: bad segment readiness layout";
+      return cudaErrorInvalidValue;
+    }
+    p.rdy = 1;
+    for (int s = 0; s < kMaxSegments; ++s) {
+      p.rdy_a[s] = s < d.nseg ? r.a_flags[s] : nullptr;
+      p.rdy_b[s] = s < d.nseg ? r.b_flags[s] : nullptr;
+      p.rdy_ea[s] = r.a_epoch[s];
+      p.rdy_eb[s] = r.b_epoch[s];
+    }
+    p.rdy_chunks = r.chunks;
+    p.rdy_chunk_rows = static_cast<int>(r.chunk_rows);
+  }
   cudaError_t e = pair        ? launch_pair(p, pair_tn, a_mn, b_mn, stream)
                   : BN == 256 ? launch_bn<256>(p, a_mn, b_mn, stream)
                               : launch_bn<128>(p, a_mn, b_mn, stream);

@@ -122,6 +122,9 @@ void k_peer_signal(uint32_t* flag, uint32_t v, cudaStream_t s);
 void k_peer_wait(const uint32_t* flag, uint32_t v, cudaStream_t s);
 // Self-test pattern: dst[i] = base + (i % 4093); check counts mismatches.
 void k_peer_fill(float* dst, size_t n, float base, cudaStream_t s);
+// *bad += number of elements whose bits differ (a vs b)
+void k_count_mismatch(const float* a, const float* b, size_t n, unsigned long long* bad,
+                      cudaStream_t s);
 void k_peer_check(const float* src, size_t n, float base, unsigned long long* bad,
                   cudaStream_t s);
 

@@ -51,7 +51,23 @@ __global__ void peer_check_kernel(const float* src, size_t n, float base,
   if (b) atomicAdd(bad, b);
 }
 
+__global__ void count_mismatch_kernel(const float* a, const float* b, size_t n,
+                                      unsigned long long* bad) {
+  unsigned long long m = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    m += __float_as_uint(a[i]) != __float_as_uint(b[i]);
+  if (m) atomicAdd(bad, m);
+}
+
 }  // namespace
+
+void k_count_mismatch(const float* a, const float* b, size_t n, unsigned long long* bad,
+                      cudaStream_t s) {
+  count_mismatch_kernel<<<148, 256, 0, s>>>(a, b, n, bad);
+  count_launch();
+  TESS_CUDA(cudaGetLastError());
+}
 
 void k_peer_signal(uint32_t* flag, uint32_t v, cudaStream_t s) {
   peer_signal_kernel<<<1, 1, 0, s>>>(flag, v);

@@ -248,21 +248,32 @@ struct WeightPanels {
   Panels qkv, proj, ff1, ff2;
 };
 
+// Panel buffers alternate with the cache slot's parity, so a stack's next
+// layer can receive its weights while this layer's GEMMs still read theirs.
 WeightPanels prefetch_weights(Ctx& c, DType t, const RankDims& rd, const tess_block_shard& p,
                               bool attn, bool ff, cudaStream_t s) {
   WeightPanels w;
   if (c.grid.q == 1) return w;
   const int64_t hq = rd.hq;
   const size_t e = dtype_size(t);
+  const std::string pf = "pf" + std::to_string(c.cache_slot & 1) + ".";
   if (attn) {
-    w.qkv = prefetch_panels(c, COL, p.w_qkv, hq, 3 * hq, e, "pf.qkv", s);
-    w.proj = prefetch_panels(c, COL, p.w_proj, hq, hq, e, "pf.proj", s);
+    w.qkv = prefetch_panels(c, COL, p.w_qkv, hq, 3 * hq, e, pf + "qkv", s);
+    w.proj = prefetch_panels(c, COL, p.w_proj, hq, hq, e, pf + "proj", s);
   }
   if (ff) {
-    w.ff1 = prefetch_panels(c, COL, p.w_ff1, hq, 4 * hq, e, "pf.ff1", s);
-    w.ff2 = prefetch_panels(c, COL, p.w_ff2, 4 * hq, hq, e, "pf.ff2", s);
+    w.ff1 = prefetch_panels(c, COL, p.w_ff1, hq, 4 * hq, e, pf + "ff1", s);
+    w.ff2 = prefetch_panels(c, COL, p.w_ff2, 4 * hq, hq, e, pf + "ff2", s);
   }
   return w;
+}
+
+// The receiver's last reads of the layer's weight panels are enqueued.
+void release_weights(Ctx& c, const WeightPanels& w, cudaStream_t s) {
+  release_panels(c, w.qkv, s);
+  release_panels(c, w.proj, s);
+  release_panels(c, w.ff1, s);
+  release_panels(c, w.ff2, s);
 }
 
 // ----------------------------------------------------------------- FF
@@ -727,6 +738,7 @@ void layer_forward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     default:
       fail(TESS_ERR_INVALID, "unknown layer op");
   }
+  release_weights(c, wp, s);
   join_comm(c, s);
   if (y != y_out) async_d2h(c, "stage.y", y_out, y, act, s);
   c.fwd_x[c.cache_slot * 8 + (int)op] = x;  // the backward needs the forward input
@@ -812,6 +824,7 @@ void layer_backward(Ctx& c, tess_layer_op op, DType t, const RankDims& rd,
     default:
       fail(TESS_ERR_INVALID, "unknown layer op");
   }
+  release_weights(c, wp, s);
   // deferred weight/LN-gradient communication completes before we return
   join_comm(c, s);
   if (dx != dx_out) async_d2h(c, "stage.dx", dx_out, dx, act, s);

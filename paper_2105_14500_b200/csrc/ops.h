@@ -21,6 +21,11 @@ struct Out {
   void* z = nullptr;  // pre-activation (Gelu)
   int64_t ldz = 0;
   float alpha = 1.0f;
+  // fused bias / dropout (GemmDesc; tess_matmul_ex)
+  const float* bias = nullptr;
+  float drop_p = 0.f;
+  uint64_t drop_seed = 0;
+  int64_t drop_row0 = 0, drop_col0 = 0;
 };
 
 // Launches one local GEMM (tcgen05 for bf16, CUDA cores for fp32); failures
@@ -29,10 +34,19 @@ struct Out {
 void run_gemm(const GemmDesc& g, cudaStream_t s);
 
 // The q panels of one operand after a family broadcast (slot t -> ptr[t]).
+// With the SM-free transport (Comm::panel_async) a remote panel may still be
+// landing: its GEMM waits on flags[t] >= epoch[t] (GemmReady), and the
+// receiver releases the link once its last reader is enqueued
+// (release_panels).
 struct Panels {
   bool valid = false;
   void* ptr[kMaxSegments] = {};
+  const uint32_t* flags[kMaxSegments] = {};
+  uint32_t epoch[kMaxSegments] = {};
+  Family fam = COL;
+  std::string tag;
 };
+void release_panels(Ctx& c, const Panels& p, cudaStream_t s);
 
 // Broadcasts every slot's panel of a weight-style operand over family f on
 // the comm stream ahead of its use (the weight panels of a whole layer do

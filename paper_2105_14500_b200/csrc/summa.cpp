@@ -19,8 +19,11 @@
 //    the remaining backward compute.
 // The collective sequence (kind, family, root, payload elements) is the
 // reference's, so the host meter reproduces its CommStats.
+#include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "kernels/kernels.h"
 #include "ops.h"
@@ -43,6 +46,11 @@ GemmDesc base_desc(DType in, int64_t M, int64_t N, const Out& out) {
   g.ldz = out.ldz ? out.ldz : g.ldc;
   g.alpha = out.alpha;
   g.epi = out.epi;
+  g.bias = out.bias;
+  g.drop_p = out.drop_p;
+  g.drop_seed = out.drop_seed;
+  g.drop_row0 = out.drop_row0;
+  g.drop_col0 = out.drop_col0;
   return g;
 }
 
@@ -118,7 +126,59 @@ void pair_reduce_owner(Ctx& c, Family f, const GemmDesc& g, int64_t k, float* pa
   if (!c.comm_noop) c.comm->pair_close(f, s);
 }
 
+// SM-free panel transport usable for family f with `in` operands: the GEMM
+// may then start before remote panels land (tcgen05 GEMMs wait on device
+// flags; the fp32 CUDA-core path does not, so it keeps the event order).
+bool panels_async(Ctx& c, Family f, DType in) {
+  return c.grid.group_size(f) > 1 && !c.comm_noop && in == DType::BF16 &&
+         c.comm->panel_async(f);
+}
+
+// Rows per transfer chunk of a panel with `rows` stored rows: about
+// 32 / q chunks (<= 16) of whole `align` rows (the GEMM's tile rows, or its
+// k-block when the panel's rows are the contraction), so the GEMM's first
+// tiles start once their chunk landed instead of the whole panel.
+int64_t chunk_rows_for(int64_t rows, int64_t align, int q) {
+  const int64_t target = std::min<int64_t>(16, 32 / std::max(q, 1));
+  int64_t cr = (rows + target - 1) / target;
+  cr = ((cr + align - 1) / align) * align;
+  return std::max<int64_t>(cr, align);
+}
+
+// One panel of a SUMMA step over family f from slot t: the receiver's copy
+// may be in flight (flags); `local` is this rank's own panel (used in place
+// at the root). Returns the panel pointer; records the flags in *flags /
+// *epoch and the link in `links` when the panel is remote.
+const void* panel_step(Ctx& c, Family f, int t, const std::string& tag, const void* local,
+                       int64_t rows, int64_t cols, size_t esz, int64_t chunk_rows,
+                       cudaStream_t cs, const uint32_t** flags, uint32_t* epoch,
+                       std::vector<std::pair<Family, std::string>>& links) {
+  const bool root = c.grid.slot_in_group(c.coord, f) == t;
+  const size_t bytes = (size_t)(rows * cols) * esz;
+  void* dst = root || c.comm->panel_owns_buffers() ? nullptr : c.ws->get(tag, bytes);
+  const Comm::PanelRecv r =
+      coll_bcast_panel(c, f, t, tag, root ? local : nullptr, dst, bytes, (uint64_t)(rows * cols),
+                       (size_t)(chunk_rows > 0 ? chunk_rows : rows) * cols * esz, cs);
+  if (r.flags) {
+    *flags = r.flags;
+    *epoch = r.epoch;
+    links.push_back({f, tag});
+  }
+  return r.buf;
+}
+
+void release_links(Ctx& c, const std::vector<std::pair<Family, std::string>>& links,
+                   cudaStream_t s) {
+  for (const auto& l : links) c.comm->panel_done(l.first, l.second, s);
+}
+
 }  // namespace
+
+void release_panels(Ctx& c, const Panels& p, cudaStream_t s) {
+  if (!p.valid || p.tag.empty()) return;
+  for (int t = 0; t < c.grid.q; ++t)
+    if (p.flags[t]) c.comm->panel_done(p.fam, p.tag + std::to_string(t), s);
+}
 
 void join_comm(Ctx& c, cudaStream_t s) { stream_dep(c, comm_stream(c, s), s); }
 
@@ -130,14 +190,34 @@ Panels prefetch_panels(Ctx& c, Family f, const void* local, int64_t rows, int64_
   cudaStream_t cs = comm_stream(c, s);
   stream_dep(c, s, cs);
   const int mine = c.grid.slot_in_group(c.coord, f);
+  // bf16 weight panels (the only prefetched operands) may use the SM-free
+  // transport: their GEMMs then wait on the panels' flags, not on cs
+  const bool async = panels_async(c, f, esz == 2 ? DType::BF16 : DType::F32);
+  std::vector<std::pair<Family, std::string>> links;
   for (int t = 0; t < q; ++t) {
+    if (async) {
+      p.ptr[t] = const_cast<void*>(panel_step(c, f, t, tag + std::to_string(t), local, rows, cols,
+                                              esz, 0, cs, &p.flags[t], &p.epoch[t], links));
+      continue;
+    }
     void* buf = t == mine ? const_cast<void*>(local)
                           : c.ws->get(tag + std::to_string(t), rows * cols * esz);
     coll_bcast(c, f, t, buf, rows * cols * esz, (uint64_t)(rows * cols), cs);
     p.ptr[t] = buf;
   }
   p.valid = true;
+  p.fam = f;
+  p.tag = async ? tag : std::string();
   return p;
+}
+
+// Are all of a prefetched operand's remote panels flag-tracked?
+bool panels_flagged(const Ctx& c, const Panels* bp, Family f) {
+  if (!bp || !bp->valid || bp->tag.empty()) return false;
+  const int mine = c.grid.slot_in_group(c.coord, f);
+  for (int t = 0; t < c.grid.q; ++t)
+    if (t != mine && !bp->flags[t]) return false;
+  return true;
 }
 
 void nn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t ak, const void* b,
@@ -150,25 +230,53 @@ void nn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t ak, const v
   g.nseg = q;
   g.lda = ak;
   g.ldb = bn;
+  // Both families are probed on every rank (the probes are collective).
+  const bool pa = panels_async(c, ROW, in);
+  const bool pb = panels_async(c, COL, in);
+  const bool prefetched = bp && bp->valid;
+  bool join = false;  // some panel moved by an event-ordered collective
+  std::vector<std::pair<Family, std::string>> links;
+  const int64_t crows = pa ? chunk_rows_for(ar, 256, q) : 0;
   stream_dep(c, s, cs);  // A (and B) produced on the compute stream
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:39: row broadcast of A(h, t) from slot t
-    void* at = c.coord.j == t ? const_cast<void*>(a)
-                              : c.ws->get("nn.a" + std::to_string(t), ar * ak * esz);
-    coll_bcast(c, ROW, t, at, ar * ak * esz, (uint64_t)(ar * ak), cs);
-    // ref algorithms.cpp:40: column broadcast of B(t, j) from slot t
-    void* bt;
-    if (bp && bp->valid) {
-      bt = bp->ptr[t];
+    const void* at;
+    if (pa) {
+      at = panel_step(c, ROW, t, "nn.a" + std::to_string(t), a, ar, ak, esz, crows, cs,
+                      &g.ready.a_flags[t], &g.ready.a_epoch[t], links);
     } else {
-      bt = c.coord.i == t ? const_cast<void*>(b)
-                          : c.ws->get("nn.b" + std::to_string(t), ak * bn * esz);
-      coll_bcast(c, COL, t, bt, ak * bn * esz, (uint64_t)(ak * bn), cs);
+      void* buf = c.coord.j == t ? const_cast<void*>(a)
+                                 : c.ws->get("nn.a" + std::to_string(t), ar * ak * esz);
+      coll_bcast(c, ROW, t, buf, ar * ak * esz, (uint64_t)(ar * ak), cs);
+      at = buf;
+      join = join || q > 1;
+    }
+    // ref algorithms.cpp:40: column broadcast of B(t, j) from slot t
+    const void* bt;
+    if (prefetched) {
+      bt = bp->ptr[t];
+      g.ready.b_flags[t] = bp->flags[t];
+      g.ready.b_epoch[t] = bp->epoch[t];
+    } else if (pb) {
+      bt = panel_step(c, COL, t, "nn.b" + std::to_string(t), b, ak, bn, esz, 0, cs,
+                      &g.ready.b_flags[t], &g.ready.b_epoch[t], links);
+    } else {
+      void* buf = c.coord.i == t ? const_cast<void*>(b)
+                                 : c.ws->get("nn.b" + std::to_string(t), ak * bn * esz);
+      coll_bcast(c, COL, t, buf, ak * bn * esz, (uint64_t)(ak * bn), cs);
+      bt = buf;
+      join = join || q > 1;
     }
     g.seg[t] = {at, bt, ak};
   }
-  stream_dep(c, cs, s);  // panels landed
+  if (prefetched && !panels_flagged(c, bp, COL)) join = join || q > 1;
+  if (join) stream_dep(c, cs, s);  // event order: every panel landed
+  if (pa) {
+    g.ready.chunk_rows = crows;
+    g.ready.chunks = (int)((ar + crows - 1) / crows);
+  }
   if (ar > 0 && bn > 0) run_gemm(g, s);
+  release_links(c, links, s);
   stream_dep(c, s, cs);  // panel buffers free for the next broadcasts
 }
 
@@ -186,21 +294,34 @@ void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
                          : (into_out ? static_cast<float*>(out.c)
                                      : static_cast<float*>(c.ws->get("nt.r", n * 4)));
   stream_dep(c, s, cs);
+  const bool pb = !direct && panels_async(c, COL, in);
+  const bool prefetched = bp && bp->valid;
   if (!direct && use_pair_reduce(c, ROW)) {
     // collectives in the reference's order (algorithms.cpp:53-56): panels
     // move now, the row reduces are fused into the owner GEMM below
-    void* bts[2];
+    const void* bts[2];
+    const uint32_t* bfl[2] = {nullptr, nullptr};
+    uint32_t bep[2] = {0, 0};
+    bool join = false;
+    std::vector<std::pair<Family, std::string>> links;
     for (int t = 0; t < 2; ++t) {
-      if (bp && bp->valid) {
+      if (prefetched) {
         bts[t] = bp->ptr[t];
+        bfl[t] = bp->flags[t];
+        bep[t] = bp->epoch[t];
+      } else if (pb) {
+        bts[t] = panel_step(c, COL, t, "nt.b" + std::to_string(t), b, br, an, esz, 0, cs, &bfl[t],
+                            &bep[t], links);
       } else {
-        bts[t] = c.coord.i == t ? const_cast<void*>(b)
-                                : c.ws->get("nt.b" + std::to_string(t), br * an * esz);
-        coll_bcast(c, COL, t, bts[t], br * an * esz, (uint64_t)(br * an), cs);
+        void* buf = c.coord.i == t ? const_cast<void*>(b)
+                                   : c.ws->get("nt.b" + std::to_string(t), br * an * esz);
+        coll_bcast(c, COL, t, buf, br * an * esz, (uint64_t)(br * an), cs);
+        bts[t] = buf;
+        join = true;
       }
       coll_reduce_note(c, ROW, t, n);
     }
-    stream_dep(c, cs, s);
+    if (join || (prefetched && !panels_flagged(c, bp, COL))) stream_dep(c, cs, s);
     const int me = c.coord.j;
     GemmDesc g = base_desc(in, ar, br, Out());
     g.trans_b = true;
@@ -208,22 +329,28 @@ void nt_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
     g.ldb = an;
     float* part = pair_part(c, ROW, "nt.p0", n, s);
     g.seg[0] = {a, bts[1 - me], an};
+    g.ready.b_flags[0] = bfl[1 - me];
+    g.ready.b_epoch[0] = bep[1 - me];
     pair_gemm(g, an, part, nullptr, n, s);  // contribution to the partner (slot 1-me)
     g.seg[0] = {a, bts[me], an};
+    g.ready.b_flags[0] = bfl[me];
+    g.ready.b_epoch[0] = bep[me];
     pair_reduce_owner(c, ROW, g, an, part, result, n, s);
+    release_links(c, links, s);
     if (!into_out) finish(result, ar, br, out, s);
     stream_dep(c, s, cs);  // panel buffers free for the next broadcasts
     return;
   }
   for (int t = 0; t < q; ++t) {
     // ref algorithms.cpp:53: column broadcast of B(t, j)
-    void* bt;
+    const void* bt;
     if (bp && bp->valid) {
       bt = bp->ptr[t];
     } else {
-      bt = c.coord.i == t ? const_cast<void*>(b)
-                          : c.ws->get("nt.b" + std::to_string(t & 1), br * an * esz);
-      coll_bcast(c, COL, t, bt, br * an * esz, (uint64_t)(br * an), cs);
+      void* buf = c.coord.i == t ? const_cast<void*>(b)
+                                 : c.ws->get("nt.b" + std::to_string(t & 1), br * an * esz);
+      coll_bcast(c, COL, t, buf, br * an * esz, (uint64_t)(br * an), cs);
+      bt = buf;
     }
     stream_dep(c, cs, s);  // B(t) landed; partial buffer t&1 released by reduce t-2
     GemmDesc g;
@@ -274,26 +401,48 @@ void tn_product(Ctx& c, DType in, const void* a, int64_t ar, int64_t an, const v
                                      : static_cast<float*>(c.ws->get(rname, n * 4)));
   stream_dep(c, s, cs);
   if (!direct && use_pair_reduce(c, COL)) {
-    void* ats[2];
+    // The activation panels A(h, t) may use the SM-free transport in chunks
+    // of the contraction (their rows): the GEMMs start on the first chunk.
+    const bool pa = panels_async(c, ROW, in);
+    const int64_t crows = pa ? chunk_rows_for(ar, 64, 2) : 0;
+    const void* ats[2];
+    const uint32_t* afl[2] = {nullptr, nullptr};
+    uint32_t aep[2] = {0, 0};
+    std::vector<std::pair<Family, std::string>> links;
     for (int t = 0; t < 2; ++t) {
       // ref algorithms.cpp:67-70: row broadcast of A(h, t), column reduce to
       // slot t (fused into the owner GEMM below)
-      ats[t] = c.coord.j == t ? const_cast<void*>(a)
-                              : c.ws->get("tn.a" + std::to_string(t), ar * an * esz);
-      coll_bcast(c, ROW, t, ats[t], ar * an * esz, (uint64_t)(ar * an), cs);
+      if (pa) {
+        ats[t] = panel_step(c, ROW, t, "tn.a" + std::to_string(t), a, ar, an, esz, crows, cs,
+                            &afl[t], &aep[t], links);
+      } else {
+        void* buf = c.coord.j == t ? const_cast<void*>(a)
+                                   : c.ws->get("tn.a" + std::to_string(t), ar * an * esz);
+        coll_bcast(c, ROW, t, buf, ar * an * esz, (uint64_t)(ar * an), cs);
+        ats[t] = buf;
+      }
       coll_reduce_note(c, COL, t, n);
     }
-    stream_dep(c, cs, s);
+    if (!pa) stream_dep(c, cs, s);
     const int me = c.coord.i;
     GemmDesc g = base_desc(in, an, bn, Out());
     g.trans_a = true;
     g.lda = an;
     g.ldb = bn;
+    if (pa) {
+      g.ready.chunk_rows = crows;
+      g.ready.chunks = (int)((ar + crows - 1) / crows);
+    }
     float* part = pair_part(c, COL, "tn.p0", n, s);
     g.seg[0] = {ats[1 - me], b, ar};
+    g.ready.a_flags[0] = afl[1 - me];
+    g.ready.a_epoch[0] = aep[1 - me];
     pair_gemm(g, ar, part, nullptr, n, s);
     g.seg[0] = {ats[me], b, ar};
+    g.ready.a_flags[0] = afl[me];
+    g.ready.a_epoch[0] = aep[me];
     pair_reduce_owner(c, COL, g, ar, part, result, n, s);
+    release_links(c, links, s);
     stream_dep(c, s, cs);
     // ref algorithms.cpp:72-74: depth all-reduce of the layer partial
     if (depth) coll_allreduce(c, DEPTH, result, n, cs);
