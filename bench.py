@@ -477,7 +477,8 @@ def main():
     # SHARE of the step, cold-cache and serialised) x this run's step time
     share = None
     sp = os.path.join(ROOT, "profiles", "ncu_launch_share.json")
-    if os.path.exists(sp):
+    # the committed ncu captures are of the cfg4 step: not quoted for cfg5
+    if os.path.exists(sp) and not cfg5:
         with open(sp) as f:
             share = json.load(f).get(top)
     achieved_ncu = (top_flops / top_n) / (share * ms / (top_n / K) * 1e-3) / 1e12 \
@@ -486,7 +487,7 @@ def main():
     # capture of one step (tools/ncu_step.py -> tools/ncu_digest.py)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_kernel_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and not cfg5:
         with open(tp) as f:
             traffic = json.load(f).get(top, {}).get("dram_bytes_per_launch")
     burst = None

@@ -102,6 +102,14 @@ class BlockGradsC(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in PARAM_NAMES]
 
 
+class EpilogueC(C.Structure):
+    """tess_epilogue: fused bias / GeLU / dropout-scale / residual of a local
+    product (tess_matmul_ex)."""
+    _fields_ = [("bias", C.c_void_p), ("gelu", C.c_int), ("pre_activation", C.c_void_p),
+                ("dropout_p", C.c_float), ("dropout_seed", C.c_uint64), ("row0", C.c_int64),
+                ("col0", C.c_int64), ("residual", C.c_void_p)]
+
+
 class CommStatsC(C.Structure):
     _fields_ = [("sent_messages", C.c_uint64), ("sent_elements", C.c_uint64),
                 ("received_messages", C.c_uint64), ("received_elements", C.c_uint64),
@@ -173,6 +181,9 @@ def _load() -> C.CDLL:
         "tess_megatron_layer_run": ([i, C.POINTER(_LayerDimsC), i, i, dp, dp, C.POINTER(dp),
                                      C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
         "tess_inject_fault": ([vp, i, i64], i),
+        "tess_matmul_ex": ([vp, i, i, vp, i64, i64, vp, i64, i64, vp, i, u32,
+                            C.POINTER(EpilogueC), vp], i),
+        "tess_dropout_keep": ([C.c_uint64, i64, i64, C.c_float], i),
         "tess_set_global_fault": ([i, i, i64], i),
         "tess_stack_run": ([i, C.POINTER(_LayerDimsC), i, i, i, i, i, dp, dp, C.POINTER(dp),
                             C.c_double, dp, dp, C.POINTER(dp), ip, u64p, u64p], i),
@@ -506,6 +517,25 @@ def megatron_1d_linear(x, w1, w2, p: int, dtype="f32",
     return AlgoResult(out, CommStats(sr, sk))
 
 
+def dropout_keep(seed: int, rows, cols, p: float) -> np.ndarray:
+    """Keep-mask of the fused dropout epilogue for global element
+    coordinates (tess_dropout_keep; vectorised host restatement)."""
+    rows = np.asarray(rows, dtype=np.uint64)
+    cols = np.asarray(cols, dtype=np.uint64)
+    if p <= 0:
+        return np.ones(np.broadcast(rows, cols).shape, dtype=bool)
+    th = np.uint64(min(1 << 24, int(np.ceil(np.float64(np.float32(p)) * (1 << 24)))))
+    with np.errstate(over="ignore"):
+        x = np.uint64(seed) ^ (rows * np.uint64(0x9E3779B97F4A7C15)) ^ \
+            (cols * np.uint64(0xC2B2AE3D27D4EB4F))
+        x ^= x >> np.uint64(31)
+        x *= np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(29)
+        x *= np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(32)
+    return (x >> np.uint64(40)) >= th
+
+
 FAULTS = {"none": 0, "perturb": 1, "rank_fail": 2, "skip_collective": 3}
 
 
@@ -712,10 +742,19 @@ class RankContext:
                                     global_ptr, stream))
 
     def matmul(self, variant: str, dtype, a, a_rows, a_cols, b, b_rows, b_cols, c, c_dtype="f32",
-               accumulate=False, sum_over_depth=False, stream=0):
+               accumulate=False, sum_over_depth=False, stream=0, epilogue=None):
+        """Local SUMMA product (tess_matmul); `epilogue` (dict of EpilogueC
+        fields: bias, gelu, pre_activation, dropout_p, dropout_seed, row0,
+        col0, residual) selects tess_matmul_ex's fused epilogue."""
         flags = (1 if accumulate else 0) | (2 if sum_over_depth else 0)
-        _check(lib.tess_matmul(self.h, _VARIANTS[variant], _dtype(dtype), a, a_rows, a_cols, b,
-                               b_rows, b_cols, c, _dtype(c_dtype), flags, stream))
+        if epilogue is None:
+            _check(lib.tess_matmul(self.h, _VARIANTS[variant], _dtype(dtype), a, a_rows, a_cols,
+                                   b, b_rows, b_cols, c, _dtype(c_dtype), flags, stream))
+            return
+        ep = EpilogueC(**epilogue)
+        _check(lib.tess_matmul_ex(self.h, _VARIANTS[variant], _dtype(dtype), a, a_rows, a_cols,
+                                  b, b_rows, b_cols, c, _dtype(c_dtype), flags, C.byref(ep),
+                                  stream))
 
     def layer_forward(self, op, dtype, dims: LayerDims, shard: BlockShardC, x, y,
                       bias_row0=None, stream=0):
