@@ -846,13 +846,14 @@ bool encode_3d(CUtensorMap* map, const void* base, int64_t cols, int64_t seq, in
 template <int HD>
 cudaError_t launch_fwd(const FwdParams& p, int grid, cudaStream_t s) {
   using C = FwdCfg<HD>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<HD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // once per instantiation and process (host threads of in-process ranks race here)
+  static cudaError_t attr = cudaSuccess;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM_BYTES);
+  });
+  if (attr != cudaSuccess) return attr;
   attn_fwd_kernel<HD><<<grid, kThreads, C::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
@@ -860,13 +861,14 @@ cudaError_t launch_fwd(const FwdParams& p, int grid, cudaStream_t s) {
 template <int HD>
 cudaError_t launch_bwd(const BwdParams& p, int grid, cudaStream_t s) {
   using C = BwdCfg<HD>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<HD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // once per instantiation and process (host threads of in-process ranks race here)
+  static cudaError_t attr = cudaSuccess;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM_BYTES);
+  });
+  if (attr != cudaSuccess) return attr;
   attn_bwd_kernel<HD><<<grid, kBwdThreads, C::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
