@@ -458,9 +458,11 @@ tess_status tess_profile_read(double* gemm_ms, double* gemm_flops, uint64_t* gem
  * {"<kernel>": [device_ms, algorithmic_flops, launches], ...}. */
 tess_status tess_profile_json(char* buf, size_t cap, size_t* needed);
 
-/* Debug: with TESS_ATTN_TRACE set, the fused attention backward records
- * per-phase clock64 stamps of its CTA 0 ([8 events][64 tiles]); copies the
- * last trace into out (up to 512 values). No reference counterpart. */
+/* Debug: copies the last attention phase trace (clock64 stamps of CTA 0,
+ * recorded with TESS_ATTN_TRACE set) into out (up to 512 values);
+ * TESS_ERR_INVALID when none was recorded. Only the tool-only kernel
+ * experiments (csrc/tools/attn_bwd_experiments.cuh) record one; the shipped
+ * kernels carry no trace code. No reference counterpart. */
 tess_status tess_debug_attn_trace(long long* out, int n);
 
 /* Test hook of the peer-window transport behind the fused pair reduce of the

@@ -32,8 +32,7 @@ struct AttnDesc {
   // backward only
   const void* dout = nullptr;  // dO bf16, same layout as o (ld_o)
   const float* delta = nullptr;  // [samples, H, S] rowsum(dO * O)
-  void* dqkv = nullptr;        // bf16, same layout as qkv (ld_qkv): dK, dV written
-  void* dst = nullptr;         // bf16 [samples * H, S keys, S queries]: dS^T for dQ = dS K
+  void* dqkv = nullptr;        // bf16, same layout as qkv (ld_qkv): dQ, dK, dV written
 };
 
 // True when the fused kernels support this shape (head_dim 64 or 128, seq a
@@ -42,14 +41,17 @@ struct AttnDesc {
 bool attn_fused_supported(const AttnDesc& d);
 
 cudaError_t attn_fwd_sm100(const AttnDesc& d, cudaStream_t s);
-// Writes dK and dV (bf16) into dqkv and the UNSCALED dS^T = (P (dP - delta))^T
-// into dst; the caller finishes dQ = scale * dS K with one batched tcgen05
-// GEMM over dst (alpha = scale; deterministic: no atomics).
-cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s);
+// The backward is two passes, neither of which writes S, P or dS to HBM
+// (both recompute them from lse and delta = rowsum(dO * O); deterministic):
+// dK, dV pass: dK = scale * dS^T Q, dV = P^T dO, one 128-key tile per CTA.
+cudaError_t attn_bwd_kv_sm100(const AttnDesc& d, cudaStream_t s);
+// dQ pass: dQ = scale * dS K, one 128-query tile per CTA.
+cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s);
 
 const char* attn_last_error();
 
-// Debug (TESS_ATTN_TRACE): device buffer of the last traced backward, or null.
+// Debug: device buffer of the last traced attention kernel (set only by the
+// tool-only experiments under csrc/tools with TESS_ATTN_TRACE), or null.
 long long* attn_debug_trace();
 
 }  // namespace tess

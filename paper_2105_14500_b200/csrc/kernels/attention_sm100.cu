@@ -76,7 +76,6 @@ constexpr int kThreads = 320;
 #define TESS_ATTN_FWD_POLY 0
 #endif
 constexpr int kFwdPolyMask = TESS_ATTN_FWD_POLY;
-constexpr int kBwdThreads = 576;  // backward: TMA + MMA warps + 16 softmax-gradient warps
 constexpr int BQ = 128;   // query rows per tile (UMMA M)
 constexpr int BKV = 128;  // keys per tile (UMMA N of S, K of P V)
 constexpr float kLog2e = 1.4426950408889634f;
@@ -382,82 +381,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 
 
 // --------------------------------------------------------------- backward
-// One CTA = one (sample, head, 128-key tile); it walks the 128-query tiles
-// i of the sequence. 320 threads:
-//   warp 0      TMA producer: K, V of the key tile once; then Q_i, dO_i
-//               (128 x hd, boxes {64, 128}) through a RING-slot FIFO.
-//   warp 1      MMA issuer + TMEM owner. Per query tile, all MMAs at
-//               M=128, N=128 (full tcgen05 rate; N=64 tiles run at ~70 %):
-//                 S^T(i) = K Q_i^T, dP^T(i) = V dO_i^T   (A = K / V, smem)
-//                 dV += P^T(i) dO_i   (A = P^T in TMEM, written by the softmax
-//                                      over the consumed S^T columns)
-//                 dK += dS^T(i) Q_i   (A = dS^T in shared memory)
-//               S^T / dP^T are single-buffered (TMEM holds S^T, dP^T, dV, dK);
-//               dP^T(i+1) is issued as soon as tile i's scores sit in
-//               registers; dV(i) as soon as P^T(i) is in TMEM (its own
-//               barrier, before the dS^T stores), S^T(i+1) right behind it,
-//               then dK(i) once dS^T(i) is in shared memory -- the next
-//               tile's softmax overlaps dK(i) (-4 %, r2_attn_bwd_order_ab).
-//   warps 2-17  four groups of 4 warps split each tile's 128 queries (group
-//               g: columns [32g, 32g+32)); thread = key row (TMEM lane):
-//               P^T = 2^(c*S^T - lse[q]) -> TMEM (bf16 pairs), dS^T = P^T
-//               (dP^T - delta[q]) -> shared memory (UMMA K-major SW128, chunk
-//               g/2) and, by TMA store, to HBM for dQ = dS K (one batched
-//               GEMM; the 1/sqrt(hd) goes to dK's epilogue and dQ's alpha).
-// Q_i and dO_i tiles are used twice with different majorness: K-major B of
-// the score MMAs ([N=q][K=hd]) and MN-major B of dV/dK ([K=q][N=hd]) -- the
-// same bytes under two descriptors.
-// TMEM: S^T / P^T [0,128), dP^T [128,256), dV [256, 256+hd), dK [384, 384+hd).
-constexpr int BQB = 128;  // queries per backward tile
 // which of every 4 exponentials of the backward use exp2_fma (bit u)
 #ifndef TESS_ATTN_BWD_POLY
 #define TESS_ATTN_BWD_POLY 8
 #endif
 constexpr int kBwdPolyMask = TESS_ATTN_BWD_POLY;
-
-struct BwdParams {
-  CUtensorMap tm_kv;   // qkv view, box {64, 128}: K, V of the key tile
-  CUtensorMap tm_q;    // qkv view, box {64, 128}: Q_i
-  CUtensorMap tm_do;   // dO view [hq cols, S, samples], box {64, 128}
-  CUtensorMap tm_dst;  // dS^T view [S q, S k, samples*H], box {64, 128} (store)
-  int S, H, n_kt, n_qt;
-  float c;      // scale * log2(e)
-  float scale;  // 1/sqrt(hd)
-  const float* lse;
-  const float* delta;
-  __nv_bfloat16* dqkv;
-  long long ld_qkv;
-  long long* trace;  // debug (TESS_ATTN_TRACE): per-phase clock64 of CTA 0, [event][tile]
-};
-
-// trace events (CTA 0 only)
-enum {
-  TR_MMA_S = 0, TR_MMA_P = 1, TR_SM_IN = 2, TR_SM_MATH = 3, TR_SM_OUT = 4,
-  TR_SM_LOADED = 5, TR_MMA_FREE = 6, TR_MMA_GDONE = 7, TR_N = 8
-};
-__device__ __forceinline__ void trace_ev(const BwdParams& p, int ev, int tile) {
-  if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
-}
-
-template <int HD>
-struct BwdCfg {
-  static constexpr int KV_BYTES = 128 * HD * 2;    // K or V tile
-  static constexpr int SLOT_BYTES = BQB * HD * 2;  // Q_i or dO_i
-  static constexpr int RING = HD == 128 ? 4 : 8;
-  static constexpr int DS_BYTES = 128 * BQB * 2;   // dS^T tile (2 chunks of 64 queries)
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = KV_BYTES;
-  static constexpr int OFF_RING = 2 * KV_BYTES;
-  static constexpr int OFF_DS = OFF_RING + RING * SLOT_BYTES;
-  static constexpr int OFF_LD = OFF_DS + DS_BYTES;  // 4 groups x 2 bufs: lse 32 | delta 32
-  static constexpr int OFF_BAR = OFF_LD + 4 * 2 * 64 * 4;
-  static constexpr int USED = OFF_BAR + 512;
-  // the dynamic window is 1024-aligned in practice; the kernel checks and
-  // traps if the slack we could afford does not cover its misalignment
-  static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
-  static constexpr int TMEM_COLS = 512;
-  static constexpr int TM_ST = 0, TM_DPT = 128, TM_DV = 256, TM_DK = 384;
-};
 
 
 // 32 bf16 values of row r (columns [u0*8, u0*8+32) of a 64-column K-major
@@ -473,53 +401,104 @@ __device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const 
   }
 }
 
+// ---------------------------------------------------- backward: dK, dV pass
+// dV = P^T dO and dK = scale * dS^T Q for one 128-key tile per CTA, walking
+// the query tiles; dQ is the separate dQ pass below (no dS leaves the SM in
+// either). 320 threads:
+//   warp 0      TMA: K, V once; Q_i (+ its lse and delta rows) and dO_i into
+//               two-slot rings.
+//   warp 1      MMA issuer (warp-wide, one elected lane; descriptors built
+//               once from warp-uniform bases), all M=128 N=128:
+//                 dV += P^T(i) dO_i          (A = P^T in TMEM)
+//                 S^T(i+1) = K Q_{i+1}^T     (over the consumed P^T, in order)
+//                 dP^T(i+1) = V dO_{i+1}^T   (once dP^T(i) is in registers)
+//                 dK += dS^T(i) Q_i          (A = dS^T in shared memory)
+//   warps 2-9   thread = key row, group g = queries [64g, 64g+64):
+//               P^T = 2^(c S^T - lse) -> bf16 pairs over the thread's own
+//               consumed S^T columns (no cross-warp barrier), then
+//               dS^T = P^T (dP^T - delta) -> shared memory (unscaled; the
+//               1/sqrt(hd) goes to dK's epilogue); at the end dK, dV out.
+// TMEM: S^T / P^T [0,128), dP^T [128,256), dV [256,256+hd), dK [384,384+hd).
+constexpr int kKvThreads = 320;
+
+struct KvParams {
+  CUtensorMap tm_kv;   // qkv view [3*H*hd, S, samples], box {64, 128}: K, V, Q tiles
+  CUtensorMap tm_do;   // dO view [H*hd, S, samples], box {64, 128}
+  CUtensorMap tm_lse;  // lse [S, samples*H] fp32, box {128, 1} (rows past S read 0)
+  CUtensorMap tm_dlt;  // delta, same view
+  int S, H, n;         // n = key tiles = query tiles
+  float c, scale;
+  __nv_bfloat16* dqkv;
+  long long ld_qkv;
+};
+
 template <int HD>
-__global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
-  using C = BwdCfg<HD>;
+struct KvCfg {
+  static constexpr int TILE = 128 * HD * 2;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = TILE;
+  static constexpr int OFF_Q = 2 * TILE;         // 2 slots
+  static constexpr int OFF_DO = 4 * TILE;        // 2 slots
+  static constexpr int OFF_DS = 6 * TILE;        // dS^T: 128 keys x 128 queries, 2 x 16 KB
+  static constexpr int OFF_LD = OFF_DS + 32768;  // per Q slot: lse[128] | delta[128]
+  static constexpr int OFF_BAR = OFF_LD + 2 * 1024;
+  static constexpr int USED = OFF_BAR + 256;
+  static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int TM_S = 0, TM_DP = 128, TM_DV = 256, TM_DK = 384;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid_constant__ KvParams p) {
+  using C = KvCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   if ((smem - smem_raw) + C::USED > C::SMEM_BYTES) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* kv_full = bars;                   // 1
-  uint64_t* r_full = bars + 1;                // RING
-  uint64_t* r_empty = r_full + C::RING;       // RING
-  uint64_t* sdp_full = r_empty + C::RING;     // 1: S^T(i) and dP^T(i) in TMEM
-  uint64_t* loaded = sdp_full + 1;            // 1: all 8 warps hold tile i's scores (count 8)
-  uint64_t* pds_full = loaded + 1;            // 1: dS^T (smem) written (count 16)
-  uint64_t* ds_free = pds_full + 1;           // 1: dK(i) done reading dS^T smem
-  uint64_t* st_free = ds_free + 1;            // 2: TMA store of dS^T chunk g done reading
-  uint64_t* fin = st_free + 2;                // 1
-  uint64_t* p_full = fin + 1;                 // 1: P^T (TMEM) written (count 16)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_full + 1);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;     // 2
+  uint64_t* q_empty = bars + 3;    // 2
+  uint64_t* do_full = bars + 5;    // 2
+  uint64_t* do_empty = bars + 7;   // 2
+  uint64_t* s_full = bars + 9;     // S^T(i) in TMEM
+  uint64_t* p_full = bars + 10;    // P^T(i) in TMEM (8 warps)
+  uint64_t* dp_full = bars + 11;   // dP^T(i) in TMEM
+  uint64_t* dp_loaded = bars + 12; // dP^T(i) in registers (8 warps)
+  uint64_t* ds_full = bars + 13;   // dS^T(i) in shared memory (8 warps)
+  uint64_t* ds_free = bars + 14;   // dK(i) has read dS^T(i)
+  uint64_t* fin = bars + 15;       // dK, dV complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int kt = blockIdx.x % p.n_kt;
-  const int head = (blockIdx.x / p.n_kt) % p.H;
-  const int smp = blockIdx.x / (p.n_kt * p.H);
+  const int n = p.n;
+  const int kt = blockIdx.x % n;
+  const int job = blockIdx.x / n;  // sample * H + head
+  const int head = job % p.H, smp = job / p.H;
   const int k0 = kt * 128;
   const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
 
   if (warp == 0 && lane == 0) {
     mbar_init(kv_full, 1);
-    for (int s = 0; s < C::RING; ++s) {
-      mbar_init(&r_full[s], 1);
-      mbar_init(&r_empty[s], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&do_full[s], 1);
+      mbar_init(&do_empty[s], 1);
     }
-    mbar_init(sdp_full, 1);
-    mbar_init(loaded, 16);
-    mbar_init(pds_full, 16);
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_loaded, 8);
+    mbar_init(ds_full, 8);
     mbar_init(ds_free, 1);
-    mbar_init(&st_free[0], 1);
-    mbar_init(&st_free[1], 1);  // chunk c's storer: group 2c
     mbar_init(fin, 1);
-    mbar_init(p_full, 16);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
-    prefetch_tmap(&p.tm_q);
     prefetch_tmap(&p.tm_do);
-    prefetch_tmap(&p.tm_dst);
+    prefetch_tmap(&p.tm_lse);
+    prefetch_tmap(&p.tm_dlt);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -535,252 +514,202 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------ TMA producer
-      mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
+      mbar_expect_tx(kv_full, 2 * C::TILE);
 #pragma unroll
       for (int c = 0; c < HD / 64; ++c) {
         tma_load_3d(smem + C::OFF_K + c * 16384, &p.tm_kv, kv_full, col_k + c * 64, k0, smp);
         tma_load_3d(smem + C::OFF_V + c * 16384, &p.tm_kv, kv_full, col_v + c * 64, k0, smp);
       }
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int i = 0; i < p.n_qt; ++i) {
+      for (int i = 0; i < n; ++i) {
+        const int s = i & 1, u = i >> 1;
+        if (u > 0) mbar_wait(&q_empty[s], (u - 1) & 1);
+        mbar_expect_tx(&q_full[s], C::TILE + 1024);
 #pragma unroll
-        for (int which = 0; which < 2; ++which) {  // Q_i then dO_i
-          mbar_wait(&r_empty[stage], phase ^ 1);
-          uint8_t* dst = smem + C::OFF_RING + stage * C::SLOT_BYTES;
-          mbar_expect_tx(&r_full[stage], C::SLOT_BYTES);
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_3d(smem + C::OFF_Q + s * C::TILE + c * 16384, &p.tm_kv, &q_full[s],
+                      col_q + c * 64, i * 128, smp);
+        tma_load_2d(smem + C::OFF_LD + s * 1024, &p.tm_lse, &q_full[s], i * 128, job);
+        tma_load_2d(smem + C::OFF_LD + s * 1024 + 512, &p.tm_dlt, &q_full[s], i * 128, job);
+        if (u > 0) mbar_wait(&do_empty[s], (u - 1) & 1);
+        mbar_expect_tx(&do_full[s], C::TILE);
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c) {
-            if (which == 0)
-              tma_load_3d(dst + c * 16384, &p.tm_q, &r_full[stage], col_q + c * 64, i * BQB, smp);
-            else
-              tma_load_3d(dst + c * 16384, &p.tm_do, &r_full[stage], head * HD + c * 64, i * BQB,
-                          smp);
-          }
-          if (++stage == C::RING) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_3d(smem + C::OFF_DO + s * C::TILE + c * 16384, &p.tm_do, &do_full[s],
+                      head * HD + c * 64, i * 128, smp);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------- MMA issuer
-      constexpr uint32_t idesc_s = idesc_bf16(128, BQB, false, false);
-      constexpr uint32_t idesc_g = idesc_bf16(128, HD, false, true);
-      const uint32_t sk = smem_u32(smem + C::OFF_K), sv = smem_u32(smem + C::OFF_V);
-      const uint32_t ring = smem_u32(smem + C::OFF_RING);
-      const uint32_t sds = smem_u32(smem + C::OFF_DS);
-      int stage = 0;
-      uint32_t phase = 0;
-      auto next_slot = [&]() {
-        const int s = stage;
-        mbar_wait(&r_full[s], phase);
-        tc_fence_after();
-        if (++stage == C::RING) {
-          stage = 0;
-          phase ^= 1;
-        }
-        return s;
-      };
-      // A [128 x HD] K-major (chunk stride 16 KB) times B [128 x HD] K-major
-      // (chunk stride 16 KB) -> TMEM columns [d, d + 128)
-      auto issue_scores = [&](uint32_t d, uint32_t a, uint32_t b) {
+    // ------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);  // S^T, dP^T
+    constexpr uint32_t idesc_g = idesc_bf16(128, HD, false, true);    // dV, dK
+    const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint64_t kmaj_k = make_sdesc(sbase + C::OFF_K, 16, 1024);
+    const uint64_t kmaj_v = make_sdesc(sbase + C::OFF_V, 16, 1024);
+    const uint64_t kmaj_q = make_sdesc(sbase + C::OFF_Q, 16, 1024);
+    const uint64_t kmaj_do = make_sdesc(sbase + C::OFF_DO, 16, 1024);
+    const uint64_t kmaj_ds = make_sdesc(sbase + C::OFF_DS, 16, 1024);
+    const uint64_t mn_q = make_sdesc(sbase + C::OFF_Q, 16384, 1024);
+    const uint64_t mn_do = make_sdesc(sbase + C::OFF_DO, 16384, 1024);
+    constexpr uint64_t kTile = (uint64_t)(C::TILE >> 4);
+    auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
+    auto issue_scores = [&](uint32_t d, uint64_t a, uint64_t b) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
-          mma_bf16(d, make_sdesc(a + off, 16, 1024), make_sdesc(b + off, 16, 1024), idesc_s,
-                   kk > 0 ? 1u : 0u);
-        }
-      };
-      mbar_wait(kv_full, 0);
+      for (int kk = 0; kk < HD / 16; ++kk)
+        mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+    };
+    mbar_wait(kv_full, 0);
+    mbar_wait(&q_full[0], 0);
+    tc_fence_after();
+    issue_scores(tm + C::TM_S, kmaj_k, kmaj_q);
+    mma_commit_warp(s_full);
+    mbar_wait(&do_full[0], 0);
+    tc_fence_after();
+    issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do);
+    mma_commit_warp(dp_full);
+    for (int i = 0; i < n; ++i) {
+      const int s = i & 1;
+      // dV += P^T(i) dO_i; P^T of queries [16kk, 16kk+16) at column 32(kk/2) + 8(kk%2)
+      mbar_wait(p_full, i & 1);
       tc_fence_after();
-      int qs = next_slot();
-      int ds = next_slot();
-      trace_ev(p, TR_MMA_S, 0);
-      issue_scores(tmem + C::TM_ST, sk, ring + qs * C::SLOT_BYTES);
-      issue_scores(tmem + C::TM_DPT, sv, ring + ds * C::SLOT_BYTES);
-      mma_commit(sdp_full);
-      for (int i = 0; i < p.n_qt; ++i) {
-        const bool more = i + 1 < p.n_qt;
-        int qn = 0, dn = 0;
-        // tile i's scores are in registers: dP^T(i+1) into the dP^T columns
-        mbar_wait(loaded, i & 1);
-        tc_fence_after();
-        trace_ev(p, TR_MMA_FREE, i);
-        if (more) {
-          qn = next_slot();
-          dn = next_slot();
-          issue_scores(tmem + C::TM_DPT, sv, ring + dn * C::SLOT_BYTES);
-        }
-        // dV(i) as soon as P^T(i) sits in TMEM
-        mbar_wait(p_full, i & 1);
-        tc_fence_after();
-        trace_ev(p, TR_MMA_P, i);
 #pragma unroll
-        for (int kk = 0; kk < BQB / 16; ++kk)  // dV += P^T dO_i, P^T from TMEM
-          mma_bf16_ts(tmem + C::TM_DV, tmem + C::TM_ST + kk * 8,
-                      make_sdesc(ring + ds * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
-                      idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&r_empty[ds]);
-        if (more) {
-          // S^T(i+1) over the P^T columns right behind dV(i) (in-order
-          // execution: dV has read them): tile i+1's softmax starts while
-          // dK(i) runs
-          trace_ev(p, TR_MMA_S, i + 1);
-          issue_scores(tmem + C::TM_ST, sk, ring + qn * C::SLOT_BYTES);
-          mma_commit(sdp_full);
-        }
-        // dK(i) once dS^T(i) is in shared memory
-        mbar_wait(pds_full, i & 1);
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_ts_warp(tm + C::TM_DV, tm + C::TM_S + 32 * (kk >> 1) + 8 * (kk & 1),
+                         mn_do + s * kTile + (uint64_t)kk * 128u, idesc_g,
+                         (i > 0 || kk > 0) ? 1u : 0u);
+      mma_commit_warp(&do_empty[s]);
+      if (i + 1 < n) {
+        const int sn = s ^ 1, un = (i + 1) >> 1;
+        mbar_wait(&q_full[sn], un & 1);
         tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BQB / 16; ++kk)  // dK += dS^T Q_i
-          mma_bf16(tmem + C::TM_DK,
-                   make_sdesc(sds + (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u, 16,
-                              1024),
-                   make_sdesc(ring + qs * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
-                   idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&r_empty[qs]);
-        mma_commit(ds_free);
-        trace_ev(p, TR_MMA_GDONE, i);
-        qs = qn;
-        ds = dn;
+        issue_scores(tm + C::TM_S, kmaj_k, kmaj_q + sn * kTile);
+        mma_commit_warp(s_full);
+        mbar_wait(dp_loaded, i & 1);
+        mbar_wait(&do_full[sn], un & 1);
+        tc_fence_after();
+        issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do + sn * kTile);
+        mma_commit_warp(dp_full);
       }
-      mma_commit(fin);
+      // dK += dS^T(i) Q_i
+      mbar_wait(ds_full, i & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_warp(tm + C::TM_DK, kmaj_ds + kmaj_off(kk), mn_q + s * kTile + (uint64_t)kk * 128u,
+                      idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
+      mma_commit_warp(&q_empty[s]);
+      mma_commit_warp(ds_free);
     }
+    mma_commit_warp(fin);
   } else {
     // ------------------------------------------ softmax-gradient warps
     const int quad = warp & 3;
-    const int g = (warp - 2) >> 2;   // query columns [32g, 32g+32) of each tile
-    const int r = quad * 32 + lane;  // key row within the tile
+    const int g = (warp - 2) >> 2;   // queries [64g, 64g+64) of each tile
+    const int r = quad * 32 + lane;  // key row within the tile (TMEM lane)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float cl2 = p.c, scale = p.scale;
-    // TMA store of dS^T chunk c (64 queries = groups 2c, 2c+1) by group 2c's thread
-    const bool storer = quad == 0 && lane == 0 && (g & 1) == 0;
-    const int chunk = g >> 1;
-    const float* lse_h = p.lse + ((long long)smp * p.H + head) * p.S;
-    const float* dlt_h = p.delta + ((long long)smp * p.H + head) * p.S;
-    // (lse, delta) of the group's 32 query columns staged through shared
-    // memory, double buffered per group: the quad-0 warp loads tile i+1's
-    // values while tile i is processed, a 128-thread named barrier at the
-    // start of each tile orders them against the readers.
-    const uint32_t ldg_base = smem_u32(smem + C::OFF_LD) + (uint32_t)g * 512u;  // [buf][lse|delta]
-    const bool ld_writer = quad == 0;
-    auto gload = [&](int i, float (&v)[2]) {
-      const int q = i * BQB + g * 32 + lane;
-      const bool ok = i < p.n_qt && q < p.S;
-      v[0] = ok ? __ldg(lse_h + q) : INFINITY;  // 2^(x - inf) = 0: no contribution
-      v[1] = ok ? __ldg(dlt_h + q) : 0.f;
-    };
-    auto sstore = [&](int i, const float (&v)[2]) {
-      const uint32_t a = ldg_base + (uint32_t)(i & 1) * 256u + lane * 4;
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[0]) : "memory");
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 128), "f"(v[1]) : "memory");
-    };
-    if (ld_writer) {
-      float v[2];
-      gload(0, v);
-      sstore(0, v);
-    }
-    const uint32_t ds_chunk = smem_u32(smem + C::OFF_DS) + (uint32_t)chunk * 16384u;
-    for (int i = 0; i < p.n_qt; ++i) {
-      const uint32_t ph = (uint32_t)i & 1u;
-      const uint32_t ldw = ldg_base + ph * 256u;  // this tile's (lse, delta)
-      named_bar_sync(1 + g, 128);  // tile i's staging written; tile i-1's readers done
-      float nv[2];
-      if (ld_writer) gload(i + 1, nv);
-      if (storer) {
-        // dS^T chunk was last stored at tile i-1 by this thread: wait for the
-        // TMA store to finish reading shared memory
-        bulk_wait_read<0>();
-        mbar_arrive(&st_free[chunk]);
-      }
-      mbar_wait(sdp_full, ph);
+    const uint32_t ds_chunk = smem_u32(smem + C::OFF_DS) + (uint32_t)g * 16384u;
+    for (int i = 0; i < n; ++i) {
+      const int s = i & 1;
+      const uint32_t ldw = smem_u32(smem + C::OFF_LD + s * 1024) + (uint32_t)g * 256u;
+      mbar_wait(&q_full[s], (i >> 1) & 1);  // lse, delta rows of the slot
+      mbar_wait(s_full, i & 1);
       tc_fence_after();
-      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_IN, i);
-      // the group's 32 columns of S^T and dP^T into registers
-      uint32_t sr[32], dr[32];
-      tmem_ld32_nowait(tmem + lane_off + C::TM_ST + g * 32, sr);
-      tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + g * 32, dr);
-      tmem_wait_ld();
-      reg_fence32(sr);
-      reg_fence32(dr);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(loaded);
-      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_LOADED, i);
-      // P^T into sr, unscaled dS^T = P^T (dP^T - delta) into dr (in place);
-      // the 1/sqrt(hd) is applied once to dK (epilogue) and dQ (GEMM alpha)
+      // ---- P^T = 2^(c S^T - lse) over the group's 64 query columns
+      float pr[64];
+      {
+        uint32_t a0[32], a1[32];
+        tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64, a0);
+        tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64 + 32, a1);
+        tmem_wait_ld();
+        reg_fence32(a0);
+        reg_fence32(a1);
 #pragma unroll
-      for (int e4 = 0; e4 < 8; ++e4) {
-        float4 l4, d4;
+        for (int e = 0; e < 32; ++e) {
+          pr[e] = __uint_as_float(a0[e]);
+          pr[32 + e] = __uint_as_float(a1[e]);
+        }
+      }
+#pragma unroll
+      for (int e4 = 0; e4 < 16; ++e4) {
+        float4 l4;
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w)
-                     : "r"(ldw + (uint32_t)(4 * e4) * 4u));
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
-                     : "r"(ldw + 128u + (uint32_t)(4 * e4) * 4u));
+                     : "r"(ldw + (uint32_t)(16 * e4)));
         const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int e = 4 * e4 + u;
-          const float xv = fmaf(__uint_as_float(sr[e]), cl2, -lv[u]);
-          const float pv = (kBwdPolyMask >> u) & 1 ? exp2_fma(xv) : ex2_approx(xv);
-          dr[e] = __float_as_uint(pv * (__uint_as_float(dr[e]) - dv[u]));
-          sr[e] = __float_as_uint(pv);
+          const float xv = fmaf(pr[e], cl2, -lv[u]);
+          pr[e] = (kBwdPolyMask >> u) & 1 ? exp2_fma(xv) : ex2_approx(xv);
         }
       }
-      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_MATH, i);
-      // P^T over the S^T columns [16g, 16g+16) once all 16 warps read theirs
-      mbar_wait(loaded, ph);
-      {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // queries [64g+32h, +32) -> cols [64g+32h, +16)
         uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = pack_bf16x2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
-        tmem_st16(tmem + lane_off + C::TM_ST + g * 16, pk);
+        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(pr[32 * h + 2 * e], pr[32 * h + 2 * e + 1]);
+        tmem_st16(tmem + lane_off + C::TM_S + g * 64 + h * 32, pk);
       }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);  // dV(i) may start
-      // dS^T chunk: free once dK(i-1) read it and its TMA store read it
-      mbar_wait(ds_free, ph ^ 1u);
-      mbar_wait(&st_free[chunk], ph);
-      store_row32(ds_chunk, r, (g & 1) * 4, *reinterpret_cast<const float(*)[32]>(dr));
+      if (lane == 0) mbar_arrive(p_full);
+      // ---- dS^T = P^T (dP^T - delta) -> shared memory (unscaled)
+      mbar_wait(dp_full, i & 1);
+      tc_fence_after();
+      uint32_t d[64];
+      {
+        uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
+        uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
+        tmem_ld32_nowait(tmem + lane_off + C::TM_DP + g * 64, d0);
+        tmem_ld32_nowait(tmem + lane_off + C::TM_DP + g * 64 + 32, d1);
+        tmem_wait_ld();
+        reg_fence32(d0);
+        reg_fence32(d1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dp_loaded);
+      if (i > 0) mbar_wait(ds_free, (i - 1) & 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          float4 d4;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
+                       : "r"(ldw + 512u + (uint32_t)(128 * h + 16 * e4)));
+          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = 32 * h + 4 * e4 + u;
+            d[e] = __float_as_uint(pr[e] * (__uint_as_float(d[e]) - dv[u]));
+          }
+        }
+        store_row32(ds_chunk, r, 4 * h, *reinterpret_cast<const float(*)[32]>(d + 32 * h));
+      }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(pds_full);
-      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_OUT, i);
-      if (storer) {
-        mbar_wait(pds_full, ph);  // all rows of the chunk written
-        tma_store_3d(&p.tm_dst, smem + C::OFF_DS + chunk * 16384, i * BQB + chunk * 64, k0,
-                     smp * p.H + head);
-        bulk_commit();
-      }
-      // tile i+1's (lse, delta) into the other staging buffer (last read at tile i-1)
-      if (ld_writer) sstore(i + 1, nv);
+      if (lane == 0) mbar_arrive(ds_full);
     }
-    // ------------------------------------------------- dK, dV epilogue
+    // ---- dK, dV out (dK carries the dS scale)
     mbar_wait(fin, 0);
     tc_fence_after();
     const int krow = k0 + r;
-    __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + krow) * p.ld_qkv + col_k;
+    __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + krow) * p.ld_qkv + col_q;
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {  // dK then dV
+    for (int which = 0; which < 2; ++which) {
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {  // group g: columns [g*HD/4, (g+1)*HD/4)
-        const int col = g * (HD / 4) + c * 16;
+      for (int c = 0; c < HD / 32; ++c) {  // group g: columns [g*HD/2, (g+1)*HD/2)
+        const int col = g * (HD / 2) + c * 16;
         uint32_t v[16];
         tmem_ld16_nowait(tmem + lane_off + (which == 0 ? C::TM_DK : C::TM_DV) + col, v);
         tmem_wait_ld();
         reg_fence16(v);
         if (krow < p.S) {
-          __nv_bfloat16* dst = drow + which * HD + col;
-          const float f = which == 0 ? scale : 1.0f;  // dK carries the dS scale
+          __nv_bfloat16* dst = drow + (which + 1) * HD + col;
+          const float f = which == 0 ? scale : 1.0f;
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             uint4 w;
@@ -793,7 +722,349 @@ __global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_c
         }
       }
     }
-    if (storer) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------- backward: dQ pass
+// dQ = scale * dS K computed per 128-query tile with S, P, dP and dS
+// recomputed on chip (the flash-attention "dQ pass"): no dS ever reaches
+// HBM, dQ accumulates in TMEM over the key tiles in order (deterministic, no
+// atomics). One CTA = one (sample, head, query tile), 320 threads:
+//   warp 0      TMA: Q_i (then copied into TMEM: S reads only K_j from
+//               shared memory), dO_i once; K_j into a 3-slot ring, V_j into
+//               a 2-slot ring.
+//   warp 1      MMA issuer (warp-wide, one elected lane), all M=128 N=128:
+//                 S(j+1) = Q K^T      (A = Q in TMEM)   once S(j) is loaded
+//                 dP(j+1) = dO V^T    (A = dO in smem)  once dP(j) is loaded
+//                 dQ += dS(j) K_j     (A = dS in its own TMEM columns, B = K_j
+//                                      read MN-major)
+//               so the next tile's S and dP run while dS(j) is computed.
+//   warps 2-9   thread = query row, group g = keys [64g, 64g+64):
+//               P = 2^(c S - lse) (lse, delta are the row's own: registers),
+//               dS = P (dP - delta) -> bf16 pairs into TMEM once dQ(j-1) has
+//               read the previous dS; at the end dQ out of TMEM (scaled)
+//               into the Q slot of dqkv.
+// TMEM: S [0,128), dP [128,256), dQ [256,256+hd), Q [384,384+hd/2),
+// dS [448,512).
+constexpr int kDqThreads = 320;
+
+struct DqParams {
+  CUtensorMap tm_kv;  // qkv view, box {64, 128}: Q_i, K_j, V_j
+  CUtensorMap tm_do;  // dO view, box {64, 128}
+  int S, H, n_qt, n_kt;
+  float c, scale;
+  const float* lse;
+  const float* delta;
+  __nv_bfloat16* dqkv;
+  long long ld_qkv;
+};
+
+template <int HD>
+struct DqCfg {
+  static constexpr int TILE = 128 * HD * 2;
+  static constexpr int K_STAGES = 3, V_STAGES = 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = TILE;
+  static constexpr int OFF_K = 2 * TILE;
+  static constexpr int OFF_V = OFF_K + K_STAGES * TILE;
+  static constexpr int OFF_BAR = OFF_V + V_STAGES * TILE;
+  static constexpr int USED = OFF_BAR + 256;
+  static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_Q = 384, TM_DS = 448;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_constant__ DqParams p) {
+  using C = DqCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if ((smem - smem_raw) + C::USED > C::SMEM_BYTES) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* qd_full = bars + 0;                 // Q_i, dO_i in shared memory
+  uint64_t* qd_tmem = bars + 1;                 // ... and in TMEM (8 warps)
+  uint64_t* k_full = bars + 2;                  // K_STAGES
+  uint64_t* k_empty = k_full + C::K_STAGES;     // K_STAGES
+  uint64_t* v_full = k_empty + C::K_STAGES;     // V_STAGES
+  uint64_t* v_empty = v_full + C::V_STAGES;     // V_STAGES
+  uint64_t* s_full = v_empty + C::V_STAGES;     // S(j) in TMEM
+  uint64_t* s_loaded = s_full + 1;              // S(j) in registers (8 warps)
+  uint64_t* dp_full = s_loaded + 1;             // dP(j) in TMEM
+  uint64_t* dp_loaded = dp_full + 1;            // dP(j) in registers (8 warps)
+  uint64_t* ds_full = dp_loaded + 1;            // dS(j) in TMEM (8 warps)
+  uint64_t* dq_done = ds_full + 1;              // dQ(j) has read dS(j)
+  uint64_t* fin = dq_done + 1;                  // dQ complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int qt = blockIdx.x % p.n_qt;
+  const int head = (blockIdx.x / p.n_qt) % p.H;
+  const int smp = blockIdx.x / (p.n_qt * p.H);
+  const int q0 = qt * 128;
+  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+  const int n = p.n_kt;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(qd_full, 1);
+    mbar_init(qd_tmem, 8);
+    for (int s = 0; s < C::K_STAGES; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::V_STAGES; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_loaded, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_loaded, 8);
+    mbar_init(ds_full, 8);
+    mbar_init(dq_done, 1);
+    mbar_init(fin, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&p.tm_kv);
+    prefetch_tmap(&p.tm_do);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------ TMA producer
+      mbar_expect_tx(qd_full, 2 * C::TILE);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_3d(smem + C::OFF_Q + c * 16384, &p.tm_kv, qd_full, col_q + c * 64, q0, smp);
+        tma_load_3d(smem + C::OFF_DO + c * 16384, &p.tm_do, qd_full, head * HD + c * 64, q0, smp);
+      }
+      for (int j = 0; j < n; ++j) {
+        const int ks = j % C::K_STAGES, ku = j / C::K_STAGES;
+        if (ku > 0) mbar_wait(&k_empty[ks], (ku - 1) & 1);
+        mbar_expect_tx(&k_full[ks], C::TILE);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_3d(smem + C::OFF_K + ks * C::TILE + c * 16384, &p.tm_kv, &k_full[ks],
+                      col_k + c * 64, j * 128, smp);
+        const int vs = j % C::V_STAGES, vu = j / C::V_STAGES;
+        if (vu > 0) mbar_wait(&v_empty[vs], (vu - 1) & 1);
+        mbar_expect_tx(&v_full[vs], C::TILE);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_3d(smem + C::OFF_V + vs * C::TILE + c * 16384, &p.tm_kv, &v_full[vs],
+                      col_v + c * 64, j * 128, smp);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128, false, false);  // S, dP: B K-major
+    constexpr uint32_t idesc_q = idesc_bf16(128, HD, false, true);    // dQ: B = K MN-major
+    const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint64_t kmaj_k = make_sdesc(sbase + C::OFF_K, 16, 1024);
+    const uint64_t kmaj_v = make_sdesc(sbase + C::OFF_V, 16, 1024);
+    const uint64_t kmaj_do = make_sdesc(sbase + C::OFF_DO, 16, 1024);
+    const uint64_t mn_k = make_sdesc(sbase + C::OFF_K, 16384, 1024);
+    constexpr uint64_t kTile = (uint64_t)(C::TILE >> 4);
+    auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
+    // A (M=128 x K=hd) from TMEM at column a, 8 columns per K=16 step
+    auto issue_ts = [&](uint32_t d, uint32_t a, uint64_t b) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        mma_bf16_ts_warp(d, a + 8 * kk, b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+    };
+    auto issue_ss = [&](uint32_t d, uint64_t a, uint64_t b) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+    };
+    auto wait_k = [&](int j) {
+      mbar_wait(&k_full[j % C::K_STAGES], (j / C::K_STAGES) & 1);
+      tc_fence_after();
+    };
+    auto wait_v = [&](int j) {
+      mbar_wait(&v_full[j % C::V_STAGES], (j / C::V_STAGES) & 1);
+      tc_fence_after();
+    };
+    mbar_wait(qd_tmem, 0);
+    tc_fence_after();
+    wait_k(0);
+    issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k);
+    mma_commit_warp(s_full);
+    wait_v(0);
+    issue_ss(tm + C::TM_DP, kmaj_do, kmaj_v);
+    mma_commit_warp(dp_full);
+    mma_commit_warp(&v_empty[0]);
+    for (int j = 0; j < n; ++j) {
+      if (j + 1 < n) {
+        // S(j+1) over S(j) once every warp holds S(j) in registers
+        mbar_wait(s_loaded, j & 1);
+        wait_k(j + 1);
+        issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + ((j + 1) % C::K_STAGES) * kTile);
+        mma_commit_warp(s_full);
+        // dP(j+1) over dP(j) once it is in registers
+        mbar_wait(dp_loaded, j & 1);
+        wait_v(j + 1);
+        issue_ss(tm + C::TM_DP, kmaj_do, kmaj_v + ((j + 1) % C::V_STAGES) * kTile);
+        mma_commit_warp(dp_full);
+        mma_commit_warp(&v_empty[(j + 1) % C::V_STAGES]);
+      }
+      // dQ += dS(j) K_j, dS (bf16 pairs) in its own columns: keys
+      // [16kk, 16kk+16) of group kk/4 at column 32(kk/4) + 8(kk%4)
+      mbar_wait(ds_full, j & 1);
+      tc_fence_after();
+      const uint64_t bk = mn_k + (j % C::K_STAGES) * kTile;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_bf16_ts_warp(tm + C::TM_DQ, tm + C::TM_DS + 32 * (kk >> 2) + 8 * (kk & 3),
+                         bk + (uint64_t)kk * 128u, idesc_q, (j > 0 || kk > 0) ? 1u : 0u);
+      mma_commit_warp(&k_empty[j % C::K_STAGES]);
+      mma_commit_warp(dq_done);
+    }
+    mma_commit_warp(fin);
+  } else {
+    // ------------------------------------------ softmax-gradient warps
+    const int quad = warp & 3;
+    const int g = (warp - 2) >> 2;   // keys [64g, 64g+64) of each key tile
+    const int r = quad * 32 + lane;  // query row within the tile (TMEM lane)
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int qrow = q0 + r;
+    const bool valid = qrow < p.S;
+    const long long lrow = ((long long)smp * p.H + head) * p.S + qrow;
+    // padded query rows: Q, dO are zero there, dS = 0 whatever lse is
+    const float lse = valid ? __ldg(p.lse + lrow) : 0.f;
+    const float dlt = valid ? __ldg(p.delta + lrow) : 0.f;
+    const float cl2 = p.c;
+    {
+      // the Q_i row into TMEM (A operand of S): group g copies its half of
+      // the head dimension (hd/2 bf16, 16-byte pieces of the SW128 tile)
+      mbar_wait(qd_full, 0);
+      constexpr int HW = HD / 2;  // bf16 per group
+      {
+        const uint32_t base = smem_u32(smem + C::OFF_Q);
+        uint32_t v[HW / 2];
+#pragma unroll
+        for (int u = 0; u < HW / 8; ++u) {
+          const int col = g * HW + 8 * u;  // first hd column of the piece
+          const uint32_t a = base + (uint32_t)(col >> 6) * 16384u + (uint32_t)(r >> 3) * 1024u +
+                             (uint32_t)(r & 7) * 128u + (uint32_t)((((col & 63) >> 3) ^ (r & 7)) << 4);
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[4 * u]), "=r"(v[4 * u + 1]), "=r"(v[4 * u + 2]), "=r"(v[4 * u + 3])
+                       : "r"(a));
+        }
+        const uint32_t t = tmem + lane_off + C::TM_Q + g * (HW / 2);
+        if constexpr (HW / 2 == 32) {
+          tmem_st32(t, *reinterpret_cast<const uint32_t(*)[32]>(v));
+        } else {
+          tmem_st16(t, *reinterpret_cast<const uint32_t(*)[16]>(v));
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qd_tmem);
+    }
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      float pr[64];
+      {
+        uint32_t a0[32], a1[32];
+        tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64, a0);
+        tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64 + 32, a1);
+        tmem_wait_ld();
+        reg_fence32(a0);
+        reg_fence32(a1);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          pr[e] = __uint_as_float(a0[e]);
+          pr[32 + e] = __uint_as_float(a1[e]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_loaded);
+      // one exponential in four on the FMA pipe (same split as attn_bwd_kernel)
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const float xv = fmaf(pr[e], cl2, -lse);
+        pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
+      }
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+      const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
+      uint32_t d[64];
+      {
+        uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
+        uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
+        tmem_ld32_nowait(dpc, d0);
+        tmem_ld32_nowait(dpc + 32, d1);
+        tmem_wait_ld();
+        reg_fence32(d0);
+        reg_fence32(d1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dp_loaded);
+      // dS = P (dP - delta), unscaled (the 1/sqrt(hd) goes to the epilogue),
+      // 64 keys -> columns [32g, 32g+32) of the dS slot, free once dQ(j-1) read it
+      uint32_t pk[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        pk[e] = pack_bf16x2(pr[2 * e] * (__uint_as_float(d[2 * e]) - dlt),
+                            pr[2 * e + 1] * (__uint_as_float(d[2 * e + 1]) - dlt));
+      if (j > 0) {
+        mbar_wait(dq_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+      tmem_st32(tmem + lane_off + C::TM_DS + g * 32, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    // ------------------------------------------------ dQ epilogue
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + qrow) * p.ld_qkv + col_q;
+    const float scale = p.scale;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {  // group g: columns [g*HD/2, (g+1)*HD/2)
+      const int col = g * (HD / 2) + c * 16;
+      uint32_t v[16];
+      tmem_ld16_nowait(tmem + lane_off + C::TM_DQ + col, v);
+      tmem_wait_ld();
+      reg_fence16(v);
+      if (valid) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * scale, __uint_as_float(v[u * 8 + 1]) * scale);
+          w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * scale, __uint_as_float(v[u * 8 + 3]) * scale);
+          w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * scale, __uint_as_float(v[u * 8 + 5]) * scale);
+          w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * scale, __uint_as_float(v[u * 8 + 7]) * scale);
+          *reinterpret_cast<uint4*>(drow + col + u * 8) = w;
+        }
+      }
+    }
   }
 
   tc_fence_before();
@@ -858,18 +1129,53 @@ cudaError_t launch_fwd(const FwdParams& p, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// 2-D fp32 view [cols, rows] (row stride cols), box {128, 1}; columns past
+// `cols` read as zero.
+bool encode_rows_f32(CUtensorMap* map, const float* base, int64_t cols, int64_t rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    g_attn_err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {128, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_attn_err = "cuTensorMapEncodeTiled (rows) failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
 template <int HD>
-cudaError_t launch_bwd(const BwdParams& p, int grid, cudaStream_t s) {
-  using C = BwdCfg<HD>;
-  // once per instantiation and process (host threads of in-process ranks race here)
+cudaError_t launch_kv(const KvParams& p, int grid, cudaStream_t s) {
+  using C = KvCfg<HD>;
   static cudaError_t attr = cudaSuccess;
   static std::once_flag once;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr = cudaFuncSetAttribute(attn_bwd_kv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::SMEM_BYTES);
   });
   if (attr != cudaSuccess) return attr;
-  attn_bwd_kernel<HD><<<grid, kBwdThreads, C::SMEM_BYTES, s>>>(p);
+  attn_bwd_kv_kernel<HD><<<grid, kKvThreads, C::SMEM_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int HD>
+cudaError_t launch_dq(const DqParams& p, int grid, cudaStream_t s) {
+  using C = DqCfg<HD>;
+  static cudaError_t attr = cudaSuccess;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(attn_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM_BYTES);
+  });
+  if (attr != cudaSuccess) return attr;
+  attn_dq_kernel<HD><<<grid, kDqThreads, C::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -915,52 +1221,74 @@ cudaError_t attn_fwd_sm100(const AttnDesc& d, cudaStream_t s) {
   return e;
 }
 
-cudaError_t attn_bwd_sm100(const AttnDesc& d, cudaStream_t s) {
+cudaError_t attn_bwd_kv_sm100(const AttnDesc& d, cudaStream_t s) {
   using namespace sm100::attn;
-  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !d.dst || !d.lse ||
-      d.ld_o % 8 != 0 || reinterpret_cast<uintptr_t>(d.dout) % 16 ||
-      reinterpret_cast<uintptr_t>(d.dqkv) % 16 || reinterpret_cast<uintptr_t>(d.dst) % 16) {
-    g_attn_err = "attn_bwd_sm100: unsupported shape or missing operand";
+  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !d.lse || d.ld_o % 8 != 0 ||
+      d.seq % 4 != 0 || reinterpret_cast<uintptr_t>(d.dout) % 16 ||
+      reinterpret_cast<uintptr_t>(d.dqkv) % 16 || reinterpret_cast<uintptr_t>(d.lse) % 16 ||
+      reinterpret_cast<uintptr_t>(d.delta) % 16) {
+    g_attn_err = "attn_bwd_kv_sm100: unsupported shape or missing operand";
     return cudaErrorInvalidValue;
   }
-  BwdParams p;
+  KvParams p;
   std::memset(&p, 0, sizeof(p));
   const int64_t cols = 3 * d.heads * d.head_dim;
   if (!encode_3d(&p.tm_kv, d.qkv, cols, d.seq, d.samples, d.ld_qkv, 128) ||
-      !encode_3d(&p.tm_q, d.qkv, cols, d.seq, d.samples, d.ld_qkv, BQB) ||
-      !encode_3d(&p.tm_do, d.dout, d.heads * d.head_dim, d.seq, d.samples, d.ld_o, BQB) ||
-      !encode_3d(&p.tm_dst, d.dst, d.seq, d.seq, d.samples * d.heads, d.seq, 128))
+      !encode_3d(&p.tm_do, d.dout, d.heads * d.head_dim, d.seq, d.samples, d.ld_o, 128) ||
+      !encode_rows_f32(&p.tm_lse, d.lse, d.seq, d.samples * d.heads) ||
+      !encode_rows_f32(&p.tm_dlt, d.delta, d.seq, d.samples * d.heads))
     return cudaErrorInvalidValue;
   p.S = (int)d.seq;
   p.H = (int)d.heads;
-  p.n_kt = (int)((d.seq + 127) / 128);
-  p.n_qt = (int)((d.seq + BQB - 1) / BQB);
+  p.n = (int)((d.seq + 127) / 128);
+  p.c = d.scale * kLog2e;
+  p.scale = d.scale;
+  p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
+  p.ld_qkv = d.ld_qkv;
+  const long long grid = (long long)p.n * d.heads * d.samples;
+  if (grid > 0x7fffffffLL) {
+    g_attn_err = "attn_bwd_kv_sm100: grid too large";
+    return cudaErrorInvalidValue;
+  }
+  cudaError_t e = d.head_dim == 128 ? launch_kv<128>(p, (int)grid, s) : launch_kv<64>(p, (int)grid, s);
+  if (e != cudaSuccess) g_attn_err = std::string("attn_bwd_kv_sm100 launch: ") + cudaGetErrorString(e);
+  return e;
+}
+
+cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s) {
+  using namespace sm100::attn;
+  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !d.lse || d.ld_o % 8 != 0 ||
+      reinterpret_cast<uintptr_t>(d.dout) % 16 || reinterpret_cast<uintptr_t>(d.dqkv) % 16) {
+    g_attn_err = "attn_dq_sm100: unsupported shape or missing operand";
+    return cudaErrorInvalidValue;
+  }
+  DqParams p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t cols = 3 * d.heads * d.head_dim;
+  if (!encode_3d(&p.tm_kv, d.qkv, cols, d.seq, d.samples, d.ld_qkv, 128) ||
+      !encode_3d(&p.tm_do, d.dout, d.heads * d.head_dim, d.seq, d.samples, d.ld_o, 128))
+    return cudaErrorInvalidValue;
+  p.S = (int)d.seq;
+  p.H = (int)d.heads;
+  p.n_qt = p.n_kt = (int)((d.seq + 127) / 128);
   p.c = d.scale * kLog2e;
   p.scale = d.scale;
   p.lse = d.lse;
   p.delta = d.delta;
   p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
   p.ld_qkv = d.ld_qkv;
-  p.trace = nullptr;
-  if (std::getenv("TESS_ATTN_TRACE")) {
-    static long long* tr = nullptr;
-    if (!tr) cudaMalloc(&tr, 8 * 64 * sizeof(long long));
-    cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), s);
-    p.trace = tr;
-    g_attn_trace = tr;
-  }
-  const long long grid = (long long)p.n_kt * d.heads * d.samples;
+  const long long grid = (long long)p.n_qt * d.heads * d.samples;
   if (grid > 0x7fffffffLL) {
-    g_attn_err = "attn_bwd_sm100: grid too large";
+    g_attn_err = "attn_dq_sm100: grid too large";
     return cudaErrorInvalidValue;
   }
-  cudaError_t e = d.head_dim == 128 ? launch_bwd<128>(p, (int)grid, s) : launch_bwd<64>(p, (int)grid, s);
-  if (e != cudaSuccess) g_attn_err = std::string("attn_bwd_sm100 launch: ") + cudaGetErrorString(e);
+  cudaError_t e = d.head_dim == 128 ? launch_dq<128>(p, (int)grid, s) : launch_dq<64>(p, (int)grid, s);
+  if (e != cudaSuccess) g_attn_err = std::string("attn_dq_sm100 launch: ") + cudaGetErrorString(e);
   return e;
 }
 
 }  // namespace tess
 // shared-memory budgets (227 KB opt-in per CTA)
 static_assert(tess::sm100::attn::FwdCfg<128>::SMEM_BYTES <= 232448, "attn fwd smem");
-static_assert(tess::sm100::attn::BwdCfg<128>::USED <= 232448, "attn bwd smem");
-static_assert(tess::sm100::attn::BwdCfg<64>::USED <= 232448, "attn bwd smem");
+static_assert(tess::sm100::attn::DqCfg<128>::USED <= 232448, "attn dQ smem");
+static_assert(tess::sm100::attn::KvCfg<128>::USED <= 232448, "attn dK/dV smem");

@@ -349,15 +349,21 @@ bool use_fused_attn(DType t, const RankDims& rd) {
   return attn_fused_supported(a);
 }
 
-void run_attn(bool fwd, const AttnDesc& a, cudaStream_t s) {
+enum class AttnPass { Fwd, BwdKV, BwdQ };
+
+void run_attn(AttnPass k, const AttnDesc& a, cudaStream_t s) {
   ProfToken tok;
-  // algorithmic flops: 2 (fwd) or 4 (bwd: dV, dP, dK; dQ is its own GEMM)
-  // contractions of 2*S*S*hd per (sample, head)
+  // algorithmic flops, in contractions of 2*S*S*hd per (sample, head): 2
+  // (fwd: S, PV), 3 (dK/dV pass: dV, dP, dK), 1 (dQ pass: dQ; its S and dP
+  // are recomputation)
   const double unit = 2.0 * (double)a.seq * a.seq * a.head_dim * a.heads * a.samples;
-  tok = prof_begin(fwd ? (a.head_dim == 128 ? "attn_fwd_kernel<128>" : "attn_fwd_kernel<64>")
-                       : (a.head_dim == 128 ? "attn_bwd_kernel<128>" : "attn_bwd_kernel<64>"),
-                   (fwd ? 2.0 : 3.0) * unit, s);
-  cudaError_t e = fwd ? attn_fwd_sm100(a, s) : attn_bwd_sm100(a, s);
+  const std::string hd = a.head_dim == 128 ? "<128>" : "<64>";
+  static const char* names[] = {"attn_fwd_kernel", "attn_bwd_kv_kernel", "attn_dq_kernel"};
+  static const double units[] = {2.0, 3.0, 1.0};
+  tok = prof_begin(names[(int)k] + hd, units[(int)k] * unit, s);
+  cudaError_t e = k == AttnPass::Fwd     ? attn_fwd_sm100(a, s)
+                  : k == AttnPass::BwdKV ? attn_bwd_kv_sm100(a, s)
+                                         : attn_dq_sm100(a, s);
   count_launch();
   if (e == cudaErrorInvalidValue) fail(TESS_ERR_UNSUPPORTED, attn_last_error());
   if (e != cudaSuccess)
@@ -377,7 +383,7 @@ void attn_fwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     void* o = wsget(c, tag + ".o", rows * hq * esz);
     float* lse = static_cast<float*>(wsget(c, tag + ".lse", (size_t)rd.samples_local * H * S * 4));
     nn_product(c, t, x, rows, rd.hin, p.w_qkv, 3 * hq, out_to(qkv, t), s, &wp.qkv);
-    run_attn(true, attn_desc(rd, qkv, o, lse), s);
+    run_attn(AttnPass::Fwd, attn_desc(rd, qkv, o, lse), s);
     nn_product(c, t, o, rows, hq, p.w_proj, rd.hin, yout, s, &wp.proj);
     return;
   }
@@ -482,7 +488,6 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     void* dout = wsget(c, "attn.dout", rows * hq * esz);
     void* dqkv = wsget(c, "attn.dqkv", rows * ld * esz);
     float* delta = static_cast<float*>(wsget(c, "attn.delta", (size_t)rd.samples_local * H * S * 4));
-    void* dst = wsget(c, "attn.dst", (size_t)rd.samples_local * H * S * S * esz);
     if (c.grid.q == 1) {
       // no row reduce: the GEMM epilogue rounds straight to bf16 (bitwise the
       // same as fp32 + convert)
@@ -501,17 +506,8 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
     a.dout = dout;
     a.delta = delta;
     a.dqkv = dqkv;
-    a.dst = dst;
-    run_attn(false, a, s);  // dK, dV -> dqkv; dS^T -> dst
-    // dQ = dS K for every (sample, head): A = dS^T stored [keys, queries]
-    GemmDesc gq;
-    gq.M = S; gq.N = hd; gq.nb0 = H; gq.nb1 = rd.samples_local; gq.in = t; gq.trans_a = true;
-    gq.seg[0] = {dst, static_cast<const char*>(qkv) + hd * esz, S};
-    gq.lda = S; gq.as0 = S * S; gq.as1 = H * S * S;
-    gq.ldb = ld; gq.bs0 = 3 * hd; gq.bs1 = S * ld;
-    gq.c = dqkv; gq.c_type = t; gq.ldc = ld; gq.cs0 = 3 * hd; gq.cs1 = S * ld;
-    gq.alpha = a.scale;  // the kernel stores dS without the 1/sqrt(hd)
-    run_gemm(gq, s);
+    run_attn(AttnPass::BwdKV, a, s);  // dK, dV -> dqkv
+    run_attn(AttnPass::BwdQ, a, s);   // dQ -> dqkv
     nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, rd.hin, out_to(dx_f32, DType::F32), s, &wp.qkv);
     weight_grad(c, t, x, rows, rd.hin, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
     return;

@@ -4,9 +4,9 @@
 // section 3). Compiled only into tools/attn_check, in one translation unit
 // with the product kernels (it reuses their helpers).
 //
-// Result: slower than the shipped split path (attn_bwd_kernel + one batched
+// Result: slower than the round-1 split path (attn_bwd_kernel + one batched
 // dQ GEMM over dS^T, 2.49 ms at the cfg4 head shape on an unconstrained
-// B200): fused dQ 3.2-3.3 ms, of which ~1 ms is the ordered fp32 exchange of
+// B200; the kernel is kept below as the harness's baseline): fused dQ 3.2-3.3 ms, of which ~1 ms is the ordered fp32 exchange of
 // dQ partials through L2 (64 KB per key tile and query tile, 6.4 GB per
 // call, twice the dS^T bytes) and ~0.65 ms the fifth MMA serialised behind
 // the TMEM drain (TMEM holds S^T, dP^T, dV, dK: dQ must reuse dP^T's
@@ -34,10 +34,437 @@ struct AttnBwdPlan {
 struct AttnBwdDqArgs {
   float* dq_acc = nullptr;     // fp32 accumulator, plan.acc_bytes
   uint32_t* dq_sem = nullptr;  // ordering counters, plan.sem_bytes (zeroed by the launch)
+  void* dst = nullptr;         // mode 3: dS^T [samples*H][S keys][S queries] bf16
 };
+// The round-1 split backward: dK, dV into dqkv, unscaled dS^T into dst.
+cudaError_t attn_bwd_split_sm100(const AttnDesc& d, void* dst, cudaStream_t s);
 
 namespace sm100 {
 namespace attn {
+
+// ------------------------------------------- the round-1 split backward
+// (shipped until round 2; the harness's baseline) dK, dV and dS^T to HBM,
+// dQ by a batched GEMM over dS^T.
+// One CTA = one (sample, head, 128-key tile); it walks the 128-query tiles
+// i of the sequence. 320 threads:
+//   warp 0      TMA producer: K, V of the key tile once; then Q_i, dO_i
+//               (128 x hd, boxes {64, 128}) through a RING-slot FIFO.
+//   warp 1      MMA issuer + TMEM owner. Per query tile, all MMAs at
+//               M=128, N=128 (full tcgen05 rate; N=64 tiles run at ~70 %):
+//                 S^T(i) = K Q_i^T, dP^T(i) = V dO_i^T   (A = K / V, smem)
+//                 dV += P^T(i) dO_i   (A = P^T in TMEM, written by the softmax
+//                                      over the consumed S^T columns)
+//                 dK += dS^T(i) Q_i   (A = dS^T in shared memory)
+//               S^T / dP^T are single-buffered (TMEM holds S^T, dP^T, dV, dK);
+//               dP^T(i+1) is issued as soon as tile i's scores sit in
+//               registers; dV(i) as soon as P^T(i) is in TMEM (its own
+//               barrier, before the dS^T stores), S^T(i+1) right behind it,
+//               then dK(i) once dS^T(i) is in shared memory -- the next
+//               tile's softmax overlaps dK(i) (-4 %, r2_attn_bwd_order_ab).
+//   warps 2-17  four groups of 4 warps split each tile's 128 queries (group
+//               g: columns [32g, 32g+32)); thread = key row (TMEM lane):
+//               P^T = 2^(c*S^T - lse[q]) -> TMEM (bf16 pairs), dS^T = P^T
+//               (dP^T - delta[q]) -> shared memory (UMMA K-major SW128, chunk
+//               g/2) and, by TMA store, to HBM for dQ = dS K (one batched
+//               GEMM; the 1/sqrt(hd) goes to dK's epilogue and dQ's alpha).
+// Q_i and dO_i tiles are used twice with different majorness: K-major B of
+// the score MMAs ([N=q][K=hd]) and MN-major B of dV/dK ([K=q][N=hd]) -- the
+// same bytes under two descriptors.
+// TMEM: S^T / P^T [0,128), dP^T [128,256), dV [256, 256+hd), dK [384, 384+hd).
+constexpr int kBwdThreads = 576;  // TMA + MMA warps + 16 softmax-gradient warps
+constexpr int BQB = 128;  // queries per backward tile
+struct BwdParams {
+  CUtensorMap tm_kv;   // qkv view, box {64, 128}: K, V of the key tile
+  CUtensorMap tm_q;    // qkv view, box {64, 128}: Q_i
+  CUtensorMap tm_do;   // dO view [hq cols, S, samples], box {64, 128}
+  CUtensorMap tm_dst;  // dS^T view [S q, S k, samples*H], box {64, 128} (store)
+  int S, H, n_kt, n_qt;
+  float c;      // scale * log2(e)
+  float scale;  // 1/sqrt(hd)
+  const float* lse;
+  const float* delta;
+  __nv_bfloat16* dqkv;
+  long long ld_qkv;
+  long long* trace;  // debug (TESS_ATTN_TRACE): per-phase clock64 of CTA 0, [event][tile]
+};
+
+// trace events (CTA 0 only)
+enum {
+  TR_MMA_S = 0, TR_MMA_P = 1, TR_SM_IN = 2, TR_SM_MATH = 3, TR_SM_OUT = 4,
+  TR_SM_LOADED = 5, TR_MMA_FREE = 6, TR_MMA_GDONE = 7, TR_N = 8
+};
+__device__ __forceinline__ void trace_ev(const BwdParams& p, int ev, int tile) {
+  if (p.trace && blockIdx.x == 0 && tile < 64) p.trace[ev * 64 + tile] = clock64();
+}
+
+template <int HD>
+struct BwdCfg {
+  static constexpr int KV_BYTES = 128 * HD * 2;    // K or V tile
+  static constexpr int SLOT_BYTES = BQB * HD * 2;  // Q_i or dO_i
+  static constexpr int RING = HD == 128 ? 4 : 8;
+  static constexpr int DS_BYTES = 128 * BQB * 2;   // dS^T tile (2 chunks of 64 queries)
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = KV_BYTES;
+  static constexpr int OFF_RING = 2 * KV_BYTES;
+  static constexpr int OFF_DS = OFF_RING + RING * SLOT_BYTES;
+  static constexpr int OFF_LD = OFF_DS + DS_BYTES;  // 4 groups x 2 bufs: lse 32 | delta 32
+  static constexpr int OFF_BAR = OFF_LD + 4 * 2 * 64 * 4;
+  static constexpr int USED = OFF_BAR + 512;
+  // the dynamic window is 1024-aligned in practice; the kernel checks and
+  // traps if the slack we could afford does not cover its misalignment
+  static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int TM_ST = 0, TM_DPT = 128, TM_DV = 256, TM_DK = 384;
+};
+
+
+template <int HD>
+__global__ void __launch_bounds__(kBwdThreads, 1) attn_bwd_kernel(const __grid_constant__ BwdParams p) {
+  using C = BwdCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if ((smem - smem_raw) + C::USED > C::SMEM_BYTES) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bars;                   // 1
+  uint64_t* r_full = bars + 1;                // RING
+  uint64_t* r_empty = r_full + C::RING;       // RING
+  uint64_t* sdp_full = r_empty + C::RING;     // 1: S^T(i) and dP^T(i) in TMEM
+  uint64_t* loaded = sdp_full + 1;            // 1: all 8 warps hold tile i's scores (count 8)
+  uint64_t* pds_full = loaded + 1;            // 1: dS^T (smem) written (count 16)
+  uint64_t* ds_free = pds_full + 1;           // 1: dK(i) done reading dS^T smem
+  uint64_t* st_free = ds_free + 1;            // 2: TMA store of dS^T chunk g done reading
+  uint64_t* fin = st_free + 2;                // 1
+  uint64_t* p_full = fin + 1;                 // 1: P^T (TMEM) written (count 16)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_full + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int kt = blockIdx.x % p.n_kt;
+  const int head = (blockIdx.x / p.n_kt) % p.H;
+  const int smp = blockIdx.x / (p.n_kt * p.H);
+  const int k0 = kt * 128;
+  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < C::RING; ++s) {
+      mbar_init(&r_full[s], 1);
+      mbar_init(&r_empty[s], 1);
+    }
+    mbar_init(sdp_full, 1);
+    mbar_init(loaded, 16);
+    mbar_init(pds_full, 16);
+    mbar_init(ds_free, 1);
+    mbar_init(&st_free[0], 1);
+    mbar_init(&st_free[1], 1);  // chunk c's storer: group 2c
+    mbar_init(fin, 1);
+    mbar_init(p_full, 16);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&p.tm_kv);
+    prefetch_tmap(&p.tm_q);
+    prefetch_tmap(&p.tm_do);
+    prefetch_tmap(&p.tm_dst);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------ TMA producer
+      mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_3d(smem + C::OFF_K + c * 16384, &p.tm_kv, kv_full, col_k + c * 64, k0, smp);
+        tma_load_3d(smem + C::OFF_V + c * 16384, &p.tm_kv, kv_full, col_v + c * 64, k0, smp);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < p.n_qt; ++i) {
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {  // Q_i then dO_i
+          mbar_wait(&r_empty[stage], phase ^ 1);
+          uint8_t* dst = smem + C::OFF_RING + stage * C::SLOT_BYTES;
+          mbar_expect_tx(&r_full[stage], C::SLOT_BYTES);
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            if (which == 0)
+              tma_load_3d(dst + c * 16384, &p.tm_q, &r_full[stage], col_q + c * 64, i * BQB, smp);
+            else
+              tma_load_3d(dst + c * 16384, &p.tm_do, &r_full[stage], head * HD + c * 64, i * BQB,
+                          smp);
+          }
+          if (++stage == C::RING) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc_s = idesc_bf16(128, BQB, false, false);
+      constexpr uint32_t idesc_g = idesc_bf16(128, HD, false, true);
+      const uint32_t sk = smem_u32(smem + C::OFF_K), sv = smem_u32(smem + C::OFF_V);
+      const uint32_t ring = smem_u32(smem + C::OFF_RING);
+      const uint32_t sds = smem_u32(smem + C::OFF_DS);
+      int stage = 0;
+      uint32_t phase = 0;
+      auto next_slot = [&]() {
+        const int s = stage;
+        mbar_wait(&r_full[s], phase);
+        tc_fence_after();
+        if (++stage == C::RING) {
+          stage = 0;
+          phase ^= 1;
+        }
+        return s;
+      };
+      // A [128 x HD] K-major (chunk stride 16 KB) times B [128 x HD] K-major
+      // (chunk stride 16 KB) -> TMEM columns [d, d + 128)
+      auto issue_scores = [&](uint32_t d, uint32_t a, uint32_t b) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
+          mma_bf16(d, make_sdesc(a + off, 16, 1024), make_sdesc(b + off, 16, 1024), idesc_s,
+                   kk > 0 ? 1u : 0u);
+        }
+      };
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      int qs = next_slot();
+      int ds = next_slot();
+      trace_ev(p, TR_MMA_S, 0);
+      issue_scores(tmem + C::TM_ST, sk, ring + qs * C::SLOT_BYTES);
+      issue_scores(tmem + C::TM_DPT, sv, ring + ds * C::SLOT_BYTES);
+      mma_commit(sdp_full);
+      for (int i = 0; i < p.n_qt; ++i) {
+        const bool more = i + 1 < p.n_qt;
+        int qn = 0, dn = 0;
+        // tile i's scores are in registers: dP^T(i+1) into the dP^T columns
+        mbar_wait(loaded, i & 1);
+        tc_fence_after();
+        trace_ev(p, TR_MMA_FREE, i);
+        if (more) {
+          qn = next_slot();
+          dn = next_slot();
+          issue_scores(tmem + C::TM_DPT, sv, ring + dn * C::SLOT_BYTES);
+        }
+        // dV(i) as soon as P^T(i) sits in TMEM
+        mbar_wait(p_full, i & 1);
+        tc_fence_after();
+        trace_ev(p, TR_MMA_P, i);
+#pragma unroll
+        for (int kk = 0; kk < BQB / 16; ++kk)  // dV += P^T dO_i, P^T from TMEM
+          mma_bf16_ts(tmem + C::TM_DV, tmem + C::TM_ST + kk * 8,
+                      make_sdesc(ring + ds * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
+                      idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&r_empty[ds]);
+        if (more) {
+          // S^T(i+1) over the P^T columns right behind dV(i) (in-order
+          // execution: dV has read them): tile i+1's softmax starts while
+          // dK(i) runs
+          trace_ev(p, TR_MMA_S, i + 1);
+          issue_scores(tmem + C::TM_ST, sk, ring + qn * C::SLOT_BYTES);
+          mma_commit(sdp_full);
+        }
+        // dK(i) once dS^T(i) is in shared memory
+        mbar_wait(pds_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQB / 16; ++kk)  // dK += dS^T Q_i
+          mma_bf16(tmem + C::TM_DK,
+                   make_sdesc(sds + (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u, 16,
+                              1024),
+                   make_sdesc(ring + qs * C::SLOT_BYTES + (uint32_t)kk * 2048u, 16384, 1024),
+                   idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&r_empty[qs]);
+        mma_commit(ds_free);
+        trace_ev(p, TR_MMA_GDONE, i);
+        qs = qn;
+        ds = dn;
+      }
+      mma_commit(fin);
+    }
+  } else {
+    // ------------------------------------------ softmax-gradient warps
+    const int quad = warp & 3;
+    const int g = (warp - 2) >> 2;   // query columns [32g, 32g+32) of each tile
+    const int r = quad * 32 + lane;  // key row within the tile
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float cl2 = p.c, scale = p.scale;
+    // TMA store of dS^T chunk c (64 queries = groups 2c, 2c+1) by group 2c's thread
+    const bool storer = quad == 0 && lane == 0 && (g & 1) == 0;
+    const int chunk = g >> 1;
+    const float* lse_h = p.lse + ((long long)smp * p.H + head) * p.S;
+    const float* dlt_h = p.delta + ((long long)smp * p.H + head) * p.S;
+    // (lse, delta) of the group's 32 query columns staged through shared
+    // memory, double buffered per group: the quad-0 warp loads tile i+1's
+    // values while tile i is processed, a 128-thread named barrier at the
+    // start of each tile orders them against the readers.
+    const uint32_t ldg_base = smem_u32(smem + C::OFF_LD) + (uint32_t)g * 512u;  // [buf][lse|delta]
+    const bool ld_writer = quad == 0;
+    auto gload = [&](int i, float (&v)[2]) {
+      const int q = i * BQB + g * 32 + lane;
+      const bool ok = i < p.n_qt && q < p.S;
+      v[0] = ok ? __ldg(lse_h + q) : INFINITY;  // 2^(x - inf) = 0: no contribution
+      v[1] = ok ? __ldg(dlt_h + q) : 0.f;
+    };
+    auto sstore = [&](int i, const float (&v)[2]) {
+      const uint32_t a = ldg_base + (uint32_t)(i & 1) * 256u + lane * 4;
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[0]) : "memory");
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 128), "f"(v[1]) : "memory");
+    };
+    if (ld_writer) {
+      float v[2];
+      gload(0, v);
+      sstore(0, v);
+    }
+    const uint32_t ds_chunk = smem_u32(smem + C::OFF_DS) + (uint32_t)chunk * 16384u;
+    for (int i = 0; i < p.n_qt; ++i) {
+      const uint32_t ph = (uint32_t)i & 1u;
+      const uint32_t ldw = ldg_base + ph * 256u;  // this tile's (lse, delta)
+      named_bar_sync(1 + g, 128);  // tile i's staging written; tile i-1's readers done
+      float nv[2];
+      if (ld_writer) gload(i + 1, nv);
+      if (storer) {
+        // dS^T chunk was last stored at tile i-1 by this thread: wait for the
+        // TMA store to finish reading shared memory
+        bulk_wait_read<0>();
+        mbar_arrive(&st_free[chunk]);
+      }
+      mbar_wait(sdp_full, ph);
+      tc_fence_after();
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_IN, i);
+      // the group's 32 columns of S^T and dP^T into registers
+      uint32_t sr[32], dr[32];
+      tmem_ld32_nowait(tmem + lane_off + C::TM_ST + g * 32, sr);
+      tmem_ld32_nowait(tmem + lane_off + C::TM_DPT + g * 32, dr);
+      tmem_wait_ld();
+      reg_fence32(sr);
+      reg_fence32(dr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(loaded);
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_LOADED, i);
+      // P^T into sr, unscaled dS^T = P^T (dP^T - delta) into dr (in place);
+      // the 1/sqrt(hd) is applied once to dK (epilogue) and dQ (GEMM alpha)
+#pragma unroll
+      for (int e4 = 0; e4 < 8; ++e4) {
+        float4 l4, d4;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(l4.x), "=f"(l4.y), "=f"(l4.z), "=f"(l4.w)
+                     : "r"(ldw + (uint32_t)(4 * e4) * 4u));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
+                     : "r"(ldw + 128u + (uint32_t)(4 * e4) * 4u));
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = 4 * e4 + u;
+          const float xv = fmaf(__uint_as_float(sr[e]), cl2, -lv[u]);
+          const float pv = (kBwdPolyMask >> u) & 1 ? exp2_fma(xv) : ex2_approx(xv);
+          dr[e] = __float_as_uint(pv * (__uint_as_float(dr[e]) - dv[u]));
+          sr[e] = __float_as_uint(pv);
+        }
+      }
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_MATH, i);
+      // P^T over the S^T columns [16g, 16g+16) once all 16 warps read theirs
+      mbar_wait(loaded, ph);
+      {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack_bf16x2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1]));
+        tmem_st16(tmem + lane_off + C::TM_ST + g * 16, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);  // dV(i) may start
+      // dS^T chunk: free once dK(i-1) read it and its TMA store read it
+      mbar_wait(ds_free, ph ^ 1u);
+      mbar_wait(&st_free[chunk], ph);
+      store_row32(ds_chunk, r, (g & 1) * 4, *reinterpret_cast<const float(*)[32]>(dr));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pds_full);
+      if (quad == 0 && lane == 0 && g == 0) trace_ev(p, TR_SM_OUT, i);
+      if (storer) {
+        mbar_wait(pds_full, ph);  // all rows of the chunk written
+        tma_store_3d(&p.tm_dst, smem + C::OFF_DS + chunk * 16384, i * BQB + chunk * 64, k0,
+                     smp * p.H + head);
+        bulk_commit();
+      }
+      // tile i+1's (lse, delta) into the other staging buffer (last read at tile i-1)
+      if (ld_writer) sstore(i + 1, nv);
+    }
+    // ------------------------------------------------- dK, dV epilogue
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const int krow = k0 + r;
+    __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + krow) * p.ld_qkv + col_k;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {  // dK then dV
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {  // group g: columns [g*HD/4, (g+1)*HD/4)
+        const int col = g * (HD / 4) + c * 16;
+        uint32_t v[16];
+        tmem_ld16_nowait(tmem + lane_off + (which == 0 ? C::TM_DK : C::TM_DV) + col, v);
+        tmem_wait_ld();
+        reg_fence16(v);
+        if (krow < p.S) {
+          __nv_bfloat16* dst = drow + which * HD + col;
+          const float f = which == 0 ? scale : 1.0f;  // dK carries the dS scale
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * f, __uint_as_float(v[u * 8 + 1]) * f);
+            w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * f, __uint_as_float(v[u * 8 + 3]) * f);
+            w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * f, __uint_as_float(v[u * 8 + 5]) * f);
+            w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * f, __uint_as_float(v[u * 8 + 7]) * f);
+            *reinterpret_cast<uint4*>(dst + u * 8) = w;
+          }
+        }
+      }
+    }
+    if (storer) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS));
+  }
+}
+
+
+template <int HD>
+cudaError_t launch_bwd(const BwdParams& p, int grid, cudaStream_t s) {
+  using C = BwdCfg<HD>;
+  // once per instantiation and process (host threads of in-process ranks race here)
+  static cudaError_t attr = cudaSuccess;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::SMEM_BYTES);
+  });
+  if (attr != cudaSuccess) return attr;
+  attn_bwd_kernel<HD><<<grid, kBwdThreads, C::SMEM_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
 
 // ------------------------------------------ backward with dQ fused (gangs)
 // The same per-(key tile) work as attn_bwd_kernel plus dQ(i) = dS(i) K as a
@@ -699,27 +1126,6 @@ cudaError_t launch_bwd_dq_mode(const Bwd2Params& p, int grid, int mode, cudaStre
   }
 }
 
-// 2-D fp32 view [cols, rows] (row stride cols), box {128, 1}; columns past
-// `cols` read as zero.
-bool encode_rows_f32(CUtensorMap* map, const float* base, int64_t cols, int64_t rows) {
-  auto fn = encode_fn();
-  if (!fn) {
-    g_attn_err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  cuuint32_t box[2] = {128, 1};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    g_attn_err = "cuTensorMapEncodeTiled (rows) failed (" + std::to_string((int)r) + ")";
-    return false;
-  }
-  return true;
-}
 
 
 int device_sms() {
@@ -732,6 +1138,50 @@ int device_sms() {
 
 }  // namespace attn
 }  // namespace sm100
+
+cudaError_t attn_bwd_split_sm100(const AttnDesc& d, void* dst, cudaStream_t s) {
+  using namespace sm100::attn;
+  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !dst || !d.lse ||
+      d.ld_o % 8 != 0 || reinterpret_cast<uintptr_t>(d.dout) % 16 ||
+      reinterpret_cast<uintptr_t>(d.dqkv) % 16 || reinterpret_cast<uintptr_t>(dst) % 16) {
+    g_attn_err = "attn_bwd_split_sm100: unsupported shape or missing operand";
+    return cudaErrorInvalidValue;
+  }
+  BwdParams p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t cols = 3 * d.heads * d.head_dim;
+  if (!encode_3d(&p.tm_kv, d.qkv, cols, d.seq, d.samples, d.ld_qkv, 128) ||
+      !encode_3d(&p.tm_q, d.qkv, cols, d.seq, d.samples, d.ld_qkv, BQB) ||
+      !encode_3d(&p.tm_do, d.dout, d.heads * d.head_dim, d.seq, d.samples, d.ld_o, BQB) ||
+      !encode_3d(&p.tm_dst, dst, d.seq, d.seq, d.samples * d.heads, d.seq, 128))
+    return cudaErrorInvalidValue;
+  p.S = (int)d.seq;
+  p.H = (int)d.heads;
+  p.n_kt = (int)((d.seq + 127) / 128);
+  p.n_qt = (int)((d.seq + BQB - 1) / BQB);
+  p.c = d.scale * kLog2e;
+  p.scale = d.scale;
+  p.lse = d.lse;
+  p.delta = d.delta;
+  p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
+  p.ld_qkv = d.ld_qkv;
+  p.trace = nullptr;
+  if (std::getenv("TESS_ATTN_TRACE")) {
+    static long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, 8 * 64 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 8 * 64 * sizeof(long long), s);
+    p.trace = tr;
+    g_attn_trace = tr;
+  }
+  const long long grid = (long long)p.n_kt * d.heads * d.samples;
+  if (grid > 0x7fffffffLL) {
+    g_attn_err = "attn_bwd_split_sm100: grid too large";
+    return cudaErrorInvalidValue;
+  }
+  cudaError_t e = d.head_dim == 128 ? launch_bwd<128>(p, (int)grid, s) : launch_bwd<64>(p, (int)grid, s);
+  if (e != cudaSuccess) g_attn_err = std::string("attn_bwd_split_sm100 launch: ") + cudaGetErrorString(e);
+  return e;
+}
 
 AttnBwdPlan attn_bwd_dq_plan(const AttnDesc& d) {
   AttnBwdPlan pl;
@@ -764,8 +1214,8 @@ cudaError_t attn_bwd_dq_sm100(const AttnDesc& d, const AttnBwdDqArgs& x, cudaStr
       !encode_rows_f32(&p.tm_lse, d.lse, d.seq, d.samples * d.heads) ||
       !encode_rows_f32(&p.tm_dlt, d.delta, d.seq, d.samples * d.heads))
     return cudaErrorInvalidValue;
-  if (mode == 3 && !d.dst) return cudaErrorInvalidValue;
-  p.dst = static_cast<__nv_bfloat16*>(d.dst);
+  if (mode == 3 && !x.dst) return cudaErrorInvalidValue;
+  p.dst = static_cast<__nv_bfloat16*>(x.dst);
   p.S = (int)d.seq;
   p.H = (int)d.heads;
   p.n = pl.n;

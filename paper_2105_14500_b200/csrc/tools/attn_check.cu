@@ -1,6 +1,6 @@
 // Standalone check + timing of the attention backward on the GPU box (cfg4
 // head shape by default: b=4, s=2048, 96 heads, hd=128):
-//   * the shipped split path: attn_bwd_sm100 + the batched dQ GEMM over the
+//   * the round-1 split path: attn_bwd_split_sm100 + the batched dQ GEMM over the
 //     stored dS^T, against
 //   * the round-2 experiment attn_bwd_dq_sm100 (attn_bwd_experiments.cuh:
 //     dQ fused with an ordered on-chip accumulation, and its modes).
@@ -123,7 +123,6 @@ int main(int argc, char** argv) {
   delta_k<<<(unsigned)((B * H * (long long)S + 127) / 128), 128>>>(dout, o, delta, S, H, hd, ldo);
   a.dout = dout;
   a.delta = delta;
-  a.dst = dst;
   AttnBwdPlan pl = attn_bwd_dq_plan(a);
   std::printf("shape b=%d s=%d heads=%d hd=%d | fused plan ok=%d n=%d gangs=%d (%d CTAs) acc %.1f MB\n",
               B, S, H, hd, pl.ok, pl.n, pl.gangs, pl.gangs * pl.n, pl.acc_bytes / 1e6);
@@ -132,6 +131,7 @@ int main(int argc, char** argv) {
   AttnBwdDqArgs dqx;
   dqx.dq_acc = acc;
   dqx.dq_sem = sem;
+  dqx.dst = dst;
 
   // split path: attention backward (dK, dV, dS^T) + batched dQ GEMM
   GemmDesc gq;
@@ -156,7 +156,7 @@ int main(int argc, char** argv) {
   gq.alpha = scale;
   auto split = [&]() {
     a.dqkv = dqkv1;
-    CK(attn_bwd_sm100(a, 0));
+    CK(attn_bwd_split_sm100(a, dst, 0));
     CK(gemm_bf16_sm100(gq, 0));
   };
   auto fused = [&]() {
@@ -177,7 +177,13 @@ int main(int argc, char** argv) {
     const int m = atoi(argv[6]);
     if (m < 0) {
       a.dqkv = dqkv1;
-      CK(attn_bwd_sm100(a, 0));
+      CK(attn_bwd_split_sm100(a, dst, 0));
+    } else if (m == 10) {
+      a.dqkv = dqkv3;
+      CK(attn_dq_sm100(a, 0));
+    } else if (m == 11) {
+      a.dqkv = dqkv3;
+      CK(attn_bwd_kv_sm100(a, 0));
     } else {
       mode_only(m);
     }
@@ -244,6 +250,36 @@ int main(int argc, char** argv) {
         std::printf("mode3+GEMM vs split %s: %.3e (bitwise equal %.4f)\n", nm[part],
                     std::sqrt(nn[part] / dd[part]), (double)same[part] / tot[part]);
     }
+    {
+      // the two-pass path: dK/dV pass + dQ pass
+      CK(cudaMemset(dqkv3, 0, rows * ldq * 2));
+      a.dqkv = dqkv3;
+      CK(attn_bwd_kv_sm100(a, 0));
+      CK(attn_dq_sm100(a, 0));
+      CK(cudaDeviceSynchronize());
+      auto d5 = to_f32(dqkv3, rows * ldq);
+      double nn[3] = {0, 0, 0}, dd[3] = {0, 0, 0};
+      long long bad = 0;
+      for (long long row = 0; row < rows; ++row)
+        for (int h = 0; h < H; ++h)
+          for (int part = 0; part < 3; ++part)
+            for (int dd_ = 0; dd_ < hd; ++dd_) {
+              const long long i = row * ldq + (long long)h * 3 * hd + part * hd + dd_;
+              const double want = part == 0 ? r[row * ldo + h * hd + dd_] : d1[i];
+              const double e = d5[i] - want;
+              if (!std::isfinite(d5[i])) ++bad;
+              nn[part] += e * e;
+              dd[part] += want * want;
+            }
+      for (int part = 0; part < 3; ++part)
+        std::printf("kv+dQpass %s vs %s: %.3e\n", nm[part], part == 0 ? "ref" : "split",
+                    std::sqrt(nn[part] / dd[part]));
+      std::printf("kv+dQpass non-finite %lld -> %s\n", bad,
+                  bad == 0 && std::sqrt(nn[0] / dd[0]) < 1e-2 && std::sqrt(nn[1] / dd[1]) < 1e-2 &&
+                          std::sqrt(nn[2] / dd[2]) < 1e-2
+                      ? "PASS"
+                      : "FAIL");
+    }
     // determinism: a second fused run must match bitwise
     if (pl.ok) {
       fused();
@@ -271,7 +307,7 @@ int main(int argc, char** argv) {
   time_it("attn_fwd", [&]() { CK(attn_fwd_sm100(a, 0)); });
   time_it("attn_bwd (split, no dQ)", [&]() {
     a.dqkv = dqkv1;
-    CK(attn_bwd_sm100(a, 0));
+    CK(attn_bwd_split_sm100(a, dst, 0));
   });
   time_it("dQ GEMM", [&]() { CK(gemm_bf16_sm100(gq, 0)); });
   time_it("split total", split);
@@ -281,6 +317,20 @@ int main(int argc, char** argv) {
     time_it("mode2 (no dQ, no store)", [&]() { mode_only(2); });
     time_it("mode3 (no dQ, dS^T store)", [&]() { mode_only(3); });
     time_it("mode3 + dQ GEMM", split3);
+    time_it("dQ pass (recompute)", [&]() {
+      a.dqkv = dqkv3;
+      CK(attn_dq_sm100(a, 0));
+    });
+    time_it("dK/dV pass", [&]() {
+      a.dqkv = dqkv3;
+      CK(attn_bwd_kv_sm100(a, 0));
+    });
+    time_it("dK/dV pass + dQ pass", [&]() {
+      a.dqkv = dqkv3;
+      CK(attn_bwd_kv_sm100(a, 0));
+      CK(attn_dq_sm100(a, 0));
+    });
+    time_it("split total (again)", split);
   }
 
   for (int tm = 0; tm < 4 && std::getenv("TESS_ATTN_TRACE") && pl.ok; ++tm) {

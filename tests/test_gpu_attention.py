@@ -69,7 +69,8 @@ def test_fused_attention_vs_oracle(tess, orc, b, s, h, nh, q, d, allow, op):
     finally:
         tess.profile_enable(False)
     hd = h // nh
-    assert f"attn_fwd_kernel<{hd}>" in kernels and f"attn_bwd_kernel<{hd}>" in kernels, kernels
+    assert f"attn_fwd_kernel<{hd}>" in kernels, kernels
+    assert f"attn_bwd_kv_kernel<{hd}>" in kernels and f"attn_dq_kernel<{hd}>" in kernels, kernels
     errs = {"y": frob(res.y, want["y"]), "dx": frob(res.dx, want["dx"])}
     for k, v in want["grads"].items():
         if np.abs(v).max() > 0:

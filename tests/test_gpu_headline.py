@@ -246,7 +246,8 @@ def test_cfg4_block_vs_torch(tess):
     ran = wide_tile_epilogues(kernels)
     assert {EPI["store"], EPI["gelu"], EPI["resid"], EPI["dgelu"]} <= ran, sorted(kernels)
     assert any(k.startswith("attn_fwd_kernel<128>") for k in kernels)
-    assert any(k.startswith("attn_bwd_kernel<128>") for k in kernels)
+    assert any(k.startswith("attn_bwd_kv_kernel<128>") for k in kernels)
+    assert any(k.startswith("attn_dq_kernel<128>") for k in kernels)
 
     ry, rdx, rg = torch_block(x, P, dy, b, s, nh)
 
