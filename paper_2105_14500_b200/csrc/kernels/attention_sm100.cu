@@ -554,9 +554,13 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
     constexpr uint64_t kTile = (uint64_t)(C::TILE >> 4);
     auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
     auto issue_scores = [&](uint32_t d, uint64_t a, uint64_t b) {
+      if constexpr (HD == 128) {
+        mma_k128_ss_kk(d, a, b, idesc_s, 0u);
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-        mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+      }
     };
     mbar_wait(kv_full, 0);
     mbar_wait(&q_full[0], 0);
@@ -572,11 +576,7 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
       // dV += P^T(i) dO_i; P^T of queries [16kk, 16kk+16) at column 32(kk/2) + 8(kk%2)
       mbar_wait(p_full, i & 1);
       tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        mma_bf16_ts_warp(tm + C::TM_DV, tm + C::TM_S + 32 * (kk >> 1) + 8 * (kk & 1),
-                         mn_do + s * kTile + (uint64_t)kk * 128u, idesc_g,
-                         (i > 0 || kk > 0) ? 1u : 0u);
+      mma_k128_ts_n_pairs(tm + C::TM_DV, tm + C::TM_S, mn_do + s * kTile, idesc_g, i > 0 ? 1u : 0u);
       mma_commit_warp(&do_empty[s]);
       if (i + 1 < n) {
         const int sn = s ^ 1, un = (i + 1) >> 1;
@@ -593,10 +593,7 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
       // dK += dS^T(i) Q_i
       mbar_wait(ds_full, i & 1);
       tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        mma_bf16_warp(tm + C::TM_DK, kmaj_ds + kmaj_off(kk), mn_q + s * kTile + (uint64_t)kk * 128u,
-                      idesc_g, (i > 0 || kk > 0) ? 1u : 0u);
+      mma_k128_ss_kn(tm + C::TM_DK, kmaj_ds, mn_q + s * kTile, idesc_g, i > 0 ? 1u : 0u);
       mma_commit_warp(&q_empty[s]);
       mma_commit_warp(ds_free);
     }
@@ -755,6 +752,20 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
 // TMEM: S [0,128), dP [128,256), dQ [256,256+hd), Q [384,384+hd/2),
 // dS [448,512).
 constexpr int kDqThreads = 320;
+// Phase stamps of CTA 0 for the bring-up harness only (csrc/tools compiles
+// this file with TESS_ATTN_TRACE_BUILD); the library build has no trace code.
+#ifdef TESS_ATTN_TRACE_BUILD
+__device__ long long* g_dq_trace = nullptr;
+#define DQ_TRACE(ev, step)                                                             \
+  do {                                                                                 \
+    if (g_dq_trace && blockIdx.x == 0 && (step) < 16)                                  \
+      g_dq_trace[((ev) * 16 + (warp)) * 16 + (step)] = clock64();                      \
+  } while (0)
+#else
+#define DQ_TRACE(ev, step) \
+  do {                     \
+  } while (0)
+#endif
 
 struct DqParams {
   CUtensorMap tm_kv;  // qkv view, box {64, 128}: Q_i, K_j, V_j
@@ -859,6 +870,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       for (int j = 0; j < n; ++j) {
         const int ks = j % C::K_STAGES, ku = j / C::K_STAGES;
         if (ku > 0) mbar_wait(&k_empty[ks], (ku - 1) & 1);
+        DQ_TRACE(10, j);
         mbar_expect_tx(&k_full[ks], C::TILE);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c)
@@ -887,17 +899,26 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
     // A (M=128 x K=hd) from TMEM at column a, 8 columns per K=16 step
     auto issue_ts = [&](uint32_t d, uint32_t a, uint64_t b) {
+      if constexpr (HD == 128) {
+        mma_k128_ts_k(d, a, b, idesc_s, 0u);
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-        mma_bf16_ts_warp(d, a + 8 * kk, b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_ts_warp(d, a + 8 * kk, b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+      }
     };
     auto issue_ss = [&](uint32_t d, uint64_t a, uint64_t b) {
+      if constexpr (HD == 128) {
+        mma_k128_ss_kk(d, a, b, idesc_s, 0u);
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-        mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+      }
     };
     auto wait_k = [&](int j) {
       mbar_wait(&k_full[j % C::K_STAGES], (j / C::K_STAGES) & 1);
+      if (lane == 0) DQ_TRACE(11, j);
       tc_fence_after();
     };
     auto wait_v = [&](int j) {
@@ -905,6 +926,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       tc_fence_after();
     };
     mbar_wait(qd_tmem, 0);
+    if (lane == 0) DQ_TRACE(0, 0);
     tc_fence_after();
     wait_k(0);
     issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k);
@@ -917,6 +939,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       if (j + 1 < n) {
         // S(j+1) over S(j) once every warp holds S(j) in registers
         mbar_wait(s_loaded, j & 1);
+        if (lane == 0) DQ_TRACE(1, j);
         wait_k(j + 1);
         issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + ((j + 1) % C::K_STAGES) * kTile);
         mma_commit_warp(s_full);
@@ -930,16 +953,16 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       // dQ += dS(j) K_j, dS (bf16 pairs) in its own columns: keys
       // [16kk, 16kk+16) of group kk/4 at column 32(kk/4) + 8(kk%4)
       mbar_wait(ds_full, j & 1);
+      if (lane == 0) DQ_TRACE(2, j);
       tc_fence_after();
       const uint64_t bk = mn_k + (j % C::K_STAGES) * kTile;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        mma_bf16_ts_warp(tm + C::TM_DQ, tm + C::TM_DS + 32 * (kk >> 2) + 8 * (kk & 3),
-                         bk + (uint64_t)kk * 128u, idesc_q, (j > 0 || kk > 0) ? 1u : 0u);
+      // dS columns: 32 per 64-key group -> contiguous 8 per K=16 step
+      mma_k128_ts_n(tm + C::TM_DQ, tm + C::TM_DS, bk, idesc_q, j > 0 ? 1u : 0u);
       mma_commit_warp(&k_empty[j % C::K_STAGES]);
       mma_commit_warp(dq_done);
     }
     mma_commit_warp(fin);
+    if (lane == 0) DQ_TRACE(3, 15);
   } else {
     // ------------------------------------------ softmax-gradient warps
     const int quad = warp & 3;
@@ -957,6 +980,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       // the Q_i row into TMEM (A operand of S): group g copies its half of
       // the head dimension (hd/2 bf16, 16-byte pieces of the SW128 tile)
       mbar_wait(qd_full, 0);
+      if (lane == 0) DQ_TRACE(4, 0);
       constexpr int HW = HD / 2;  // bf16 per group
       {
         const uint32_t base = smem_u32(smem + C::OFF_Q);
@@ -984,6 +1008,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     }
     for (int j = 0; j < n; ++j) {
       mbar_wait(s_full, j & 1);
+      if (lane == 0) DQ_TRACE(5, j);
       tc_fence_after();
       float pr[64];
       {
@@ -1002,6 +1027,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_loaded);
+      if (lane == 0) DQ_TRACE(6, j);
       // one exponential in four on the FMA pipe (same split as attn_bwd_kernel)
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
@@ -1009,6 +1035,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
       }
       mbar_wait(dp_full, j & 1);
+      if (lane == 0) DQ_TRACE(7, j);
       tc_fence_after();
       const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
       uint32_t d[64];
@@ -1040,9 +1067,11 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      if (lane == 0) DQ_TRACE(8, j);
     }
     // ------------------------------------------------ dQ epilogue
     mbar_wait(fin, 0);
+    DQ_TRACE(9, 0);
     tc_fence_after();
     __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + qrow) * p.ld_qkv + col_q;
     const float scale = p.scale;

@@ -342,6 +342,198 @@ __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
       : "memory");
 }
 
+
+// One K=128 block (8 MMAs of K=16) as ONE warp-wide statement: a single
+// elect, descriptors advanced in PTX registers (K-major SW128 operands +32 B
+// per step and the next 16 KB chunk after four; MN-major ones +2 KB; TMEM A
+// +8 columns). The attention kernels' MMA warp shares its SM sub-partition
+// with two busy softmax warps; per-MMA elect / R2UR sequences there kept the
+// tensor pipe waiting for instructions.
+// A, B K-major (smem)
+__device__ __forceinline__ void mma_k128_ss_kk(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q, e;\n\t"
+      ".reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 a, %1;\n\t"
+      "mov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 1018;\n\t"
+      "add.u64 b, b, 1018;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc0));
+}
+// A K-major, B MN-major (smem)
+__device__ __forceinline__ void mma_k128_ss_kn(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q, e;\n\t"
+      ".reg .b64 a, b;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 a, %1;\n\t"
+      "mov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 1018;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "add.u64 a, a, 2;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, q;\n\t"
+      "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc0));
+}
+// A in TMEM, B K-major (smem)
+__device__ __forceinline__ void mma_k128_ts_k(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q, e;\n\t"
+      ".reg .b64 b;\n\t"
+      ".reg .b32 ta;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 ta, %1;\n\t"
+      "mov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, p;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 1018;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "}" ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc0));
+}
+// A in TMEM, B MN-major (smem)
+__device__ __forceinline__ void mma_k128_ts_n(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q, e;\n\t"
+      ".reg .b64 b;\n\t"
+      ".reg .b32 ta;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 ta, %1;\n\t"
+      "mov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, p;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "}" ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc0));
+}
+// A in TMEM in 8-column pairs 32 columns apart (columns 0, 8, 32, 40, ...),
+// B MN-major (smem)
+__device__ __forceinline__ void mma_k128_ts_n_pairs(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q, e;\n\t"
+      ".reg .b64 b;\n\t"
+      ".reg .b32 ta;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 ta, %1;\n\t"
+      "mov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, p;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 24;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 24;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 24;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "}" ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc0));
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]: the A operand (M x 16, bf16 packed two per
 // 32-bit column, K-major) is read from tensor memory at column tmem_a.
 __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
