@@ -317,6 +317,8 @@ __global__ void ln_params_partial_kernel(const TD* dy, const TX* x, const float*
 // of the configs hit (4096 * k, 6144, 3072, 2048, ...).
 constexpr int kLnMaxThreads = 1024;
 
+
+
 __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&v)[8]) {
   const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -457,10 +459,34 @@ __global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_fwd_kern
   const int span = (TH ? TH : (int)blockDim.x) * 8;
   const int w = NV * span;
   const int c0 = threadIdx.x * 8;
+  // the thread's gain / bias columns are the same for every row: registers
+  // (one 512-thread block per SM then, but with the next row in flight:
+  // 0.282 -> 0.237 ms per step for the two launches, r2_ln_fwd_prefetch_ab.log)
+  float g[NV][8], b[NV][8];
+  if (!SPLIT) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      ld8(gain + c0 + k * span, g[k]);
+      ld8(bias + c0 + k * span, b[k]);
+    }
+  }
+  // raw 16-byte vectors of the next row are loaded before this row's
+  // reduction, so the HBM latency of row r+grid overlaps row r's work
+  constexpr int RV = sizeof(T) / 2;  // uint4 per 8 elements
+  uint4 nxt[NV][RV];
+  auto load_raw = [&](int64_t rr) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int u = 0; u < RV; ++u)
+        nxt[k][u] = __ldg(reinterpret_cast<const uint4*>(x + rr * w + c0 + k * span) + u);
+  };
+  if (blockIdx.x < rows) load_raw(blockIdx.x);
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     float v[NV][8];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) ld8(x + r * w + c0 + k * span, v[k]);
+    for (int k = 0; k < NV; ++k) unpack8(nxt[k], v[k]);
+    if (r + gridDim.x < rows) load_raw(r + gridDim.x);
     const float2 t = row_meanvar<NV, TH>(v, red);
     if (SPLIT) {
       if (threadIdx.x == 0) {
@@ -475,11 +501,9 @@ __global__ void __launch_bounds__(NV == 1 ? kLnMaxThreads : 512) ln_vec_fwd_kern
     const float rstd = 1.0f / sqrtf(var + eps);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      float g[8], b[8], o[8];
-      ld8(gain + c0 + k * span, g);
-      ld8(bias + c0 + k * span, b);
+      float o[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = g[e] * ((v[k][e] - mu) * rstd) + b[e];
+      for (int e = 0; e < 8; ++e) o[e] = g[k][e] * ((v[k][e] - mu) * rstd) + b[k][e];
       st8(y + r * w + c0 + k * span, o);
     }
     if (threadIdx.x == 0) {
