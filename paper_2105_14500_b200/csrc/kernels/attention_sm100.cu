@@ -388,18 +388,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 constexpr int kBwdPolyMask = TESS_ATTN_BWD_POLY;
 
 
-// 32 bf16 values of row r (columns [u0*8, u0*8+32) of a 64-column K-major
-// SW128 tile) -> shared memory.
-__device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const float (&v)[32]) {
-  const uint32_t row_base = base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int k0 = u * 8;
-    st_shared_v4(row_base + (uint32_t)(((u0 + u) ^ (r & 7)) << 4), pack_bf16x2(v[k0], v[k0 + 1]),
-                 pack_bf16x2(v[k0 + 2], v[k0 + 3]), pack_bf16x2(v[k0 + 4], v[k0 + 5]),
-                 pack_bf16x2(v[k0 + 6], v[k0 + 7]));
-  }
-}
 
 // ---------------------------------------------------- backward: dK, dV pass
 // dV = P^T dO and dK = scale * dS^T Q for one 128-key tile per CTA, walking
@@ -407,18 +395,22 @@ __device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const 
 // either). 320 threads:
 //   warp 0      TMA: K, V once; Q_i (+ its lse and delta rows) and dO_i into
 //               two-slot rings.
-//   warp 1      MMA issuer (warp-wide, one elected lane; descriptors built
-//               once from warp-uniform bases), all M=128 N=128:
+//   warp 1      MMA issuer (warp-wide, one elected lane; each K=128 block
+//               of MMAs one PTX statement), all M=128 N=128:
 //                 dV += P^T(i) dO_i          (A = P^T in TMEM)
 //                 S^T(i+1) = K Q_{i+1}^T     (over the consumed P^T, in order)
-//                 dP^T(i+1) = V dO_{i+1}^T   (once dP^T(i) is in registers)
-//                 dK += dS^T(i) Q_i          (A = dS^T in shared memory)
+//                 dK += dS^T(i) Q_i          (A = dS^T in TMEM)
+//                 dP^T(i+1) = V dO_{i+1}^T   (over dS^T(i), in order behind dK)
 //   warps 2-9   thread = key row, group g = queries [64g, 64g+64):
 //               P^T = 2^(c S^T - lse) -> bf16 pairs over the thread's own
-//               consumed S^T columns (no cross-warp barrier), then
-//               dS^T = P^T (dP^T - delta) -> shared memory (unscaled; the
-//               1/sqrt(hd) goes to dK's epilogue); at the end dK, dV out.
-// TMEM: S^T / P^T [0,128), dP^T [128,256), dV [256,256+hd), dK [384,384+hd).
+//               consumed S^T columns, then dS^T = P^T (dP^T - delta) -> bf16
+//               over its own consumed dP^T columns (unscaled; the 1/sqrt(hd)
+//               goes to dK's epilogue); at the end dK, dV out.
+// No dS^T in shared memory: the kernel is bound by the shared-memory port
+// (SS score MMAs alone need all 128 B/clk), and a dS^T store + its dK read
+// were 64 KB of the ~320 KB it moved per query tile.
+// TMEM: S^T / P^T [0,128), dP^T / dS^T [128,256), dV [256,256+hd),
+// dK [384,384+hd).
 constexpr int kKvThreads = 320;
 
 struct KvParams {
@@ -439,8 +431,7 @@ struct KvCfg {
   static constexpr int OFF_V = TILE;
   static constexpr int OFF_Q = 2 * TILE;         // 2 slots
   static constexpr int OFF_DO = 4 * TILE;        // 2 slots
-  static constexpr int OFF_DS = 6 * TILE;        // dS^T: 128 keys x 128 queries, 2 x 16 KB
-  static constexpr int OFF_LD = OFF_DS + 32768;  // per Q slot: lse[128] | delta[128]
+  static constexpr int OFF_LD = 6 * TILE;        // per Q slot: lse[128] | delta[128]
   static constexpr int OFF_BAR = OFF_LD + 2 * 1024;
   static constexpr int USED = OFF_BAR + 256;
   static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
@@ -464,10 +455,8 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
   uint64_t* s_full = bars + 9;     // S^T(i) in TMEM
   uint64_t* p_full = bars + 10;    // P^T(i) in TMEM (8 warps)
   uint64_t* dp_full = bars + 11;   // dP^T(i) in TMEM
-  uint64_t* dp_loaded = bars + 12; // dP^T(i) in registers (8 warps)
-  uint64_t* ds_full = bars + 13;   // dS^T(i) in shared memory (8 warps)
-  uint64_t* ds_free = bars + 14;   // dK(i) has read dS^T(i)
-  uint64_t* fin = bars + 15;       // dK, dV complete
+  uint64_t* ds_full = bars + 12;   // dS^T(i) in TMEM (8 warps)
+  uint64_t* fin = bars + 13;       // dK, dV complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x / 32;
@@ -490,9 +479,7 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
     mbar_init(s_full, 1);
     mbar_init(p_full, 8);
     mbar_init(dp_full, 1);
-    mbar_init(dp_loaded, 8);
     mbar_init(ds_full, 8);
-    mbar_init(ds_free, 1);
     mbar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
@@ -548,7 +535,6 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
     const uint64_t kmaj_v = make_sdesc(sbase + C::OFF_V, 16, 1024);
     const uint64_t kmaj_q = make_sdesc(sbase + C::OFF_Q, 16, 1024);
     const uint64_t kmaj_do = make_sdesc(sbase + C::OFF_DO, 16, 1024);
-    const uint64_t kmaj_ds = make_sdesc(sbase + C::OFF_DS, 16, 1024);
     const uint64_t mn_q = make_sdesc(sbase + C::OFF_Q, 16384, 1024);
     const uint64_t mn_do = make_sdesc(sbase + C::OFF_DO, 16384, 1024);
     constexpr uint64_t kTile = (uint64_t)(C::TILE >> 4);
@@ -578,24 +564,26 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
       tc_fence_after();
       mma_k128_ts_n_pairs(tm + C::TM_DV, tm + C::TM_S, mn_do + s * kTile, idesc_g, i > 0 ? 1u : 0u);
       mma_commit_warp(&do_empty[s]);
+      const int sn = s ^ 1, un = (i + 1) >> 1;
       if (i + 1 < n) {
-        const int sn = s ^ 1, un = (i + 1) >> 1;
         mbar_wait(&q_full[sn], un & 1);
         tc_fence_after();
         issue_scores(tm + C::TM_S, kmaj_k, kmaj_q + sn * kTile);
         mma_commit_warp(s_full);
-        mbar_wait(dp_loaded, i & 1);
+      }
+      // dK += dS^T(i) Q_i; dS^T of queries [16kk, 16kk+16) at column
+      // 64(kk/4) + 8(kk%4) of the dP^T columns
+      mbar_wait(ds_full, i & 1);
+      tc_fence_after();
+      mma_k128_ts_n_quads(tm + C::TM_DK, tm + C::TM_DP, mn_q + s * kTile, idesc_g, i > 0 ? 1u : 0u);
+      mma_commit_warp(&q_empty[s]);
+      if (i + 1 < n) {
+        // dP^T(i+1) over dS^T(i): in order behind dK(i), its reader
         mbar_wait(&do_full[sn], un & 1);
         tc_fence_after();
         issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do + sn * kTile);
         mma_commit_warp(dp_full);
       }
-      // dK += dS^T(i) Q_i
-      mbar_wait(ds_full, i & 1);
-      tc_fence_after();
-      mma_k128_ss_kn(tm + C::TM_DK, kmaj_ds, mn_q + s * kTile, idesc_g, i > 0 ? 1u : 0u);
-      mma_commit_warp(&q_empty[s]);
-      mma_commit_warp(ds_free);
     }
     mma_commit_warp(fin);
   } else {
@@ -605,7 +593,6 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
     const int r = quad * 32 + lane;  // key row within the tile (TMEM lane)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float cl2 = p.c, scale = p.scale;
-    const uint32_t ds_chunk = smem_u32(smem + C::OFF_DS) + (uint32_t)g * 16384u;
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
       const uint32_t ldw = smem_u32(smem + C::OFF_LD + s * 1024) + (uint32_t)g * 256u;
@@ -652,41 +639,37 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      // ---- dS^T = P^T (dP^T - delta) -> shared memory (unscaled)
+      // ---- dS^T = P^T (dP^T - delta) (unscaled) over the thread's own
+      // consumed dP^T columns: 64 queries -> 32 bf16-pair columns
       mbar_wait(dp_full, i & 1);
       tc_fence_after();
+      const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
       uint32_t d[64];
       {
         uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
         uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
-        tmem_ld32_nowait(tmem + lane_off + C::TM_DP + g * 64, d0);
-        tmem_ld32_nowait(tmem + lane_off + C::TM_DP + g * 64 + 32, d1);
+        tmem_ld32_nowait(dpc, d0);
+        tmem_ld32_nowait(dpc + 32, d1);
         tmem_wait_ld();
         reg_fence32(d0);
         reg_fence32(d1);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dp_loaded);
-      if (i > 0) mbar_wait(ds_free, (i - 1) & 1);
+      uint32_t pk[32];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int e4 = 0; e4 < 8; ++e4) {
-          float4 d4;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
-                       : "r"(ldw + 512u + (uint32_t)(128 * h + 16 * e4)));
-          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = 32 * h + 4 * e4 + u;
-            d[e] = __float_as_uint(pr[e] * (__uint_as_float(d[e]) - dv[u]));
-          }
-        }
-        store_row32(ds_chunk, r, 4 * h, *reinterpret_cast<const float(*)[32]>(d + 32 * h));
+      for (int e4 = 0; e4 < 16; ++e4) {
+        float4 d4;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
+                     : "r"(ldw + 512u + (uint32_t)(16 * e4)));
+        const int e = 4 * e4;
+        pk[2 * e4] = pack_bf16x2(pr[e] * (__uint_as_float(d[e]) - d4.x),
+                                 pr[e + 1] * (__uint_as_float(d[e + 1]) - d4.y));
+        pk[2 * e4 + 1] = pack_bf16x2(pr[e + 2] * (__uint_as_float(d[e + 2]) - d4.z),
+                                     pr[e + 3] * (__uint_as_float(d[e + 3]) - d4.w));
       }
-      fence_proxy_async_smem();
+      tmem_st32(dpc, pk);
+      tmem_wait_st();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
     }

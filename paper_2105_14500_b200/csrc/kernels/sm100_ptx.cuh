@@ -533,6 +533,44 @@ __device__ __forceinline__ void mma_k128_ts_n_pairs(uint32_t tmem_d, uint32_t tm
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
       "}" ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc0));
 }
+// A in TMEM in 32-column quads 64 columns apart (columns 0, 8, 16, 24, 64,
+// 72, 80, 88), B MN-major (smem)
+__device__ __forceinline__ void mma_k128_ts_n_quads(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                   uint32_t acc0) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q, e;\n\t"
+      ".reg .b64 b;\n\t"
+      ".reg .b32 ta;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b32 ta, %1;\n\t"
+      "mov.b64 b, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, p;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 40;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "add.u32 ta, ta, 8;\n\t"
+      "add.u64 b, b, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, q;\n\t"
+      "}" ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc0));
+}
 
 // D[tmem] (+)= A[tmem] * B[smem]: the A operand (M x 16, bf16 packed two per
 // 32-bit column, K-major) is read from tensor memory at column tmem_a.

@@ -42,6 +42,19 @@ cudaError_t attn_bwd_split_sm100(const AttnDesc& d, void* dst, cudaStream_t s);
 namespace sm100 {
 namespace attn {
 
+// 32 bf16 values of row r (columns [u0*8, u0*8+32) of a 64-column K-major
+// SW128 tile) -> shared memory.
+__device__ __forceinline__ void store_row32(uint32_t base, int r, int u0, const float (&v)[32]) {
+  const uint32_t row_base = base + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k0 = u * 8;
+    st_shared_v4(row_base + (uint32_t)(((u0 + u) ^ (r & 7)) << 4), pack_bf16x2(v[k0], v[k0 + 1]),
+                 pack_bf16x2(v[k0 + 2], v[k0 + 3]), pack_bf16x2(v[k0 + 4], v[k0 + 5]),
+                 pack_bf16x2(v[k0 + 6], v[k0 + 7]));
+  }
+}
+
 // ------------------------------------------- the round-1 split backward
 // (shipped until round 2; the harness's baseline) dK, dV and dS^T to HBM,
 // dQ by a batched GEMM over dS^T.
