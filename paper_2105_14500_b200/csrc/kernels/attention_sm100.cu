@@ -718,22 +718,22 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
 // recomputed on chip (the flash-attention "dQ pass"): no dS ever reaches
 // HBM, dQ accumulates in TMEM over the key tiles in order (deterministic, no
 // atomics). One CTA = one (sample, head, query tile), 320 threads:
-//   warp 0      TMA: Q_i (then copied into TMEM: S reads only K_j from
-//               shared memory), dO_i once; K_j into a 3-slot ring, V_j into
-//               a 2-slot ring.
-//   warp 1      MMA issuer (warp-wide, one elected lane), all M=128 N=128:
+//   warp 0      TMA: Q_i, dO_i once (then copied into TMEM: the score MMAs
+//               read only K_j / V_j from shared memory); K_j into a 3-slot
+//               ring, V_j into a 2-slot ring.
+//   warp 1      MMA issuer (warp-wide, one elected lane; each K=128 block
+//               one PTX statement), all M=128 N=128:
 //                 S(j+1) = Q K^T      (A = Q in TMEM)   once S(j) is loaded
-//                 dP(j+1) = dO V^T    (A = dO in smem)  once dP(j) is loaded
-//                 dQ += dS(j) K_j     (A = dS in its own TMEM columns, B = K_j
-//                                      read MN-major)
-//               so the next tile's S and dP run while dS(j) is computed.
+//                 dQ += dS(j) K_j     (A = dS in TMEM over the consumed dP
+//                                      columns, B = K_j read MN-major)
+//                 dP(j+1) = dO V^T    (A = dO in TMEM)  in order behind dQ(j)
 //   warps 2-9   thread = query row, group g = keys [64g, 64g+64):
 //               P = 2^(c S - lse) (lse, delta are the row's own: registers),
-//               dS = P (dP - delta) -> bf16 pairs into TMEM once dQ(j-1) has
-//               read the previous dS; at the end dQ out of TMEM (scaled)
-//               into the Q slot of dqkv.
-// TMEM: S [0,128), dP [128,256), dQ [256,256+hd), Q [384,384+hd/2),
-// dS [448,512).
+//               dS = P (dP - delta) -> bf16 pairs over its own consumed dP
+//               columns; at the end dQ out of TMEM (scaled) into the Q slot
+//               of dqkv.
+// TMEM: S [0,128), dP / dS [128,256), dQ [256,256+hd), Q [384,384+hd/2),
+// dO [448,448+hd/2).
 constexpr int kDqThreads = 320;
 // Phase stamps of CTA 0 for the bring-up harness only (csrc/tools compiles
 // this file with TESS_ATTN_TRACE_BUILD); the library build has no trace code.
@@ -773,7 +773,7 @@ struct DqCfg {
   static constexpr int USED = OFF_BAR + 256;
   static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_Q = 384, TM_DS = 448;
+  static constexpr int TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_Q = 384, TM_DO = 448;
 };
 
 template <int HD>
@@ -793,10 +793,8 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
   uint64_t* s_full = v_empty + C::V_STAGES;     // S(j) in TMEM
   uint64_t* s_loaded = s_full + 1;              // S(j) in registers (8 warps)
   uint64_t* dp_full = s_loaded + 1;             // dP(j) in TMEM
-  uint64_t* dp_loaded = dp_full + 1;            // dP(j) in registers (8 warps)
-  uint64_t* ds_full = dp_loaded + 1;            // dS(j) in TMEM (8 warps)
-  uint64_t* dq_done = ds_full + 1;              // dQ(j) has read dS(j)
-  uint64_t* fin = dq_done + 1;                  // dQ complete
+  uint64_t* ds_full = dp_full + 1;              // dS(j) in TMEM (8 warps)
+  uint64_t* fin = ds_full + 1;                  // dQ complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
 
   const int warp = threadIdx.x / 32;
@@ -822,9 +820,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     mbar_init(s_full, 1);
     mbar_init(s_loaded, 8);
     mbar_init(dp_full, 1);
-    mbar_init(dp_loaded, 8);
     mbar_init(ds_full, 8);
-    mbar_init(dq_done, 1);
     mbar_init(fin, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
@@ -876,7 +872,6 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint64_t kmaj_k = make_sdesc(sbase + C::OFF_K, 16, 1024);
     const uint64_t kmaj_v = make_sdesc(sbase + C::OFF_V, 16, 1024);
-    const uint64_t kmaj_do = make_sdesc(sbase + C::OFF_DO, 16, 1024);
     const uint64_t mn_k = make_sdesc(sbase + C::OFF_K, 16384, 1024);
     constexpr uint64_t kTile = (uint64_t)(C::TILE >> 4);
     auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
@@ -888,15 +883,6 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           mma_bf16_ts_warp(d, a + 8 * kk, b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
-      }
-    };
-    auto issue_ss = [&](uint32_t d, uint64_t a, uint64_t b) {
-      if constexpr (HD == 128) {
-        mma_k128_ss_kk(d, a, b, idesc_s, 0u);
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
       }
     };
     auto wait_k = [&](int j) {
@@ -915,7 +901,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k);
     mma_commit_warp(s_full);
     wait_v(0);
-    issue_ss(tm + C::TM_DP, kmaj_do, kmaj_v);
+    issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v);
     mma_commit_warp(dp_full);
     mma_commit_warp(&v_empty[0]);
     for (int j = 0; j < n; ++j) {
@@ -926,23 +912,22 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         wait_k(j + 1);
         issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + ((j + 1) % C::K_STAGES) * kTile);
         mma_commit_warp(s_full);
-        // dP(j+1) over dP(j) once it is in registers
-        mbar_wait(dp_loaded, j & 1);
-        wait_v(j + 1);
-        issue_ss(tm + C::TM_DP, kmaj_do, kmaj_v + ((j + 1) % C::V_STAGES) * kTile);
-        mma_commit_warp(dp_full);
-        mma_commit_warp(&v_empty[(j + 1) % C::V_STAGES]);
       }
-      // dQ += dS(j) K_j, dS (bf16 pairs) in its own columns: keys
-      // [16kk, 16kk+16) of group kk/4 at column 32(kk/4) + 8(kk%4)
+      // dQ += dS(j) K_j; dS of keys [16kk, 16kk+16) at column 64(kk/4) +
+      // 8(kk%4) of the dP columns
       mbar_wait(ds_full, j & 1);
       if (lane == 0) DQ_TRACE(2, j);
       tc_fence_after();
       const uint64_t bk = mn_k + (j % C::K_STAGES) * kTile;
-      // dS columns: 32 per 64-key group -> contiguous 8 per K=16 step
-      mma_k128_ts_n(tm + C::TM_DQ, tm + C::TM_DS, bk, idesc_q, j > 0 ? 1u : 0u);
+      mma_k128_ts_n_quads(tm + C::TM_DQ, tm + C::TM_DP, bk, idesc_q, j > 0 ? 1u : 0u);
       mma_commit_warp(&k_empty[j % C::K_STAGES]);
-      mma_commit_warp(dq_done);
+      if (j + 1 < n) {
+        // dP(j+1) over dS(j): in order behind dQ(j), its reader
+        wait_v(j + 1);
+        issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v + ((j + 1) % C::V_STAGES) * kTile);
+        mma_commit_warp(dp_full);
+        mma_commit_warp(&v_empty[(j + 1) % C::V_STAGES]);
+      }
     }
     mma_commit_warp(fin);
     if (lane == 0) DQ_TRACE(3, 15);
@@ -960,13 +945,14 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     const float dlt = valid ? __ldg(p.delta + lrow) : 0.f;
     const float cl2 = p.c;
     {
-      // the Q_i row into TMEM (A operand of S): group g copies its half of
-      // the head dimension (hd/2 bf16, 16-byte pieces of the SW128 tile)
+      // the Q_i and dO_i rows into TMEM (A operands of S and dP): group g
+      // copies its half of the head dimension (hd/2 bf16, 16-byte pieces of
+      // the SW128 tiles)
       mbar_wait(qd_full, 0);
-      if (lane == 0) DQ_TRACE(4, 0);
       constexpr int HW = HD / 2;  // bf16 per group
-      {
-        const uint32_t base = smem_u32(smem + C::OFF_Q);
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        const uint32_t base = smem_u32(smem + (which == 0 ? C::OFF_Q : C::OFF_DO));
         uint32_t v[HW / 2];
 #pragma unroll
         for (int u = 0; u < HW / 8; ++u) {
@@ -977,7 +963,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
                        : "=r"(v[4 * u]), "=r"(v[4 * u + 1]), "=r"(v[4 * u + 2]), "=r"(v[4 * u + 3])
                        : "r"(a));
         }
-        const uint32_t t = tmem + lane_off + C::TM_Q + g * (HW / 2);
+        const uint32_t t = tmem + lane_off + (which == 0 ? C::TM_Q : C::TM_DO) + g * (HW / 2);
         if constexpr (HW / 2 == 32) {
           tmem_st32(t, *reinterpret_cast<const uint32_t(*)[32]>(v));
         } else {
@@ -1031,21 +1017,14 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         reg_fence32(d0);
         reg_fence32(d1);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dp_loaded);
       // dS = P (dP - delta), unscaled (the 1/sqrt(hd) goes to the epilogue),
-      // 64 keys -> columns [32g, 32g+32) of the dS slot, free once dQ(j-1) read it
+      // 64 keys -> columns [64g, 64g+32) of the consumed dP
       uint32_t pk[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e)
         pk[e] = pack_bf16x2(pr[2 * e] * (__uint_as_float(d[2 * e]) - dlt),
                             pr[2 * e + 1] * (__uint_as_float(d[2 * e + 1]) - dlt));
-      if (j > 0) {
-        mbar_wait(dq_done, (j - 1) & 1);
-        tc_fence_after();
-      }
-      tmem_st32(tmem + lane_off + C::TM_DS + g * 32, pk);
+      tmem_st32(dpc, pk);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
