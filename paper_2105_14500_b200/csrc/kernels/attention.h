@@ -31,7 +31,8 @@ struct AttnDesc {
   float scale = 1.0f;  // 1/sqrt(head_dim)
   // backward only
   const void* dout = nullptr;  // dO bf16, same layout as o (ld_o)
-  const float* delta = nullptr;  // [samples, H, S] rowsum(dO * O)
+  float* delta = nullptr;       // [samples, H, S] rowsum(dO * O): written by the dQ pass,
+                               // read by the dK/dV pass after it
   void* dqkv = nullptr;        // bf16, same layout as qkv (ld_qkv): dQ, dK, dV written
 };
 
@@ -42,11 +43,14 @@ bool attn_fused_supported(const AttnDesc& d);
 
 cudaError_t attn_fwd_sm100(const AttnDesc& d, cudaStream_t s);
 // The backward is two passes, neither of which writes S, P or dS to HBM
-// (both recompute them from lse and delta = rowsum(dO * O); deterministic):
-// dK, dV pass: dK = scale * dS^T Q, dV = P^T dO, one 128-key tile per CTA.
-cudaError_t attn_bwd_kv_sm100(const AttnDesc& d, cudaStream_t s);
-// dQ pass: dQ = scale * dS K, one 128-query tile per CTA.
+// (both recompute them from lse and delta = rowsum(dO * O); deterministic),
+// run in this order:
+// dQ pass: delta (written to d.delta) and dQ = scale * dS K, one 128-query
+// tile per CTA.
 cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s);
+// dK, dV pass: dK = scale * dS^T Q, dV = P^T dO, one 128-key tile per CTA
+// (reads d.delta).
+cudaError_t attn_bwd_kv_sm100(const AttnDesc& d, cudaStream_t s);
 
 const char* attn_last_error();
 

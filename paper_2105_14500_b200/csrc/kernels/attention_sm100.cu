@@ -727,7 +727,10 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
 //                 dQ += dS(j) K_j     (A = dS in TMEM over the consumed dP
 //                                      columns, B = K_j read MN-major)
 //                 dP(j+1) = dO V^T    (A = dO in TMEM)  in order behind dQ(j)
-//   warps 2-9   thread = query row, group g = keys [64g, 64g+64):
+//   warps 2-9   thread = query row, group g = keys [64g, 64g+64): first
+//               delta = rowsum(dO * O) of its row (each group one half of
+//               hd, summed through shared memory; written out for the dK/dV
+//               pass, which runs after this one), then per key tile
 //               P = 2^(c S - lse) (lse, delta are the row's own: registers),
 //               dS = P (dP - delta) -> bf16 pairs over its own consumed dP
 //               columns; at the end dQ out of TMEM (scaled) into the Q slot
@@ -756,7 +759,9 @@ struct DqParams {
   int S, H, n_qt, n_kt;
   float c, scale;
   const float* lse;
-  const float* delta;
+  float* delta;                // out: rowsum(dO * O) [samples, H, S]
+  const __nv_bfloat16* o;      // forward output O (ld_o)
+  long long ld_o;
   __nv_bfloat16* dqkv;
   long long ld_qkv;
 };
@@ -770,7 +775,8 @@ struct DqCfg {
   static constexpr int OFF_K = 2 * TILE;
   static constexpr int OFF_V = OFF_K + K_STAGES * TILE;
   static constexpr int OFF_BAR = OFF_V + V_STAGES * TILE;
-  static constexpr int USED = OFF_BAR + 256;
+  static constexpr int OFF_RED = OFF_BAR + 256;  // delta halves: 2 x 128 fp32
+  static constexpr int USED = OFF_RED + 1024;
   static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
   static constexpr int TMEM_COLS = 512;
   static constexpr int TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_Q = 384, TM_DO = 448;
@@ -942,14 +948,22 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     const long long lrow = ((long long)smp * p.H + head) * p.S + qrow;
     // padded query rows: Q, dO are zero there, dS = 0 whatever lse is
     const float lse = valid ? __ldg(p.lse + lrow) : 0.f;
-    const float dlt = valid ? __ldg(p.delta + lrow) : 0.f;
     const float cl2 = p.c;
+    constexpr int HW = HD / 2;  // hd columns per group
+    // the row's O half, loaded while Q / dO arrive
+    uint4 ov[HW / 8];
+    {
+      const uint4* orow = reinterpret_cast<const uint4*>(
+          p.o + ((long long)smp * p.S + qrow) * p.ld_o + (long long)head * HD + g * HW);
+#pragma unroll
+      for (int u = 0; u < HW / 8; ++u) ov[u] = valid ? __ldg(orow + u) : make_uint4(0, 0, 0, 0);
+    }
+    float dpart = 0.f;
     {
       // the Q_i and dO_i rows into TMEM (A operands of S and dP): group g
       // copies its half of the head dimension (hd/2 bf16, 16-byte pieces of
       // the SW128 tiles)
       mbar_wait(qd_full, 0);
-      constexpr int HW = HD / 2;  // bf16 per group
 #pragma unroll
       for (int which = 0; which < 2; ++which) {
         const uint32_t base = smem_u32(smem + (which == 0 ? C::OFF_Q : C::OFF_DO));
@@ -963,6 +977,20 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
                        : "=r"(v[4 * u]), "=r"(v[4 * u + 1]), "=r"(v[4 * u + 2]), "=r"(v[4 * u + 3])
                        : "r"(a));
         }
+        if (which == 1) {
+          // this half of rowsum(dO * O), in column order
+#pragma unroll
+          for (int u = 0; u < HW / 8; ++u) {
+            const uint32_t ow[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[4 * u + e]));
+              const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[e]));
+              dpart = fmaf(a2.x, b2.x, dpart);
+              dpart = fmaf(a2.y, b2.y, dpart);
+            }
+          }
+        }
         const uint32_t t = tmem + lane_off + (which == 0 ? C::TM_Q : C::TM_DO) + g * (HW / 2);
         if constexpr (HW / 2 == 32) {
           tmem_st32(t, *reinterpret_cast<const uint32_t(*)[32]>(v));
@@ -975,6 +1003,12 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive(qd_tmem);
     }
+    // delta = (low half) + (high half), the same order in both groups
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);
+    red[g * 128 + r] = dpart;
+    named_bar_sync(1, 256);
+    const float dlt = red[r] + red[128 + r];
+    if (g == 0 && valid) p.delta[lrow] = dlt;
     for (int j = 0; j < n; ++j) {
       mbar_wait(s_full, j & 1);
       if (lane == 0) DQ_TRACE(5, j);
@@ -1248,8 +1282,9 @@ cudaError_t attn_bwd_kv_sm100(const AttnDesc& d, cudaStream_t s) {
 
 cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s) {
   using namespace sm100::attn;
-  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !d.lse || d.ld_o % 8 != 0 ||
-      reinterpret_cast<uintptr_t>(d.dout) % 16 || reinterpret_cast<uintptr_t>(d.dqkv) % 16) {
+  if (!attn_fused_supported(d) || !d.dout || !d.delta || !d.dqkv || !d.lse || !d.o ||
+      d.ld_o % 8 != 0 || reinterpret_cast<uintptr_t>(d.dout) % 16 ||
+      reinterpret_cast<uintptr_t>(d.dqkv) % 16) {
     g_attn_err = "attn_dq_sm100: unsupported shape or missing operand";
     return cudaErrorInvalidValue;
   }
@@ -1266,6 +1301,8 @@ cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s) {
   p.scale = d.scale;
   p.lse = d.lse;
   p.delta = d.delta;
+  p.o = static_cast<const __nv_bfloat16*>(d.o);
+  p.ld_o = d.ld_o;
   p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
   p.ld_qkv = d.ld_qkv;
   const long long grid = (long long)p.n_qt * d.heads * d.samples;
@@ -1282,4 +1319,5 @@ cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s) {
 // shared-memory budgets (227 KB opt-in per CTA)
 static_assert(tess::sm100::attn::FwdCfg<128>::SMEM_BYTES <= 232448, "attn fwd smem");
 static_assert(tess::sm100::attn::DqCfg<128>::USED <= 232448, "attn dQ smem");
+static_assert(tess::sm100::attn::DqCfg<128>::OFF_RED % 16 == 0, "attn dQ smem");
 static_assert(tess::sm100::attn::KvCfg<128>::USED <= 232448, "attn dK/dV smem");

@@ -497,17 +497,12 @@ void attn_bwd(Ctx& c, DType t, const RankDims& rd, const std::string& tag,
       k_convert(dout32, DType::F32, dout, t, (size_t)rows * hq, s);
     }
     weight_grad(c, t, o, rows, hq, dy, rd.hin, g ? g->w_proj : nullptr, accumulate, s);
-    {
-      ProfMem pm("attn_delta_vec_kernel",
-                 (double)rows * hq * 2.0 * dtype_size(t) + (double)rd.samples_local * H * S * 4, s);
-      k_attn_delta(dout, o, t, hq, S, H, hd, delta, s, rd.samples_local);
-    }
     AttnDesc a = attn_desc(rd, qkv, o, lse);
     a.dout = dout;
     a.delta = delta;
     a.dqkv = dqkv;
+    run_attn(AttnPass::BwdQ, a, s);   // delta = rowsum(dO * O) -> delta, dQ -> dqkv
     run_attn(AttnPass::BwdKV, a, s);  // dK, dV -> dqkv
-    run_attn(AttnPass::BwdQ, a, s);   // dQ -> dqkv
     nt_product(c, t, dqkv, rows, 3 * hq, p.w_qkv, rd.hin, out_to(dx_f32, DType::F32), s, &wp.qkv);
     weight_grad(c, t, x, rows, rd.hin, dqkv, 3 * hq, g ? g->w_qkv : nullptr, accumulate, s);
     return;
