@@ -24,7 +24,7 @@ def our_name(ncu_name):
     if m:
         b = lambda v: "1" if v in ("true", "1") else "0"  # noqa: E731
         return f"gemm_bf16_kernel<{m[1]},{b(m[2])},{b(m[3])}>"
-    m = re.search(r"(attn_(fwd|bwd)_kernel<\d+>)", ncu_name)
+    m = re.search(r"(attn_\w+_kernel<\d+>)", ncu_name)
     if m:
         return m[1]
     m = re.search(r"(\w+_kernel)\b", ncu_name)  # memory-bound kernels: base name
