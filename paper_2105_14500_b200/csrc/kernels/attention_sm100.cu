@@ -390,11 +390,14 @@ constexpr int kBwdPolyMask = TESS_ATTN_BWD_POLY;
 
 
 // ---------------------------------------------------- backward: dK, dV pass
-// dV = P^T dO and dK = scale * dS^T Q for one 128-key tile per CTA, walking
-// the query tiles; dQ is the separate dQ pass below (no dS leaves the SM in
-// either). 320 threads:
-//   warp 0      TMA: K, V once; Q_i (+ its lse and delta rows) and dO_i into
-//               two-slot rings.
+// dV = P^T dO and dK = scale * dS^T Q per 128-key tile, walking the query
+// tiles; dQ is the separate dQ pass (no dS leaves the SM in either).
+// Persistent: one CTA per SM takes (sample, head, key tile) units in a
+// strided order; the next unit's K / V load as soon as the current unit's
+// last score MMAs have read theirs, and its first scores run while the
+// current unit's dK / dV are written out. 320 threads:
+//   warp 0      TMA: K, V per unit; Q_i (+ its lse and delta rows) and dO_i
+//               into two-slot rings (continuing across units).
 //   warp 1      MMA issuer (warp-wide, one elected lane; each K=128 block
 //               of MMAs one PTX statement), all M=128 N=128:
 //                 dV += P^T(i) dO_i          (A = P^T in TMEM)
@@ -419,6 +422,7 @@ struct KvParams {
   CUtensorMap tm_lse;  // lse [S, samples*H] fp32, box {128, 1} (rows past S read 0)
   CUtensorMap tm_dlt;  // delta, same view
   int S, H, n;         // n = key tiles = query tiles
+  int units;           // samples * H * n
   float c, scale;
   __nv_bfloat16* dqkv;
   long long ld_qkv;
@@ -456,17 +460,15 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
   uint64_t* p_full = bars + 10;    // P^T(i) in TMEM (8 warps)
   uint64_t* dp_full = bars + 11;   // dP^T(i) in TMEM
   uint64_t* ds_full = bars + 12;   // dS^T(i) in TMEM (8 warps)
-  uint64_t* fin = bars + 13;       // dK, dV complete
+  uint64_t* fin = bars + 13;       // dK, dV of the unit complete
+  uint64_t* kv_empty = bars + 14;  // the unit's last MMA reading K / V done
+  uint64_t* acc_free = bars + 15;  // dK, dV read out of TMEM (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int n = p.n;
-  const int kt = blockIdx.x % n;
-  const int job = blockIdx.x / n;  // sample * H + head
-  const int head = job % p.H, smp = job / p.H;
-  const int k0 = kt * 128;
-  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+  const int units = p.units;  // (sample * H + head) * n + key tile
 
   if (warp == 0 && lane == 0) {
     mbar_init(kv_full, 1);
@@ -481,6 +483,8 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
     mbar_init(dp_full, 1);
     mbar_init(ds_full, 8);
     mbar_init(fin, 1);
+    mbar_init(kv_empty, 1);
+    mbar_init(acc_free, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
     prefetch_tmap(&p.tm_do);
@@ -501,28 +505,35 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------ TMA producer
-      mbar_expect_tx(kv_full, 2 * C::TILE);
+      int gs = 0, round = 0;
+      for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
+        const int job = unit / n, k0 = (unit % n) * 128;  // job = sample * H + head
+        const int head = job % p.H, smp = job / p.H;
+        const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+        if (round > 0) mbar_wait(kv_empty, (round - 1) & 1);
+        mbar_expect_tx(kv_full, 2 * C::TILE);
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        tma_load_3d(smem + C::OFF_K + c * 16384, &p.tm_kv, kv_full, col_k + c * 64, k0, smp);
-        tma_load_3d(smem + C::OFF_V + c * 16384, &p.tm_kv, kv_full, col_v + c * 64, k0, smp);
-      }
-      for (int i = 0; i < n; ++i) {
-        const int s = i & 1, u = i >> 1;
-        if (u > 0) mbar_wait(&q_empty[s], (u - 1) & 1);
-        mbar_expect_tx(&q_full[s], C::TILE + 1024);
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_load_3d(smem + C::OFF_K + c * 16384, &p.tm_kv, kv_full, col_k + c * 64, k0, smp);
+          tma_load_3d(smem + C::OFF_V + c * 16384, &p.tm_kv, kv_full, col_v + c * 64, k0, smp);
+        }
+        for (int i = 0; i < n; ++i, ++gs) {
+          const int s = gs & 1, u = gs >> 1;
+          if (u > 0) mbar_wait(&q_empty[s], (u - 1) & 1);
+          mbar_expect_tx(&q_full[s], C::TILE + 1024);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_3d(smem + C::OFF_Q + s * C::TILE + c * 16384, &p.tm_kv, &q_full[s],
-                      col_q + c * 64, i * 128, smp);
-        tma_load_2d(smem + C::OFF_LD + s * 1024, &p.tm_lse, &q_full[s], i * 128, job);
-        tma_load_2d(smem + C::OFF_LD + s * 1024 + 512, &p.tm_dlt, &q_full[s], i * 128, job);
-        if (u > 0) mbar_wait(&do_empty[s], (u - 1) & 1);
-        mbar_expect_tx(&do_full[s], C::TILE);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_3d(smem + C::OFF_Q + s * C::TILE + c * 16384, &p.tm_kv, &q_full[s],
+                        col_q + c * 64, i * 128, smp);
+          tma_load_2d(smem + C::OFF_LD + s * 1024, &p.tm_lse, &q_full[s], i * 128, job);
+          tma_load_2d(smem + C::OFF_LD + s * 1024 + 512, &p.tm_dlt, &q_full[s], i * 128, job);
+          if (u > 0) mbar_wait(&do_empty[s], (u - 1) & 1);
+          mbar_expect_tx(&do_full[s], C::TILE);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_3d(smem + C::OFF_DO + s * C::TILE + c * 16384, &p.tm_do, &do_full[s],
-                      head * HD + c * 64, i * 128, smp);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_3d(smem + C::OFF_DO + s * C::TILE + c * 16384, &p.tm_do, &do_full[s],
+                        head * HD + c * 64, i * 128, smp);
+        }
       }
     }
   } else if (warp == 1) {
@@ -548,44 +559,50 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
           mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
       }
     };
-    mbar_wait(kv_full, 0);
-    mbar_wait(&q_full[0], 0);
-    tc_fence_after();
-    issue_scores(tm + C::TM_S, kmaj_k, kmaj_q);
-    mma_commit_warp(s_full);
-    mbar_wait(&do_full[0], 0);
-    tc_fence_after();
-    issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do);
-    mma_commit_warp(dp_full);
-    for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
-      // dV += P^T(i) dO_i; P^T of queries [16kk, 16kk+16) at column 32(kk/2) + 8(kk%2)
-      mbar_wait(p_full, i & 1);
+    int gs = 0, round = 0;
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
+      mbar_wait(kv_full, round & 1);
+      mbar_wait(&q_full[gs & 1], (gs >> 1) & 1);
       tc_fence_after();
-      mma_k128_ts_n_pairs(tm + C::TM_DV, tm + C::TM_S, mn_do + s * kTile, idesc_g, i > 0 ? 1u : 0u);
-      mma_commit_warp(&do_empty[s]);
-      const int sn = s ^ 1, un = (i + 1) >> 1;
-      if (i + 1 < n) {
-        mbar_wait(&q_full[sn], un & 1);
-        tc_fence_after();
-        issue_scores(tm + C::TM_S, kmaj_k, kmaj_q + sn * kTile);
-        mma_commit_warp(s_full);
-      }
-      // dK += dS^T(i) Q_i; dS^T of queries [16kk, 16kk+16) at column
-      // 64(kk/4) + 8(kk%4) of the dP^T columns
-      mbar_wait(ds_full, i & 1);
+      issue_scores(tm + C::TM_S, kmaj_k, kmaj_q + (gs & 1) * kTile);
+      mma_commit_warp(s_full);
+      mbar_wait(&do_full[gs & 1], (gs >> 1) & 1);
       tc_fence_after();
-      mma_k128_ts_n_quads(tm + C::TM_DK, tm + C::TM_DP, mn_q + s * kTile, idesc_g, i > 0 ? 1u : 0u);
-      mma_commit_warp(&q_empty[s]);
-      if (i + 1 < n) {
-        // dP^T(i+1) over dS^T(i): in order behind dK(i), its reader
-        mbar_wait(&do_full[sn], un & 1);
+      issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do + (gs & 1) * kTile);
+      mma_commit_warp(dp_full);
+      if (n == 1) mma_commit_warp(kv_empty);
+      for (int i = 0; i < n; ++i, ++gs) {
+        const int s = gs & 1;
+        // dV += P^T(i) dO_i; P^T of queries [16kk, 16kk+16) at column 32(kk/2) + 8(kk%2)
+        mbar_wait(p_full, gs & 1);
+        if (i == 0 && round > 0) mbar_wait(acc_free, (round - 1) & 1);  // previous dK, dV out
         tc_fence_after();
-        issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do + sn * kTile);
-        mma_commit_warp(dp_full);
+        mma_k128_ts_n_pairs(tm + C::TM_DV, tm + C::TM_S, mn_do + s * kTile, idesc_g, i > 0 ? 1u : 0u);
+        mma_commit_warp(&do_empty[s]);
+        const int sn = s ^ 1, un = (gs + 1) >> 1;
+        if (i + 1 < n) {
+          mbar_wait(&q_full[sn], un & 1);
+          tc_fence_after();
+          issue_scores(tm + C::TM_S, kmaj_k, kmaj_q + sn * kTile);
+          mma_commit_warp(s_full);
+        }
+        // dK += dS^T(i) Q_i; dS^T of queries [16kk, 16kk+16) at column
+        // 64(kk/4) + 8(kk%4) of the dP^T columns
+        mbar_wait(ds_full, gs & 1);
+        tc_fence_after();
+        mma_k128_ts_n_quads(tm + C::TM_DK, tm + C::TM_DP, mn_q + s * kTile, idesc_g, i > 0 ? 1u : 0u);
+        mma_commit_warp(&q_empty[s]);
+        if (i + 1 < n) {
+          // dP^T(i+1) over dS^T(i): in order behind dK(i), its reader
+          mbar_wait(&do_full[sn], un & 1);
+          tc_fence_after();
+          issue_scores(tm + C::TM_DP, kmaj_v, kmaj_do + sn * kTile);
+          mma_commit_warp(dp_full);
+          if (i + 2 == n) mma_commit_warp(kv_empty);  // the unit's last K / V readers issued
+        }
       }
+      mma_commit_warp(fin);
     }
-    mma_commit_warp(fin);
   } else {
     // ------------------------------------------ softmax-gradient warps
     const int quad = warp & 3;
@@ -593,11 +610,16 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
     const int r = quad * 32 + lane;  // key row within the tile (TMEM lane)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float cl2 = p.c, scale = p.scale;
-    for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
+    int gs = 0, round = 0;
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
+    const int job = unit / n, k0 = (unit % n) * 128;
+    const int head = job % p.H, smp = job / p.H;
+    const int col_q = head * 3 * HD;
+    for (int i = 0; i < n; ++i, ++gs) {
+      const int s = gs & 1;
       const uint32_t ldw = smem_u32(smem + C::OFF_LD + s * 1024) + (uint32_t)g * 256u;
-      mbar_wait(&q_full[s], (i >> 1) & 1);  // lse, delta rows of the slot
-      mbar_wait(s_full, i & 1);
+      mbar_wait(&q_full[s], (gs >> 1) & 1);  // lse, delta rows of the slot
+      mbar_wait(s_full, gs & 1);
       tc_fence_after();
       // ---- P^T = 2^(c S^T - lse) over the group's 64 query columns
       float pr[64];
@@ -641,7 +663,7 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
       if (lane == 0) mbar_arrive(p_full);
       // ---- dS^T = P^T (dP^T - delta) (unscaled) over the thread's own
       // consumed dP^T columns: 64 queries -> 32 bf16-pair columns
-      mbar_wait(dp_full, i & 1);
+      mbar_wait(dp_full, gs & 1);
       tc_fence_after();
       const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
       uint32_t d[64];
@@ -674,7 +696,7 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
       if (lane == 0) mbar_arrive(ds_full);
     }
     // ---- dK, dV out (dK carries the dS scale)
-    mbar_wait(fin, 0);
+    mbar_wait(fin, round & 1);
     tc_fence_after();
     const int krow = k0 + r;
     __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + krow) * p.ld_qkv + col_q;
@@ -701,6 +723,10 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
           }
         }
       }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_free);
     }
   }
 
@@ -1176,6 +1202,17 @@ bool encode_rows_f32(CUtensorMap* map, const float* base, int64_t cols, int64_t 
   return true;
 }
 
+int device_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static int cache[64] = {0};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev];
+}
+
 template <int HD>
 cudaError_t launch_kv(const KvParams& p, int grid, cudaStream_t s) {
   using C = KvCfg<HD>;
@@ -1270,12 +1307,14 @@ cudaError_t attn_bwd_kv_sm100(const AttnDesc& d, cudaStream_t s) {
   p.scale = d.scale;
   p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
   p.ld_qkv = d.ld_qkv;
-  const long long grid = (long long)p.n * d.heads * d.samples;
-  if (grid > 0x7fffffffLL) {
-    g_attn_err = "attn_bwd_kv_sm100: grid too large";
+  const long long units = (long long)p.n * d.heads * d.samples;
+  if (units > 0x7fffffffLL) {
+    g_attn_err = "attn_bwd_kv_sm100: too many units";
     return cudaErrorInvalidValue;
   }
-  cudaError_t e = d.head_dim == 128 ? launch_kv<128>(p, (int)grid, s) : launch_kv<64>(p, (int)grid, s);
+  p.units = (int)units;
+  const int grid = (int)std::min<long long>(units, std::max(1, device_sms()));
+  cudaError_t e = d.head_dim == 128 ? launch_kv<128>(p, grid, s) : launch_kv<64>(p, grid, s);
   if (e != cudaSuccess) g_attn_err = std::string("attn_bwd_kv_sm100 launch: ") + cudaGetErrorString(e);
   return e;
 }

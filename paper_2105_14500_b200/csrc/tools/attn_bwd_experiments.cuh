@@ -1141,13 +1141,6 @@ cudaError_t launch_bwd_dq_mode(const Bwd2Params& p, int grid, int mode, cudaStre
 
 
 
-int device_sms() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int v = 0;
-  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  return v;
-}
 
 }  // namespace attn
 }  // namespace sm100
