@@ -743,8 +743,10 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
 // dQ = scale * dS K computed per 128-query tile with S, P, dP and dS
 // recomputed on chip (the flash-attention "dQ pass"): no dS ever reaches
 // HBM, dQ accumulates in TMEM over the key tiles in order (deterministic, no
-// atomics). One CTA = one (sample, head, query tile), 320 threads:
-//   warp 0      TMA: Q_i, dO_i once (then copied into TMEM: the score MMAs
+// atomics). Persistent: one CTA per SM takes (sample, head, query tile)
+// units in a strided order; the next unit's Q / dO load as soon as the
+// current unit has copied its own into TMEM. 320 threads:
+//   warp 0      TMA: Q_i, dO_i per unit (then copied into TMEM: the score MMAs
 //               read only K_j / V_j from shared memory); K_j into a 3-slot
 //               ring, V_j into a 2-slot ring.
 //   warp 1      MMA issuer (warp-wide, one elected lane; each K=128 block
@@ -764,25 +766,12 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
 // TMEM: S [0,128), dP / dS [128,256), dQ [256,256+hd), Q [384,384+hd/2),
 // dO [448,448+hd/2).
 constexpr int kDqThreads = 320;
-// Phase stamps of CTA 0 for the bring-up harness only (csrc/tools compiles
-// this file with TESS_ATTN_TRACE_BUILD); the library build has no trace code.
-#ifdef TESS_ATTN_TRACE_BUILD
-__device__ long long* g_dq_trace = nullptr;
-#define DQ_TRACE(ev, step)                                                             \
-  do {                                                                                 \
-    if (g_dq_trace && blockIdx.x == 0 && (step) < 16)                                  \
-      g_dq_trace[((ev) * 16 + (warp)) * 16 + (step)] = clock64();                      \
-  } while (0)
-#else
-#define DQ_TRACE(ev, step) \
-  do {                     \
-  } while (0)
-#endif
 
 struct DqParams {
   CUtensorMap tm_kv;  // qkv view, box {64, 128}: Q_i, K_j, V_j
   CUtensorMap tm_do;  // dO view, box {64, 128}
   int S, H, n_qt, n_kt;
+  int units;          // samples * H * n_qt
   float c, scale;
   const float* lse;
   float* delta;                // out: rowsum(dO * O) [samples, H, S]
@@ -816,8 +805,8 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   if ((smem - smem_raw) + C::USED > C::SMEM_BYTES) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* qd_full = bars + 0;                 // Q_i, dO_i in shared memory
-  uint64_t* qd_tmem = bars + 1;                 // ... and in TMEM (8 warps)
+  uint64_t* qd_full = bars + 0;                 // Q_i, dO_i of the unit in shared memory
+  uint64_t* qd_tmem = bars + 1;                 // ... copied into TMEM (8 warps)
   uint64_t* k_full = bars + 2;                  // K_STAGES
   uint64_t* k_empty = k_full + C::K_STAGES;     // K_STAGES
   uint64_t* v_full = k_empty + C::K_STAGES;     // V_STAGES
@@ -826,17 +815,14 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
   uint64_t* s_loaded = s_full + 1;              // S(j) in registers (8 warps)
   uint64_t* dp_full = s_loaded + 1;             // dP(j) in TMEM
   uint64_t* ds_full = dp_full + 1;              // dS(j) in TMEM (8 warps)
-  uint64_t* fin = ds_full + 1;                  // dQ complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  uint64_t* fin = ds_full + 1;                  // dQ of the unit complete
+  uint64_t* acc_free = fin + 1;                 // dQ read out of TMEM (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int qt = blockIdx.x % p.n_qt;
-  const int head = (blockIdx.x / p.n_qt) % p.H;
-  const int smp = blockIdx.x / (p.n_qt * p.H);
-  const int q0 = qt * 128;
-  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
   const int n = p.n_kt;
+  const int units = p.units;  // (sample * H + head) * n_qt + query tile
 
   if (warp == 0 && lane == 0) {
     mbar_init(qd_full, 1);
@@ -854,6 +840,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     mbar_init(dp_full, 1);
     mbar_init(ds_full, 8);
     mbar_init(fin, 1);
+    mbar_init(acc_free, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tm_kv);
     prefetch_tmap(&p.tm_do);
@@ -872,28 +859,36 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------ TMA producer
-      mbar_expect_tx(qd_full, 2 * C::TILE);
+      int gk = 0, round = 0;  // key steps over all units, units of this CTA
+      for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
+        const int job = unit / p.n_qt, q0 = (unit % p.n_qt) * 128;
+        const int head = job % p.H, smp = job / p.H;
+        const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+        // Q / dO tiles: free once the previous unit copied them into TMEM
+        if (round > 0) mbar_wait(qd_tmem, (round - 1) & 1);
+        mbar_expect_tx(qd_full, 2 * C::TILE);
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        tma_load_3d(smem + C::OFF_Q + c * 16384, &p.tm_kv, qd_full, col_q + c * 64, q0, smp);
-        tma_load_3d(smem + C::OFF_DO + c * 16384, &p.tm_do, qd_full, head * HD + c * 64, q0, smp);
-      }
-      for (int j = 0; j < n; ++j) {
-        const int ks = j % C::K_STAGES, ku = j / C::K_STAGES;
-        if (ku > 0) mbar_wait(&k_empty[ks], (ku - 1) & 1);
-        DQ_TRACE(10, j);
-        mbar_expect_tx(&k_full[ks], C::TILE);
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_load_3d(smem + C::OFF_Q + c * 16384, &p.tm_kv, qd_full, col_q + c * 64, q0, smp);
+          tma_load_3d(smem + C::OFF_DO + c * 16384, &p.tm_do, qd_full, head * HD + c * 64, q0,
+                      smp);
+        }
+        for (int j = 0; j < n; ++j, ++gk) {
+          const int ks = gk % C::K_STAGES, ku = gk / C::K_STAGES;
+          if (ku > 0) mbar_wait(&k_empty[ks], (ku - 1) & 1);
+          mbar_expect_tx(&k_full[ks], C::TILE);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_3d(smem + C::OFF_K + ks * C::TILE + c * 16384, &p.tm_kv, &k_full[ks],
-                      col_k + c * 64, j * 128, smp);
-        const int vs = j % C::V_STAGES, vu = j / C::V_STAGES;
-        if (vu > 0) mbar_wait(&v_empty[vs], (vu - 1) & 1);
-        mbar_expect_tx(&v_full[vs], C::TILE);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_3d(smem + C::OFF_K + ks * C::TILE + c * 16384, &p.tm_kv, &k_full[ks],
+                        col_k + c * 64, j * 128, smp);
+          const int vs = gk % C::V_STAGES, vu = gk / C::V_STAGES;
+          if (vu > 0) mbar_wait(&v_empty[vs], (vu - 1) & 1);
+          mbar_expect_tx(&v_full[vs], C::TILE);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_3d(smem + C::OFF_V + vs * C::TILE + c * 16384, &p.tm_kv, &v_full[vs],
-                      col_v + c * 64, j * 128, smp);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_3d(smem + C::OFF_V + vs * C::TILE + c * 16384, &p.tm_kv, &v_full[vs],
+                        col_v + c * 64, j * 128, smp);
+        }
       }
     }
   } else if (warp == 1) {
@@ -917,204 +912,210 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
           mma_bf16_ts_warp(d, a + 8 * kk, b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
       }
     };
-    auto wait_k = [&](int j) {
-      mbar_wait(&k_full[j % C::K_STAGES], (j / C::K_STAGES) & 1);
-      if (lane == 0) DQ_TRACE(11, j);
+    auto wait_k = [&](int g2) {
+      mbar_wait(&k_full[g2 % C::K_STAGES], (g2 / C::K_STAGES) & 1);
       tc_fence_after();
     };
-    auto wait_v = [&](int j) {
-      mbar_wait(&v_full[j % C::V_STAGES], (j / C::V_STAGES) & 1);
+    auto wait_v = [&](int g2) {
+      mbar_wait(&v_full[g2 % C::V_STAGES], (g2 / C::V_STAGES) & 1);
       tc_fence_after();
     };
-    mbar_wait(qd_tmem, 0);
-    if (lane == 0) DQ_TRACE(0, 0);
-    tc_fence_after();
-    wait_k(0);
-    issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k);
-    mma_commit_warp(s_full);
-    wait_v(0);
-    issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v);
-    mma_commit_warp(dp_full);
-    mma_commit_warp(&v_empty[0]);
-    for (int j = 0; j < n; ++j) {
-      if (j + 1 < n) {
-        // S(j+1) over S(j) once every warp holds S(j) in registers
-        mbar_wait(s_loaded, j & 1);
-        if (lane == 0) DQ_TRACE(1, j);
-        wait_k(j + 1);
-        issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + ((j + 1) % C::K_STAGES) * kTile);
-        mma_commit_warp(s_full);
-      }
-      // dQ += dS(j) K_j; dS of keys [16kk, 16kk+16) at column 64(kk/4) +
-      // 8(kk%4) of the dP columns
-      mbar_wait(ds_full, j & 1);
-      if (lane == 0) DQ_TRACE(2, j);
+    int gk = 0, round = 0;
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
+      mbar_wait(qd_tmem, round & 1);
       tc_fence_after();
-      const uint64_t bk = mn_k + (j % C::K_STAGES) * kTile;
-      mma_k128_ts_n_quads(tm + C::TM_DQ, tm + C::TM_DP, bk, idesc_q, j > 0 ? 1u : 0u);
-      mma_commit_warp(&k_empty[j % C::K_STAGES]);
-      if (j + 1 < n) {
-        // dP(j+1) over dS(j): in order behind dQ(j), its reader
-        wait_v(j + 1);
-        issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v + ((j + 1) % C::V_STAGES) * kTile);
-        mma_commit_warp(dp_full);
-        mma_commit_warp(&v_empty[(j + 1) % C::V_STAGES]);
+      wait_k(gk);
+      issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + (gk % C::K_STAGES) * kTile);
+      mma_commit_warp(s_full);
+      wait_v(gk);
+      issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v + (gk % C::V_STAGES) * kTile);
+      mma_commit_warp(dp_full);
+      mma_commit_warp(&v_empty[gk % C::V_STAGES]);
+      for (int j = 0; j < n; ++j, ++gk) {
+        if (j + 1 < n) {
+          // S(j+1) over S(j) once every warp holds S(j) in registers
+          mbar_wait(s_loaded, gk & 1);
+          wait_k(gk + 1);
+          issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + ((gk + 1) % C::K_STAGES) * kTile);
+          mma_commit_warp(s_full);
+        }
+        // dQ += dS(j) K_j; dS of keys [16kk, 16kk+16) at column 64(kk/4) +
+        // 8(kk%4) of the dP columns
+        mbar_wait(ds_full, gk & 1);
+        if (j == 0 && round > 0) mbar_wait(acc_free, (round - 1) & 1);  // previous dQ out
+        tc_fence_after();
+        mma_k128_ts_n_quads(tm + C::TM_DQ, tm + C::TM_DP, mn_k + (gk % C::K_STAGES) * kTile, idesc_q,
+                            j > 0 ? 1u : 0u);
+        mma_commit_warp(&k_empty[gk % C::K_STAGES]);
+        if (j + 1 < n) {
+          // dP(j+1) over dS(j): in order behind dQ(j), its reader
+          wait_v(gk + 1);
+          issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v + ((gk + 1) % C::V_STAGES) * kTile);
+          mma_commit_warp(dp_full);
+          mma_commit_warp(&v_empty[(gk + 1) % C::V_STAGES]);
+        }
       }
+      mma_commit_warp(fin);
     }
-    mma_commit_warp(fin);
-    if (lane == 0) DQ_TRACE(3, 15);
   } else {
     // ------------------------------------------ softmax-gradient warps
     const int quad = warp & 3;
     const int g = (warp - 2) >> 2;   // keys [64g, 64g+64) of each key tile
     const int r = quad * 32 + lane;  // query row within the tile (TMEM lane)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const int qrow = q0 + r;
-    const bool valid = qrow < p.S;
-    const long long lrow = ((long long)smp * p.H + head) * p.S + qrow;
-    // padded query rows: Q, dO are zero there, dS = 0 whatever lse is
-    const float lse = valid ? __ldg(p.lse + lrow) : 0.f;
-    const float cl2 = p.c;
+    const float cl2 = p.c, scale = p.scale;
     constexpr int HW = HD / 2;  // hd columns per group
-    // the row's O half, loaded while Q / dO arrive
-    uint4 ov[HW / 8];
-    {
-      const uint4* orow = reinterpret_cast<const uint4*>(
-          p.o + ((long long)smp * p.S + qrow) * p.ld_o + (long long)head * HD + g * HW);
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);
+    int gk = 0, round = 0;
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
+      const int job = unit / p.n_qt, q0 = (unit % p.n_qt) * 128;
+      const int head = job % p.H, smp = job / p.H;
+      const int qrow = q0 + r;
+      const bool valid = qrow < p.S;
+      const long long lrow = (long long)job * p.S + qrow;
+      // padded query rows: Q, dO are zero there, dS = 0 whatever lse is
+      const float lse = valid ? __ldg(p.lse + lrow) : 0.f;
+      // the row's O half, loaded while Q / dO arrive
+      uint4 ov[HW / 8];
+      {
+        const uint4* orow = reinterpret_cast<const uint4*>(
+            p.o + ((long long)smp * p.S + qrow) * p.ld_o + (long long)head * HD + g * HW);
 #pragma unroll
-      for (int u = 0; u < HW / 8; ++u) ov[u] = valid ? __ldg(orow + u) : make_uint4(0, 0, 0, 0);
-    }
-    float dpart = 0.f;
-    {
-      // the Q_i and dO_i rows into TMEM (A operands of S and dP): group g
-      // copies its half of the head dimension (hd/2 bf16, 16-byte pieces of
-      // the SW128 tiles)
-      mbar_wait(qd_full, 0);
+        for (int u = 0; u < HW / 8; ++u) ov[u] = valid ? __ldg(orow + u) : make_uint4(0, 0, 0, 0);
+      }
+      float dpart = 0.f;
+      {
+        // the Q_i and dO_i rows into TMEM (A operands of S and dP): group g
+        // copies its half of the head dimension (hd/2 bf16, 16-byte pieces of
+        // the SW128 tiles). The previous unit's scores have all completed:
+        // this warp waited for its fin.
+        mbar_wait(qd_full, round & 1);
 #pragma unroll
-      for (int which = 0; which < 2; ++which) {
-        const uint32_t base = smem_u32(smem + (which == 0 ? C::OFF_Q : C::OFF_DO));
-        uint32_t v[HW / 2];
-#pragma unroll
-        for (int u = 0; u < HW / 8; ++u) {
-          const int col = g * HW + 8 * u;  // first hd column of the piece
-          const uint32_t a = base + (uint32_t)(col >> 6) * 16384u + (uint32_t)(r >> 3) * 1024u +
-                             (uint32_t)(r & 7) * 128u + (uint32_t)((((col & 63) >> 3) ^ (r & 7)) << 4);
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(v[4 * u]), "=r"(v[4 * u + 1]), "=r"(v[4 * u + 2]), "=r"(v[4 * u + 3])
-                       : "r"(a));
-        }
-        if (which == 1) {
-          // this half of rowsum(dO * O), in column order
+        for (int which = 0; which < 2; ++which) {
+          const uint32_t base = smem_u32(smem + (which == 0 ? C::OFF_Q : C::OFF_DO));
+          uint32_t v[HW / 2];
 #pragma unroll
           for (int u = 0; u < HW / 8; ++u) {
-            const uint32_t ow[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
+            const int col = g * HW + 8 * u;  // first hd column of the piece
+            const uint32_t a = base + (uint32_t)(col >> 6) * 16384u + (uint32_t)(r >> 3) * 1024u +
+                               (uint32_t)(r & 7) * 128u +
+                               (uint32_t)((((col & 63) >> 3) ^ (r & 7)) << 4);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[4 * u]), "=r"(v[4 * u + 1]), "=r"(v[4 * u + 2]), "=r"(v[4 * u + 3])
+                         : "r"(a));
+          }
+          if (which == 1) {
+            // this half of rowsum(dO * O), in column order
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[4 * u + e]));
-              const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[e]));
-              dpart = fmaf(a2.x, b2.x, dpart);
-              dpart = fmaf(a2.y, b2.y, dpart);
+            for (int u = 0; u < HW / 8; ++u) {
+              const uint32_t ow[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 a2 =
+                    __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[4 * u + e]));
+                const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[e]));
+                dpart = fmaf(a2.x, b2.x, dpart);
+                dpart = fmaf(a2.y, b2.y, dpart);
+              }
             }
           }
+          const uint32_t t = tmem + lane_off + (which == 0 ? C::TM_Q : C::TM_DO) + g * (HW / 2);
+          if constexpr (HW / 2 == 32) {
+            tmem_st32(t, *reinterpret_cast<const uint32_t(*)[32]>(v));
+          } else {
+            tmem_st16(t, *reinterpret_cast<const uint32_t(*)[16]>(v));
+          }
         }
-        const uint32_t t = tmem + lane_off + (which == 0 ? C::TM_Q : C::TM_DO) + g * (HW / 2);
-        if constexpr (HW / 2 == 32) {
-          tmem_st32(t, *reinterpret_cast<const uint32_t(*)[32]>(v));
-        } else {
-          tmem_st16(t, *reinterpret_cast<const uint32_t(*)[16]>(v));
-        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qd_tmem);  // also: Q / dO shared memory free
       }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(qd_tmem);
-    }
-    // delta = (low half) + (high half), the same order in both groups
-    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);
-    red[g * 128 + r] = dpart;
-    named_bar_sync(1, 256);
-    const float dlt = red[r] + red[128 + r];
-    if (g == 0 && valid) p.delta[lrow] = dlt;
-    for (int j = 0; j < n; ++j) {
-      mbar_wait(s_full, j & 1);
-      if (lane == 0) DQ_TRACE(5, j);
+      // delta = (low half) + (high half), the same order in both groups
+      red[g * 128 + r] = dpart;
+      named_bar_sync(1, 256);
+      const float dlt = red[r] + red[128 + r];
+      named_bar_sync(1, 256);  // red is rewritten by the next unit
+      if (g == 0 && valid) p.delta[lrow] = dlt;
+      for (int j = 0; j < n; ++j, ++gk) {
+        mbar_wait(s_full, gk & 1);
+        tc_fence_after();
+        float pr[64];
+        {
+          uint32_t a0[32], a1[32];
+          tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64, a0);
+          tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64 + 32, a1);
+          tmem_wait_ld();
+          reg_fence32(a0);
+          reg_fence32(a1);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            pr[e] = __uint_as_float(a0[e]);
+            pr[32 + e] = __uint_as_float(a1[e]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_loaded);
+        // one exponential in four on the FMA pipe (same split as the dK/dV pass)
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const float xv = fmaf(pr[e], cl2, -lse);
+          pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
+        }
+        mbar_wait(dp_full, gk & 1);
+        tc_fence_after();
+        const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
+        uint32_t d[64];
+        {
+          uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
+          uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
+          tmem_ld32_nowait(dpc, d0);
+          tmem_ld32_nowait(dpc + 32, d1);
+          tmem_wait_ld();
+          reg_fence32(d0);
+          reg_fence32(d1);
+        }
+        // dS = P (dP - delta), unscaled (the 1/sqrt(hd) goes to the epilogue),
+        // 64 keys -> columns [64g, 64g+32) of the consumed dP
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          pk[e] = pack_bf16x2(pr[2 * e] * (__uint_as_float(d[2 * e]) - dlt),
+                              pr[2 * e + 1] * (__uint_as_float(d[2 * e + 1]) - dlt));
+        tmem_st32(dpc, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_full);
+      }
+      // ---------------------------------------------- dQ of the unit out
+      mbar_wait(fin, round & 1);
       tc_fence_after();
-      float pr[64];
-      {
-        uint32_t a0[32], a1[32];
-        tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64, a0);
-        tmem_ld32_nowait(tmem + lane_off + C::TM_S + g * 64 + 32, a1);
-        tmem_wait_ld();
-        reg_fence32(a0);
-        reg_fence32(a1);
+      __nv_bfloat16* drow =
+          p.dqkv + ((long long)smp * p.S + qrow) * p.ld_qkv + (long long)head * 3 * HD;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          pr[e] = __uint_as_float(a0[e]);
-          pr[32 + e] = __uint_as_float(a1[e]);
+      for (int c = 0; c < HD / 32; ++c) {  // group g: columns [g*HD/2, (g+1)*HD/2)
+        const int col = g * (HD / 2) + c * 16;
+        uint32_t v[16];
+        tmem_ld16_nowait(tmem + lane_off + C::TM_DQ + col, v);
+        tmem_wait_ld();
+        reg_fence16(v);
+        if (valid) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * scale, __uint_as_float(v[u * 8 + 1]) * scale);
+            w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * scale, __uint_as_float(v[u * 8 + 3]) * scale);
+            w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * scale, __uint_as_float(v[u * 8 + 5]) * scale);
+            w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * scale, __uint_as_float(v[u * 8 + 7]) * scale);
+            *reinterpret_cast<uint4*>(drow + col + u * 8) = w;
+          }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(s_loaded);
-      if (lane == 0) DQ_TRACE(6, j);
-      // one exponential in four on the FMA pipe (same split as attn_bwd_kernel)
-#pragma unroll
-      for (int e = 0; e < 64; ++e) {
-        const float xv = fmaf(pr[e], cl2, -lse);
-        pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
-      }
-      mbar_wait(dp_full, j & 1);
-      if (lane == 0) DQ_TRACE(7, j);
-      tc_fence_after();
-      const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
-      uint32_t d[64];
-      {
-        uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
-        uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
-        tmem_ld32_nowait(dpc, d0);
-        tmem_ld32_nowait(dpc + 32, d1);
-        tmem_wait_ld();
-        reg_fence32(d0);
-        reg_fence32(d1);
-      }
-      // dS = P (dP - delta), unscaled (the 1/sqrt(hd) goes to the epilogue),
-      // 64 keys -> columns [64g, 64g+32) of the consumed dP
-      uint32_t pk[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        pk[e] = pack_bf16x2(pr[2 * e] * (__uint_as_float(d[2 * e]) - dlt),
-                            pr[2 * e + 1] * (__uint_as_float(d[2 * e + 1]) - dlt));
-      tmem_st32(dpc, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
-      if (lane == 0) DQ_TRACE(8, j);
-    }
-    // ------------------------------------------------ dQ epilogue
-    mbar_wait(fin, 0);
-    DQ_TRACE(9, 0);
-    tc_fence_after();
-    __nv_bfloat16* drow = p.dqkv + ((long long)smp * p.S + qrow) * p.ld_qkv + col_q;
-    const float scale = p.scale;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {  // group g: columns [g*HD/2, (g+1)*HD/2)
-      const int col = g * (HD / 2) + c * 16;
-      uint32_t v[16];
-      tmem_ld16_nowait(tmem + lane_off + C::TM_DQ + col, v);
-      tmem_wait_ld();
-      reg_fence16(v);
-      if (valid) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * scale, __uint_as_float(v[u * 8 + 1]) * scale);
-          w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * scale, __uint_as_float(v[u * 8 + 3]) * scale);
-          w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * scale, __uint_as_float(v[u * 8 + 5]) * scale);
-          w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * scale, __uint_as_float(v[u * 8 + 7]) * scale);
-          *reinterpret_cast<uint4*>(drow + col + u * 8) = w;
-        }
-      }
+      if (lane == 0) mbar_arrive(acc_free);
     }
   }
 
@@ -1344,12 +1345,14 @@ cudaError_t attn_dq_sm100(const AttnDesc& d, cudaStream_t s) {
   p.ld_o = d.ld_o;
   p.dqkv = static_cast<__nv_bfloat16*>(d.dqkv);
   p.ld_qkv = d.ld_qkv;
-  const long long grid = (long long)p.n_qt * d.heads * d.samples;
-  if (grid > 0x7fffffffLL) {
-    g_attn_err = "attn_dq_sm100: grid too large";
+  const long long units = (long long)p.n_qt * d.heads * d.samples;
+  if (units > 0x7fffffffLL) {
+    g_attn_err = "attn_dq_sm100: too many units";
     return cudaErrorInvalidValue;
   }
-  cudaError_t e = d.head_dim == 128 ? launch_dq<128>(p, (int)grid, s) : launch_dq<64>(p, (int)grid, s);
+  p.units = (int)units;
+  const int grid = (int)std::min<long long>(units, std::max(1, device_sms()));
+  cudaError_t e = d.head_dim == 128 ? launch_dq<128>(p, grid, s) : launch_dq<64>(p, grid, s);
   if (e != cudaSuccess) g_attn_err = std::string("attn_dq_sm100 launch: ") + cudaGetErrorString(e);
   return e;
 }

@@ -333,46 +333,6 @@ int main(int argc, char** argv) {
     time_it("split total (again)", split);
   }
 
-#ifdef TESS_ATTN_TRACE_BUILD
-  if (std::getenv("TESS_DQ_TRACE")) {
-    long long* tr = nullptr;
-    const size_t nb = 12 * 16 * 16 * sizeof(long long);
-    CK(cudaMalloc(&tr, nb));
-    CK(cudaMemset(tr, 0, nb));
-    CK(cudaMemcpyToSymbol(sm100::attn::g_dq_trace, &tr, sizeof(tr)));
-    a.dqkv = dqkv3;
-    CK(attn_dq_sm100(a, 0));
-    CK(cudaDeviceSynchronize());
-    std::vector<long long> h(12 * 16 * 16);
-    CK(cudaMemcpy(h.data(), tr, nb, cudaMemcpyDeviceToHost));
-    long long t0 = 0;
-    for (long long v : h)
-      if (v && (!t0 || v < t0)) t0 = v;
-    auto at = [&](int ev, int w, int st) {
-      long long v = h[(ev * 16 + w) * 16 + st];
-      return v ? v - t0 : -1;
-    };
-    std::printf("dQ pass CTA 0: MMA qd_tmem %lld, fin %lld | softmax w2 qd_full %lld, fin seen %lld\n",
-                at(0, 1, 0), at(3, 1, 15), at(4, 2, 0), at(9, 2, 0));
-    std::printf("step | MMA: S(j+1) dQ(j) | w2: S_in s_loaded dP_in ds_out | w9: S_in ds_out\n");
-    for (int st = 0; st < 16; ++st)
-      std::printf("%4d | %6lld %6lld | %6lld %6lld %6lld %6lld | %6lld %6lld\n", st, at(1, 1, st),
-                  at(2, 1, st), at(5, 2, st), at(6, 2, st), at(7, 2, st), at(8, 2, st), at(5, 9, st),
-                  at(8, 9, st));
-    std::printf("K_j load issued / K_j seen by MMA:");
-    for (int st = 0; st < 16; ++st) std::printf(" %lld/%lld", at(10, 0, st), at(11, 1, st));
-    std::printf("\nper-warp s_loaded, ds_out (warps 2..9) steps 4-6:\n");
-    for (int st = 4; st < 7; ++st) {
-      std::printf("%d s_loaded:", st);
-      for (int w = 2; w < 10; ++w) std::printf(" %lld", at(6, w, st));
-      std::printf("\n%d ds_out  :", st);
-      for (int w = 2; w < 10; ++w) std::printf(" %lld", at(8, w, st));
-      std::printf("\n");
-    }
-    long long* z = nullptr;
-    CK(cudaMemcpyToSymbol(sm100::attn::g_dq_trace, &z, sizeof(z)));
-  }
-#endif
   for (int tm = 0; tm < 4 && std::getenv("TESS_ATTN_TRACE") && pl.ok; ++tm) {
     mode_only(tm);
     std::printf("trace mode %d\n", tm);
