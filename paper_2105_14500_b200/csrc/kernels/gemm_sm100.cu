@@ -73,6 +73,11 @@ struct Params {
   int M, N;
   int nb0;
   int tiles_m, tiles_n, tiles_per_batch, num_tiles;
+  // pair kernel, NH = 2: tile ids >= num_full are HALF tiles (256 x 256):
+  // the tiles of a partial last wave, split in two so they fill the pairs a
+  // 256 x 512 remainder would leave idle (id num_full + 2t + h = half h of
+  // full tile num_full + t); num_tiles counts both kinds
+  int num_full;
   int group_m;
   int mma_lead;                 // NH == 2: half-0 MMAs lead while half 1 drains
   int* tile_counter;            // pair kernel: dynamic tile order (zeroed per launch)
@@ -909,6 +914,21 @@ __device__ __forceinline__ void decode_pair_tile(const Params& p, int tile, int&
   n0 = (in / gm) * p.tile_n;
 }
 
+// Tile id -> tile coordinates; `half` for the split tiles of the last wave
+// (n0 then names the 256-column half).
+template <int BNP>
+__device__ __forceinline__ void decode_pair_id(const Params& p, int id, int& b0, int& b1, int& m0,
+                                               int& n0, bool& half) {
+  half = id >= p.num_full;
+  if (!half) {
+    decode_pair_tile(p, id, b0, b1, m0, n0);
+    return;
+  }
+  const int t = p.num_full + ((id - p.num_full) >> 1);
+  decode_pair_tile(p, t, b0, b1, m0, n0);
+  n0 += ((id - p.num_full) & 1) * BNP;
+}
+
 template <bool A_MN, bool B_MN, int ST, int NH, int BNP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2cta_kernel(const __grid_constant__ Params p) {
@@ -984,7 +1004,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (tile < 0) break;
         }
         int b0, b1, m0, n0;
-        decode_pair_tile(p, tile, b0, b1, m0, n0);
+        bool half;
+        decode_pair_id<BNP>(p, tile, b0, b1, m0, n0, half);
+        const int nh = half ? 1 : NH;
         const int mr = m0 + (int)cta * C::HALF;
         // Serpentine K: odd waves walk K backwards, so a wave starts on the
         // k-blocks the previous wave touched last -- still in L2 for the
@@ -1005,7 +1027,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * C::STAGE_BYTES;
             uint8_t* sb = sa + C::A_BYTES;
-            if (cta == 0) mbar_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+            if (cta == 0)
+              mbar_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + nh * C::BH * BK * 2));
             const int k = kb * BK;
             if (!A_MN) {
               tma_load_4d_2sm(sa, ma, &full_bar[stage], k, mr, b0, b1);
@@ -1016,6 +1039,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
+              if (h >= nh) break;
               // the pair's columns [n0 + 256h, +256): this CTA stages its 128
               const int nr = n0 + h * BNP + (int)cta * C::BH;
               uint8_t* sbh = sb + h * (C::BH * BK * 2);
@@ -1046,9 +1070,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;  // NH == 1: alternating slot; NH == 2: both slots every tile
       uint32_t slot_phase = 0;  // bit s = phase of slot s
       for (;;) {
-        if (tq.pop(rank, false) < 0) break;
+        const int id = tq.pop(rank, false);
+        if (id < 0) break;
+        const bool half = id >= p.num_full;  // one 256-column half only
+        const int nh = half ? 1 : NH;
         int kb0 = 0;
-        if (NH == 2 && p.mma_lead) {
+        if (NH == 2 && p.mma_lead && !half) {
           // Lead phase: the epilogue drains half 0 first, so start this
           // tile's half-0 MMAs on up to STAGES k-blocks while it is still
           // draining half 1, then catch half 1 up on the same (still held)
@@ -1099,6 +1126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
           for (int h = 0; h < NH; ++h) {
+            if (h >= nh) break;
             const int slot = NH == 1 ? acc : h;
             if (kb == 0 && kb0 == 0) {
               // the accumulator slot must have been drained by the epilogue
@@ -1124,6 +1152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
+          if (h >= nh) break;
           const int slot = NH == 1 ? acc : h;
           mma_commit_2sm(&tfull_bar[slot]);
           slot_phase ^= 1u << slot;
@@ -1142,11 +1171,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int tile = tq.pop(rank, true);
       if (tile < 0) break;
       int b0, b1, m0, n0;
-      decode_pair_tile(p, tile, b0, b1, m0, n0);
+      bool half;
+      decode_pair_id<BNP>(p, tile, b0, b1, m0, n0, half);
+      const int nh = half ? 1 : NH;
       const int mrow0 = m0 + (int)cta * C::HALF + quad * 32;
       const int m = mrow0 + lane;
 #pragma unroll 1
-      for (int h = 0; h < NH; ++h) {
+      for (int h = 0; h < nh; ++h) {
         const int slot = NH == 1 ? acc : h;
         mbar_wait(&tfull_bar[slot], (slot_phase >> slot) & 1);
         tc_fence_after();
@@ -1334,6 +1365,16 @@ cudaError_t launch_2cta(const Params& p_in, cudaStream_t stream) {
   if (!p.tile_counter) return cudaErrorMemoryAllocation;
   const int n = std::min(p.num_tiles, std::max(1, num_sms() / 2));  // persistent: one pair per TPC
   p.wave = n;
+  p.num_full = p.num_tiles;
+  if (NH == 2) {
+    // a partial last wave of at most half the pairs runs as twice as many
+    // 256 x 256 halves: all of it in half a tile's time instead of one
+    const int rem = p.num_tiles % n;
+    if (p.num_tiles > n && rem > 0 && 2 * rem <= n) {
+      p.num_full = p.num_tiles - rem;
+      p.num_tiles = p.num_full + 2 * rem;
+    }
+  }
   kern<<<2 * n, kThreads, C::SMEM_BYTES, stream>>>(p);
   return cudaGetLastError();
 }
