@@ -150,6 +150,30 @@ def test_fused_attention_cfg4_head_shape_vs_torch(tess):
     assert max(errs.values()) <= 2e-2, errs
 
 
+@pytest.mark.parametrize("b,s,nh,hd", [(4, 392, 40, 64), (3, 520, 24, 128)])
+def test_fused_attention_persistent_units_vs_torch(tess, b, s, nh, hd):
+    """More (sample, head, tile) units than SMs, so every persistent CTA of
+    the two backward passes runs several units back to back (ring phases,
+    K/V and Q/dO reloads, accumulator hand-over across units), with ragged
+    sequences (392 = 3 x 128 + 8, 520 = 4 x 128 + 8) and both head dims."""
+    import torch
+    torch.manual_seed(1)
+    h = nh * hd
+    dev = torch.device("cuda", 0)
+
+    def bf(t):
+        return t.to(torch.bfloat16).float()
+    x = bf(torch.randn(b * s, h, device=dev))
+    wqkv = bf(torch.randn(h, 3 * h, device=dev) * h ** -0.5)
+    wproj = bf(torch.randn(h, h, device=dev) * h ** -0.5)
+    dy = bf(torch.randn(b * s, h, device=dev))
+    ry, rdx, rgq, rgp = _torch_attention_layer(x, wqkv, wproj, dy, b, s, nh)
+    gy, gdx, ggq, ggp = _run_attention_device(tess, b, s, h, nh, x, wqkv, wproj, dy)
+    errs = {"y": _rel(gy, ry), "dx": _rel(gdx, rdx), "w_qkv": _rel(ggq, rgq),
+            "w_proj": _rel(ggp, rgp)}
+    assert max(errs.values()) <= 2e-2, errs
+
+
 def test_fused_attention_deterministic(tess, orc):
     b, s, h, nh = 2, 256, 256, 2
     x, dy, P = _inputs(orc, b, s, h, 5)
