@@ -70,6 +70,24 @@ __device__ __forceinline__ float exp2_fma(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// exp2_fma on a pair with packed fp32 ops (FFMA2 / FADD2): 2 lanes' worth of
+// the polynomial per issue slot, for the pair-aligned share of the forward's
+// exponentials moved off the MUFU pipe.
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 K = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23
+  const float2 t = add2(x, K);
+  const float2 j = add2(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = fma2(j, make_float2(-1.0f, -1.0f), x);
+  float2 q = fma2(make_float2(0.05286731571f, 0.05286731571f), f,
+                  make_float2(0.2421521395f, 0.2421521395f));
+  q = fma2(q, f, make_float2(0.6935868263f, 0.6935868263f));
+  q = fma2(q, f, make_float2(0.9999627471f, 0.9999627471f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
 constexpr int kThreads = 320;
 // which of every 8 exponentials of the forward use exp2_fma (bit e & 7)
 #ifndef TESS_ATTN_FWD_POLY
@@ -290,12 +308,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           if (e >= nvalid) s[e] = -INFINITY;
       }
       // row max / row sum as 8 independent chains (a single 128-long
-      // dependent fmax / fadd chain is ~4 clk x 128 of latency per tile)
+      // dependent fmax / fadd chain is ~4 clk x 128 of latency per tile);
+      // 3-input max and packed fp32 pairs halve their issue slots
       float mp[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) mp[k] = s[k];
 #pragma unroll
-      for (int e = 8; e < BKV; ++e) mp[e & 7] = fmaxf(mp[e & 7], s[e]);
+      for (int e = 8; e < BKV; e += 16)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mp[k] = max3f(mp[k], s[e + k], s[e + 8 + k < BKV ? e + 8 + k : e + k]);
       const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                              fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
       const float m_new = fmaxf(m_used, mx * cl2);
@@ -322,14 +343,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       // all exponentials on MUFU: moving a share to the FMA pipe (a degree-5
       // polynomial exp2) measured slower (25 %: +6 %, 50 %: +22 %) -- the
       // softmax is issue-bound, not MUFU-bound
-      float rp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float2 rp[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      const float2 c2 = make_float2(cl2, cl2), nm2 = make_float2(-m_used, -m_used);
 #pragma unroll
-      for (int e = 0; e < BKV; ++e) {
-        const float xv = fmaf(s[e], cl2, -m_used);
-        s[e] = (kFwdPolyMask >> (e & 7)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
-        rp[e & 7] += s[e];
+      for (int e = 0; e < BKV; e += 2) {
+        const float2 xv = fma2(make_float2(s[e], s[e + 1]), c2, nm2);
+        if ((kFwdPolyMask >> (e & 7)) & 1) {  // pair on the FMA pipe
+          const float2 pv = exp2_fma2(xv);
+          s[e] = pv.x;
+          s[e + 1] = pv.y;
+        } else {
+          s[e] = ex2_approx(xv.x);
+          s[e + 1] = ex2_approx(xv.y);
+        }
+        rp[(e >> 1) & 3] = add2(rp[(e >> 1) & 3], make_float2(s[e], s[e + 1]));
       }
-      l += ((rp[0] + rp[1]) + (rp[2] + rp[3])) + ((rp[4] + rp[5]) + (rp[6] + rp[7]));
+      l += ((rp[0].x + rp[0].y) + (rp[1].x + rp[1].y)) + ((rp[2].x + rp[2].y) + (rp[3].x + rp[3].y));
       // P (bf16 pairs, lower key in the low half) over the consumed S columns
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -644,10 +673,12 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
                      : "r"(ldw + (uint32_t)(16 * e4)));
         const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; u += 2) {
           const int e = 4 * e4 + u;
-          const float xv = fmaf(pr[e], cl2, -lv[u]);
-          pr[e] = (kBwdPolyMask >> u) & 1 ? exp2_fma(xv) : ex2_approx(xv);
+          const float2 xv = fma2(make_float2(pr[e], pr[e + 1]), make_float2(cl2, cl2),
+                                 make_float2(-lv[u], -lv[u + 1]));
+          pr[e] = (kBwdPolyMask >> u) & 1 ? exp2_fma(xv.x) : ex2_approx(xv.x);
+          pr[e + 1] = (kBwdPolyMask >> (u + 1)) & 1 ? exp2_fma(xv.y) : ex2_approx(xv.y);
         }
       }
 #pragma unroll
@@ -684,10 +715,14 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
                      : "=f"(d4.x), "=f"(d4.y), "=f"(d4.z), "=f"(d4.w)
                      : "r"(ldw + 512u + (uint32_t)(16 * e4)));
         const int e = 4 * e4;
-        pk[2 * e4] = pack_bf16x2(pr[e] * (__uint_as_float(d[e]) - d4.x),
-                                 pr[e + 1] * (__uint_as_float(d[e + 1]) - d4.y));
-        pk[2 * e4 + 1] = pack_bf16x2(pr[e + 2] * (__uint_as_float(d[e + 2]) - d4.z),
-                                     pr[e + 3] * (__uint_as_float(d[e + 3]) - d4.w));
+        const float2 a = mul2(make_float2(pr[e], pr[e + 1]),
+                              add2(make_float2(__uint_as_float(d[e]), __uint_as_float(d[e + 1])),
+                                   make_float2(-d4.x, -d4.y)));
+        const float2 b = mul2(make_float2(pr[e + 2], pr[e + 3]),
+                              add2(make_float2(__uint_as_float(d[e + 2]), __uint_as_float(d[e + 3])),
+                                   make_float2(-d4.z, -d4.w)));
+        pk[2 * e4] = pack_bf16x2(a.x, a.y);
+        pk[2 * e4 + 1] = pack_bf16x2(b.x, b.y);
       }
       tmem_st32(dpc, pk);
       tmem_wait_st();
@@ -1059,9 +1094,11 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         if (lane == 0) mbar_arrive(s_loaded);
         // one exponential in four on the FMA pipe (same split as the dK/dV pass)
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          const float xv = fmaf(pr[e], cl2, -lse);
-          pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv) : ex2_approx(xv);
+        for (int e = 0; e < 64; e += 2) {
+          const float2 xv =
+              fma2(make_float2(pr[e], pr[e + 1]), make_float2(cl2, cl2), make_float2(-lse, -lse));
+          pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv.x) : ex2_approx(xv.x);
+          pr[e + 1] = (kBwdPolyMask >> ((e + 1) & 3)) & 1 ? exp2_fma(xv.y) : ex2_approx(xv.y);
         }
         mbar_wait(dp_full, gk & 1);
         tc_fence_after();
@@ -1080,9 +1117,12 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         // 64 keys -> columns [64g, 64g+32) of the consumed dP
         uint32_t pk[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          pk[e] = pack_bf16x2(pr[2 * e] * (__uint_as_float(d[2 * e]) - dlt),
-                              pr[2 * e + 1] * (__uint_as_float(d[2 * e + 1]) - dlt));
+        for (int e = 0; e < 32; ++e) {
+          const float2 v = mul2(make_float2(pr[2 * e], pr[2 * e + 1]),
+                                add2(make_float2(__uint_as_float(d[2 * e]), __uint_as_float(d[2 * e + 1])),
+                                     make_float2(-dlt, -dlt)));
+          pk[e] = pack_bf16x2(v.x, v.y);
+        }
         tmem_st32(dpc, pk);
         tmem_wait_st();
         tc_fence_before();
