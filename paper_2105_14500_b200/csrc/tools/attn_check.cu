@@ -3,11 +3,14 @@
 //   * the round-1 split path: attn_bwd_split_sm100 + the batched dQ GEMM over the
 //     stored dS^T, against
 //   * the round-2 experiment attn_bwd_dq_sm100 (attn_bwd_experiments.cuh:
-//     dQ fused with an ordered on-chip accumulation, and its modes).
+//     dQ fused with an ordered on-chip accumulation, and its modes);
+//   * the single-query-tile forward experiment (attn_fwd_experiments.cuh)
+//     against the product forward: max |dO|, |dlse| and timing
+//     (TESS_FWD_ONLY=1 stops after it).
 // dQ of the split path is also recomputed by a CUDA-core loop over dS^T, so
 // both dQs have an independent check; dK / dV are compared between the two
 // kernels. The product parity tests go through the C-ABI and the fp64 oracle.
-//   attn_check [b s heads hd] [reps]      (TESS_ATTN_TRACE=1: step timeline)
+//   attn_check [b s heads hd] [reps] [profile mode: -1 split, 10 dQ pass, 11 dK/dV pass, 12 fwd1]
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -19,6 +22,7 @@
 
 #include "../kernels/gemm.h"
 #include "attn_bwd_experiments.cuh"
+#include "attn_fwd_experiments.cuh"
 
 using namespace tess;
 
@@ -120,6 +124,53 @@ int main(int argc, char** argv) {
   a.head_dim = hd;
   a.scale = scale;
   CK(attn_fwd_sm100(a, 0));
+  {  // single-tile forward vs the two-tile forward
+    __nv_bfloat16* o1;
+    float* lse1;
+    CK(cudaMalloc(&o1, rows * ldo * 2));
+    CK(cudaMalloc(&lse1, (size_t)B * H * S * 4));
+    AttnDesc a1 = a;
+    a1.o = o1;
+    a1.lse = lse1;
+    CK(attn_fwd1_sm100(a1, 0));
+    CK(cudaDeviceSynchronize());
+    std::vector<__nv_bfloat16> h0(rows * ldo), h1(rows * ldo);
+    std::vector<float> l0((size_t)B * H * S), l1((size_t)B * H * S);
+    CK(cudaMemcpy(h0.data(), o, rows * ldo * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h1.data(), o1, rows * ldo * 2, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(l0.data(), lse, l0.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(l1.data(), lse1, l1.size() * 4, cudaMemcpyDeviceToHost));
+    double dmax = 0, ref = 0, lmax = 0;
+    for (size_t i = 0; i < h0.size(); ++i) {
+      const double x = __bfloat162float(h0[i]), y = __bfloat162float(h1[i]);
+      dmax = std::max(dmax, std::fabs(x - y));
+      ref = std::max(ref, std::fabs(x));
+    }
+    for (size_t i = 0; i < l0.size(); ++i) lmax = std::max(lmax, (double)std::fabs(l0[i] - l1[i]));
+    std::printf("fwd1 vs fwd: max|dO| %.3e (max|O| %.3e), max|dlse| %.3e\n", dmax, ref, lmax);
+    if (argc >= 7 && atoi(argv[6]) == 12) {
+      std::printf("profiled fwd1\n");
+      return 0;
+    }
+    auto t1 = [&](const char* name, auto fn) {
+      cudaEvent_t x0, x1;
+      cudaEventCreate(&x0);
+      cudaEventCreate(&x1);
+      for (int w = 0; w < 2; ++w) fn();
+      CK(cudaEventRecord(x0));
+      for (int i = 0; i < reps; ++i) fn();
+      CK(cudaEventRecord(x1));
+      CK(cudaEventSynchronize(x1));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, x0, x1);
+      std::printf("%-26s %8.3f ms/iter\n", name, ms / reps);
+    };
+    t1("attn_fwd (two-tile)", [&]() { CK(attn_fwd_sm100(a, 0)); });
+    t1("attn_fwd1 (one-tile)", [&]() { CK(attn_fwd1_sm100(a1, 0)); });
+    t1("attn_fwd (two-tile) again", [&]() { CK(attn_fwd_sm100(a, 0)); });
+    t1("attn_fwd1 (one-tile) again", [&]() { CK(attn_fwd1_sm100(a1, 0)); });
+    if (std::getenv("TESS_FWD_ONLY")) return 0;
+  }
   delta_k<<<(unsigned)((B * H * (long long)S + 127) / 128), 128>>>(dout, o, delta, S, H, hd, ldo);
   a.dout = dout;
   a.delta = delta;
