@@ -409,7 +409,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 }
 
 
-
 // --------------------------------------------------------------- backward
 // which of every 4 exponentials of the backward use exp2_fma (bit u)
 #ifndef TESS_ATTN_BWD_POLY
