@@ -1,0 +1,5 @@
+# forward: exponentials against the running maximum with the row max alongside (rare redo), same-box A/B; parity vs the one-tile experiment
+export TESS_FWD_ONLY=1
+for a in "1 512 4 128 3" "2 1000 4 64 3" "1 136 3 128 3" "3 520 24 128 3" "4 392 40 64 3" "2 128 8 128 3" "3 256 50 64 3" "4 2048 96 128 3"; do
+  timeout 120 tools/libvar/attn_check_e1 $a | grep -E "fwd1 vs|FAIL|rror"; done
+for r in 1 2 3; do for v in e0 e1; do echo "== $v"; timeout 300 tools/libvar/attn_check_$v 4 2048 96 128 20 | grep -E "two-tile"; done; done
