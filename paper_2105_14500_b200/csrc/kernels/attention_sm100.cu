@@ -780,26 +780,31 @@ __global__ void __launch_bounds__(kKvThreads, 1) attn_bwd_kv_kernel(const __grid
 // HBM, dQ accumulates in TMEM over the key tiles in order (deterministic, no
 // atomics). Persistent: one CTA per SM takes (sample, head, query tile)
 // units in a strided order; the next unit's Q / dO load as soon as the
-// current unit has copied its own into TMEM. 320 threads:
-//   warp 0      TMA: Q_i, dO_i per unit (then copied into TMEM: the score MMAs
-//               read only K_j / V_j from shared memory); K_j into a 3-slot
-//               ring, V_j into a 2-slot ring.
+// current unit's last score MMA has read its own. 320 threads:
+//   warp 0      TMA: Q_i, dO_i per unit; K_j into a 3-slot ring, V_j into a
+//               2-slot ring.
 //   warp 1      MMA issuer (warp-wide, one elected lane; each K=128 block
 //               one PTX statement), all M=128 N=128:
-//                 S(j+1) = Q K^T      (A = Q in TMEM)   once S(j) is loaded
-//                 dQ += dS(j) K_j     (A = dS in TMEM over the consumed dP
-//                                      columns, B = K_j read MN-major)
-//                 dP(j+1) = dO V^T    (A = dO in TMEM)  in order behind dQ(j)
+//                 S(j+1) = Q K^T      (A = Q in smem)   once S(j) is loaded
+//                 dP(j+1) = dO V^T    (A = dO in smem)  into the other dP
+//                                      buffer, right behind S(j+1)
+//                 dQ += dS(j) K_j     (A = dS in TMEM over the consumed
+//                                      columns of dP(j)'s buffer, B = K_j
+//                                      read MN-major)
+//               dP is double-buffered, so dP(j+1) does not wait for dQ(j):
+//               the softmax warps find S and dP of the next key tile ready.
 //   warps 2-9   thread = query row, group g = keys [64g, 64g+64): first
 //               delta = rowsum(dO * O) of its row (each group one half of
-//               hd, summed through shared memory; written out for the dK/dV
-//               pass, which runs after this one), then per key tile
-//               P = 2^(c S - lse) (lse, delta are the row's own: registers),
-//               dS = P (dP - delta) -> bf16 pairs over its own consumed dP
-//               columns; at the end dQ out of TMEM (scaled) into the Q slot
-//               of dqkv.
-// TMEM: S [0,128), dP / dS [128,256), dQ [256,256+hd), Q [384,384+hd/2),
-// dO [448,448+hd/2).
+//               hd, dO from shared memory, summed through shared memory;
+//               written out for the dK/dV pass, which runs after this one),
+//               then per key tile P = 2^(c S - lse) (lse, delta are the
+//               row's own: registers) while dP loads, dS = P (dP - delta) ->
+//               bf16 pairs over its own consumed dP columns; at the end dQ
+//               out of TMEM (scaled) into the Q slot of dqkv.
+// TMEM: S [0,128), dP / dS buffers [128,256) and [256,384), dQ [384,384+hd).
+// (Q and dO in TMEM as TS operands instead -- round 2's earlier form --
+// leaves no room for the second dP buffer: 3-4 % slower,
+// profiles/r2_attn_dq_dp_double_buffer_ab.log.)
 constexpr int kDqThreads = 320;
 
 struct DqParams {
@@ -829,7 +834,8 @@ struct DqCfg {
   static constexpr int USED = OFF_RED + 1024;
   static constexpr int SMEM_BYTES = USED + 1024 <= 232448 ? USED + 1024 : 232448;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_Q = 384, TM_DO = 448;
+  // dP / dS double-buffered: dP(j+1) is computed while dS(j) waits for dQ(j)
+  static constexpr int TM_S = 0, TM_DP = 128, TM_DQ = 384;
 };
 
 template <int HD>
@@ -841,16 +847,17 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
   if ((smem - smem_raw) + C::USED > C::SMEM_BYTES) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* qd_full = bars + 0;                 // Q_i, dO_i of the unit in shared memory
-  uint64_t* qd_tmem = bars + 1;                 // ... copied into TMEM (8 warps)
+  uint64_t* qd_free = bars + 1;                 // ... read by the unit's last score MMA
   uint64_t* k_full = bars + 2;                  // K_STAGES
   uint64_t* k_empty = k_full + C::K_STAGES;     // K_STAGES
   uint64_t* v_full = k_empty + C::K_STAGES;     // V_STAGES
   uint64_t* v_empty = v_full + C::V_STAGES;     // V_STAGES
   uint64_t* s_full = v_empty + C::V_STAGES;     // S(j) in TMEM
   uint64_t* s_loaded = s_full + 1;              // S(j) in registers (8 warps)
-  uint64_t* dp_full = s_loaded + 1;             // dP(j) in TMEM
-  uint64_t* ds_full = dp_full + 1;              // dS(j) in TMEM (8 warps)
-  uint64_t* fin = ds_full + 1;                  // dQ of the unit complete
+  // per dP buffer: the softmax warps run up to one step ahead of the issuer
+  uint64_t* dp_full = s_loaded + 1;             // 2: dP(j) in TMEM buffer j & 1
+  uint64_t* ds_full = dp_full + 2;              // 2: dS(j) in TMEM buffer j & 1 (8 warps)
+  uint64_t* fin = ds_full + 2;                  // dQ of the unit complete
   uint64_t* acc_free = fin + 1;                 // dQ read out of TMEM (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
 
@@ -861,7 +868,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
 
   if (warp == 0 && lane == 0) {
     mbar_init(qd_full, 1);
-    mbar_init(qd_tmem, 8);
+    mbar_init(qd_free, 1);
     for (int s = 0; s < C::K_STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -872,8 +879,10 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     }
     mbar_init(s_full, 1);
     mbar_init(s_loaded, 8);
-    mbar_init(dp_full, 1);
-    mbar_init(ds_full, 8);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dp_full[b], 1);
+      mbar_init(&ds_full[b], 8);
+    }
     mbar_init(fin, 1);
     mbar_init(acc_free, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -899,8 +908,8 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         const int job = unit / p.n_qt, q0 = (unit % p.n_qt) * 128;
         const int head = job % p.H, smp = job / p.H;
         const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
-        // Q / dO tiles: free once the previous unit copied them into TMEM
-        if (round > 0) mbar_wait(qd_tmem, (round - 1) & 1);
+        // Q / dO tiles: free once the previous unit's last score MMA read them
+        if (round > 0) mbar_wait(qd_free, (round - 1) & 1);
         mbar_expect_tx(qd_full, 2 * C::TILE);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) {
@@ -934,17 +943,18 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint64_t kmaj_k = make_sdesc(sbase + C::OFF_K, 16, 1024);
     const uint64_t kmaj_v = make_sdesc(sbase + C::OFF_V, 16, 1024);
+    const uint64_t kmaj_q = make_sdesc(sbase + C::OFF_Q, 16, 1024);
+    const uint64_t kmaj_do = make_sdesc(sbase + C::OFF_DO, 16, 1024);
     const uint64_t mn_k = make_sdesc(sbase + C::OFF_K, 16384, 1024);
     constexpr uint64_t kTile = (uint64_t)(C::TILE >> 4);
     auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
-    // A (M=128 x K=hd) from TMEM at column a, 8 columns per K=16 step
-    auto issue_ts = [&](uint32_t d, uint32_t a, uint64_t b) {
+    auto issue_scores = [&](uint32_t d, uint64_t a, uint64_t b) {  // A, B K-major in smem
       if constexpr (HD == 128) {
-        mma_k128_ts_k(d, a, b, idesc_s, 0u);
+        mma_k128_ss_kk(d, a, b, idesc_s, 0u);
       } else {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          mma_bf16_ts_warp(d, a + 8 * kk, b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+          mma_bf16_warp(d, a + kmaj_off(kk), b + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
       }
     };
     auto wait_k = [&](int g2) {
@@ -955,40 +965,41 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       mbar_wait(&v_full[g2 % C::V_STAGES], (g2 / C::V_STAGES) & 1);
       tc_fence_after();
     };
+    auto issue_s = [&](int g2) {
+      wait_k(g2);
+      issue_scores(tm + C::TM_S, kmaj_q, kmaj_k + (g2 % C::K_STAGES) * kTile);
+      mma_commit_warp(s_full);
+    };
+    auto issue_dp = [&](int g2) {  // into buffer g2 & 1, whose dS(g2 - 2) dQ has read
+      wait_v(g2);
+      issue_scores(tm + C::TM_DP + (uint32_t)(g2 & 1) * 128u, kmaj_do, kmaj_v + (g2 % C::V_STAGES) * kTile);
+      mma_commit_warp(&dp_full[g2 & 1]);
+      mma_commit_warp(&v_empty[g2 % C::V_STAGES]);
+    };
     int gk = 0, round = 0;
     for (int unit = blockIdx.x; unit < units; unit += gridDim.x, ++round) {
-      mbar_wait(qd_tmem, round & 1);
+      mbar_wait(qd_full, round & 1);
       tc_fence_after();
-      wait_k(gk);
-      issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + (gk % C::K_STAGES) * kTile);
-      mma_commit_warp(s_full);
-      wait_v(gk);
-      issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v + (gk % C::V_STAGES) * kTile);
-      mma_commit_warp(dp_full);
-      mma_commit_warp(&v_empty[gk % C::V_STAGES]);
+      issue_s(gk);
+      issue_dp(gk);
       for (int j = 0; j < n; ++j, ++gk) {
         if (j + 1 < n) {
-          // S(j+1) over S(j) once every warp holds S(j) in registers
+          // S(j+1) over S(j) once every warp holds S(j) in registers, and
+          // dP(j+1) into the other buffer right behind it
           mbar_wait(s_loaded, gk & 1);
-          wait_k(gk + 1);
-          issue_ts(tm + C::TM_S, tm + C::TM_Q, kmaj_k + ((gk + 1) % C::K_STAGES) * kTile);
-          mma_commit_warp(s_full);
+          issue_s(gk + 1);
+          issue_dp(gk + 1);
+          if (j + 2 == n) mma_commit_warp(qd_free);  // the unit's last reads of Q / dO
         }
         // dQ += dS(j) K_j; dS of keys [16kk, 16kk+16) at column 64(kk/4) +
-        // 8(kk%4) of the dP columns
-        mbar_wait(ds_full, gk & 1);
+        // 8(kk%4) of its dP buffer
+        mbar_wait(&ds_full[gk & 1], (gk >> 1) & 1);
         if (j == 0 && round > 0) mbar_wait(acc_free, (round - 1) & 1);  // previous dQ out
         tc_fence_after();
-        mma_k128_ts_n_quads(tm + C::TM_DQ, tm + C::TM_DP, mn_k + (gk % C::K_STAGES) * kTile, idesc_q,
-                            j > 0 ? 1u : 0u);
+        mma_k128_ts_n_quads(tm + C::TM_DQ, tm + C::TM_DP + (uint32_t)(gk & 1) * 128u,
+                            mn_k + (gk % C::K_STAGES) * kTile, idesc_q, j > 0 ? 1u : 0u);
         mma_commit_warp(&k_empty[gk % C::K_STAGES]);
-        if (j + 1 < n) {
-          // dP(j+1) over dS(j): in order behind dQ(j), its reader
-          wait_v(gk + 1);
-          issue_ts(tm + C::TM_DP, tm + C::TM_DO, kmaj_v + ((gk + 1) % C::V_STAGES) * kTile);
-          mma_commit_warp(dp_full);
-          mma_commit_warp(&v_empty[(gk + 1) % C::V_STAGES]);
-        }
+        if (n == 1) mma_commit_warp(qd_free);
       }
       mma_commit_warp(fin);
     }
@@ -1020,51 +1031,28 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
       }
       float dpart = 0.f;
       {
-        // the Q_i and dO_i rows into TMEM (A operands of S and dP): group g
-        // copies its half of the head dimension (hd/2 bf16, 16-byte pieces of
-        // the SW128 tiles). The previous unit's scores have all completed:
-        // this warp waited for its fin.
+        // this half of rowsum(dO * O), dO from the unit's shared-memory tile
+        // (16-byte pieces of the SW128 tile), in column order
         mbar_wait(qd_full, round & 1);
+        const uint32_t base = smem_u32(smem + C::OFF_DO);
 #pragma unroll
-        for (int which = 0; which < 2; ++which) {
-          const uint32_t base = smem_u32(smem + (which == 0 ? C::OFF_Q : C::OFF_DO));
-          uint32_t v[HW / 2];
+        for (int u = 0; u < HW / 8; ++u) {
+          const int col = g * HW + 8 * u;  // first hd column of the piece
+          const uint32_t a = base + (uint32_t)(col >> 6) * 16384u + (uint32_t)(r >> 3) * 1024u +
+                             (uint32_t)(r & 7) * 128u + (uint32_t)((((col & 63) >> 3) ^ (r & 7)) << 4);
+          uint32_t v[4];
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                       : "r"(a));
+          const uint32_t ow[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
 #pragma unroll
-          for (int u = 0; u < HW / 8; ++u) {
-            const int col = g * HW + 8 * u;  // first hd column of the piece
-            const uint32_t a = base + (uint32_t)(col >> 6) * 16384u + (uint32_t)(r >> 3) * 1024u +
-                               (uint32_t)(r & 7) * 128u +
-                               (uint32_t)((((col & 63) >> 3) ^ (r & 7)) << 4);
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v[4 * u]), "=r"(v[4 * u + 1]), "=r"(v[4 * u + 2]), "=r"(v[4 * u + 3])
-                         : "r"(a));
-          }
-          if (which == 1) {
-            // this half of rowsum(dO * O), in column order
-#pragma unroll
-            for (int u = 0; u < HW / 8; ++u) {
-              const uint32_t ow[4] = {ov[u].x, ov[u].y, ov[u].z, ov[u].w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 a2 =
-                    __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[4 * u + e]));
-                const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[e]));
-                dpart = fmaf(a2.x, b2.x, dpart);
-                dpart = fmaf(a2.y, b2.y, dpart);
-              }
-            }
-          }
-          const uint32_t t = tmem + lane_off + (which == 0 ? C::TM_Q : C::TM_DO) + g * (HW / 2);
-          if constexpr (HW / 2 == 32) {
-            tmem_st32(t, *reinterpret_cast<const uint32_t(*)[32]>(v));
-          } else {
-            tmem_st16(t, *reinterpret_cast<const uint32_t(*)[16]>(v));
+          for (int e = 0; e < 4; ++e) {
+            const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[e]));
+            const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[e]));
+            dpart = fmaf(a2.x, b2.x, dpart);
+            dpart = fmaf(a2.y, b2.y, dpart);
           }
         }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(qd_tmem);  // also: Q / dO shared memory free
       }
       // delta = (low half) + (high half), the same order in both groups
       red[g * 128 + r] = dpart;
@@ -1092,6 +1080,15 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_loaded);
+        // dP(j) (computed alongside S(j)) loads while the exponentials run
+        mbar_wait(&dp_full[gk & 1], (gk >> 1) & 1);
+        tc_fence_after();
+        const uint32_t dpc = tmem + lane_off + C::TM_DP + (gk & 1) * 128 + g * 64;
+        uint32_t d[64];
+        uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
+        uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
+        tmem_ld32_nowait(dpc, d0);
+        tmem_ld32_nowait(dpc + 32, d1);
         // one exponential in four on the FMA pipe (same split as the dK/dV pass)
 #pragma unroll
         for (int e = 0; e < 64; e += 2) {
@@ -1100,19 +1097,9 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
           pr[e] = (kBwdPolyMask >> (e & 3)) & 1 ? exp2_fma(xv.x) : ex2_approx(xv.x);
           pr[e + 1] = (kBwdPolyMask >> ((e + 1) & 3)) & 1 ? exp2_fma(xv.y) : ex2_approx(xv.y);
         }
-        mbar_wait(dp_full, gk & 1);
-        tc_fence_after();
-        const uint32_t dpc = tmem + lane_off + C::TM_DP + g * 64;
-        uint32_t d[64];
-        {
-          uint32_t (&d0)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
-          uint32_t (&d1)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
-          tmem_ld32_nowait(dpc, d0);
-          tmem_ld32_nowait(dpc + 32, d1);
-          tmem_wait_ld();
-          reg_fence32(d0);
-          reg_fence32(d1);
-        }
+        tmem_wait_ld();
+        reg_fence32(d0);
+        reg_fence32(d1);
         // dS = P (dP - delta), unscaled (the 1/sqrt(hd) goes to the epilogue),
         // 64 keys -> columns [64g, 64g+32) of the consumed dP
         uint32_t pk[32];
@@ -1127,7 +1114,7 @@ __global__ void __launch_bounds__(kDqThreads, 1) attn_dq_kernel(const __grid_con
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(ds_full);
+        if (lane == 0) mbar_arrive(&ds_full[gk & 1]);
       }
       // ---------------------------------------------- dQ of the unit out
       mbar_wait(fin, round & 1);
