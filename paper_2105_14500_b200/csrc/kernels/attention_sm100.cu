@@ -14,7 +14,8 @@
 // every K/V tile (halving K/V traffic). 320 threads:
 //   warp 0      TMA producer: Q_A, Q_B once, then K_j, V_j into a ring of
 //               KV_STAGES 128-key tiles (128B-swizzled boxes {64, 128}).
-//   warp 1      MMA issuer + TMEM owner. Per key tile j:
+//   warp 1      MMA issuer + TMEM owner (warp-wide, one elected lane; each
+//               K=128 block of MMAs one PTX statement). Per key tile j:
 //                 S_A(j+1) = Q_A K_{j+1}^T, S_B(j+1) = Q_B K_{j+1}^T
 //                 O_A += P_A(j) V_j,         O_B += P_B(j) V_j
 //               interleaved so the tensor core works on one tile's MMAs
@@ -202,72 +203,74 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------- MMA issuer
-      constexpr uint32_t idesc_s = idesc_bf16(BQ, BKV, false, false);
-      constexpr uint32_t idesc_pv = idesc_bf16(BQ, HD, false, true);
-      const uint32_t sq0 = smem_u32(smem + C::OFF_QA);  // Q_B, P_B follow at fixed offsets
-      int stage = 0;
-      uint32_t phase = 0;
-      auto next_kv = [&]() {
-        const int s = stage;
-        mbar_wait(&kv_full[s], phase);
-        tc_fence_after();
-        if (++stage == C::KV_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-        return s;
-      };
-      auto issue_s = [&](int t, uint32_t skv) {
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (uint32_t)(kk >> 2) * 16384u + (uint32_t)(kk & 3) * 32u;
-          mma_bf16(tmem + C::TM_S0 + t * BKV, make_sdesc(sq0 + t * C::Q_BYTES + off, 16, 1024),
-                   make_sdesc(skv + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&s_full[t]);
-      };
-      // O += P V with P (bf16 pairs) in tensor memory: the consumed S columns
-      // [0, 64) of the tile's S buffer, 8 columns per 16 keys
-      auto issue_pv = [&](int t, uint32_t skv, bool acc) {
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ts(tmem + C::TM_O0 + t * 128, tmem + C::TM_S0 + t * BKV + kk * 8,
-                      make_sdesc(skv + (uint32_t)kk * 2048u, 16384, 1024), idesc_pv,
-                      (acc || kk > 0) ? 1u : 0u);
-      };
-      mbar_wait(q_full, 0);
+    // --------------------------------------------------------- MMA issuer
+    // warp-wide: one elected lane issues each K=128 block of MMAs as one PTX
+    // statement (descriptors advanced in registers)
+    constexpr uint32_t idesc_s = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idesc_pv = idesc_bf16(BQ, HD, false, true);
+    const uint32_t sbase = __shfl_sync(0xffffffffu, smem_u32(smem), 0);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint64_t kmaj_q = make_sdesc(sbase + C::OFF_QA, 16, 1024);  // Q_B at Q_BYTES
+    const uint64_t kmaj_kv = make_sdesc(sbase + C::OFF_KV, 16, 1024);
+    const uint64_t mn_kv = make_sdesc(sbase + C::OFF_KV, 16384, 1024);
+    constexpr uint64_t kQ = (uint64_t)(C::Q_BYTES >> 4), kKV = (uint64_t)(C::KV_BYTES >> 4);
+    auto kmaj_off = [](int kk) { return (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4); };
+    int stage = 0;
+    uint32_t phase = 0;
+    auto next_kv = [&]() {
+      const int s = stage;
+      mbar_wait(&kv_full[s], phase);
       tc_fence_after();
-      int ks = next_kv();
-      const uint32_t sk0 = smem_u32(smem + C::OFF_KV + ks * C::KV_BYTES);
-      issue_s(0, sk0);
-      issue_s(1, sk0);
-      mma_commit(&kv_empty[ks]);
-      for (int j = 0; j < p.n_kv; ++j) {
-        const int vs = next_kv();
-        const uint32_t sv = smem_u32(smem + C::OFF_KV + vs * C::KV_BYTES);
-        const bool more = j + 1 < p.n_kv;
-        uint32_t skn = 0;
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        issue_pv(0, sv, j > 0);
-        if (more) {
-          ks = next_kv();
-          skn = smem_u32(smem + C::OFF_KV + ks * C::KV_BYTES);
-          issue_s(0, skn);
-        }
-        mbar_wait(&p_full[1], j & 1);
-        tc_fence_after();
-        issue_pv(1, sv, j > 0);
-        mma_commit(&kv_empty[vs]);
-        if (more) {
-          issue_s(1, skn);
-          mma_commit(&kv_empty[ks]);
-        }
+      if (++stage == C::KV_STAGES) {
+        stage = 0;
+        phase ^= 1;
       }
-      mma_commit(o_full);
+      return s;
+    };
+    auto issue_s = [&](int t, int ks) {
+      const uint32_t d = tm + C::TM_S0 + t * BKV;
+      const uint64_t qa = kmaj_q + (uint64_t)t * kQ, kb = kmaj_kv + (uint64_t)ks * kKV;
+      if constexpr (HD == 128) {
+        mma_k128_ss_kk(d, qa, kb, idesc_s, 0u);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_warp(d, qa + kmaj_off(kk), kb + kmaj_off(kk), idesc_s, kk > 0 ? 1u : 0u);
+      }
+      mma_commit_warp(&s_full[t]);
+    };
+    // O += P V with P (bf16 pairs) in tensor memory: the consumed S columns
+    // [0, 64) of the tile's S buffer, 8 columns per 16 keys
+    auto issue_pv = [&](int t, int vs, bool acc) {
+      mma_k128_ts_n(tm + C::TM_O0 + t * 128, tm + C::TM_S0 + t * BKV, mn_kv + (uint64_t)vs * kKV,
+                    idesc_pv, acc ? 1u : 0u);
+    };
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    int ks = next_kv();
+    issue_s(0, ks);
+    issue_s(1, ks);
+    mma_commit_warp(&kv_empty[ks]);
+    for (int j = 0; j < p.n_kv; ++j) {
+      const int vs = next_kv();
+      const bool more = j + 1 < p.n_kv;
+      mbar_wait(&p_full[0], j & 1);
+      tc_fence_after();
+      issue_pv(0, vs, j > 0);
+      if (more) {
+        ks = next_kv();
+        issue_s(0, ks);
+      }
+      mbar_wait(&p_full[1], j & 1);
+      tc_fence_after();
+      issue_pv(1, vs, j > 0);
+      mma_commit_warp(&kv_empty[vs]);
+      if (more) {
+        issue_s(1, ks);
+        mma_commit_warp(&kv_empty[ks]);
+      }
     }
+    mma_commit_warp(o_full);
   } else {
     // --------------------------------------------------- softmax warps
     const int t = (warp - 2) >> 2;   // tile A (0) or B (1)
