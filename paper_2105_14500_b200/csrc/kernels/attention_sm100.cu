@@ -10,10 +10,14 @@
 // row, the backward recomputes P from it.
 //
 // ---------------------------------------------------------------- forward
-// One CTA = one (sample, head) and two 128-query tiles A and B that share
-// every K/V tile (halving K/V traffic). 320 threads:
-//   warp 0      TMA producer: Q_A, Q_B once, then K_j, V_j into a ring of
-//               KV_STAGES 128-key tiles (128B-swizzled boxes {64, 128}).
+// Unit = one (sample, head) and two 128-query tiles A and B that share
+// every K/V tile (halving K/V traffic). Persistent: one CTA per SM takes
+// units in a strided order; the next unit's Q tiles load once the current
+// unit's last score MMAs have read its own, its first scores run while the
+// current unit's O is written out. 320 threads:
+//   warp 0      TMA producer: Q_A, Q_B per unit, K_j, V_j into a ring of
+//               KV_STAGES 128-key tiles (128B-swizzled boxes {64, 128}),
+//               continuing across units.
 //   warp 1      MMA issuer + TMEM owner (warp-wide, one elected lane; each
 //               K=128 block of MMAs one PTX statement). Per key tile j:
 //                 S_A(j+1) = Q_A K_{j+1}^T, S_B(j+1) = Q_B K_{j+1}^T
@@ -105,7 +109,8 @@ struct FwdParams {
   CUtensorMap tm_qkv;  // 3-D view [cols, S, samples] of qkv, box {64, 128, 1}
   int S, H, n_pairs, n_kv;
   int hd;
-  float c;  // scale * log2(e)
+  int units;  // samples * H * n_pairs
+  float c;    // scale * log2(e)
   __nv_bfloat16* o;
   long long ld_o;
   float* lse;
@@ -132,24 +137,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;                        // 1
-  uint64_t* kv_full = bars + 1;                   // KV_STAGES
+  uint64_t* q_full = bars;                        // 1: Q_A, Q_B of the unit
+  uint64_t* q_free = bars + 1;                    // 1: ... read by its last S MMA
+  uint64_t* kv_full = bars + 2;                   // KV_STAGES
   uint64_t* kv_empty = kv_full + C::KV_STAGES;    // KV_STAGES
   uint64_t* s_full = kv_empty + C::KV_STAGES;     // 2 (tile A, B)
   uint64_t* p_full = s_full + 2;                  // 2
   uint64_t* o_full = p_full + 2;                  // 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+  uint64_t* acc_free = o_full + 1;                // 2: O_t read out (4 warps each)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int pair = blockIdx.x % p.n_pairs;
-  const int head = (blockIdx.x / p.n_pairs) % p.H;
-  const int smp = blockIdx.x / (p.n_pairs * p.H);
-  const int q0 = pair * 2 * BQ;
-  const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+  const int n = p.n_kv;
+  // unit = (sample * H + head) * n_pairs + pair
+  auto unit_coords = [&](int unit, int& q0, int& head, int& smp) {
+    q0 = (unit % p.n_pairs) * 2 * BQ;
+    head = (unit / p.n_pairs) % p.H;
+    smp = unit / (p.n_pairs * p.H);
+  };
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_free, 1);
     for (int s = 0; s < C::KV_STAGES; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -157,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4);
+      mbar_init(&acc_free[t], 4);
     }
     mbar_init(o_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -176,6 +187,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------ TMA producer
+      int stage = 0, round = 0;
+      uint32_t phase = 0;
+      for (int unit = blockIdx.x; unit < p.units; unit += gridDim.x, ++round) {
+      int q0, head, smp;
+      unit_coords(unit, q0, head, smp);
+      const int col_q = head * 3 * HD, col_k = col_q + HD, col_v = col_q + 2 * HD;
+      // Q_A, Q_B: free once the previous unit's last score MMA has read them
+      if (round > 0) mbar_wait(q_free, (round - 1) & 1);
       mbar_expect_tx(q_full, 2 * C::Q_BYTES);
 #pragma unroll
       for (int c = 0; c < HD / 64; ++c) {
@@ -183,9 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         tma_load_3d(smem + C::OFF_QB + c * 16384, &p.tm_qkv, q_full, col_q + c * 64, q0 + BQ,
                     smp);
       }
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < p.n_kv; ++j) {
+      for (int j = 0; j < n; ++j) {
 #pragma unroll
         for (int which = 0; which < 2; ++which) {  // K_j then V_j
           mbar_wait(&kv_empty[stage], phase ^ 1);
@@ -200,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             phase ^= 1;
           }
         }
+      }
       }
     }
   } else if (warp == 1) {
@@ -245,32 +263,40 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       mma_k128_ts_n(tm + C::TM_O0 + t * 128, tm + C::TM_S0 + t * BKV, mn_kv + (uint64_t)vs * kKV,
                     idesc_pv, acc ? 1u : 0u);
     };
-    mbar_wait(q_full, 0);
-    tc_fence_after();
-    int ks = next_kv();
-    issue_s(0, ks);
-    issue_s(1, ks);
-    mma_commit_warp(&kv_empty[ks]);
-    for (int j = 0; j < p.n_kv; ++j) {
-      const int vs = next_kv();
-      const bool more = j + 1 < p.n_kv;
-      mbar_wait(&p_full[0], j & 1);
+    // persistent over units; g counts key steps over all units (barrier
+    // parities), round the units of this CTA
+    int g = 0, round = 0;
+    for (int unit = blockIdx.x; unit < p.units; unit += gridDim.x, ++round) {
+      mbar_wait(q_full, round & 1);
       tc_fence_after();
-      issue_pv(0, vs, j > 0);
-      if (more) {
-        ks = next_kv();
-        issue_s(0, ks);
+      int ks = next_kv();
+      issue_s(0, ks);  // over the previous unit's P_A: in order behind its P V
+      issue_s(1, ks);
+      mma_commit_warp(&kv_empty[ks]);
+      if (n == 1) mma_commit_warp(q_free);
+      for (int j = 0; j < n; ++j, ++g) {
+        const int vs = next_kv();
+        const bool more = j + 1 < n;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&p_full[t], g & 1);
+          if (j == 0 && round > 0) mbar_wait(&acc_free[t], (round - 1) & 1);  // O_t read out
+          tc_fence_after();
+          issue_pv(t, vs, j > 0);
+          if (t == 0 && more) {
+            ks = next_kv();
+            issue_s(0, ks);
+          }
+        }
+        mma_commit_warp(&kv_empty[vs]);
+        if (more) {
+          issue_s(1, ks);
+          mma_commit_warp(&kv_empty[ks]);
+          if (j + 2 == n) mma_commit_warp(q_free);  // the unit's last reads of Q_A, Q_B
+        }
       }
-      mbar_wait(&p_full[1], j & 1);
-      tc_fence_after();
-      issue_pv(1, vs, j > 0);
-      mma_commit_warp(&kv_empty[vs]);
-      if (more) {
-        issue_s(1, ks);
-        mma_commit_warp(&kv_empty[ks]);
-      }
+      mma_commit_warp(o_full);
     }
-    mma_commit_warp(o_full);
   } else {
     // --------------------------------------------------- softmax warps
     const int t = (warp - 2) >> 2;   // tile A (0) or B (1)
@@ -280,9 +306,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const uint32_t t_s = tmem + lane_off + C::TM_S0 + t * BKV;
     const uint32_t t_o = tmem + lane_off + C::TM_O0 + t * 128;
     const float cl2 = p.c;
+    int g = 0, round = 0;
+    for (int unit = blockIdx.x; unit < p.units; unit += gridDim.x, ++round) {
+    int q0, head, smp;
+    unit_coords(unit, q0, head, smp);
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < p.n_kv; ++j) {
-      mbar_wait(&s_full[t], j & 1);
+    for (int j = 0; j < n; ++j, ++g) {
+      mbar_wait(&s_full[t], g & 1);
       tc_fence_after();
       float s[BKV];
       {
@@ -376,30 +406,37 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(&p_full[t]);
     }
     // ------------------------------------------------------------ epilogue
-    mbar_wait(o_full, 0);
+    mbar_wait(o_full, round & 1);
     tc_fence_after();
     const int qrow = q0 + t * BQ + r;
     const float inv = 1.0f / l;
     __nv_bfloat16* orow = p.o + ((long long)smp * p.S + qrow) * p.ld_o + (long long)head * HD;
+    // the row of O_t: all loads in flight, one wait, then O_t is released to
+    // the next unit's first P V before the stores
+    uint32_t ov[HD];
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t ov[32];
-      tmem_ld32_nowait(t_o + c * 32, ov);
-      tmem_wait_ld();
-      reg_fence32(ov);
-      if (qrow < p.S) {
+    for (int c = 0; c < HD / 32; ++c)
+      tmem_ld32_nowait(t_o + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
+    tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(ov[u * 8 + 0]) * inv, __uint_as_float(ov[u * 8 + 1]) * inv);
-          w.y = pack_bf16x2(__uint_as_float(ov[u * 8 + 2]) * inv, __uint_as_float(ov[u * 8 + 3]) * inv);
-          w.z = pack_bf16x2(__uint_as_float(ov[u * 8 + 4]) * inv, __uint_as_float(ov[u * 8 + 5]) * inv);
-          w.w = pack_bf16x2(__uint_as_float(ov[u * 8 + 6]) * inv, __uint_as_float(ov[u * 8 + 7]) * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + u * 8) = w;
-        }
+    for (int c = 0; c < HD / 32; ++c) reg_fence32(*reinterpret_cast<uint32_t(*)[32]>(&ov[c * 32]));
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&acc_free[t]);
+    if (qrow < p.S) {
+#pragma unroll
+      for (int u = 0; u < HD / 8; ++u) {
+        const uint32_t* x = &ov[u * 8];
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(x[0]) * inv, __uint_as_float(x[1]) * inv);
+        w.y = pack_bf16x2(__uint_as_float(x[2]) * inv, __uint_as_float(x[3]) * inv);
+        w.z = pack_bf16x2(__uint_as_float(x[4]) * inv, __uint_as_float(x[5]) * inv);
+        w.w = pack_bf16x2(__uint_as_float(x[6]) * inv, __uint_as_float(x[7]) * inv);
+        *reinterpret_cast<uint4*>(orow + u * 8) = w;
       }
     }
     if (qrow < p.S) p.lse[((long long)smp * p.H + head) * p.S + qrow] = m_used + __log2f(l);
+    }
   }
 
   tc_fence_before();
@@ -1304,12 +1341,14 @@ cudaError_t attn_fwd_sm100(const AttnDesc& d, cudaStream_t s) {
   p.o = static_cast<__nv_bfloat16*>(d.o);
   p.ld_o = d.ld_o;
   p.lse = d.lse;
-  const long long grid = (long long)p.n_pairs * d.heads * d.samples;
-  if (grid > 0x7fffffffLL) {
-    g_attn_err = "attn_fwd_sm100: grid too large";
+  const long long units = (long long)p.n_pairs * d.heads * d.samples;
+  if (units > 0x7fffffffLL) {
+    g_attn_err = "attn_fwd_sm100: too many units";
     return cudaErrorInvalidValue;
   }
-  cudaError_t e = d.head_dim == 128 ? launch_fwd<128>(p, (int)grid, s) : launch_fwd<64>(p, (int)grid, s);
+  p.units = (int)units;
+  const int grid = (int)std::min<long long>(units, device_sms());  // persistent
+  cudaError_t e = d.head_dim == 128 ? launch_fwd<128>(p, grid, s) : launch_fwd<64>(p, grid, s);
   if (e != cudaSuccess) g_attn_err = std::string("attn_fwd_sm100 launch: ") + cudaGetErrorString(e);
   return e;
 }
