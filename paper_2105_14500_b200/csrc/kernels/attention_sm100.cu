@@ -5,7 +5,7 @@
 //   S = Q K^T / sqrt(hd), P = softmax_rows(S) (layers.cpp:44-58, no mask),
 //   O = P V; backward dV = P^T dO, dP = dO V^T, dS = P * (dP - rowsum(dP*P))
 //   / sqrt(hd) (layers.cpp:60-74), dQ = dS K, dK = dS^T Q. The row term
-//   rowsum(dP*P) is computed as rowsum(dO*O) (k_attn_delta).
+//   rowsum(dP*P) is computed as rowsum(dO*O) inside the dQ pass.
 // Neither S nor P reaches HBM: the forward keeps one log2-sum-exp per query
 // row, the backward recomputes P from it.
 //
